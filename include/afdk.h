@@ -1,0 +1,97 @@
+/*
+ * afdk.h — C-ABI of the B200-native Step-3 decode hot path.
+ *
+ * This is the drop-in boundary below the reference's C++ operator API
+ * (/root/reference/proj/include/afdsim/*.hpp).  The reference *accounts* for
+ * each operation analytically; every entry point here *executes* the
+ * operation it accounts for, on an sm_100a GPU:
+ *
+ *   afdk_mfa_decode_attention   executes what kv_state_bytes / attn_core_flops
+ *                               account for           (costmodel.cpp:10-58)
+ *   afdk_mfa_layer              + attn_linear_flops    (costmodel.cpp:60-66,
+ *                               params builtin_catalog.cpp:243-247)
+ *   afdk_router_topk, afdk_quant_fp8, afdk_moe_permute,
+ *   afdk_moe_ffn                what ffn_flops accounts for (costmodel.cpp:68-74,
+ *                               params builtin_catalog.cpp:248-251)
+ *   afdk_exchange_*             what ffn_net_bytes accounts for (moeplan.cpp:17-20)
+ *   afdk_stage_times            the measured counterpart of derive_stage_times
+ *                               (pipesim.cpp:59-127, pipesim.hpp:28-29)
+ *
+ * Conventions: plain pointers and sizes only.  Device
+ * pointers are caller-owned and never freed here; the opaque afdk_ctx owns
+ * workspaces and tensor-map state.  Every call returns an afdk_status; the
+ * message of the last failure on the calling thread is afdk_last_error().
+ * A context is used from one host thread at a time; work is enqueued on the
+ * caller's CUDA stream (afdk_stream == cudaStream_t, NULL = legacy stream)
+ * and calls do not synchronise the device unless stated.
+ *
+ * Tensor formats: bf16 = IEEE bfloat16 (uint16 storage), e4m3 = OCP FP8
+ * E4M3FN (max 448), all tensors dense row-major unless stated.
+ */
+#ifndef AFDK_H
+#define AFDK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AFDK_ABI_VERSION 1
+
+typedef enum afdk_status {
+  AFDK_OK = 0,
+  AFDK_ERR_INVALID = 1,     /* bad argument / unsupported shape (afd::SpecError) */
+  AFDK_ERR_CUDA = 2,        /* CUDA runtime/driver failure                       */
+  AFDK_ERR_UNSUPPORTED = 3, /* device is not sm_100 / feature not built          */
+  AFDK_ERR_NO_DEVICE = 4    /* no CUDA device visible                            */
+} afdk_status;
+
+typedef struct afdk_ctx afdk_ctx;
+typedef void* afdk_stream; /* cudaStream_t */
+
+typedef struct afdk_cfg {
+  int device;  /* CUDA device ordinal */
+  int num_sms; /* 0 = all SMs of the device */
+} afdk_cfg;
+
+int afdk_abi_version(void);
+const char* afdk_last_error(void);
+afdk_status afdk_create(afdk_ctx** out, const afdk_cfg* cfg);
+void afdk_destroy(afdk_ctx* ctx);
+/* SMs the persistent kernels of this context are sized for */
+int afdk_num_sms(const afdk_ctx* ctx);
+
+/* ---------------------------------------------------------------- K2 + K3
+ * MFA decode attention core.  One shared K head and one shared V head of
+ * head_dim serve n_heads query heads.  Supported: n_heads 64,
+ * head_dim 256, page_size 64, bf16 everywhere (Step-3, configs 2 and 4).
+ *   q          [batch, n_heads, head_dim] bf16 (post-RoPE)
+ *   k_cache    [num_pages, page_size, head_dim] bf16, v_cache same
+ *   block_table[batch, max_pages] int32 page ids, seq_lens [batch] int32
+ *   out        [batch, n_heads, head_dim] bf16
+ *   lse        [batch, n_heads] fp32 natural-log LSE, optional (NULL)
+ * Any seq_len >= 0 (ragged); the split-KV factor is chosen internally so
+ * every SM streams the same number of pages (flash-decoding).            */
+typedef struct afdk_mfa_decode_args {
+  int batch, n_heads, head_dim, page_size;
+  const void* q;
+  const void* k_cache;
+  const void* v_cache;
+  int num_pages;
+  const int32_t* block_table;
+  int max_pages;
+  const int32_t* seq_lens;
+  float softmax_scale;
+  void* out;
+  float* lse;
+} afdk_mfa_decode_args;
+
+afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args* a,
+                                      afdk_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AFDK_H */

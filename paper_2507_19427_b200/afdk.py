@@ -1,0 +1,114 @@
+"""ctypes binding of include/afdk.h (the C-ABI of the B200 decode hot path).
+
+This is the Python view of the same entry points the C++ host layer
+(afd::ops, csrc/afd_ops.cpp) calls.  It carries no fallback: if
+libafdk.so is missing or the device is not sm_100, every call raises.
+Device tensors are passed as raw pointers (torch is only the allocator).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, Structure, c_char_p, c_float, c_int, c_int32, c_size_t, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libafdk.so")
+
+AFDK_OK = 0
+_STATUS = {1: "AFDK_ERR_INVALID", 2: "AFDK_ERR_CUDA", 3: "AFDK_ERR_UNSUPPORTED", 4: "AFDK_ERR_NO_DEVICE"}
+
+
+class AfdkError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class SpecError(AfdkError):
+    """Mirrors afd::SpecError (types.hpp:23): a shape/argument invariant failed."""
+
+
+class Cfg(Structure):
+    _fields_ = [("device", c_int), ("num_sms", c_int)]
+
+
+class MfaDecodeArgs(Structure):
+    _fields_ = [
+        ("batch", c_int), ("n_heads", c_int), ("head_dim", c_int), ("page_size", c_int),
+        ("q", c_void_p), ("k_cache", c_void_p), ("v_cache", c_void_p),
+        ("num_pages", c_int), ("block_table", c_void_p), ("max_pages", c_int),
+        ("seq_lens", c_void_p), ("softmax_scale", c_float), ("out", c_void_p), ("lse", c_void_p),
+    ]
+
+
+# exported symbol -> (restype, argtypes); the CPU test checks every symbol of
+# include/afdk.h is present in the built library
+SIGNATURES = {
+    "afdk_abi_version": (c_int, []),
+    "afdk_last_error": (c_char_p, []),
+    "afdk_create": (c_int, [POINTER(c_void_p), POINTER(Cfg)]),
+    "afdk_destroy": (None, [c_void_p]),
+    "afdk_num_sms": (c_int, [c_void_p]),
+    "afdk_mfa_decode_attention": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_void_p]),
+}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != AFDK_OK:
+        msg = load().afdk_last_error().decode()
+        raise (SpecError if status == 1 else AfdkError)(status, msg)
+
+
+def ptr(t) -> int:
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+class Context:
+    """RAII wrapper of afdk_ctx (afdk_create / afdk_destroy)."""
+
+    def __init__(self, device: int = 0, num_sms: int = 0):
+        self.lib = load()
+        h = c_void_p()
+        check(self.lib.afdk_create(ctypes.byref(h), ctypes.byref(Cfg(device, num_sms))))
+        self.handle = h
+
+    @property
+    def num_sms(self) -> int:
+        return self.lib.afdk_num_sms(self.handle)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.afdk_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------- K2 + K3
+    def mfa_decode_attention(self, q, k_cache, v_cache, block_table, seq_lens, out,
+                             softmax_scale: float, lse=None, stream: int = 0) -> None:
+        B, H, D = q.shape
+        a = MfaDecodeArgs(B, H, D, k_cache.shape[1], ptr(q), ptr(k_cache), ptr(v_cache),
+                          k_cache.shape[0], ptr(block_table), block_table.shape[1], ptr(seq_lens),
+                          softmax_scale, ptr(out), ptr(lse))
+        check(self.lib.afdk_mfa_decode_attention(self.handle, ctypes.byref(a), c_void_p(stream)))

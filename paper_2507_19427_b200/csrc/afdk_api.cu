@@ -1,0 +1,152 @@
+// afdk_api.cu — the extern "C" entry points of include/afdk.h.
+//
+// Validation mirrors the reference's error convention (types.hpp:12-25: the
+// message names the offending field); the C++ wrapper in afd_ops.cpp maps
+// AFDK_ERR_INVALID back to afd::SpecError.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/afdk.h"
+#include "afdk_internal.h"
+
+namespace afdk {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+void* workspace(Ctx& ctx, size_t bytes) {
+  if (bytes <= ctx.ws_bytes) return ctx.ws;
+  if (ctx.ws) cudaFree(ctx.ws);
+  ctx.ws = nullptr;
+  ctx.ws_bytes = 0;
+  const size_t want = align_up(bytes, size_t(1) << 21);
+  if (cudaMalloc(&ctx.ws, want) != cudaSuccess) return nullptr;
+  ctx.ws_bytes = want;
+  return ctx.ws;
+}
+
+bool encode_tma(Ctx& ctx, CUtensorMap* map, CUtensorMapDataType dt, int rank, void* base,
+                const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                CUtensorMapSwizzle swizzle) {
+  cuuint64_t d[5];
+  cuuint64_t s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i + 1 < rank) s[i] = strides[i];
+  }
+  const CUresult r = ctx.encode(map, dt, (cuuint32_t)rank, base, d, s, b, e,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return false;
+  }
+  return true;
+}
+
+}  // namespace afdk
+
+struct afdk_ctx {
+  afdk::Ctx c;
+};
+
+using afdk::set_error;
+
+static afdk_status cuda_fail(const char* what, cudaError_t e) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return AFDK_ERR_CUDA;
+}
+
+extern "C" {
+
+int afdk_abi_version(void) { return AFDK_ABI_VERSION; }
+
+const char* afdk_last_error(void) { return afdk::g_last_error.c_str(); }
+
+afdk_status afdk_create(afdk_ctx** out, const afdk_cfg* cfg) {
+  if (!out) { set_error("afdk_create: out is NULL"); return AFDK_ERR_INVALID; }
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    set_error("afdk_create: no CUDA device visible");
+    return AFDK_ERR_NO_DEVICE;
+  }
+  const int dev = cfg ? cfg->device : 0;
+  if (dev < 0 || dev >= n) { set_error("afdk_create: cfg.device out of range"); return AFDK_ERR_INVALID; }
+  cudaError_t e = cudaSetDevice(dev);
+  if (e != cudaSuccess) return cuda_fail("cudaSetDevice", e);
+  cudaDeviceProp prop{};
+  e = cudaGetDeviceProperties(&prop, dev);
+  if (e != cudaSuccess) return cuda_fail("cudaGetDeviceProperties", e);
+  if (prop.major != 10) {
+    set_error("afdk_create: device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
+              ", this library is built for sm_100a only");
+    return AFDK_ERR_UNSUPPORTED;
+  }
+  auto* ctx = new afdk_ctx();
+  ctx->c.device = dev;
+  ctx->c.sm_major = prop.major;
+  ctx->c.sm_minor = prop.minor;
+  ctx->c.num_sms = (cfg && cfg->num_sms > 0 && cfg->num_sms < prop.multiProcessorCount)
+                       ? cfg->num_sms
+                       : prop.multiProcessorCount;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || fn == nullptr) {
+    delete ctx;
+    set_error("afdk_create: cuTensorMapEncodeTiled unavailable");
+    return AFDK_ERR_CUDA;
+  }
+  ctx->c.encode = reinterpret_cast<afdk::EncodeTiledFn>(fn);
+  *out = ctx;
+  return AFDK_OK;
+}
+
+void afdk_destroy(afdk_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->c.ws) cudaFree(ctx->c.ws);
+  delete ctx;
+}
+
+int afdk_num_sms(const afdk_ctx* ctx) { return ctx ? ctx->c.num_sms : 0; }
+
+afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args* a,
+                                      afdk_stream stream) {
+  if (!ctx || !a) { set_error("afdk_mfa_decode_attention: NULL ctx/args"); return AFDK_ERR_INVALID; }
+  if (a->n_heads != 64) { set_error("mfa_decode: n_heads must be 64"); return AFDK_ERR_INVALID; }
+  if (a->head_dim != 256) { set_error("mfa_decode: head_dim must be 256"); return AFDK_ERR_INVALID; }
+  if (a->page_size != 64) { set_error("mfa_decode: page_size must be 64"); return AFDK_ERR_INVALID; }
+  if (a->batch <= 0) { set_error("mfa_decode: batch must be > 0"); return AFDK_ERR_INVALID; }
+  if (a->num_pages <= 0 || a->max_pages <= 0) { set_error("mfa_decode: num_pages/max_pages must be > 0"); return AFDK_ERR_INVALID; }
+  if (!a->q || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->out) {
+    set_error("mfa_decode: NULL tensor pointer");
+    return AFDK_ERR_INVALID;
+  }
+  if ((reinterpret_cast<uintptr_t>(a->q) | reinterpret_cast<uintptr_t>(a->k_cache) |
+       reinterpret_cast<uintptr_t>(a->v_cache) | reinterpret_cast<uintptr_t>(a->out)) & 15) {
+    set_error("mfa_decode: q/k_cache/v_cache/out must be 16-byte aligned");
+    return AFDK_ERR_INVALID;
+  }
+  afdk::Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  void* ws = afdk::workspace(c, afdk::mfa_decode_workspace_bytes(a->batch, c.num_sms));
+  if (!ws) { set_error("mfa_decode: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  afdk::MfaDecodeArgs m{a->batch, a->q, a->k_cache, a->v_cache, a->num_pages, a->block_table,
+                        a->max_pages, a->seq_lens, a->softmax_scale, a->out, a->lse, ws};
+  const cudaError_t e = afdk::mfa_decode_launch(c, m, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("mfa_decode launch", e);
+  return AFDK_OK;
+}
+
+}  // extern "C"

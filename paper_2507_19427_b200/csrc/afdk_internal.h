@@ -1,0 +1,56 @@
+// afdk_internal.h — shared host-side state of the C-ABI implementation.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+namespace afdk {
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 0;
+  int sm_major = 0, sm_minor = 0;
+  EncodeTiledFn encode = nullptr;
+  void* ws = nullptr;  // grow-only device workspace
+  size_t ws_bytes = 0;
+};
+
+// Returns a device workspace of at least `bytes` (grows; not graph-capturable
+// the first time a larger size is requested).
+void* workspace(Ctx& ctx, size_t bytes);
+
+// Tiled tensor map, innermost dimension first; strides in bytes for dims 1..
+bool encode_tma(Ctx& ctx, CUtensorMap* map, CUtensorMapDataType dt, int rank, void* base,
+                const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                CUtensorMapSwizzle swizzle);
+
+void set_error(const std::string& msg);
+
+struct MfaDecodeArgs {
+  int batch;
+  const void* q;
+  const void* k_cache;
+  const void* v_cache;
+  int num_pages;
+  const int32_t* block_table;
+  int max_pages;
+  const int32_t* seq_lens;
+  float softmax_scale;
+  void* out;
+  float* lse;
+  void* workspace;
+};
+size_t mfa_decode_workspace_bytes(int batch, int num_sms);
+cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream);
+
+}  // namespace afdk

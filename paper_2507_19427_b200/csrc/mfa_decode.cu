@@ -1,0 +1,547 @@
+// mfa_decode.cu — K2/K3: Step-3 MFA decode attention core on sm_100a.
+//
+// Computes, for every decode request b and every one of the 64 query heads,
+//   O[b,h,:] = softmax(scale * q[b,h,:] . K[b,:,:]^T) V[b,:,:]
+// against ONE shared 256-dim K head and ONE shared V head held in a paged
+// cache (accounting costmodel.cpp:26-44: 2*64*(256+256)*ctx FLOPs
+// and 2*256*elt bytes per cached token).  Because the 64 heads share K/V, each
+// 64-token page is read from HBM exactly once and consumed as a dense
+// [64 heads x 64 tokens x 256] tensor-core contraction:
+//
+//   S  = Q[64x256] . K_page^T        tcgen05.mma M=64 N=64  K=256 -> TMEM
+//   P  = exp2(S*scale*log2e - m)     4 softmax warps, one head per lane
+//   O += P[64x64] . V_page[64x256]   tcgen05.mma M=64 N=256 K=64  -> TMEM
+//
+// Work distribution (flash-decoding, load balanced): the flattened
+// (request, page) space is cut into one contiguous range per CTA
+// (grid = #SMs, 1 CTA/SM).  A range that covers a whole request writes bf16
+// O directly; otherwise it writes a normalised fp32 partial + log2-LSE into
+// slot (request + cta), and mfa_combine (K3) merges the partials.
+//
+// Warp roles (224 threads):  w0 = Q/K TMA producer, w1 = MMA issuer + TMEM
+// owner, w2..w5 = softmax / O-correction / epilogue (TMEM lanes 0-15 of each
+// 32-lane sub-partition hold the M=64 accumulator rows), w6 = V TMA producer.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "afdk_internal.h"
+#include "sm100.cuh"
+
+namespace afdk {
+namespace mfa {
+
+using namespace sm100;
+
+constexpr int kHeads = 64;
+constexpr int kDim = 256;
+constexpr int kPage = 64;                    // tokens per KV page == one tile
+constexpr int kTileBytes = kPage * kDim * 2;  // 32 KB (K or V of one page, bf16)
+constexpr int kChunkBytes = 64 * 128;         // one 64-row x 128B swizzle panel
+constexpr int kNK = 2;                        // K ring depth
+constexpr int kNV = 3;                        // V ring depth
+constexpr int kThreads = 224;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColO = 0, kColS = 256;    // O: 256 cols, S: 2 x 64 cols
+constexpr float kRescaleThresh = 8.0f;        // lazy O rescale (log2 units)
+
+struct __align__(1024) Smem {
+  uint8_t q[4 * kChunkBytes];       // 32 KB  Q of the current request
+  uint8_t k[kNK][kTileBytes];       // 64 KB
+  uint8_t v[kNV][kTileBytes];       // 96 KB
+  uint8_t p[2][kHeads * kPage * 2];  // 16 KB  bf16 probabilities (K-major SW128)
+  uint64_t q_full, q_empty;
+  uint64_t k_full[kNK], k_empty[kNK];
+  uint64_t v_full[kNV], v_empty[kNV];
+  uint64_t s_full[2], s_empty[2];
+  uint64_t p_full[2], p_empty[2];
+  uint64_t o_free;
+  uint32_t tmem_base;
+};
+
+struct Params {
+  const int32_t* block_table;  // [B, max_pages]
+  const int32_t* seq_lens;     // [B]
+  const int32_t* tile_prefix;  // [B+1] pages per request, exclusive prefix (plan kernel)
+  __nv_bfloat16* out;          // [B, 64, 256]
+  float* lse;                  // [B, 64] natural log, optional
+  float* part_o;               // [(B+G), 64, 256]
+  float* part_lse;             // [(B+G), 64] log2 domain
+  int batch, max_pages;
+  float scale_log2;            // softmax scale * log2(e)
+};
+
+// Contiguous page range of CTA c out of G over T total pages.
+__device__ __forceinline__ void cta_range(int c, int G, int T, int& lo, int& hi) {
+  lo = (int)(((long long)c * T) / G);
+  hi = (int)(((long long)(c + 1) * T) / G);
+}
+
+// First request whose page range contains global page index `t` (prefix is
+// non-decreasing; empty requests are skipped because prefix[r+1] > t fails).
+__device__ __forceinline__ int find_request(const int32_t* prefix, int B, int t) {
+  int lo = 0, hi = B - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(prefix + mid + 1) > t) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// Walks the segments (request, [lo,hi) local pages) of one CTA in order.
+struct SegmentWalker {
+  const int32_t* prefix;
+  int B, end, r, pos;
+  __device__ SegmentWalker(const int32_t* pf, int b, int start, int stop)
+      : prefix(pf), B(b), end(stop), r(0), pos(start) {
+    if (start < stop) r = find_request(pf, b, start);
+  }
+  // returns false when the range is exhausted
+  __device__ bool next(int& req, int& lo, int& hi, bool& whole) {
+    if (pos >= end) return false;
+    while (__ldg(prefix + r + 1) <= pos) ++r;
+    const int p0 = __ldg(prefix + r), p1 = __ldg(prefix + r + 1);
+    const int seg_hi = p1 < end ? p1 : end;
+    req = r;
+    lo = pos - p0;
+    hi = seg_hi - p0;
+    whole = (pos == p0) && (seg_hi == p1);
+    pos = seg_hi;
+    return true;
+  }
+};
+
+__global__ void plan_kernel(const int32_t* __restrict__ seq_lens, int B,
+                            int32_t* __restrict__ prefix) {
+  // single CTA, 1024 threads: exclusive scan of ceil(len/64) in chunks
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < B; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int v = (i < B) ? (max(__ldg(seq_lens + i), 0) + kPage - 1) / kPage : 0;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffff, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) warp_sums[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int w = (threadIdx.x < (blockDim.x >> 5)) ? warp_sums[threadIdx.x] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffff, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      warp_sums[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const int incl = x + ((threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0) + carry;
+    if (i < B) prefix[i + 1] = incl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) prefix[0] = 0;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
+                  const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, const Params prm) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = warp_id();
+  const int lane = threadIdx.x & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int T = __ldg(prm.tile_prefix + prm.batch);
+  int range_lo, range_hi;
+  cta_range(cta, G, T, range_lo, range_hi);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_init(&sm.q_full, 1);
+    mbar_init(&sm.q_empty, 1);
+    for (int i = 0; i < kNK; ++i) { mbar_init(&sm.k_full[i], 1); mbar_init(&sm.k_empty[i], 1); }
+    for (int i = 0; i < kNV; ++i) { mbar_init(&sm.v_full[i], 1); mbar_init(&sm.v_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.s_empty[i], 4);
+      mbar_init(&sm.p_full[i], 4);
+      mbar_init(&sm.p_empty[i], 1);
+    }
+    mbar_init(&sm.o_free, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------ Q + K TMA producer
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      SegmentWalker walk(prm.tile_prefix, prm.batch, range_lo, range_hi);
+      int req, lo, hi, seg = 0, g = 0;
+      bool whole;
+      while (walk.next(req, lo, hi, whole)) {
+        if (seg > 0) mbar_wait(&sm.q_empty, (seg & 1) ^ 1);
+        mbar_expect_tx(&sm.q_full, 4 * kChunkBytes);
+        for (int c = 0; c < 4; ++c)
+          tma_load_2d(sm.q + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, req * kHeads, pol_keep);
+        for (int t = lo; t < hi; ++t, ++g) {
+          const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
+          const int s = g % kNK, n = g / kNK;
+          if (n > 0) mbar_wait(&sm.k_empty[s], (n & 1) ^ 1);
+          mbar_expect_tx(&sm.k_full[s], kTileBytes);
+          for (int c = 0; c < 4; ++c)
+            tma_load_3d(sm.k[s] + c * kChunkBytes, &tm_k, &sm.k_full[s], c * 64, 0, page, pol_stream);
+        }
+        ++seg;
+      }
+    }
+  } else if (warp == 6) {
+    // ---------------------------------------------------- V TMA producer
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      SegmentWalker walk(prm.tile_prefix, prm.batch, range_lo, range_hi);
+      int req, lo, hi, g = 0;
+      bool whole;
+      while (walk.next(req, lo, hi, whole)) {
+        for (int t = lo; t < hi; ++t, ++g) {
+          const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
+          const int s = g % kNV, n = g / kNV;
+          if (n > 0) mbar_wait(&sm.v_empty[s], (n & 1) ^ 1);
+          mbar_expect_tx(&sm.v_full[s], kTileBytes);
+          for (int c = 0; c < 4; ++c)
+            tma_load_3d(sm.v[s] + c * kChunkBytes, &tm_v, &sm.v_full[s], c * 64, 0, page, pol_stream);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16(64, 64, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(64, 256, false, true);
+      const uint32_t q_base = smem_u32(sm.q);
+      SegmentWalker walk(prm.tile_prefix, prm.batch, range_lo, range_hi);
+      int req, lo, hi, seg = 0, g = 0;
+      bool whole;
+      auto issue_pv = [&](int gg, bool first_in_seg, int seg_idx) {
+        const int vs = gg % kNV, pb = gg & 1;
+        mbar_wait(&sm.v_full[vs], (gg / kNV) & 1);
+        mbar_wait(&sm.p_full[pb], (gg >> 1) & 1);
+        if (first_in_seg && seg_idx > 0) mbar_wait(&sm.o_free, (seg_idx - 1) & 1);
+        tc_fence_after();
+        const uint32_t p_base = smem_u32(sm.p[pb]);
+        const uint32_t v_base = smem_u32(sm.v[vs]);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t a = sdesc_sw128(p_base + kk * 32, 0, 1024);
+          const uint64_t b = sdesc_sw128(v_base + kk * 2048, kChunkBytes, 1024);
+          mma_bf16(tmem + kColO, a, b, idesc_pv, (first_in_seg && kk == 0) ? 0u : 1u);
+        }
+        mma_commit(&sm.v_empty[vs]);
+        mma_commit(&sm.p_empty[pb]);
+      };
+      while (walk.next(req, lo, hi, whole)) {
+        const int n = hi - lo;
+        mbar_wait(&sm.q_full, seg & 1);
+        for (int j = 0; j < n; ++j) {
+          const int gg = g + j;
+          const int ks = gg % kNK, sb = gg & 1;
+          mbar_wait(&sm.k_full[ks], (gg / kNK) & 1);
+          if (gg >= 2) mbar_wait(&sm.s_empty[sb], ((gg >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_base = smem_u32(sm.k[ks]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t a = sdesc_sw128(q_base + c * kChunkBytes + kk * 32, 0, 1024);
+              const uint64_t b = sdesc_sw128(k_base + c * kChunkBytes + kk * 32, 0, 1024);
+              mma_bf16(tmem + kColS + sb * 64, a, b, idesc_qk, (c | kk) ? 1u : 0u);
+            }
+          mma_commit(&sm.s_full[sb]);
+          mma_commit(&sm.k_empty[ks]);
+          if (j == n - 1) mma_commit(&sm.q_empty);
+          if (j >= 1) issue_pv(gg - 1, j == 1, seg);
+        }
+        issue_pv(g + n - 1, n == 1, seg);
+        g += n;
+        ++seg;
+      }
+    }
+  } else {
+    // ------------------------------- softmax / correction / epilogue (w2-5)
+    const int sub = warp & 3;                 // TMEM sub-partition of this warp
+    const bool active = lane < 16;            // M=64: lanes 0-15 hold rows
+    const int head = sub * 16 + (lane & 15);
+    const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
+    const uint32_t p_row_off = (uint32_t)head * 128;  // K-major SW128: 128B per head row
+    SegmentWalker walk(prm.tile_prefix, prm.batch, range_lo, range_hi);
+    int req, lo, hi, seg = 0, g = 0;
+    bool whole;
+    while (walk.next(req, lo, hi, whole)) {
+      const int n = hi - lo;
+      const int seq_len = __ldg(prm.seq_lens + req);
+      float m_used = -INFINITY, l_sum = 0.0f;
+      for (int j = 0; j < n; ++j, ++g) {
+        const int sb = g & 1, pb = g & 1;
+        mbar_wait(&sm.s_full[sb], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[64];
+        tmem_ld32(t_row + kColS + sb * 64, sr);
+        tmem_ld32(t_row + kColS + sb * 64 + 32, sr + 32);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.s_empty[sb]);
+
+        const int tok0 = (lo + j) * kPage;
+        const int nvalid = min(kPage, seq_len - tok0);
+        float s[64];
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          s[i] = (i < nvalid) ? __uint_as_float(sr[i]) * prm.scale_log2 : -INFINITY;
+          tmax = fmaxf(tmax, s[i]);
+        }
+        const bool need = tmax > m_used + kRescaleThresh;
+        float alpha = 1.0f;
+        if (need) {
+          alpha = fast_exp2(m_used - tmax);  // m_used=-inf -> 0
+          m_used = tmax;
+        }
+        l_sum *= alpha;
+        uint32_t pk[32];
+        float psum = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float p0 = fast_exp2(s[2 * i] - m_used);
+          const float p1 = fast_exp2(s[2 * i + 1] - m_used);
+          psum += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        l_sum += psum;
+
+        // P slot (and, for a rescale, the O accumulator) must be quiescent
+        if (g >= 2) mbar_wait(&sm.p_empty[pb], ((g >> 1) & 1) ^ 1);
+        const bool warp_rescale = __any_sync(0xffffffff, active && need && j > 0);
+        if (warp_rescale) {
+          const int gp = g - 1;  // PV(g-1) must have landed in O
+          mbar_wait(&sm.p_empty[gp & 1], (gp >> 1) & 1);
+          tc_fence_after();
+          const float a = (active && need) ? alpha : 1.0f;
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t o[32];
+            tmem_ld32(t_row + kColO + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+            tmem_st32(t_row + kColO + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+        // Last page of a request: zero V rows past seq_len so P=0 x garbage stays 0.
+        if (nvalid < kPage) {
+          const int vs = g % kNV;
+          mbar_wait(&sm.v_full[vs], (g / kNV) & 1);
+          const int tid = (warp - 2) * 32 + lane;  // 0..127
+          uint8_t* vt = sm.v[vs];
+          for (int idx = tid; idx < (kPage - nvalid) * 4 * 8; idx += 128) {
+            const int row = nvalid + idx / 32, chunk = (idx / 8) & 3, q16 = idx & 7;
+            *reinterpret_cast<uint4*>(vt + chunk * kChunkBytes + row * 128 + q16 * 16) = make_uint4(0, 0, 0, 0);
+          }
+        }
+        if (active) {
+          const uint32_t pbase = smem_u32(sm.p[pb]) + p_row_off;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t addr = pbase + ((uint32_t)(c ^ (head & 7)) << 4);
+            st_shared_v4(addr, pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.p_full[pb]);
+      }
+      // ---------------- epilogue of this segment: O / l -> global
+      const int gl = g - 1;
+      mbar_wait(&sm.p_empty[gl & 1], (gl >> 1) & 1);
+      tc_fence_after();
+      const float inv_l = 1.0f / l_sum;
+      const int slot = req + cta;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t o[32];
+        tmem_ld32(t_row + kColO + c * 32, o);
+        tmem_wait_ld();
+        if (active) {
+          if (whole) {
+            uint4* dst = reinterpret_cast<uint4*>(prm.out + ((size_t)req * kHeads + head) * kDim + c * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint4 v;
+              v.x = pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv_l, __uint_as_float(o[8 * q4 + 1]) * inv_l);
+              v.y = pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv_l, __uint_as_float(o[8 * q4 + 3]) * inv_l);
+              v.z = pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv_l, __uint_as_float(o[8 * q4 + 5]) * inv_l);
+              v.w = pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv_l, __uint_as_float(o[8 * q4 + 7]) * inv_l);
+              dst[q4] = v;
+            }
+          } else {
+            float4* dst = reinterpret_cast<float4*>(prm.part_o + ((size_t)slot * kHeads + head) * kDim + c * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4)
+              dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv_l, __uint_as_float(o[4 * q4 + 1]) * inv_l,
+                                    __uint_as_float(o[4 * q4 + 2]) * inv_l, __uint_as_float(o[4 * q4 + 3]) * inv_l);
+          }
+        }
+      }
+      if (active) {
+        const float lse2 = m_used + __log2f(l_sum);
+        if (whole) {
+          if (prm.lse) prm.lse[(size_t)req * kHeads + head] = lse2 * 0.69314718055994531f;
+        } else {
+          prm.part_lse[(size_t)slot * kHeads + head] = lse2;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.o_free);
+      ++seg;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+// K3: merge split partials of requests that spanned >1 CTA; zero-fill empty
+// requests.  grid (B, 8): each CTA handles 8 heads of one request, 32 threads
+// per head, 8 dims per thread.
+__global__ void __launch_bounds__(256)
+mfa_combine_kernel(const Params prm, int G) {
+  const int req = blockIdx.x;
+  const int T = __ldg(prm.tile_prefix + prm.batch);
+  const int p0 = __ldg(prm.tile_prefix + req), p1 = __ldg(prm.tile_prefix + req + 1);
+  const int head = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int d0 = (threadIdx.x & 31) * 8;
+  __nv_bfloat16* dst = prm.out + ((size_t)req * kHeads + head) * kDim + d0;
+  if (p1 <= p0) {  // empty request
+    *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    if (prm.lse && (threadIdx.x & 31) == 0) prm.lse[(size_t)req * kHeads + head] = -INFINITY;
+    return;
+  }
+  // CTAs whose ranges intersect [p0, p1)
+  int c_lo = (int)(((long long)p0 * G) / T);
+  while (c_lo > 0 && (((long long)c_lo * T) / G) > p0) --c_lo;
+  while ((((long long)(c_lo + 1) * T) / G) <= p0) ++c_lo;
+  int c_hi = (int)(((long long)(p1 - 1) * G) / T);
+  while (c_hi > 0 && (((long long)c_hi * T) / G) > p1 - 1) --c_hi;
+  while ((((long long)(c_hi + 1) * T) / G) <= p1 - 1) ++c_hi;
+  if (c_lo == c_hi) return;  // written directly by the main kernel
+  float m = -INFINITY;
+  for (int c = c_lo; c <= c_hi; ++c) m = fmaxf(m, prm.part_lse[(size_t)(req + c) * kHeads + head]);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float wsum = 0.0f;
+  for (int c = c_lo; c <= c_hi; ++c) {
+    const size_t slot = (size_t)(req + c);
+    const float w = exp2f(prm.part_lse[slot * kHeads + head] - m);
+    wsum += w;
+    const float4* src = reinterpret_cast<const float4*>(prm.part_o + (slot * kHeads + head) * kDim + d0);
+    const float4 a = src[0], b = src[1];
+    acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
+    acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
+  }
+  const float inv = 1.0f / wsum;
+  uint4 v;
+  v.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+  v.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+  v.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+  v.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+  *reinterpret_cast<uint4*>(dst) = v;
+  if (prm.lse && (threadIdx.x & 31) == 0)
+    prm.lse[(size_t)req * kHeads + head] = (m + __log2f(wsum)) * 0.69314718055994531f;
+}
+
+}  // namespace mfa
+
+// ------------------------------------------------------------------ host side
+size_t mfa_decode_workspace_bytes(int batch, int num_sms) {
+  const size_t slots = (size_t)batch + num_sms;
+  size_t b = 0;
+  b += align_up((size_t)(batch + 1) * sizeof(int32_t), 256);                 // prefix
+  b += align_up(slots * mfa::kHeads * mfa::kDim * sizeof(float), 256);      // part_o
+  b += align_up(slots * mfa::kHeads * sizeof(float), 256);                  // part_lse
+  return b;
+}
+
+cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream) {
+  using namespace mfa;
+  const int G = ctx.num_sms;
+  uint8_t* ws = static_cast<uint8_t*>(a.workspace);
+  Params prm{};
+  prm.block_table = a.block_table;
+  prm.seq_lens = a.seq_lens;
+  prm.tile_prefix = reinterpret_cast<int32_t*>(ws);
+  ws += align_up((size_t)(a.batch + 1) * sizeof(int32_t), 256);
+  const size_t slots = (size_t)a.batch + G;
+  prm.part_o = reinterpret_cast<float*>(ws);
+  ws += align_up(slots * kHeads * kDim * sizeof(float), 256);
+  prm.part_lse = reinterpret_cast<float*>(ws);
+  prm.out = static_cast<__nv_bfloat16*>(a.out);
+  prm.lse = a.lse;
+  prm.batch = a.batch;
+  prm.max_pages = a.max_pages;
+  prm.scale_log2 = a.softmax_scale * 1.4426950408889634f;
+
+  CUtensorMap tq, tk, tv;
+  {
+    const uint64_t dims[2] = {(uint64_t)kDim, (uint64_t)a.batch * kHeads};
+    const uint64_t strides[1] = {kDim * 2};
+    const uint32_t box[2] = {64, 64};
+    if (!encode_tma(ctx, &tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.q), dims, strides, box,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)kDim, (uint64_t)kPage, (uint64_t)a.num_pages};
+    const uint64_t strides[2] = {kDim * 2, (uint64_t)kPage * kDim * 2};
+    const uint32_t box[3] = {64, 64, 1};
+    if (!encode_tma(ctx, &tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.k_cache), dims, strides,
+                    box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    if (!encode_tma(ctx, &tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.v_cache), dims, strides,
+                    box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  }
+  plan_kernel<<<1, 1024, 0, stream>>>(a.seq_lens, a.batch, const_cast<int32_t*>(prm.tile_prefix));
+  const size_t smem = sizeof(Smem) + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(mfa_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  mfa_decode_kernel<<<G, kThreads, smem, stream>>>(tq, tk, tv, prm);
+  mfa_combine_kernel<<<dim3(a.batch, kHeads / 8), 256, 0, stream>>>(prm, G);
+  return cudaGetLastError();
+}
+
+}  // namespace afdk

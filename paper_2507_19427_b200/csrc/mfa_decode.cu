@@ -456,11 +456,17 @@ mfa_combine_kernel(const Params prm, int G) {
   while (c_hi > 0 && (((long long)c_hi * T) / G) > p1 - 1) --c_hi;
   while ((((long long)(c_hi + 1) * T) / G) <= p1 - 1) ++c_hi;
   if (c_lo == c_hi) return;  // written directly by the main kernel
+  // CTAs strictly inside (c_lo, c_hi) may own empty ranges when T < G: skip them
+  auto owns_pages = [&](int c) {
+    return (((long long)(c + 1) * T) / G) > (((long long)c * T) / G);
+  };
   float m = -INFINITY;
-  for (int c = c_lo; c <= c_hi; ++c) m = fmaxf(m, prm.part_lse[(size_t)(req + c) * kHeads + head]);
+  for (int c = c_lo; c <= c_hi; ++c)
+    if (owns_pages(c)) m = fmaxf(m, prm.part_lse[(size_t)(req + c) * kHeads + head]);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   float wsum = 0.0f;
   for (int c = c_lo; c <= c_hi; ++c) {
+    if (!owns_pages(c)) continue;
     const size_t slot = (size_t)(req + c);
     const float w = exp2f(prm.part_lse[slot * kHeads + head] - m);
     wsum += w;

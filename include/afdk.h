@@ -91,6 +91,44 @@ typedef struct afdk_mfa_decode_args {
 afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args* a,
                                       afdk_stream stream);
 
+/* ------------------------------------------------------------ K1/K4 GEMM
+ * y[m, n] = x[m, k] . w[n, k]^T, bf16 inputs, fp32 accumulate, decode-shaped
+ * (1 <= m <= 256, k % 64 == 0).  out is bf16 (out_fp32 = 0) or fp32.      */
+afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, int m, int n, int k,
+                        int out_fp32, afdk_stream stream);
+
+/* --------------------------------------------- attention-side decode layer
+ * input RMSNorm -> [q_down|k|v] -> q RMSNorm -> q_up -> NeoX RoPE(q, k)
+ * -> paged KV append (position seq_lens[b]-1) -> MFA decode core -> o_proj
+ * + residual -> post-attention RMSNorm.  Step-3 dims: hidden 7168, q_lora
+ * 2048, 64 heads x 256 (builtin_catalog.cpp:241-247).   */
+typedef struct afdk_mfa_weights {
+  int hidden, q_lora, n_heads, head_dim;
+  const void* in_norm;   /* bf16 [hidden]                                */
+  const void* w_qkv;     /* bf16 [q_lora + 2*head_dim, hidden] q|k|v rows */
+  const void* q_norm;    /* bf16 [q_lora]                                */
+  const void* w_q_up;    /* bf16 [n_heads*head_dim, q_lora]              */
+  const void* w_o;       /* bf16 [hidden, n_heads*head_dim]              */
+  const void* post_norm; /* bf16 [hidden]                                */
+  float rms_eps, rope_theta, softmax_scale;
+} afdk_mfa_weights;
+
+typedef struct afdk_mfa_layer_args {
+  int batch;
+  const void* x;   /* bf16 [batch, hidden] layer input (residual stream)  */
+  void* k_cache;   /* bf16 [num_pages, page_size, head_dim], appended     */
+  void* v_cache;
+  int num_pages, page_size;
+  const int32_t* block_table; /* [batch, max_pages]                       */
+  int max_pages;
+  const int32_t* seq_lens;    /* [batch] lengths INCLUDING the new token  */
+  void* h_res;     /* bf16 [batch, hidden] x + attention output           */
+  void* h_norm;    /* bf16 [batch, hidden] RMSNorm(h_res): FFN input      */
+} afdk_mfa_layer_args;
+
+afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
+                           afdk_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,23 @@ class MfaDecodeArgs(Structure):
     ]
 
 
+class MfaWeights(Structure):
+    _fields_ = [
+        ("hidden", c_int), ("q_lora", c_int), ("n_heads", c_int), ("head_dim", c_int),
+        ("in_norm", c_void_p), ("w_qkv", c_void_p), ("q_norm", c_void_p), ("w_q_up", c_void_p),
+        ("w_o", c_void_p), ("post_norm", c_void_p),
+        ("rms_eps", c_float), ("rope_theta", c_float), ("softmax_scale", c_float),
+    ]
+
+
+class MfaLayerArgs(Structure):
+    _fields_ = [
+        ("batch", c_int), ("x", c_void_p), ("k_cache", c_void_p), ("v_cache", c_void_p),
+        ("num_pages", c_int), ("page_size", c_int), ("block_table", c_void_p), ("max_pages", c_int),
+        ("seq_lens", c_void_p), ("h_res", c_void_p), ("h_norm", c_void_p),
+    ]
+
+
 # exported symbol -> (restype, argtypes); the CPU test checks every symbol of
 # include/afdk.h is present in the built library
 SIGNATURES = {
@@ -50,6 +67,8 @@ SIGNATURES = {
     "afdk_destroy": (None, [c_void_p]),
     "afdk_num_sms": (c_int, [c_void_p]),
     "afdk_mfa_decode_attention": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_void_p]),
+    "afdk_linear": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]),
+    "afdk_mfa_layer": (c_int, [c_void_p, POINTER(MfaWeights), POINTER(MfaLayerArgs), c_void_p]),
 }
 
 _lib = None
@@ -112,3 +131,27 @@ class Context:
                           k_cache.shape[0], ptr(block_table), block_table.shape[1], ptr(seq_lens),
                           softmax_scale, ptr(out), ptr(lse))
         check(self.lib.afdk_mfa_decode_attention(self.handle, ctypes.byref(a), c_void_p(stream)))
+
+    # ------------------------------------------------------------ K1/K4
+    def linear(self, x, w, out, stream: int = 0) -> None:
+        import torch
+
+        m, k = x.shape
+        n = w.shape[0]
+        check(self.lib.afdk_linear(self.handle, ptr(x), ptr(w), ptr(out), m, n, k,
+                                   int(out.dtype == torch.float32), c_void_p(stream)))
+
+    def mfa_layer(self, w: dict, x, k_cache, v_cache, block_table, seq_lens, h_res, h_norm,
+                  rms_eps=1e-5, rope_theta=5e5, softmax_scale=None, stream: int = 0) -> None:
+        """Attention-side decode layer; `w` holds bf16 device tensors
+        in_norm, qkv, q_norm, q_up, o, post_norm (shapes as in include/afdk.h)."""
+        hidden = x.shape[1]
+        q_lora = w["q_norm"].shape[0]
+        head_dim = k_cache.shape[2]
+        n_heads = w["q_up"].shape[0] // head_dim
+        scale = head_dim ** -0.5 if softmax_scale is None else softmax_scale
+        mw = MfaWeights(hidden, q_lora, n_heads, head_dim, ptr(w["in_norm"]), ptr(w["qkv"]), ptr(w["q_norm"]),
+                        ptr(w["q_up"]), ptr(w["o"]), ptr(w["post_norm"]), rms_eps, rope_theta, scale)
+        a = MfaLayerArgs(x.shape[0], ptr(x), ptr(k_cache), ptr(v_cache), k_cache.shape[0], k_cache.shape[1],
+                         ptr(block_table), block_table.shape[1], ptr(seq_lens), ptr(h_res), ptr(h_norm))
+        check(self.lib.afdk_mfa_layer(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))

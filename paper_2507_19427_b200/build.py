@@ -19,6 +19,8 @@ OUT = os.path.join(HERE, "libafdk.so")
 CU_SOURCES = [
     "afdk_api.cu",
     "mfa_decode.cu",
+    "linear.cu",
+    "mfa_layer.cu",
 ]
 CXX_SOURCES: list[str] = []
 

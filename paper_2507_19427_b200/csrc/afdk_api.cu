@@ -116,6 +116,7 @@ afdk_status afdk_create(afdk_ctx** out, const afdk_cfg* cfg) {
 void afdk_destroy(afdk_ctx* ctx) {
   if (!ctx) return;
   if (ctx->c.ws) cudaFree(ctx->c.ws);
+  if (ctx->c.rope_freq) cudaFree(ctx->c.rope_freq);
   delete ctx;
 }
 
@@ -146,6 +147,53 @@ afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args*
                         a->max_pages, a->seq_lens, a->softmax_scale, a->out, a->lse, ws};
   const cudaError_t e = afdk::mfa_decode_launch(c, m, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail("mfa_decode launch", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, int m, int n, int k,
+                        int out_fp32, afdk_stream stream) {
+  if (!ctx || !x || !w || !out) { set_error("afdk_linear: NULL argument"); return AFDK_ERR_INVALID; }
+  if (m < 1 || m > 256) { set_error("afdk_linear: m must be in [1, 256]"); return AFDK_ERR_INVALID; }
+  if (n < 1 || k < 64 || k % 64) { set_error("afdk_linear: k must be a positive multiple of 64"); return AFDK_ERR_INVALID; }
+  afdk::Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  const afdk::LinearPlan p = afdk::make_linear_plan(m, n, k);
+  float* part = static_cast<float*>(afdk::workspace(c, afdk::linear_workspace_bytes(p, c.num_sms)));
+  if (!part) { set_error("afdk_linear: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  auto st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = afdk::linear_bf16_launch(c, p, x, w, part, st);
+  if (e == cudaSuccess) e = afdk::linear_store_launch(c, p, part, out, out_fp32 != 0, st);
+  if (e != cudaSuccess) return cuda_fail("afdk_linear", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
+                           afdk_stream stream) {
+  if (!ctx || !w || !a) { set_error("afdk_mfa_layer: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }
+  if (w->n_heads != 64 || w->head_dim != 256 || a->page_size != 64) {
+    set_error("afdk_mfa_layer: n_heads/head_dim/page_size must be 64/256/64");
+    return AFDK_ERR_INVALID;
+  }
+  if (w->hidden % 64 || w->q_lora % 64 || w->q_lora < 64) {
+    set_error("afdk_mfa_layer: hidden and q_lora must be multiples of 64");
+    return AFDK_ERR_INVALID;
+  }
+  if (a->batch < 1 || a->batch > 256) { set_error("afdk_mfa_layer: batch must be in [1, 256]"); return AFDK_ERR_INVALID; }
+  if (!a->x || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->h_res || !a->h_norm ||
+      !w->in_norm || !w->w_qkv || !w->q_norm || !w->w_q_up || !w->w_o || !w->post_norm) {
+    set_error("afdk_mfa_layer: NULL tensor pointer");
+    return AFDK_ERR_INVALID;
+  }
+  afdk::Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  afdk::MfaLayerArgs m{a->batch, w->hidden, w->q_lora, w->n_heads, w->head_dim, a->page_size,
+                       w->in_norm, w->w_qkv, w->q_norm, w->w_q_up, w->w_o, w->post_norm,
+                       w->rms_eps, w->rope_theta, w->softmax_scale, a->x, a->k_cache, a->v_cache,
+                       a->num_pages, a->block_table, a->max_pages, a->seq_lens, a->h_res, a->h_norm};
+  void* ws = afdk::workspace(c, afdk::mfa_layer_workspace_bytes(m, c.num_sms));
+  if (!ws) { set_error("afdk_mfa_layer: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  const cudaError_t e = afdk::mfa_layer_launch(c, m, ws, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("afdk_mfa_layer", e);
   return AFDK_OK;
 }
 

@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <string>
 
+#include "linear.cuh"
+
 namespace afdk {
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -23,6 +25,9 @@ struct Ctx {
   EncodeTiledFn encode = nullptr;
   void* ws = nullptr;  // grow-only device workspace
   size_t ws_bytes = 0;
+  double* rope_freq = nullptr;  // NeoX inv_freq table (host-computed in double)
+  int rope_dim = 0;
+  float rope_theta = 0.0f;
 };
 
 // Returns a device workspace of at least `bytes` (grows; not graph-capturable
@@ -52,5 +57,30 @@ struct MfaDecodeArgs {
 };
 size_t mfa_decode_workspace_bytes(int batch, int num_sms);
 cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream);
+
+LinearPlan make_linear_plan(int m_tok, int n_out, int k);
+size_t linear_workspace_bytes(const LinearPlan& p, int num_sms);
+cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
+                               cudaStream_t stream);
+cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,
+                                cudaStream_t stream);
+
+struct MfaLayerArgs {
+  int batch, hidden, q_lora, n_heads, head_dim, page_size;
+  const void *w_in_norm, *w_qkv, *w_q_norm, *w_q_up, *w_o, *w_post_norm;
+  float rms_eps, rope_theta, softmax_scale;
+  const void* x;
+  void* k_cache;
+  void* v_cache;
+  int num_pages;
+  const int32_t* block_table;
+  int max_pages;
+  const int32_t* seq_lens;
+  void* h_res;
+  void* h_norm;
+};
+const double* rope_inv_freq(Ctx& ctx, int head_dim, float theta);
+size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms);
+cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws, cudaStream_t stream);
 
 }  // namespace afdk

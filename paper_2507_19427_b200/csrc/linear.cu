@@ -1,0 +1,231 @@
+// linear.cu — decode-shaped weight-streaming GEMM on sm_100a (K1/K4 projections).
+//
+// Y[m_tok, n_out] = X[m_tok, K] . W[n_out, K]^T with m_tok <= 256 decode tokens
+// and large bf16 weights (q_down|k|v 2560x7168, q_up 16384x2048, o 7168x16384;
+// builtin_catalog.cpp:243-247).  At decode batch sizes the op is bound by
+// streaming W from HBM once, so the kernel is "swap-AB": the weight tile is
+// the MMA's M=128 side and the tokens are N (<=256), accumulating in TMEM:
+//
+//   D[128 feats x N tok] += W[128 x 64k] . X[N x 64k]^T   tcgen05.mma kind::f16
+//
+// Work is split stream-K style: the (tile, k-block) unit space is cut into one
+// contiguous range per SM so every SM streams the same weight bytes whatever
+// the layer shape; each (tile, k-range) segment writes a deterministic fp32
+// partial to slot (tile + cta) that the row epilogues (mfa_layer.cu) sum in
+// fixed order and fuse with RMSNorm / RoPE / KV-append / residual.
+//
+// Roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2-5 epilogue.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "afdk_internal.h"
+#include "linear.cuh"
+#include "sm100.cuh"
+
+namespace afdk {
+namespace lin {
+
+using namespace sm100;
+
+constexpr int kThreads = 192;
+constexpr int kABytes = kBM * 128;  // 16 KB weight panel per k-block
+
+struct KParams {
+  LinearPlan plan;
+  float* part;
+  int stage_bytes, stages;
+};
+
+__device__ __forceinline__ void unit_range(int c, int G, int U, int& lo, int& hi) {
+  lo = (int)(((long long)c * U) / G);
+  hi = (int)(((long long)(c + 1) * U) / G);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                   const KParams kp) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const LinearPlan& P = kp.plan;
+  const int S = kp.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kp.stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* acc_full = empty + S;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = warp_id(), lane = threadIdx.x & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int U = P.tiles * P.kblocks;
+  int u_lo, u_hi;
+  unit_range(cta, G, U, u_lo, u_hi);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_w);
+    tma_prefetch_desc(&tm_x);
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_mma = P.n_mma;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      const uint32_t bytes = kABytes + n_mma * 128;
+      for (int u = u_lo, i = 0; u < u_hi; ++u, ++i) {
+        const int s = i % S, n = i / S;
+        if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
+        const int tile = u / P.kblocks, kb = u % P.kblocks;
+        uint8_t* st = smem + s * kp.stage_bytes;
+        mbar_expect_tx(&full[s], bytes);
+        tma_load_2d(st, &tm_w, &full[s], kb * 64, tile * kBM, pol_w);
+        tma_load_2d(st + kABytes, &tm_x, &full[s], kb * 64, 0, pol_x);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(128, (uint32_t)n_mma, false, false);
+      int seg = 0;
+      for (int u = u_lo, i = 0; u < u_hi; ++seg) {
+        const int tile = u / P.kblocks;
+        const int seg_end = min(u_hi, (tile + 1) * P.kblocks);
+        const int ab = seg & 1, na = seg >> 1;
+        if (seg >= 2) mbar_wait(&acc_empty[ab], (na & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + ab * 256;
+        for (bool first = true; u < seg_end; ++u, ++i, first = false) {
+          const int s = i % S, n = i / S;
+          mbar_wait(&full[s], n & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem + s * kp.stage_bytes);
+          const uint32_t b_base = a_base + kABytes;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t a = sdesc_sw128(a_base + kk * 32, 0, 1024);
+            const uint64_t b = sdesc_sw128(b_base + kk * 32, 0, 1024);
+            mma_bf16(d, a, b, idesc, (first && kk == 0) ? 0u : 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full[ab]);
+      }
+    }
+  } else {
+    // epilogue: TMEM lane = weight row = output feature, column = token
+    const int sub = warp & 3;
+    const int feat = sub * 32 + lane;
+    int seg = 0;
+    for (int u = u_lo; u < u_hi; ++seg) {
+      const int tile = u / P.kblocks;
+      const int seg_end = min(u_hi, (tile + 1) * P.kblocks);
+      u = seg_end;
+      const int ab = seg & 1, na = seg >> 1;
+      mbar_wait(&acc_full[ab], na & 1);
+      tc_fence_after();
+      float* dst = kp.part + ((size_t)(tile + cta) * P.m_tok) * kBM + feat;
+      const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16) + ab * 256;
+      for (int c = 0; c < n_mma; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(t_row + c, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c + j < P.m_tok) dst[(size_t)(c + j) * kBM] = __uint_as_float(v[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// Plain bf16/fp32 output: out[row, f] = sum of partials (fixed order).
+__global__ void linear_store_kernel(const LinearPlan P, const float* __restrict__ part, int G,
+                                    void* __restrict__ out, int out_fp32) {
+  const int row = blockIdx.x;
+  for (int f = threadIdx.x; f < P.n_out; f += blockDim.x) {
+    const float v = linear_partial_sum(P, part, G, row, f);
+    if (out_fp32) static_cast<float*>(out)[(size_t)row * P.n_out + f] = v;
+    else static_cast<__nv_bfloat16*>(out)[(size_t)row * P.n_out + f] = __float2bfloat16_rn(v);
+  }
+}
+
+}  // namespace lin
+
+LinearPlan make_linear_plan(int m_tok, int n_out, int k) {
+  LinearPlan p{};
+  p.m_tok = m_tok;
+  p.n_mma = ((m_tok + 15) / 16) * 16;
+  if (p.n_mma < 16) p.n_mma = 16;
+  p.n_out = n_out;
+  p.k = k;
+  p.tiles = (n_out + lin::kBM - 1) / lin::kBM;
+  p.kblocks = k / 64;
+  return p;
+}
+
+size_t linear_workspace_bytes(const LinearPlan& p, int num_sms) {
+  return align_up((size_t)(p.tiles + num_sms) * p.m_tok * lin::kBM * sizeof(float), 256);
+}
+
+cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
+                               cudaStream_t stream) {
+  using namespace lin;
+  CUtensorMap tw, tx;
+  {
+    const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.n_out};
+    const uint64_t strides[1] = {(uint64_t)p.k * 2};
+    const uint32_t box[2] = {64, kBM};
+    if (!encode_tma(ctx, &tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.m_tok};
+    const uint64_t strides[1] = {(uint64_t)p.k * 2};
+    const uint32_t box[2] = {64, (uint32_t)p.n_mma};
+    if (!encode_tma(ctx, &tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  }
+  KParams kp{};
+  kp.plan = p;
+  kp.part = part;
+  kp.stage_bytes = kABytes + p.n_mma * 128;
+  const int budget = 200 * 1024;
+  kp.stages = budget / kp.stage_bytes;
+  if (kp.stages > 8) kp.stages = 8;
+  const size_t smem = (size_t)kp.stages * kp.stage_bytes + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(linear_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  linear_bf16_kernel<<<ctx.num_sms, kThreads, smem, stream>>>(tw, tx, kp);
+  return cudaGetLastError();
+}
+
+cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,
+                                cudaStream_t stream) {
+  lin::linear_store_kernel<<<p.m_tok, 256, 0, stream>>>(p, part, ctx.num_sms, out, out_fp32 ? 1 : 0);
+  return cudaGetLastError();
+}
+
+}  // namespace afdk

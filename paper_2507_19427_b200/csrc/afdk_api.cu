@@ -109,6 +109,11 @@ afdk_status afdk_create(afdk_ctx** out, const afdk_cfg* cfg) {
     return AFDK_ERR_CUDA;
   }
   ctx->c.encode = reinterpret_cast<afdk::EncodeTiledFn>(fn);
+  if ((e = cudaMalloc(&ctx->c.counters, afdk::kCounterSlots * sizeof(int))) != cudaSuccess ||
+      (e = cudaMemset(ctx->c.counters, 0, afdk::kCounterSlots * sizeof(int))) != cudaSuccess) {
+    delete ctx;
+    return cuda_fail("afdk_create: counters", e);
+  }
   *out = ctx;
   return AFDK_OK;
 }
@@ -117,6 +122,7 @@ void afdk_destroy(afdk_ctx* ctx) {
   if (!ctx) return;
   if (ctx->c.ws) cudaFree(ctx->c.ws);
   if (ctx->c.rope_freq) cudaFree(ctx->c.rope_freq);
+  if (ctx->c.counters) cudaFree(ctx->c.counters);
   delete ctx;
 }
 

@@ -11,6 +11,8 @@
 
 namespace afdk {
 
+constexpr int kCounterSlots = 8192;  // [0,4096) GEMM tiles, [4096,8192) attention requests
+
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -25,6 +27,7 @@ struct Ctx {
   EncodeTiledFn encode = nullptr;
   void* ws = nullptr;  // grow-only device workspace
   size_t ws_bytes = 0;
+  int* counters = nullptr;      // zeroed arrival counters (self-resetting kernels)
   double* rope_freq = nullptr;  // NeoX inv_freq table (host-computed in double)
   int rope_dim = 0;
   float rope_theta = 0.0f;
@@ -60,6 +63,9 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
 
 LinearPlan make_linear_plan(int m_tok, int n_out, int k);
 size_t linear_workspace_bytes(const LinearPlan& p, int num_sms);
+// partials of y = x . w^T into `part` (linear_workspace_bytes); reduce with a
+// SlotTable epilogue or linear_store_launch.  linear_grid = CTAs the GEMM uses.
+int linear_grid(const Ctx& ctx, const LinearPlan& p);
 cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
                                cudaStream_t stream);
 cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,

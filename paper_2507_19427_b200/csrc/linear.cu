@@ -10,9 +10,10 @@
 //
 // Work is split stream-K style: the (tile, k-block) unit space is cut into one
 // contiguous range per SM so every SM streams the same weight bytes whatever
-// the layer shape; each (tile, k-range) segment writes a deterministic fp32
-// partial to slot (tile + cta) that the row epilogues (mfa_layer.cu) sum in
-// fixed order and fuse with RMSNorm / RoPE / KV-append / residual.
+// the layer shape.  Each (tile, k-range) segment writes an fp32 partial to
+// slot (tile + cta); the row epilogues (mfa_layer.cu, linear_store_kernel) sum
+// a tile's partials in CTA order — deterministic, no float atomics — fused
+// with the row op that follows (RMSNorm, RoPE, KV append, residual).
 //
 // Roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2-5 epilogue.
 #include <cuda.h>
@@ -35,7 +36,7 @@ constexpr int kABytes = kBM * 128;  // 16 KB weight panel per k-block
 
 struct KParams {
   LinearPlan plan;
-  float* part;
+  float* part;  // [(tiles + G)][m_tok][128] fp32 segment partials
   int stage_bytes, stages;
 };
 
@@ -121,7 +122,8 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       }
     }
   } else {
-    // epilogue: TMEM lane = weight row = output feature, column = token
+    // epilogue: TMEM lane = weight row = output feature, column = token;
+    // each (tile, k-range) segment writes its fp32 partial to slot tile + cta.
     const int sub = warp & 3;
     const int feat = sub * 32 + lane;
     int seg = 0;
@@ -155,18 +157,36 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
   }
 }
 
-// Plain bf16/fp32 output: out[row, f] = sum of partials (fixed order).
-__global__ void linear_store_kernel(const LinearPlan P, const float* __restrict__ part, int G,
-                                    void* __restrict__ out, int out_fp32) {
+// Plain output: out[row, f] = sum of partials (fixed order), bf16 or fp32.
+__global__ void __launch_bounds__(256) linear_store_kernel(const LinearPlan P, const float* __restrict__ part,
+                                                           int G, void* __restrict__ out, int out_fp32) {
+  __shared__ SlotTable tab;
+  build_slot_table(P, G, tab);
   const int row = blockIdx.x;
-  for (int f = threadIdx.x; f < P.n_out; f += blockDim.x) {
-    const float v = linear_partial_sum(P, part, G, row, f);
+  for (int f = blockIdx.y * 256 + threadIdx.x; f < P.n_out; f += 256 * gridDim.y) {
+    const float v = tab.sum(P, part, row, f);
     if (out_fp32) static_cast<float*>(out)[(size_t)row * P.n_out + f] = v;
     else static_cast<__nv_bfloat16*>(out)[(size_t)row * P.n_out + f] = __float2bfloat16_rn(v);
   }
 }
 
 }  // namespace lin
+
+int linear_grid(const Ctx& ctx, const LinearPlan& p) {
+  // no CTA without units, and no tile shared by more than kMaxSegs CTAs
+  long long g = ctx.num_sms;
+  const long long U = (long long)p.tiles * p.kblocks;
+  if (g > U) g = U;
+  if (g > (long long)(lin::kMaxSegs - 1) * p.tiles) g = (long long)(lin::kMaxSegs - 1) * p.tiles;
+  return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,
+                                cudaStream_t stream) {
+  lin::linear_store_kernel<<<dim3(p.m_tok, (p.n_out + 255) / 256 > 8 ? 8 : (p.n_out + 255) / 256), 256, 0, stream>>>(
+      p, part, linear_grid(ctx, p), out, out_fp32 ? 1 : 0);
+  return cudaGetLastError();
+}
 
 LinearPlan make_linear_plan(int m_tok, int n_out, int k) {
   LinearPlan p{};
@@ -212,20 +232,15 @@ cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, con
   kp.stages = budget / kp.stage_bytes;
   if (kp.stages > 8) kp.stages = 8;
   const size_t smem = (size_t)kp.stages * kp.stage_bytes + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(linear_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(linear_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr = smem;
   }
-  linear_bf16_kernel<<<ctx.num_sms, kThreads, smem, stream>>>(tw, tx, kp);
+  linear_bf16_kernel<<<linear_grid(ctx, p), kThreads, smem, stream>>>(tw, tx, kp);
   return cudaGetLastError();
 }
 
-cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,
-                                cudaStream_t stream) {
-  lin::linear_store_kernel<<<p.m_tok, 256, 0, stream>>>(p, part, ctx.num_sms, out, out_fp32 ? 1 : 0);
-  return cudaGetLastError();
-}
 
 }  // namespace afdk

@@ -18,25 +18,41 @@ struct LinearPlan {
 
 namespace lin {
 constexpr int kBM = 128;
+constexpr int kMaxSegs = 16;    // CTAs that may share one tile (linear_grid caps G)
+constexpr int kMaxTiles = 128;  // tiles a row epilogue may span (n_out <= 16384)
 
-// Sum, in CTA order, of the partials covering (row, feature f).  CTA c owns the
-// unit range [c*U/G, (c+1)*U/G) of U = tiles*kblocks units; the partial of the
-// (tile, c) segment lives in slot tile + c (layout [slot][m_tok][128]).
-__device__ __forceinline__ float linear_partial_sum(const LinearPlan& P, const float* __restrict__ part,
-                                                    int G, int row, int f) {
-  const int tile = f / kBM;
-  const long long U = (long long)P.tiles * P.kblocks;
-  const long long u0 = (long long)tile * P.kblocks, u1 = u0 + P.kblocks - 1;
-  int c = (int)((u0 * G) / U);
-  while (c > 0 && ((long long)c * U) / G > u0) --c;
-  while (((long long)(c + 1) * U) / G <= u0) ++c;
-  float acc = 0.0f;
-  for (;; ++c) {
-    const long long lo = ((long long)c * U) / G, hi = ((long long)(c + 1) * U) / G;
-    if (lo > u1) break;
-    if (hi > lo) acc += __ldg(part + ((size_t)(tile + c) * P.m_tok + row) * kBM + (f % kBM));
+// Which partial slots hold tile t: CTAs c_lo[t] .. c_lo[t]+n[t]-1 (the grid
+// never has empty CTAs), slot = t + c.  Built once per epilogue CTA in smem.
+struct SlotTable {
+  int c_lo[kMaxTiles];
+  int n[kMaxTiles];
+  __device__ __forceinline__ float sum(const LinearPlan& P, const float* __restrict__ part, int row,
+                                       int f) const {
+    const int t = f / kBM, c0 = c_lo[t], nn = n[t];
+    const float* base = part + ((size_t)(t + c0) * P.m_tok + row) * kBM + (f % kBM);
+    const size_t stride = (size_t)P.m_tok * kBM;
+    float acc = 0.0f;
+#pragma unroll 4
+    for (int k = 0; k < nn; ++k) acc += __ldcg(base + (size_t)k * stride);
+    return acc;
   }
-  return acc;
+};
+
+__device__ __forceinline__ void build_slot_table(const LinearPlan& P, int G, SlotTable& tab) {
+  const long long U = (long long)P.tiles * P.kblocks;
+  for (int t = threadIdx.x; t < P.tiles; t += blockDim.x) {
+    const long long u0 = (long long)t * P.kblocks, u1 = u0 + P.kblocks;  // [u0, u1)
+    const int c_lo = (int)((u0 * G) / U);   // CTA c owns [cU/G, (c+1)U/G): floor-based
+    int lo = c_lo;
+    while (lo > 0 && ((long long)lo * U) / G > u0) --lo;
+    while (((long long)(lo + 1) * U) / G <= u0) ++lo;
+    int hi = (int)(((u1 - 1) * G) / U);
+    while (hi > 0 && ((long long)hi * U) / G > u1 - 1) --hi;
+    while (((long long)(hi + 1) * U) / G <= u1 - 1) ++hi;
+    tab.c_lo[t] = lo;
+    tab.n[t] = hi - lo + 1;
+  }
+  __syncthreads();
 }
 }  // namespace lin
 

@@ -16,7 +16,8 @@
 // (request, page) space is cut into one contiguous range per CTA
 // (grid = #SMs, 1 CTA/SM).  A range that covers a whole request writes bf16
 // O directly; otherwise it writes a normalised fp32 partial + log2-LSE into
-// slot (request + cta), and mfa_combine (K3) merges the partials.
+// slot (request + cta), and mfa_combine (K3) merges the partials.  Each CTA
+// derives the page prefix of the batch itself (no planning launch).
 //
 // Warp roles (224 threads):  w0 = Q/K TMA producer, w1 = MMA issuer + TMEM
 // owner, w2..w5 = softmax / O-correction / epilogue (TMEM lanes 0-15 of each
@@ -62,10 +63,13 @@ struct __align__(1024) Smem {
   uint32_t tmem_base;
 };
 
+constexpr int kMaxBatch = 2048;  // prefix of pages per request lives in smem
+constexpr int kMaxSplit = 160;   // >= #SMs + 1: CTAs one request may span
+
 struct Params {
   const int32_t* block_table;  // [B, max_pages]
   const int32_t* seq_lens;     // [B]
-  const int32_t* tile_prefix;  // [B+1] pages per request, exclusive prefix (plan kernel)
+  int32_t* prefix_out;         // [B+1] pages-per-request prefix, written by CTA 0 for K3
   __nv_bfloat16* out;          // [B, 64, 256]
   float* lse;                  // [B, 64] natural log, optional
   float* part_o;               // [(B+G), 64, 256]
@@ -86,7 +90,7 @@ __device__ __forceinline__ int find_request(const int32_t* prefix, int B, int t)
   int lo = 0, hi = B - 1;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (__ldg(prefix + mid + 1) > t) hi = mid; else lo = mid + 1;
+    if (prefix[mid + 1] > t) hi = mid; else lo = mid + 1;
   }
   return lo;
 }
@@ -102,8 +106,8 @@ struct SegmentWalker {
   // returns false when the range is exhausted
   __device__ bool next(int& req, int& lo, int& hi, bool& whole) {
     if (pos >= end) return false;
-    while (__ldg(prefix + r + 1) <= pos) ++r;
-    const int p0 = __ldg(prefix + r), p1 = __ldg(prefix + r + 1);
+    while (prefix[r + 1] <= pos) ++r;
+    const int p0 = prefix[r], p1 = prefix[r + 1];
     const int seg_hi = p1 < end ? p1 : end;
     req = r;
     lo = pos - p0;
@@ -114,51 +118,50 @@ struct SegmentWalker {
   }
 };
 
-__global__ void plan_kernel(const int32_t* __restrict__ seq_lens, int B,
-                            int32_t* __restrict__ prefix) {
-  // single CTA, 1024 threads: exclusive scan of ceil(len/64) in chunks
-  __shared__ int warp_sums[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < B; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const int v = (i < B) ? (max(__ldg(seq_lens + i), 0) + kPage - 1) / kPage : 0;
-    int x = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffff, x, o);
-      if ((threadIdx.x & 31) >= o) x += y;
-    }
-    if ((threadIdx.x & 31) == 31) warp_sums[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      int w = (threadIdx.x < (blockDim.x >> 5)) ? warp_sums[threadIdx.x] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffff, w, o);
-        if (threadIdx.x >= o) w += y;
-      }
-      warp_sums[threadIdx.x] = w;
-    }
-    __syncthreads();
-    const int incl = x + ((threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0) + carry;
-    if (i < B) prefix[i + 1] = incl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = incl;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) prefix[0] = 0;
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
 mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
                   const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const Params prm) {
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  int32_t* prefix = reinterpret_cast<int32_t*>(&sm + 1);  // [B+1] after the Smem block
+  __shared__ int s_scan[kThreads];
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
-  const int T = __ldg(prm.tile_prefix + prm.batch);
+  {
+    // pages per request -> exclusive prefix in smem (every CTA; B <= kMaxBatch)
+    __shared__ int s_wsum[kThreads / 32];
+    __shared__ int s_carry;
+    const int nw = kThreads / 32;
+    if (threadIdx.x == 0) { s_carry = 0; prefix[0] = 0; }
+    for (int base = 0; base < prm.batch; base += kThreads) {
+      const int i = base + threadIdx.x;
+      const int v = (i < prm.batch) ? (max(__ldg(prm.seq_lens + i), 0) + kPage - 1) / kPage : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffff, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_wsum[warp] = x;
+      __syncthreads();
+      int off = s_carry;
+      for (int w = 0; w < warp; ++w) off += s_wsum[w];
+      if (i < prm.batch) prefix[i + 1] = off + x;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < nw; ++w) t += s_wsum[w];
+        s_carry += t;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (cta == 0)
+    for (int i = threadIdx.x; i <= prm.batch; i += kThreads) prm.prefix_out[i] = prefix[i];
+  const int T = prefix[prm.batch];
   int range_lo, range_hi;
   cta_range(cta, G, T, range_lo, range_hi);
 
@@ -190,7 +193,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
-      SegmentWalker walk(prm.tile_prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -213,7 +216,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     // ---------------------------------------------------- V TMA producer
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
-      SegmentWalker walk(prm.tile_prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
       int req, lo, hi, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -233,7 +236,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
       constexpr uint32_t idesc_qk = idesc_bf16(64, 64, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16(64, 256, false, true);
       const uint32_t q_base = smem_u32(sm.q);
-      SegmentWalker walk(prm.tile_prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       auto issue_pv = [&](int gg, bool first_in_seg, int seg_idx) {
@@ -288,7 +291,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int head = sub * 16 + (lane & 15);
     const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
     const uint32_t p_row_off = (uint32_t)head * 128;  // K-major SW128: 128B per head row
-    SegmentWalker walk(prm.tile_prefix, prm.batch, range_lo, range_hi);
+    SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
     int req, lo, hi, seg = 0, g = 0;
     bool whole;
     while (walk.next(req, lo, hi, whole)) {
@@ -432,58 +435,58 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   }
 }
 
-// K3: merge split partials of requests that spanned >1 CTA; zero-fill empty
-// requests.  grid (B, 8): each CTA handles 8 heads of one request, 32 threads
-// per head, 8 dims per thread.
-__global__ void __launch_bounds__(256)
-mfa_combine_kernel(const Params prm, int G) {
+// K3: merge the split partials of requests that spanned several CTAs (fixed
+// CTA order => deterministic), zero-fill empty requests.  grid (B, 16): 4
+// heads per CTA, 64 threads per head, 4 dims (one float4) per thread.
+__global__ void __launch_bounds__(256) mfa_combine_kernel(const Params prm, int G) {
+  __shared__ int s_slot[kMaxSplit];
+  __shared__ float s_w[4][kMaxSplit];
+  __shared__ int s_n;
   const int req = blockIdx.x;
-  const int T = __ldg(prm.tile_prefix + prm.batch);
-  const int p0 = __ldg(prm.tile_prefix + req), p1 = __ldg(prm.tile_prefix + req + 1);
-  const int head = blockIdx.y * 8 + (threadIdx.x >> 5);
-  const int d0 = (threadIdx.x & 31) * 8;
-  __nv_bfloat16* dst = prm.out + ((size_t)req * kHeads + head) * kDim + d0;
-  if (p1 <= p0) {  // empty request
-    *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-    if (prm.lse && (threadIdx.x & 31) == 0) prm.lse[(size_t)req * kHeads + head] = -INFINITY;
+  const int T = prm.prefix_out[prm.batch];
+  const int p0 = prm.prefix_out[req], p1 = prm.prefix_out[req + 1];
+  const int hl = threadIdx.x >> 6, head = blockIdx.y * 4 + hl;
+  const int d = (threadIdx.x & 63) * 4;
+  if (p1 <= p0) {
+    *reinterpret_cast<uint2*>(prm.out + ((size_t)req * kHeads + head) * kDim + d) = make_uint2(0, 0);
+    if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * kHeads + head] = -INFINITY;
     return;
   }
-  // CTAs whose ranges intersect [p0, p1)
-  int c_lo = (int)(((long long)p0 * G) / T);
-  while (c_lo > 0 && (((long long)c_lo * T) / G) > p0) --c_lo;
-  while ((((long long)(c_lo + 1) * T) / G) <= p0) ++c_lo;
-  int c_hi = (int)(((long long)(p1 - 1) * G) / T);
-  while (c_hi > 0 && (((long long)c_hi * T) / G) > p1 - 1) --c_hi;
-  while ((((long long)(c_hi + 1) * T) / G) <= p1 - 1) ++c_hi;
-  if (c_lo == c_hi) return;  // written directly by the main kernel
-  // CTAs strictly inside (c_lo, c_hi) may own empty ranges when T < G: skip them
-  auto owns_pages = [&](int c) {
-    return (((long long)(c + 1) * T) / G) > (((long long)c * T) / G);
-  };
+  if (threadIdx.x == 0) {
+    int c = (int)(((long long)p0 * G) / T);
+    while (c > 0 && (((long long)c * T) / G) > p0) --c;
+    while ((((long long)(c + 1) * T) / G) <= p0) ++c;
+    int n = 0;
+    for (; c < G && n < kMaxSplit; ++c) {
+      const int lo = (int)(((long long)c * T) / G), hi = (int)(((long long)(c + 1) * T) / G);
+      if (lo >= p1) break;
+      if (hi > lo) s_slot[n++] = req + c;
+    }
+    s_n = n;
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (n == 1) return;  // whole request: written by the main kernel
+  for (int i = threadIdx.x; i < 4 * n; i += blockDim.x)
+    s_w[i / n][i % n] = __ldcg(prm.part_lse + (size_t)s_slot[i % n] * kHeads + blockIdx.y * 4 + i / n);
+  __syncthreads();
   float m = -INFINITY;
-  for (int c = c_lo; c <= c_hi; ++c)
-    if (owns_pages(c)) m = fmaxf(m, prm.part_lse[(size_t)(req + c) * kHeads + head]);
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < n; ++k) m = fmaxf(m, s_w[hl][k]);
   float wsum = 0.0f;
-  for (int c = c_lo; c <= c_hi; ++c) {
-    if (!owns_pages(c)) continue;
-    const size_t slot = (size_t)(req + c);
-    const float w = exp2f(prm.part_lse[slot * kHeads + head] - m);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+  for (int k = 0; k < n; ++k) {
+    const float w = exp2f(s_w[hl][k] - m);
     wsum += w;
-    const float4* src = reinterpret_cast<const float4*>(prm.part_o + (slot * kHeads + head) * kDim + d0);
-    const float4 a = src[0], b = src[1];
-    acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
-    acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(prm.part_o + ((size_t)s_slot[k] * kHeads + head) * kDim + d));
+    acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
   }
   const float inv = 1.0f / wsum;
-  uint4 v;
-  v.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
-  v.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
-  v.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
-  v.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
-  *reinterpret_cast<uint4*>(dst) = v;
-  if (prm.lse && (threadIdx.x & 31) == 0)
-    prm.lse[(size_t)req * kHeads + head] = (m + __log2f(wsum)) * 0.69314718055994531f;
+  uint2 o;
+  o.x = pack_bf16x2(acc.x * inv, acc.y * inv);
+  o.y = pack_bf16x2(acc.z * inv, acc.w * inv);
+  *reinterpret_cast<uint2*>(prm.out + ((size_t)req * kHeads + head) * kDim + d) = o;
+  if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * kHeads + head] = (m + __log2f(wsum)) * 0.69314718055994531f;
 }
 
 }  // namespace mfa
@@ -491,21 +494,21 @@ mfa_combine_kernel(const Params prm, int G) {
 // ------------------------------------------------------------------ host side
 size_t mfa_decode_workspace_bytes(int batch, int num_sms) {
   const size_t slots = (size_t)batch + num_sms;
-  size_t b = 0;
-  b += align_up((size_t)(batch + 1) * sizeof(int32_t), 256);                 // prefix
-  b += align_up(slots * mfa::kHeads * mfa::kDim * sizeof(float), 256);      // part_o
-  b += align_up(slots * mfa::kHeads * sizeof(float), 256);                  // part_lse
+  size_t b = align_up((size_t)(batch + 1) * sizeof(int32_t), 256);     // prefix
+  b += align_up(slots * mfa::kHeads * mfa::kDim * sizeof(float), 256);  // part_o
+  b += align_up(slots * mfa::kHeads * sizeof(float), 256);              // part_lse
   return b;
 }
 
 cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream) {
   using namespace mfa;
   const int G = ctx.num_sms;
+  if (a.batch > kMaxBatch) return cudaErrorInvalidValue;
   uint8_t* ws = static_cast<uint8_t*>(a.workspace);
   Params prm{};
   prm.block_table = a.block_table;
   prm.seq_lens = a.seq_lens;
-  prm.tile_prefix = reinterpret_cast<int32_t*>(ws);
+  prm.prefix_out = reinterpret_cast<int32_t*>(ws);
   ws += align_up((size_t)(a.batch + 1) * sizeof(int32_t), 256);
   const size_t slots = (size_t)a.batch + G;
   prm.part_o = reinterpret_cast<float*>(ws);
@@ -537,16 +540,16 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
                     box, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
-  plan_kernel<<<1, 1024, 0, stream>>>(a.seq_lens, a.batch, const_cast<int32_t*>(prm.tile_prefix));
-  const size_t smem = sizeof(Smem) + 1024;
+  const size_t smem = sizeof(Smem) + 1024 + (size_t)(a.batch + 1) * sizeof(int32_t);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(mfa_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(mfa_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(Smem) + 1024 + (kMaxBatch + 1) * sizeof(int32_t)));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   mfa_decode_kernel<<<G, kThreads, smem, stream>>>(tq, tk, tv, prm);
-  mfa_combine_kernel<<<dim3(a.batch, kHeads / 8), 256, 0, stream>>>(prm, G);
+  mfa_combine_kernel<<<dim3(a.batch, kHeads / 4), 256, 0, stream>>>(prm, G);
   return cudaGetLastError();
 }
 

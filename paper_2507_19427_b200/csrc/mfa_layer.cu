@@ -8,7 +8,7 @@
 //
 // The GEMMs run on the stream-K tcgen05 kernel (linear.cu); everything that
 // needs a whole row (RMSNorm, RoPE pairs, KV append, residual) is fused into
-// the row epilogue that reduces that GEMM's partials.  Intermediates are
+// the row epilogue that sums that GEMM's partials (lin::SlotTable).  Intermediates are
 // stored in bf16 exactly where the oracle (orc_mfa_layer) rounds.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -37,25 +37,38 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-// xn = RMSNorm(x) * w, bf16 out (input_layernorm)
-__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-                               __nv_bfloat16* __restrict__ out, int dim, float eps) {
+// xn = RMSNorm(x) * w, bf16 out (input_layernorm); dim % 4 == 0
+__global__ void __launch_bounds__(1024) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                       const __nv_bfloat16* __restrict__ w,
+                                                       __nv_bfloat16* __restrict__ out, int dim, float eps) {
   __shared__ float red[32];
   const size_t row = blockIdx.x;
   const __nv_bfloat16* xr = x + row * dim;
   float ss = 0.0f;
-  for (int i = threadIdx.x; i < dim; i += blockDim.x) {
-    const float v = __bfloat162float(xr[i]);
-    ss += v * v;
+  for (int i = threadIdx.x * 4; i < dim; i += blockDim.x * 4) {
+    const uint2 xb = *reinterpret_cast<const uint2*>(xr + i);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.y));
+    ss += a.x * a.x + a.y * a.y + b.x * b.x + b.y * b.y;
   }
   ss = block_sum(ss, red);
   const float inv = rsqrtf(ss / dim + eps);
-  for (int i = threadIdx.x; i < dim; i += blockDim.x)
-    out[row * dim + i] = __float2bfloat16_rn((__bfloat162float(xr[i]) * inv) * __bfloat162float(w[i]));
+  for (int i = threadIdx.x * 4; i < dim; i += blockDim.x * 4) {
+    const uint2 xb = *reinterpret_cast<const uint2*>(xr + i);
+    const uint2 wb = *reinterpret_cast<const uint2*>(w + i);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.y));
+    const float2 wa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb.x));
+    const float2 wc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb.y));
+    uint2 o;
+    o.x = sm100::pack_bf16x2((a.x * inv) * wa.x, (a.y * inv) * wa.y);
+    o.y = sm100::pack_bf16x2((b.x * inv) * wc.x, (b.y * inv) * wc.y);
+    *reinterpret_cast<uint2*>(out + row * dim + i) = o;
+  }
 }
 
 struct QkvEpi {
-  int q_lora, head_dim, page, max_pages;
+  int q_lora, head_dim, page, max_pages, n_out;
   float eps;
   const __nv_bfloat16* q_norm_w;
   __nv_bfloat16* qa;            // [B, q_lora]
@@ -66,15 +79,18 @@ struct QkvEpi {
   const double* inv_freq;       // [head_dim/2]
 };
 
-// reduce [q_down|k|v] partials of one token row; q: RMSNorm -> qa; k: RoPE ->
-// K cache slot of position seq_len-1; v -> V cache slot.
-__global__ void qkv_epilogue_kernel(const LinearPlan P, const float* __restrict__ part, int G, const QkvEpi e) {
+// y = [q_down|k|v] projection of one token row (fp32): q -> RMSNorm -> qa;
+// k -> RoPE -> K cache slot of position seq_len-1; v -> V cache slot.
+__global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
+                                                           int G, const QkvEpi e) {
   extern __shared__ float row_s[];  // n_out floats
   __shared__ float red[32];
+  __shared__ lin::SlotTable tab;
+  lin::build_slot_table(P, G, tab);
   const int row = blockIdx.x;
   float ss = 0.0f;
-  for (int f = threadIdx.x; f < P.n_out; f += blockDim.x) {
-    const float v = bf16r(lin::linear_partial_sum(P, part, G, row, f));
+  for (int f = threadIdx.x; f < e.n_out; f += blockDim.x) {
+    const float v = bf16r(tab.sum(P, part, row, f));
     row_s[f] = v;
     if (f < e.q_lora) ss += v * v;
   }
@@ -100,45 +116,72 @@ __global__ void qkv_epilogue_kernel(const LinearPlan P, const float* __restrict_
   for (int i = threadIdx.x; i < e.head_dim; i += blockDim.x) e.v_cache[slot + i] = __float2bfloat16_rn(v[i]);
 }
 
-// reduce q_up partials; per-head NeoX RoPE; q [B, n_heads, head_dim] bf16
-__global__ void qup_epilogue_kernel(const LinearPlan P, const float* __restrict__ part, int G, int head_dim,
-                                    const int32_t* __restrict__ seq_lens, const double* __restrict__ inv_freq,
-                                    __nv_bfloat16* __restrict__ q) {
+// y = q_up projection (fp32 [B, n_heads*head_dim]); per-head NeoX RoPE -> q bf16.
+// grid (B, n_heads/8), 8 heads x head_dim/2 pairs per CTA.
+__global__ void __launch_bounds__(1024) qup_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
+                                                            int G, int n_out, int head_dim,
+                                                            const int32_t* __restrict__ seq_lens,
+                                                            const double* __restrict__ inv_freq,
+                                                            __nv_bfloat16* __restrict__ q) {
+  __shared__ lin::SlotTable tab;
+  lin::build_slot_table(P, G, tab);
   const int row = blockIdx.x;
   const int half = head_dim / 2;
   const int pos = max(__ldg(seq_lens + row) - 1, 0);
-  for (int idx = threadIdx.x; idx < P.n_out / 2; idx += blockDim.x) {
-    const int h = idx / half, i = idx % half;
-    const int f1 = h * head_dim + i, f2 = f1 + half;
-    const float x1 = bf16r(lin::linear_partial_sum(P, part, G, row, f1));
-    const float x2 = bf16r(lin::linear_partial_sum(P, part, G, row, f2));
-    double sn, cs;
-    sincos((double)pos * inv_freq[i], &sn, &cs);
-    const float c = (float)cs, s = (float)sn;
-    q[(size_t)row * P.n_out + f1] = __float2bfloat16_rn(x1 * c - x2 * s);
-    q[(size_t)row * P.n_out + f2] = __float2bfloat16_rn(x2 * c + x1 * s);
-  }
+  const int idx = blockIdx.y * blockDim.x + threadIdx.x;  // pair index in the row
+  if (idx >= n_out / 2) return;
+  const int h = idx / half, i = idx % half;
+  const int c1 = h * head_dim + i;
+  const size_t f1 = (size_t)row * n_out + c1, f2 = f1 + half;
+  const float x1 = bf16r(tab.sum(P, part, row, c1)), x2 = bf16r(tab.sum(P, part, row, c1 + half));
+  double sn, cs;
+  sincos((double)pos * inv_freq[i], &sn, &cs);
+  const float c = (float)cs, s = (float)sn;
+  q[f1] = __float2bfloat16_rn(x1 * c - x2 * s);
+  q[f2] = __float2bfloat16_rn(x2 * c + x1 * s);
 }
 
-// reduce o_proj partials; h_res = bf16(x + o); h_norm = RMSNorm(h_res) (post_attention_layernorm)
-__global__ void o_epilogue_kernel(const LinearPlan P, const float* __restrict__ part, int G,
-                                  const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w_post,
-                                  float eps, __nv_bfloat16* __restrict__ h_res, __nv_bfloat16* __restrict__ h_norm) {
+// y = o_proj (fp32); h_res = bf16(x + y); h_norm = RMSNorm(h_res) (post_attention_layernorm)
+__global__ void __launch_bounds__(1024) o_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
+                                                          int G, int n, const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ w_post, float eps,
+                                                          __nv_bfloat16* __restrict__ h_res,
+                                                          __nv_bfloat16* __restrict__ h_norm) {
   extern __shared__ float row_s[];
   __shared__ float red[32];
-  const int row = blockIdx.x;
-  const int n = P.n_out;
+  __shared__ lin::SlotTable tab;
+  lin::build_slot_table(P, G, tab);
+  const size_t row = blockIdx.x;
   float ss = 0.0f;
-  for (int f = threadIdx.x; f < n; f += blockDim.x) {
-    const float r = bf16r(__bfloat162float(x[(size_t)row * n + f]) + lin::linear_partial_sum(P, part, G, row, f));
-    row_s[f] = r;
-    h_res[(size_t)row * n + f] = __float2bfloat16_rn(r);
-    ss += r * r;
+  for (int f = threadIdx.x * 4; f < n; f += blockDim.x * 4) {
+    const float4 o = make_float4(tab.sum(P, part, (int)row, f), tab.sum(P, part, (int)row, f + 1),
+                                 tab.sum(P, part, (int)row, f + 2), tab.sum(P, part, (int)row, f + 3));
+    const uint2 xb = *reinterpret_cast<const uint2*>(x + row * n + f);
+    const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&xb.x);
+    const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&xb.y);
+    const float r[4] = {bf16r(__low2float(x01) + o.x), bf16r(__high2float(x01) + o.y),
+                        bf16r(__low2float(x23) + o.z), bf16r(__high2float(x23) + o.w)};
+    uint2 ob;
+    ob.x = sm100::pack_bf16x2(r[0], r[1]);
+    ob.y = sm100::pack_bf16x2(r[2], r[3]);
+    *reinterpret_cast<uint2*>(h_res + row * n + f) = ob;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      row_s[f + q] = r[q];
+      ss += r[q] * r[q];
+    }
   }
   ss = block_sum(ss, red);
   const float inv = rsqrtf(ss / n + eps);
-  for (int f = threadIdx.x; f < n; f += blockDim.x)
-    h_norm[(size_t)row * n + f] = __float2bfloat16_rn((row_s[f] * inv) * __bfloat162float(w_post[f]));
+  for (int f = threadIdx.x * 4; f < n; f += blockDim.x * 4) {
+    const uint2 wb = *reinterpret_cast<const uint2*>(w_post + f);
+    const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&wb.x);
+    const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&wb.y);
+    uint2 ob;
+    ob.x = sm100::pack_bf16x2((row_s[f] * inv) * __low2float(w01), (row_s[f + 1] * inv) * __high2float(w01));
+    ob.y = sm100::pack_bf16x2((row_s[f + 2] * inv) * __low2float(w23), (row_s[f + 3] * inv) * __high2float(w23));
+    *reinterpret_cast<uint2*>(h_norm + row * n + f) = ob;
+  }
 }
 
 }  // namespace layer
@@ -159,10 +202,10 @@ const double* rope_inv_freq(Ctx& ctx, int head_dim, float theta) {
 size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms) {
   const int B = a.batch, Hd = a.hidden, QL = a.q_lora, NQ = a.n_heads * a.head_dim;
   size_t b = 0;
-  b += align_up((size_t)B * Hd * 2, 256);  // xn
-  b += align_up((size_t)B * QL * 2, 256);  // qa
-  b += align_up((size_t)B * NQ * 2, 256);  // q
-  b += align_up((size_t)B * NQ * 2, 256);  // attn
+  b += align_up((size_t)B * Hd * 2, 256);                       // xn
+  b += align_up((size_t)B * QL * 2, 256);                       // qa
+  b += align_up((size_t)B * NQ * 2, 256);                       // q
+  b += align_up((size_t)B * NQ * 2, 256);                       // attn
   size_t part = linear_workspace_bytes(make_linear_plan(B, QL + 2 * a.head_dim, Hd), num_sms);
   const size_t p2 = linear_workspace_bytes(make_linear_plan(B, NQ, QL), num_sms);
   const size_t p3 = linear_workspace_bytes(make_linear_plan(B, Hd, NQ), num_sms);
@@ -176,7 +219,6 @@ size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms) {
 cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cudaStream_t stream) {
   using namespace layer;
   const int B = a.batch, Hd = a.hidden, QL = a.q_lora, D = a.head_dim, NQ = a.n_heads * a.head_dim;
-  const int G = ctx.num_sms;
   uint8_t* ws = static_cast<uint8_t*>(ws_base);
   auto take = [&](size_t bytes) { void* p = ws; ws += align_up(bytes, 256); return p; };
   auto* xn = static_cast<__nv_bfloat16*>(take((size_t)B * Hd * 2));
@@ -189,30 +231,32 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   cudaError_t e;
 
   // K1a: input RMSNorm
-  rmsnorm_kernel<<<B, 512, 0, stream>>>(static_cast<const __nv_bfloat16*>(a.x),
-                                         static_cast<const __nv_bfloat16*>(a.w_in_norm), xn, Hd, a.rms_eps);
-  // K1b: [q_down | k | v] projection + q RMSNorm + RoPE(k) + paged KV append
+  rmsnorm_kernel<<<B, 1024, 0, stream>>>(static_cast<const __nv_bfloat16*>(a.x),
+                                          static_cast<const __nv_bfloat16*>(a.w_in_norm), xn, Hd, a.rms_eps);
+  // K1b: [q_down | k | v] projection, then q RMSNorm + RoPE(k) + paged KV append
   const LinearPlan p1 = make_linear_plan(B, QL + 2 * D, Hd);
   if ((e = linear_bf16_launch(ctx, p1, xn, a.w_qkv, part, stream)) != cudaSuccess) return e;
-  QkvEpi qe{QL, D, a.page_size, a.max_pages, a.rms_eps, static_cast<const __nv_bfloat16*>(a.w_q_norm), qa,
-            static_cast<__nv_bfloat16*>(a.k_cache), static_cast<__nv_bfloat16*>(a.v_cache), a.block_table,
-            a.seq_lens, inv_freq};
-  qkv_epilogue_kernel<<<B, 256, p1.n_out * sizeof(float), stream>>>(p1, part, G, qe);
+  QkvEpi qe{QL, D, a.page_size, a.max_pages, p1.n_out, a.rms_eps,
+            static_cast<const __nv_bfloat16*>(a.w_q_norm), qa, static_cast<__nv_bfloat16*>(a.k_cache),
+            static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq};
+  qkv_epilogue_kernel<<<B, 512, p1.n_out * sizeof(float), stream>>>(p1, part, linear_grid(ctx, p1), qe);
   // K1c: q_up projection + RoPE(q)
   const LinearPlan p2 = make_linear_plan(B, NQ, QL);
   if ((e = linear_bf16_launch(ctx, p2, qa, a.w_q_up, part, stream)) != cudaSuccess) return e;
-  qup_epilogue_kernel<<<B, 512, 0, stream>>>(p2, part, G, D, a.seq_lens, inv_freq, q);
+  qup_epilogue_kernel<<<dim3(B, (NQ / 2 + 1023) / 1024), 1024, 0, stream>>>(p2, part, linear_grid(ctx, p2), NQ, D,
+                                                                           a.seq_lens, inv_freq, q);
   // K2/K3: MFA decode core over the paged cache (now including this token)
   MfaDecodeArgs md{B, q, a.k_cache, a.v_cache, a.num_pages, a.block_table, a.max_pages, a.seq_lens,
                    a.softmax_scale, attn, nullptr, part};
   if ((e = mfa_decode_launch(ctx, md, stream)) != cudaSuccess) return e;
-  // K4: o_proj + residual + post-attention RMSNorm
+  // K4: o_proj, then residual + post-attention RMSNorm
   const LinearPlan p3 = make_linear_plan(B, Hd, NQ);
   if ((e = linear_bf16_launch(ctx, p3, attn, a.w_o, part, stream)) != cudaSuccess) return e;
-  o_epilogue_kernel<<<B, 512, Hd * sizeof(float), stream>>>(p3, part, G, static_cast<const __nv_bfloat16*>(a.x),
-                                                            static_cast<const __nv_bfloat16*>(a.w_post_norm),
-                                                            a.rms_eps, static_cast<__nv_bfloat16*>(a.h_res),
-                                                            static_cast<__nv_bfloat16*>(a.h_norm));
+  o_epilogue_kernel<<<B, 1024, Hd * sizeof(float), stream>>>(p3, part, linear_grid(ctx, p3), Hd,
+                                                             static_cast<const __nv_bfloat16*>(a.x),
+                                                             static_cast<const __nv_bfloat16*>(a.w_post_norm),
+                                                             a.rms_eps, static_cast<__nv_bfloat16*>(a.h_res),
+                                                             static_cast<__nv_bfloat16*>(a.h_norm));
   return cudaGetLastError();
 }
 

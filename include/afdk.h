@@ -129,6 +129,59 @@ typedef struct afdk_mfa_layer_args {
 afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
                            afdk_stream stream);
 
+/* ------------------------------------------------ K5 router + FP8 dispatch
+ * Attention-side router: logits = h . gate_w^T (fp32), softmax,
+ * top-k by logit (ties -> lower expert id), weights = softmax probability
+ * (renormalize != 0 divides by their sum).  When xq != NULL the FP8 dispatch
+ * payload is produced as well: per token and 128-feature
+ * block, xs = max(amax, 1e-10)/448, xq = e4m3_rn_satfinite(h / xs).
+ *   h [T, H] bf16, gate_w [E, H] bf16; logits [T, E] fp32 (optional);
+ *   ids [T, k] int32; weights [T, k] fp32; xq [T, H] e4m3; xs [T, H/128] fp32.
+ * Limits: E <= 64, k <= 8, H % 256 == 0.                                   */
+afdk_status afdk_router_topk(afdk_ctx* ctx, const void* h, const void* gate_w, int T, int H, int E, int k,
+                             int renormalize, float* logits, int32_t* ids, float* weights, void* xq,
+                             float* xs, afdk_stream stream);
+
+/* ---------------------------------------------- K6 expert distribution
+ * Stable expert-major permutation of the [T, k] routing: offsets [E+1]
+ * (exclusive prefix of per-expert counts), perm [T*k] (slot -> t*k+j in
+ * (expert, token, j) order), inv [T*k] (t*k+j -> slot).                   */
+afdk_status afdk_moe_permute(afdk_ctx* ctx, const int32_t* ids, int T, int k, int E, int32_t* offsets,
+                             int32_t* perm, int32_t* inv, afdk_stream stream);
+
+/* ----------------------------------------------- K7/K8/K9 MoE FFN (FP8)
+ * One MoE layer on an FFN rank: dispatched FP8 tokens in, this rank's bf16
+ * partial out = sum over its routed experts [expert_lo, expert_hi) of
+ * w_j * expert(x) + the shared expert for tokens [shared_lo, shared_hi).
+ * Gated experts (SiLU(gate) * up, then down), e4m3 weights with 128x128
+ * fp32 block scales; the intermediate is re-quantised to e4m3 with 1x128
+ * scales.  Weight tensors hold the local routed experts followed by the
+ * shared expert (index n_local = expert_hi - expert_lo):
+ *   w13 [(n_local+1), 2*inter, hidden] (rows: gate then up),
+ *   s13 [(n_local+1), 2*inter/128, hidden/128],
+ *   w2  [(n_local+1), hidden, inter],  s2 [(n_local+1), hidden/128, inter/128].
+ * Limits: hidden % 128 == 0, inter % 128 == 0, E <= 64, k <= 8, T*k <= 65536. */
+typedef struct afdk_moe_weights {
+  int hidden, inter, n_experts, top_k;
+  int expert_lo, expert_hi;
+  const void* w13;
+  const float* s13;
+  const void* w2;
+  const float* s2;
+} afdk_moe_weights;
+
+typedef struct afdk_moe_args {
+  int T;
+  const void* xq;        /* e4m3 [T, hidden] dispatch payload        */
+  const float* xs;       /* [T, hidden/128] its scales               */
+  const int32_t* ids;    /* [T, top_k]                               */
+  const float* weights;  /* [T, top_k]                               */
+  int shared_lo, shared_hi;
+  void* out;             /* bf16 [T, hidden] this rank's partial     */
+} afdk_moe_args;
+
+afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a, afdk_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

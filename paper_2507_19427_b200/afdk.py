@@ -58,6 +58,21 @@ class MfaLayerArgs(Structure):
     ]
 
 
+class MoeWeights(Structure):
+    _fields_ = [
+        ("hidden", c_int), ("inter", c_int), ("n_experts", c_int), ("top_k", c_int),
+        ("expert_lo", c_int), ("expert_hi", c_int),
+        ("w13", c_void_p), ("s13", c_void_p), ("w2", c_void_p), ("s2", c_void_p),
+    ]
+
+
+class MoeArgs(Structure):
+    _fields_ = [
+        ("T", c_int), ("xq", c_void_p), ("xs", c_void_p), ("ids", c_void_p), ("weights", c_void_p),
+        ("shared_lo", c_int), ("shared_hi", c_int), ("out", c_void_p),
+    ]
+
+
 # exported symbol -> (restype, argtypes); the CPU test checks every symbol of
 # include/afdk.h is present in the built library
 SIGNATURES = {
@@ -69,6 +84,10 @@ SIGNATURES = {
     "afdk_mfa_decode_attention": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_void_p]),
     "afdk_linear": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]),
     "afdk_mfa_layer": (c_int, [c_void_p, POINTER(MfaWeights), POINTER(MfaLayerArgs), c_void_p]),
+    "afdk_router_topk": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p,
+                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "afdk_moe_permute": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "afdk_moe_ffn": (c_int, [c_void_p, POINTER(MoeWeights), POINTER(MoeArgs), c_void_p]),
 }
 
 _lib = None
@@ -155,3 +174,29 @@ class Context:
         a = MfaLayerArgs(x.shape[0], ptr(x), ptr(k_cache), ptr(v_cache), k_cache.shape[0], k_cache.shape[1],
                          ptr(block_table), block_table.shape[1], ptr(seq_lens), ptr(h_res), ptr(h_norm))
         check(self.lib.afdk_mfa_layer(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+
+    # -------------------------------------------------------- K5/K6/K7-K9
+    def router_topk(self, h, gate_w, k, ids, weights, logits=None, xq=None, xs=None, renormalize=False,
+                    stream: int = 0) -> None:
+        T, Hd = h.shape
+        E = gate_w.shape[0]
+        check(self.lib.afdk_router_topk(self.handle, ptr(h), ptr(gate_w), T, Hd, E, k, int(renormalize),
+                                        ptr(logits), ptr(ids), ptr(weights), ptr(xq), ptr(xs), c_void_p(stream)))
+
+    def moe_permute(self, ids, n_experts, offsets, perm, inv, stream: int = 0) -> None:
+        T, k = ids.shape
+        check(self.lib.afdk_moe_permute(self.handle, ptr(ids), T, k, n_experts, ptr(offsets), ptr(perm),
+                                        ptr(inv), c_void_p(stream)))
+
+    def moe_ffn(self, w: dict, xq, xs, ids, weights, out, expert_lo=0, expert_hi=None, shared=(0, None),
+                stream: int = 0) -> None:
+        """w: n_experts, w13, s13, w2, s2 (local experts then the shared one)."""
+        T, Hd = xq.shape
+        k = ids.shape[1]
+        inter = w["w2"].shape[2]
+        E = w["n_experts"]
+        hi = E if expert_hi is None else expert_hi
+        sh_lo, sh_hi = shared[0], (T if shared[1] is None else shared[1])
+        mw = MoeWeights(Hd, inter, E, k, expert_lo, hi, ptr(w["w13"]), ptr(w["s13"]), ptr(w["w2"]), ptr(w["s2"]))
+        a = MoeArgs(T, ptr(xq), ptr(xs), ptr(ids), ptr(weights), sh_lo, sh_hi, ptr(out))
+        check(self.lib.afdk_moe_ffn(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))

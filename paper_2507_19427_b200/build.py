@@ -21,6 +21,9 @@ CU_SOURCES = [
     "mfa_decode.cu",
     "linear.cu",
     "mfa_layer.cu",
+    "moe_route.cu",
+    "moe_gemm.cu",
+    "moe_ffn.cu",
 ]
 CXX_SOURCES: list[str] = []
 

@@ -203,4 +203,72 @@ afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_
   return AFDK_OK;
 }
 
+afdk_status afdk_router_topk(afdk_ctx* ctx, const void* h, const void* gate_w, int T, int H, int E, int k,
+                             int renormalize, float* logits, int32_t* ids, float* weights, void* xq,
+                             float* xs, afdk_stream stream) {
+  if (!ctx || !h || !gate_w || !ids || !weights) { set_error("afdk_router_topk: NULL argument"); return AFDK_ERR_INVALID; }
+  if (E < 1 || E > afdk::moe::kMaxExperts) { set_error("afdk_router_topk: E must be in [1, 64]"); return AFDK_ERR_INVALID; }
+  if (k < 1 || k > afdk::moe::kMaxTopK || k > E) { set_error("afdk_router_topk: k must be in [1, min(8, E)]"); return AFDK_ERR_INVALID; }
+  if (T < 1 || H < 256 || H % 256) { set_error("afdk_router_topk: H must be a positive multiple of 256"); return AFDK_ERR_INVALID; }
+  if (xq && !xs) { set_error("afdk_router_topk: xq requires xs"); return AFDK_ERR_INVALID; }
+  cudaSetDevice(ctx->c.device);
+  afdk::moe::RouterArgs a{static_cast<const __nv_bfloat16*>(h), static_cast<const __nv_bfloat16*>(gate_w), T, H, E, k,
+                          renormalize, logits, ids, weights, static_cast<uint8_t*>(xq), xs};
+  const cudaError_t e = afdk::router_launch(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("afdk_router_topk", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_moe_permute(afdk_ctx* ctx, const int32_t* ids, int T, int k, int E, int32_t* offsets,
+                             int32_t* perm, int32_t* inv, afdk_stream stream) {
+  if (!ctx || !ids || !offsets || !perm || !inv) { set_error("afdk_moe_permute: NULL argument"); return AFDK_ERR_INVALID; }
+  if (E < 1 || E > afdk::moe::kMaxExperts || k < 1 || k > afdk::moe::kMaxTopK || T < 1 || T * k > 65536) {
+    set_error("afdk_moe_permute: need 1 <= E <= 64, 1 <= k <= 8, T*k <= 65536");
+    return AFDK_ERR_INVALID;
+  }
+  afdk::Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  const size_t wbytes = afdk::align_up((size_t)afdk::moe::max_work(T, k, E) * sizeof(afdk::moe::Work), 256) + 256;
+  uint8_t* ws = static_cast<uint8_t*>(afdk::workspace(c, wbytes));
+  if (!ws) { set_error("afdk_moe_permute: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  afdk::moe::PermuteArgs a{ids, T, k, E, 0, E, 0, 0, 0, offsets, perm, inv,
+                           reinterpret_cast<afdk::moe::Work*>(ws), reinterpret_cast<int*>(ws + wbytes - 256)};
+  const cudaError_t e = afdk::permute_launch(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("afdk_moe_permute", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a, afdk_stream stream) {
+  if (!ctx || !w || !a) { set_error("afdk_moe_ffn: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }
+  if (w->hidden % 128 || w->inter % 128 || w->hidden < 128 || w->inter < 128) {
+    set_error("afdk_moe_ffn: hidden and inter must be positive multiples of 128");
+    return AFDK_ERR_INVALID;
+  }
+  if (w->n_experts < 1 || w->n_experts > afdk::moe::kMaxExperts || w->top_k < 1 || w->top_k > afdk::moe::kMaxTopK) {
+    set_error("afdk_moe_ffn: need 1 <= n_experts <= 64 and 1 <= top_k <= 8");
+    return AFDK_ERR_INVALID;
+  }
+  if (w->expert_lo < 0 || w->expert_hi > w->n_experts || w->expert_lo > w->expert_hi) {
+    set_error("afdk_moe_ffn: expert range out of bounds");
+    return AFDK_ERR_INVALID;
+  }
+  if (a->T < 1 || a->T * w->top_k > 65536) { set_error("afdk_moe_ffn: T out of range"); return AFDK_ERR_INVALID; }
+  if (!a->xq || !a->xs || !a->ids || !a->weights || !a->out || !w->w13 || !w->s13 || !w->w2 || !w->s2) {
+    set_error("afdk_moe_ffn: NULL tensor pointer");
+    return AFDK_ERR_INVALID;
+  }
+  afdk::Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  const int sh_lo = a->shared_lo < 0 ? 0 : a->shared_lo;
+  const int sh_hi = a->shared_hi > a->T ? a->T : a->shared_hi;
+  afdk::MoeFfnArgs m{a->T, w->top_k, w->n_experts, w->hidden, w->inter, w->expert_lo, w->expert_hi,
+                     w->w13, w->s13, w->w2, w->s2, static_cast<const uint8_t*>(a->xq), a->xs, a->ids,
+                     a->weights, sh_lo, sh_hi, a->out};
+  void* ws = afdk::workspace(c, afdk::moe_ffn_workspace_bytes(a->T, w->top_k, w->n_experts, w->hidden, w->inter));
+  if (!ws) { set_error("afdk_moe_ffn: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  const cudaError_t e = afdk::moe_ffn_launch(c, m, ws, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("afdk_moe_ffn", e);
+  return AFDK_OK;
+}
+
 }  // extern "C"

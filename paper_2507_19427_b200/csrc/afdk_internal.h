@@ -8,6 +8,7 @@
 #include <string>
 
 #include "linear.cuh"
+#include "moe.cuh"
 
 namespace afdk {
 
@@ -88,5 +89,42 @@ struct MfaLayerArgs {
 const double* rope_inv_freq(Ctx& ctx, int head_dim, float theta);
 size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms);
 cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws, cudaStream_t stream);
+
+// ---------------------------------------------------------------- MoE FFN
+cudaError_t router_launch(const moe::RouterArgs& a, cudaStream_t stream);
+cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream);
+cudaError_t gather_launch(const moe::GatherArgs& a, cudaStream_t stream);
+cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream);
+
+struct MoeGemmArgs {
+  const void* w;         // e4m3 [(n_local+1) * w_rows, K]
+  const float* w_scale;  // [(n_local+1)][w_rows/128][K/128]
+  const void* x;         // e4m3 [rows_pad, K] dispatch-ordered rows
+  const float* xs_t;     // [K/128][rows_pad]
+  const moe::Work* work;
+  const int* n_work;
+  int H, I, E, expert_lo, n_local, rows_pad;
+  uint8_t* hq;           // GLU outputs
+  float* hs_t;
+  float* y;              // W2 output
+};
+cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream_t stream);
+
+struct MoeFfnArgs {
+  int T, k, E, H, I;
+  int expert_lo, expert_hi;
+  const void* w13;
+  const float* s13;
+  const void* w2;
+  const float* s2;
+  const uint8_t* xq;
+  const float* xs;
+  const int32_t* ids;
+  const float* weights;
+  int shared_lo, shared_hi;
+  void* out;
+};
+size_t moe_ffn_workspace_bytes(int T, int k, int E, int H, int I);
+cudaError_t moe_ffn_launch(Ctx& ctx, const MoeFfnArgs& a, void* ws, cudaStream_t stream);
 
 }  // namespace afdk

@@ -1,0 +1,66 @@
+// moe.cuh — argument blocks of the MoE FFN kernels (K5-K9).
+#pragma once
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+namespace afdk {
+namespace moe {
+
+constexpr int kMaxExperts = 64;  // routed experts (Step-3: 48)
+constexpr int kMaxTopK = 8;      // Step-3: 3
+constexpr int kChunk = 64;       // dispatched rows per GEMM work item (MMA N <= 64)
+
+struct RouterArgs {
+  const __nv_bfloat16* h;       // [T, H] post-attention RMSNorm output
+  const __nv_bfloat16* gate_w;  // [E, H]
+  int T, H, E, k, renormalize;
+  float* logits;                // [T, E] optional
+  int32_t* ids;                 // [T, k]
+  float* weights;               // [T, k]
+  uint8_t* xq;                  // [T, H] e4m3, optional (dispatch payload)
+  float* xs;                    // [T, H/128]
+};
+
+struct Work {
+  int group;  // expert id, or E for the shared expert
+  int row0;   // first row in the dispatch buffer
+  int rows;   // <= kChunk
+};
+
+struct PermuteArgs {
+  const int32_t* ids;  // [T, k]
+  int T, k, E;
+  int expert_lo, expert_hi;        // routed experts owned by this FFN rank
+  int shared_local, shared_lo, shared_hi;  // shared-expert token range owned here
+  int32_t* offsets;    // [E+1]
+  int32_t* perm;       // [T*k] slot -> t*k+j
+  int32_t* inv;        // [T*k] t*k+j -> slot
+  Work* work;          // [max work]
+  int* n_work;
+};
+
+struct GatherArgs {
+  const uint8_t* xq;   // [T, H]
+  const float* xs;     // [T, H/128]
+  const int32_t* perm;
+  int T, k, H, rows_pad;
+  uint8_t* xp;         // [rows_pad, H]  routed rows then shared rows
+  float* xs_t;         // [H/128, rows_pad]
+};
+
+struct CombineArgs {
+  const float* y;      // [rows_pad, H] expert outputs in dispatch order
+  const int32_t* ids;
+  const float* weights;
+  const int32_t* inv;
+  int T, k, H;
+  int expert_lo, expert_hi, shared_local, shared_lo, shared_hi;
+  __nv_bfloat16* out;  // [T, H]
+};
+
+inline int max_work(int T, int k, int E) { return E + (T * k) / kChunk + 1 + T / kChunk + 1; }
+inline int rows_pad(int T, int k) { return ((T * k + T + 127) / 128) * 128; }
+
+}  // namespace moe
+}  // namespace afdk

@@ -1,0 +1,272 @@
+// moe_route.cu — K5 router + FP8 dispatch quantization, K6 permutation,
+// dispatch gather and K9 combine for the Step-3 MoE FFN.
+//
+// Semantics (restated in oracle/afd_oracle.c, pinned by tests/golden/router.npz):
+//   router   logits = h . Wg^T (fp32, fixed summation order), softmax over E,
+//            top-k by logit with ties to the lower expert id, weights =
+//            softmax probabilities of the selected experts (vllm FusedMoE,
+//            renormalize = norm_expert_weight = False); runs on the ATTENTION
+//            side.
+//   quant    per token, per 128 contiguous features: scale = max(amax,1e-10)/448,
+//            q = e4m3_rn_satfinite(x / scale) — the FP8 dispatch payload and its
+//            scale factors.
+//   permute  expert-major, then token, then k (stable): the "expert
+//            distribution" metadata that organises the FFN input.
+//   combine  out[t] = sum_j w[t,j] * y[slot(t,j)] + y_shared[t]  -> bf16
+//            (BF16 return).
+#include <cuda_bf16.h>
+#include <cuda_fp8.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "afdk_internal.h"
+#include "moe.cuh"
+
+namespace afdk {
+namespace moe {
+
+constexpr int kRouterTok = 8;  // tokens per router CTA
+
+__device__ __forceinline__ uint8_t to_e4m3(float v) {
+  return (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E4M3);
+}
+
+// ---------------------------------------------------------------- K5 router
+// grid ceil(T/8), 256 threads.  Warp w computes experts e = w, w+8, ... for the
+// CTA's 8 tokens; lane l owns k = 8l + 256i; reduction is a fixed xor-tree so
+// the logits are bitwise reproducible run to run.
+__global__ void __launch_bounds__(256) router_kernel(RouterArgs a) {
+  __shared__ float s_logit[kRouterTok][kMaxExperts];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * kRouterTok;
+  const int nt = min(kRouterTok, a.T - t0);
+  const int H = a.H;
+  for (int e0 = warp; e0 < a.E; e0 += 8 * 2) {
+    // two experts per pass to reuse the token loads
+    const int e1 = e0 + 8;
+    float acc0[kRouterTok], acc1[kRouterTok];
+#pragma unroll
+    for (int t = 0; t < kRouterTok; ++t) acc0[t] = acc1[t] = 0.0f;
+    const __nv_bfloat16* w0 = a.gate_w + (size_t)e0 * H;
+    const __nv_bfloat16* w1 = a.gate_w + (size_t)(e1 < a.E ? e1 : e0) * H;
+    for (int k = lane * 8; k < H; k += 256) {
+      const uint4 wa = __ldg(reinterpret_cast<const uint4*>(w0 + k));
+      const uint4 wb = __ldg(reinterpret_cast<const uint4*>(w1 + k));
+      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&wa);
+      const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&wb);
+#pragma unroll
+      for (int t = 0; t < kRouterTok; ++t) {
+        if (t < nt) {
+          const uint4 xa = __ldg(reinterpret_cast<const uint4*>(a.h + (size_t)(t0 + t) * H + k));
+          const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&xa);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 xf = __bfloat1622float2(px[q]);
+            const float2 fa = __bfloat1622float2(pa[q]);
+            const float2 fb = __bfloat1622float2(pb[q]);
+            acc0[t] = fmaf(xf.x, fa.x, acc0[t]);
+            acc0[t] = fmaf(xf.y, fa.y, acc0[t]);
+            acc1[t] = fmaf(xf.x, fb.x, acc1[t]);
+            acc1[t] = fmaf(xf.y, fb.y, acc1[t]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kRouterTok; ++t) {
+      float v0 = acc0[t], v1 = acc1[t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffff, v0, o);
+        v1 += __shfl_xor_sync(0xffffffff, v1, o);
+      }
+      if (lane == 0) {
+        s_logit[t][e0] = v0;
+        if (e1 < a.E) s_logit[t][e1] = v1;
+      }
+    }
+  }
+  __syncthreads();
+  // softmax + top-k: one thread per token, sequential in expert order (matches
+  // orc_router_topk's summation order exactly)
+  if (threadIdx.x < nt) {
+    const int t = threadIdx.x, tok = t0 + t;
+    const float* lg = s_logit[t];
+    float mx = lg[0];
+    for (int e = 1; e < a.E; ++e) mx = lg[e] > mx ? lg[e] : mx;
+    float sum = 0.0f;
+    for (int e = 0; e < a.E; ++e) sum += expf(lg[e] - mx);
+    uint64_t taken = 0;
+    float wsum = 0.0f;
+    float wk[kMaxTopK];
+    for (int j = 0; j < a.k; ++j) {
+      int best = -1;
+      for (int e = 0; e < a.E; ++e) {
+        if ((taken >> e) & 1) continue;
+        if (best < 0 || lg[e] > lg[best]) best = e;
+      }
+      taken |= 1ull << best;
+      a.ids[(size_t)tok * a.k + j] = best;
+      wk[j] = expf(lg[best] - mx) / sum;
+      wsum += wk[j];
+    }
+    for (int j = 0; j < a.k; ++j) a.weights[(size_t)tok * a.k + j] = a.renormalize ? wk[j] / wsum : wk[j];
+    if (a.logits)
+      for (int e = 0; e < a.E; ++e) a.logits[(size_t)tok * a.E + e] = lg[e];
+  }
+  // FP8 dispatch payload: one warp per 128-feature block, 4 features per lane
+  if (a.xq) {
+    const int nb = H / 128;
+    for (int blk = warp; blk < nt * nb; blk += 8) {
+      const int t = blk / nb, b = blk % nb;
+      const __nv_bfloat16* src = a.h + (size_t)(t0 + t) * H + b * 128 + lane * 4;
+      const uint2 raw = *reinterpret_cast<const uint2*>(src);
+      const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+      const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+      float amax = fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y)));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, o));
+      const float sc = __fdiv_rn(fmaxf(amax, 1e-10f), 448.0f);
+      const uint32_t q = (uint32_t)to_e4m3(__fdiv_rn(f01.x, sc)) | ((uint32_t)to_e4m3(__fdiv_rn(f01.y, sc)) << 8) |
+                         ((uint32_t)to_e4m3(__fdiv_rn(f23.x, sc)) << 16) |
+                         ((uint32_t)to_e4m3(__fdiv_rn(f23.y, sc)) << 24);
+      *reinterpret_cast<uint32_t*>(a.xq + (size_t)(t0 + t) * H + b * 128 + lane * 4) = q;
+      if (lane == 0) a.xs[(size_t)(t0 + t) * nb + b] = sc;
+    }
+  }
+}
+
+// ------------------------------------------------------------- K6 permute
+// One CTA.  ids staged in smem; warp w owns experts w and w+32.  Two ballot
+// passes (count, scatter) give the stable (expert, token, j) order exactly.
+// Also emits the grouped-GEMM work list: chunks of <= kChunk rows per group,
+// groups 0..E-1 routed (rows at offsets[e]) and group E = shared expert over
+// all T tokens (rows 3T.. of the dispatch buffer).
+__global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
+  extern __shared__ uint8_t s_ids[];
+  __shared__ int s_cnt[kMaxExperts], s_off[kMaxExperts + 1];
+  const int n = a.T * a.k;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_ids[i] = (uint8_t)a.ids[i];
+  __syncthreads();
+  for (int e = warp; e < a.E; e += 32) {
+    int c = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      c += __popc(__ballot_sync(0xffffffff, i < n && s_ids[i] == e));
+    }
+    if (lane == 0) s_cnt[e] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int e = 0; e < a.E; ++e) { s_off[e] = run; run += s_cnt[e]; }
+    s_off[a.E] = run;
+    for (int e = 0; e <= a.E; ++e) a.offsets[e] = s_off[e];
+    // work list (group, first row, rows)
+    int g = 0;
+    for (int e = 0; e <= a.E; ++e) {
+      const bool local = (e == a.E) ? a.shared_local : (e >= a.expert_lo && e < a.expert_hi);
+      if (!local) continue;
+      const int row0 = (e == a.E) ? n + a.shared_lo : s_off[e];
+      const int rows = (e == a.E) ? a.shared_hi - a.shared_lo : s_cnt[e];
+      for (int r = 0; r < rows; r += kChunk) {
+        a.work[g].group = e;
+        a.work[g].row0 = row0 + r;
+        a.work[g].rows = min(kChunk, rows - r);
+        ++g;
+      }
+    }
+    *a.n_work = g;
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int e = warp; e < a.E; e += 32) {
+    int run = s_off[e];
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const bool hit = i < n && s_ids[i] == e;
+      const unsigned m = __ballot_sync(0xffffffff, hit);
+      if (hit) {
+        const int pos = run + __popc(m & lt);
+        a.perm[pos] = i;
+        a.inv[i] = pos;
+      }
+      run += __popc(m);
+    }
+  }
+}
+
+// ---------------------------------------------------------- dispatch gather
+// rows [0, T*k): routed copies in permuted order; rows [T*k, T*k + T): the
+// shared expert's tokens in order.  Scales are written transposed
+// [H/128][rows] so the GEMM fetches one k-block's row scales with a TMA box.
+__global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+  const int s = blockIdx.x;
+  const int n_routed = a.T * a.k;
+  const int src = (s < n_routed) ? __ldg(a.perm + s) / a.k : s - n_routed;
+  const uint4* in = reinterpret_cast<const uint4*>(a.xq + (size_t)src * a.H);
+  uint4* out = reinterpret_cast<uint4*>(a.xp + (size_t)s * a.H);
+  for (int i = threadIdx.x; i < a.H / 16; i += blockDim.x) out[i] = __ldg(in + i);
+  const int nb = a.H / 128;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) a.xs_t[(size_t)b * a.rows_pad + s] = __ldg(a.xs + (size_t)src * nb + b);
+}
+
+// --------------------------------------------------------------- K9 combine
+// out[t] = sum_j w[t,j] y[inv[t,j]] (local experts only) + y[shared row of t]
+__global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
+  const int t = blockIdx.x;
+  const int n_routed = a.T * a.k;
+  float w[kMaxTopK];
+  int slot[kMaxTopK];
+  for (int j = 0; j < a.k; ++j) {
+    const int e = __ldg(a.ids + (size_t)t * a.k + j);
+    const bool local = e >= a.expert_lo && e < a.expert_hi;
+    w[j] = local ? __ldg(a.weights + (size_t)t * a.k + j) : 0.0f;
+    slot[j] = local ? __ldg(a.inv + (size_t)t * a.k + j) : -1;
+  }
+  const bool sh = a.shared_local && t >= a.shared_lo && t < a.shared_hi;
+  const size_t sh_row = (size_t)n_routed + t;
+  for (int f = threadIdx.x * 4; f < a.H; f += blockDim.x * 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sh) acc = __ldcg(reinterpret_cast<const float4*>(a.y + sh_row * a.H + f));
+    for (int j = 0; j < a.k; ++j) {
+      if (slot[j] < 0) continue;
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(a.y + (size_t)slot[j] * a.H + f));
+      acc.x = fmaf(w[j], v.x, acc.x);
+      acc.y = fmaf(w[j], v.y, acc.y);
+      acc.z = fmaf(w[j], v.z, acc.z);
+      acc.w = fmaf(w[j], v.w, acc.w);
+    }
+    __nv_bfloat162 o0 = __floats2bfloat162_rn(acc.x, acc.y), o1 = __floats2bfloat162_rn(acc.z, acc.w);
+    uint2 o;
+    o.x = *reinterpret_cast<uint32_t*>(&o0);
+    o.y = *reinterpret_cast<uint32_t*>(&o1);
+    *reinterpret_cast<uint2*>(a.out + (size_t)t * a.H + f) = o;
+  }
+}
+
+}  // namespace moe
+
+cudaError_t router_launch(const moe::RouterArgs& a, cudaStream_t stream) {
+  moe::router_kernel<<<(a.T + moe::kRouterTok - 1) / moe::kRouterTok, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream) {
+  moe::permute_kernel<<<1, 1024, (size_t)a.T * a.k, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_launch(const moe::GatherArgs& a, cudaStream_t stream) {
+  moe::gather_kernel<<<a.T * a.k + a.T, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream) {
+  moe::combine_kernel<<<a.T, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace afdk

@@ -1,0 +1,145 @@
+"""MoE FFN path (K5 router + FP8 quant, K6 permute, K7-K9 grouped FP8 GEMMs
++ combine) vs the CPU oracle.
+
+Stated bars:
+  * router top-k ids, expert offsets, permutation and inverse: bit-exact
+    (top-k fed the GPU's own fp32 logits)
+  * router weights: |gpu - oracle| <= 1e-6; logits vs torch fp32: rel <= 1e-5
+  * FP8 dispatch payload (e4m3 codes and fp32 scales): bit-exact
+  * MoE FFN output vs the oracle on the same e4m3 inputs/weights:
+    max|gpu-ref|/max|ref| <= 2e-2 (bf16 output, fp8 re-quantised intermediate)
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests.helpers import rel_err
+
+
+def rand_e4m3(torch, shape, gen, dev):
+    """random finite e4m3 codes (no NaN 0x7f/0xff), |v| <= ~2 for sane sums"""
+    mag = torch.randint(0x18, 0x40, shape, generator=gen, dtype=torch.int32)
+    sign = torch.randint(0, 2, shape, generator=gen, dtype=torch.int32) * 0x80
+    return (mag | sign).to(torch.uint8).to(dev)
+
+
+def make_experts(torch, n_local, H, I, gen, dev, scale=1.0):
+    w13 = rand_e4m3(torch, (n_local + 1, 2 * I, H), gen, dev)
+    w2 = rand_e4m3(torch, (n_local + 1, H, I), gen, dev)
+    s13 = (torch.rand(n_local + 1, 2 * I // 128, H // 128, generator=gen) * 0.5 + 0.5) * scale / H ** 0.5
+    s2 = (torch.rand(n_local + 1, H // 128, I // 128, generator=gen) * 0.5 + 0.5) * scale / I ** 0.5
+    return {"w13": w13, "s13": s13.float().to(dev), "w2": w2, "s2": s2.float().to(dev)}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T", [1, 5, 256])
+def test_router_topk_and_quant(ctx, T):
+    import torch
+
+    H, E, k = 7168, 48, 3
+    g = torch.Generator().manual_seed(T)
+    h = torch.randn(T, H, generator=g).to(torch.bfloat16)
+    gw = (torch.randn(E, H, generator=g) / H ** 0.5).to(torch.bfloat16)
+    gw[9] = gw[5]   # identical gate rows -> identical logits: tie must go to expert 5
+    gw[30] = gw[5]
+    dev = torch.device("cuda:0")
+    hd, gwd = h.to(dev), gw.to(dev)
+    logits = torch.empty(T, E, device=dev)
+    ids = torch.empty(T, k, dtype=torch.int32, device=dev)
+    wts = torch.empty(T, k, device=dev)
+    xq = torch.empty(T, H, dtype=torch.uint8, device=dev)
+    xs = torch.empty(T, H // 128, device=dev)
+    ctx.router_topk(hd, gwd, k, ids, wts, logits=logits, xq=xq, xs=xs)
+    torch.cuda.synchronize()
+    lg = logits.cpu().numpy()
+    assert rel_err(lg, (h.float() @ gw.float().T).numpy()) <= 1e-5
+    rid, rw = orc.router_topk(lg, k)
+    np.testing.assert_array_equal(ids.cpu().numpy(), rid)
+    np.testing.assert_allclose(wts.cpu().numpy(), rw, rtol=0, atol=1e-6)
+    assert np.all(lg[:, 5] == lg[:, 9])
+    qr, sr = orc.quant_fp8_rowblock(h.float().numpy())
+    np.testing.assert_array_equal(xq.cpu().numpy(), qr)
+    np.testing.assert_array_equal(xs.cpu().numpy(), sr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T,k,E", [(1, 3, 48), (7, 3, 48), (256, 3, 48), (4096, 3, 48), (100, 8, 64)])
+def test_permute_bit_exact(ctx, T, k, E):
+    import torch
+
+    rng = np.random.default_rng(T + k)
+    ids = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    if T > 10:
+        ids[: T // 2, 0] = 7  # a hot expert
+        ids[: T // 2, 1:] = np.where(ids[: T // 2, 1:] == 7, (ids[: T // 2, 1:] + 1) % E, ids[: T // 2, 1:])
+    dev = torch.device("cuda:0")
+    idd = torch.from_numpy(ids).to(dev)
+    off = torch.empty(E + 1, dtype=torch.int32, device=dev)
+    perm = torch.empty(T * k, dtype=torch.int32, device=dev)
+    inv = torch.empty(T * k, dtype=torch.int32, device=dev)
+    ctx.moe_permute(idd, E, off, perm, inv)
+    torch.cuda.synchronize()
+    ro, rp, ri = orc.moe_permute(ids, E)
+    np.testing.assert_array_equal(off.cpu().numpy(), ro)
+    np.testing.assert_array_equal(perm.cpu().numpy(), rp)
+    np.testing.assert_array_equal(inv.cpu().numpy(), ri)
+
+
+def run_moe(ctx, T, H, I, E, k, seed, ranges=None):
+    import torch
+
+    g = torch.Generator().manual_seed(seed)
+    dev = torch.device("cuda:0")
+    ex = make_experts(torch, E, H, I, g, dev)
+    x = torch.randn(T, H, generator=g)
+    xq_np, xs_np = orc.quant_fp8_rowblock(x.numpy())
+    logits = torch.randn(T, E, generator=g).numpy()
+    ids_np, w_np = orc.router_topk(logits, k)
+    xq, xs = torch.from_numpy(xq_np).to(dev), torch.from_numpy(xs_np).to(dev)
+    ids, wts = torch.from_numpy(ids_np).to(dev), torch.from_numpy(w_np).to(dev)
+    if ranges is None:
+        out = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+        ctx.moe_ffn(dict(n_experts=E, **ex), xq, xs, ids, wts, out)
+        torch.cuda.synchronize()
+        got = out.float().cpu().numpy()
+    else:  # expert-parallel shards: every rank's partial, summed like the attention side does
+        got = np.zeros((T, H), np.float32)
+        for (lo, hi), (slo, shi) in ranges:
+            sub = {"w13": torch.cat([ex["w13"][lo:hi], ex["w13"][E:]]), "s13": torch.cat([ex["s13"][lo:hi], ex["s13"][E:]]),
+                   "w2": torch.cat([ex["w2"][lo:hi], ex["w2"][E:]]), "s2": torch.cat([ex["s2"][lo:hi], ex["s2"][E:]])}
+            out = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+            ctx.moe_ffn(dict(n_experts=E, **sub), xq, xs, ids, wts, out, expert_lo=lo, expert_hi=hi, shared=(slo, shi))
+            torch.cuda.synchronize()
+            got += out.float().cpu().numpy()
+    ref = orc.moe_layer_fp8(xq_np, xs_np, ids_np, w_np, ex["w13"].cpu().numpy(), ex["s13"].cpu().numpy(),
+                            ex["w2"].cpu().numpy(), ex["s2"].cpu().numpy())
+    return got, ref
+
+
+@pytest.mark.gpu
+def test_moe_ffn_small(ctx):
+    got, ref = run_moe(ctx, 33, 256, 256, 8, 2, 1)
+    assert np.isfinite(got).all()
+    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+
+
+@pytest.mark.gpu
+def test_moe_ffn_step3_dims_reduced_experts(ctx):
+    """hidden 7168 / inter 5120 (Step-3 expert shape), 8 routed + shared, top-3."""
+    got, ref = run_moe(ctx, 40, 7168, 5120, 8, 3, 2)
+    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+
+
+@pytest.mark.gpu
+def test_moe_ffn_many_rows_per_expert(ctx):
+    """> 64 rows for one expert (several GEMM work chunks) and the shared expert over 300 tokens."""
+    got, ref = run_moe(ctx, 300, 256, 384, 4, 2, 3)
+    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+
+
+@pytest.mark.gpu
+def test_moe_ffn_expert_parallel_partials(ctx):
+    """Two EP ranks (experts split, shared expert tokens split) sum to the whole layer."""
+    T = 50
+    got, ref = run_moe(ctx, T, 256, 256, 8, 3, 4, ranges=[((0, 4), (0, 20)), ((4, 8), (20, T))])
+    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)

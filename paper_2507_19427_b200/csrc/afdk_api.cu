@@ -267,7 +267,7 @@ afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_mo
   void* ws = afdk::workspace(c, afdk::moe_ffn_workspace_bytes(a->T, w->top_k, w->n_experts, w->hidden, w->inter));
   if (!ws) { set_error("afdk_moe_ffn: workspace allocation failed"); return AFDK_ERR_CUDA; }
   const cudaError_t e = afdk::moe_ffn_launch(c, m, ws, static_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail("afdk_moe_ffn", e);
+  if (e != cudaSuccess) return AFDK_ERR_CUDA;  // message set by moe_ffn_launch
   return AFDK_OK;
 }
 

@@ -4,6 +4,9 @@
 // reduces EP partials of several FFN ranks).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "afdk_internal.h"
 #include "moe.cuh"
 
@@ -41,20 +44,27 @@ cudaError_t moe_ffn_launch(Ctx& ctx, const MoeFfnArgs& a, void* ws_base, cudaStr
   auto* y = static_cast<float*>(take((size_t)rp * H * 4));
   const bool shared_local = a.shared_hi > a.shared_lo;
   cudaError_t e;
+  // AFDK_DEBUG_SYNC=1: synchronise after every launch and name the failing kernel
+  static const bool dbg = std::getenv("AFDK_DEBUG_SYNC") != nullptr;
+  auto chk = [&](cudaError_t err, const char* what) {
+    if (err == cudaSuccess && dbg) err = cudaStreamSynchronize(stream);
+    if (err != cudaSuccess) set_error(std::string("moe_ffn/") + what + ": " + cudaGetErrorString(err));
+    return err;
+  };
 
   moe::PermuteArgs pa{a.ids, T, k, E, a.expert_lo, a.expert_hi, shared_local ? 1 : 0, a.shared_lo, a.shared_hi,
                       offsets, perm, inv, work, n_work};
-  if ((e = permute_launch(pa, stream)) != cudaSuccess) return e;
+  if ((e = chk(permute_launch(pa, stream), "permute")) != cudaSuccess) return e;
   moe::GatherArgs ga{a.xq, a.xs, perm, T, k, H, rp, xp, xs_t};
-  if ((e = gather_launch(ga, stream)) != cudaSuccess) return e;
+  if ((e = chk(gather_launch(ga, stream), "gather")) != cudaSuccess) return e;
   const int n_local = a.expert_hi - a.expert_lo;
   MoeGemmArgs g13{a.w13, a.s13, xp, xs_t, work, n_work, H, I, E, a.expert_lo, n_local, rp, hq, hs_t, nullptr};
-  if ((e = moe_gemm_launch(ctx, true, g13, stream)) != cudaSuccess) return e;
+  if ((e = chk(moe_gemm_launch(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
   MoeGemmArgs g2{a.w2, a.s2, hq, hs_t, work, n_work, H, I, E, a.expert_lo, n_local, rp, nullptr, nullptr, y};
-  if ((e = moe_gemm_launch(ctx, false, g2, stream)) != cudaSuccess) return e;
+  if ((e = chk(moe_gemm_launch(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
   moe::CombineArgs ca{y, a.ids, a.weights, inv, T, k, H, a.expert_lo, a.expert_hi, shared_local ? 1 : 0,
                       a.shared_lo, a.shared_hi, static_cast<__nv_bfloat16*>(a.out)};
-  return combine_launch(ca, stream);
+  return chk(combine_launch(ca, stream), "combine");
 }
 
 }  // namespace afdk

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "afdk_internal.h"
 #include "moe.cuh"
@@ -53,6 +54,7 @@ struct GemmParams {
   uint8_t* hq;       // GLU out: [rows_pad, I] e4m3
   float* hs_t;       // GLU out: [I/128, rows_pad]
   float* y;          // W2 out:  [rows_pad, H] fp32
+  const float* xs_t;  // [K/128][rows_pad] activation row scales
   int stage_bytes, stages;
 };
 
@@ -67,13 +69,12 @@ __device__ __forceinline__ int weight_index(const GemmParams& p, int group) {
 template <bool kGLU>
 __global__ void __launch_bounds__(kThreads, 1)
 moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                const __grid_constant__ CUtensorMap tm_xs, const GemmParams p) {
+                const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kA = 128 * 128;                 // 16 KB weight panel
   constexpr int kAOps = kGLU ? 2 : 1;
   constexpr int kB = kChunk * 128;              // 8 KB activation panel
-  constexpr int kXsOff = kAOps * kA + kB;       // 64 row scales of this k-block
   const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * p.stage_bytes);
   uint64_t* empty = full + S;
@@ -89,8 +90,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
-    tma_prefetch_desc(&tm_xs);
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1 + 4); }
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < kAccSlots; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
     fence_barrier_init();
   }
@@ -114,11 +114,10 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
           const int s = i % S, n = i / S;
           if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
           uint8_t* st = smem + s * p.stage_bytes;
-          mbar_expect_tx(&full[s], kAOps * kA + kB + kChunk * 4);
+          mbar_expect_tx(&full[s], kAOps * kA + kB);
           tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol_w);
           if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol_w);
           tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, wk.row0, pol_x);
-          tma_load_2d(st + kXsOff, &tm_xs, &full[s], wk.row0, kb, pol_x);
         }
       }
     }
@@ -171,11 +170,16 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
       }
       const int n_ld = (wk.rows + 31) >> 5;  // 32-column TMEM loads needed
       for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
-        const int s = i % S, a = i % kAccSlots, na = i / kAccSlots;
+        const int a = i % kAccSlots, na = i / kAccSlots;
+        // activation row scales of this k-block (uniform across the warp: broadcast loads)
+        float xs[kChunk];
+        {
+          const float* src = p.xs_t + (size_t)kb * p.rows_pad + wk.row0;
+#pragma unroll
+          for (int q = 0; q < kChunk; ++q) xs[q] = (q < wk.rows) ? __ldg(src + q) : 0.0f;
+        }
         mbar_wait(&acc_full[a], na & 1);
-        mbar_wait(&full[s], (i / S) & 1);  // TMA-written row scales visible (already complete)
         tc_fence_after();
-        const float* xs = reinterpret_cast<const float*>(smem + s * p.stage_bytes + kXsOff);
         const float swg = __ldg(sw + (size_t)mt * p.kblocks + kb);
         const float swu = kGLU ? __ldg(sw + (size_t)(mt + p.up_offset / 128) * p.kblocks + kb) : 0.0f;
 #pragma unroll
@@ -196,10 +200,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&acc_empty[a]);
-          mbar_arrive(&empty[s]);
-        }
+        if (lane == 0) mbar_arrive(&acc_empty[a]);
       }
       if (kGLU) {
         // h = SiLU(gate) * up; per dispatched row, quantise the tile's 128
@@ -250,7 +251,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
 // W13 (kGLU) or W2 over the work list built by permute_launch.
 cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream_t stream) {
   using namespace moe;
-  CUtensorMap tw, tx, txs;
+  CUtensorMap tw, tx;
   const int K = glu ? a.H : a.I;
   const int w_rows = glu ? 2 * a.I : a.H;
   {
@@ -269,14 +270,6 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
                     CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
-  {
-    const uint64_t dims[2] = {(uint64_t)a.rows_pad, (uint64_t)(K / 128)};
-    const uint64_t strides[1] = {(uint64_t)a.rows_pad * 4};
-    const uint32_t box[2] = {kChunk, 1};
-    if (!encode_tma(ctx, &txs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.xs_t), dims, strides, box,
-                    CU_TENSOR_MAP_SWIZZLE_NONE))
-      return cudaErrorInvalidValue;
-  }
   GemmParams p{};
   p.work = a.work;
   p.n_work = a.n_work;
@@ -293,8 +286,9 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
   p.hq = a.hq;
   p.hs_t = a.hs_t;
   p.y = a.y;
+  p.xs_t = a.xs_t;
   const int a_bytes = (glu ? 2 : 1) * 128 * 128;
-  p.stage_bytes = (int)align_up((size_t)a_bytes + kChunk * 128 + kChunk * 4, 1024);
+  p.stage_bytes = (int)align_up((size_t)a_bytes + kChunk * 128, 1024);
   p.stages = (200 * 1024) / p.stage_bytes;
   if (p.stages > 8) p.stages = 8;
   const size_t smem = (size_t)p.stages * p.stage_bytes + 1024 + 512;
@@ -306,7 +300,7 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
         return e;
       attr = smem;
     }
-    moe_gemm_kernel<true><<<ctx.num_sms, kThreads, smem, stream>>>(tw, tx, txs, p);
+    moe_gemm_kernel<true><<<ctx.num_sms, kThreads, smem, stream>>>(tw, tx, p);
   } else {
     static size_t attr = 0;
     if (smem > attr) {
@@ -314,7 +308,7 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
         return e;
       attr = smem;
     }
-    moe_gemm_kernel<false><<<ctx.num_sms, kThreads, smem, stream>>>(tw, tx, txs, p);
+    moe_gemm_kernel<false><<<ctx.num_sms, kThreads, smem, stream>>>(tw, tx, p);
   }
   return cudaGetLastError();
 }

@@ -39,6 +39,7 @@ def parse():
     p.add_argument("--batch", type=int, default=BATCH)
     p.add_argument("--ctx", type=int, default=CTX)
     p.add_argument("--workload", default="layer", choices=["layer", "attn"])
+    p.add_argument("--no-moe", action="store_true", help="skip the config-3 MoE FFN sub-measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -131,6 +132,67 @@ def make_workload(torch, dev, batch, ctx_len, seed=0):
     s["h_res"] = torch.empty(batch, HIDDEN, dtype=torch.bfloat16, device=dev)
     s["h_norm"] = torch.empty(batch, HIDDEN, dtype=torch.bfloat16, device=dev)
     return s
+
+
+# ------------------------------------------------- config 3: MoE FFN layer
+E_ROUTED, TOPK, INTER = 48, 3, 5120
+
+
+def moe_weight_bytes(n_experts):
+    return n_experts * (3 * HIDDEN * INTER + 4 * (2 * INTER // 128 * HIDDEN // 128 + HIDDEN // 128 * INTER // 128))
+
+
+def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0):
+    """One FFN-side MoE layer (permute, gather, W13+SwiGLU+requant, W2, combine)
+    over T dispatched tokens, all 48 routed experts + the shared one on this GPU."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    n = E_ROUTED + 1
+
+    def e4m3(shape):
+        mag = torch.randint(0x18, 0x40, shape, dtype=torch.int32, device=dev)
+        sgn = torch.randint(0, 2, shape, dtype=torch.int32, device=dev) * 0x80
+        return (mag | sgn).to(torch.uint8)
+
+    w = {"n_experts": E_ROUTED,
+         "w13": e4m3((n, 2 * INTER, HIDDEN)), "w2": e4m3((n, HIDDEN, INTER)),
+         "s13": torch.full((n, 2 * INTER // 128, HIDDEN // 128), 0.5 / HIDDEN ** 0.5, device=dev),
+         "s2": torch.full((n, HIDDEN // 128, INTER // 128), 0.5 / INTER ** 0.5, device=dev)}
+    xq = e4m3((T, HIDDEN))
+    xs = torch.full((T, HIDDEN // 128), 0.01, device=dev)
+    logits = torch.randn(T, E_ROUTED, generator=g).to(dev)
+    top = torch.topk(logits, TOPK, dim=1)
+    ids = top.indices.to(torch.int32).contiguous()
+    wts = torch.softmax(logits, dim=1).gather(1, top.indices).contiguous()
+    out = torch.empty(T, HIDDEN, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step(i):
+        ctx.moe_ffn(w, xq, xs, ids, wts, out, stream=sp)
+
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(steps):
+        step(i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    touched = len(set(ids.flatten().tolist())) + 1
+    wbytes = moe_weight_bytes(touched)
+    flops = 2.0 * 3 * HIDDEN * INTER * (TOPK + 1) * T
+    hbm_peak, tf_peak, kind = peaks()
+    del w
+    return {"T": T, "ms_per_layer": ms, "tokens_per_s": T / (ms * 1e-3),
+            "hbm": {"achieved": wbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": wbytes / (ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": wbytes,
+                    "experts_touched": touched},
+            "tensor": {"achieved": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                       "peak": 2 * tf_peak, "peak_kind": f"fp8 = 2 x {kind} bf16 cuBLAS",
+                       "frac": flops / (ms * 1e-3) / 1e12 / (2 * tf_peak)},
+            "gpu_launches_per_layer": 5}
 
 
 # ------------------------------------------------- CPU port (oracle) legs
@@ -272,6 +334,10 @@ def main():
     e2e_ms = timed(e2e_step, args.steps)
     e2e_value = world * args.batch / (e2e_ms * 1e-3)
 
+    moe = None
+    if not args.no_moe:
+        moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=rank) for T in (256, 4096)]
+
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -302,6 +368,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "tokens/s",
                     "h2d_bytes_per_step": in_host.numel() * in_host.element_size(),
                     "d2h_bytes_per_step": out_host.numel() * out_host.element_size()},
+            "moe_ffn": moe,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }

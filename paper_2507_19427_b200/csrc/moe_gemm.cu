@@ -76,7 +76,8 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
   constexpr int kAOps = kGLU ? 2 : 1;
   constexpr int kB = kChunk * 128;              // 8 KB activation panel
   const int S = p.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * p.stage_bytes);
+  float* xs_ring = reinterpret_cast<float*>(smem + S * p.stage_bytes);  // [S][kChunk] row scales
+  uint64_t* full = reinterpret_cast<uint64_t*>(xs_ring + S * kChunk);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;
   uint64_t* acc_empty = acc_full + kAccSlots;
@@ -90,7 +91,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1 + 32); mbar_init(&empty[i], 1 + 4); }
     for (int i = 0; i < kAccSlots; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
     fence_barrier_init();
   }
@@ -102,23 +103,31 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
   const int n_work = *p.n_work;
 
   if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
-      int i = 0;
-      for (int it = cta; it < n_items; it += G) {
-        const int mt = it / n_work, gc = it % n_work;
-        const Work wk = p.work[gc];
-        const int wrow = weight_index(p, wk.group) * p.w_rows + mt * 128;
-        for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
-          const int s = i % S, n = i / S;
-          if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
-          uint8_t* st = smem + s * p.stage_bytes;
+    // whole warp: lane 0 issues the TMA loads, every lane stages two of the
+    // chunk's activation row scales for this k-block into the stage (plain
+    // loads: dispatch rows start at arbitrary offsets) and arrives on full[s]
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    int i = 0;
+    for (int it = cta; it < n_items; it += G) {
+      const int mt = it / n_work, gc = it % n_work;
+      const Work wk = p.work[gc];
+      const int wrow = weight_index(p, wk.group) * p.w_rows + mt * 128;
+      for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
+        const int s = i % S, n = i / S;
+        if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
+        uint8_t* st = smem + s * p.stage_bytes;
+        if (lane == 0) {
           mbar_expect_tx(&full[s], kAOps * kA + kB);
           tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol_w);
           if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol_w);
           tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, wk.row0, pol_x);
         }
+        const float* src = p.xs_t + (size_t)kb * p.rows_pad + wk.row0;
+        float* dst = xs_ring + s * kChunk;
+        dst[lane] = (lane < wk.rows) ? __ldg(src + lane) : 0.0f;
+        dst[lane + 32] = (lane + 32 < wk.rows) ? __ldg(src + lane + 32) : 0.0f;
+        mbar_arrive(&full[s]);
       }
     }
   } else if (warp == 1) {
@@ -171,15 +180,11 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
       const int n_ld = (wk.rows + 31) >> 5;  // 32-column TMEM loads needed
       for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
         const int a = i % kAccSlots, na = i / kAccSlots;
-        // activation row scales of this k-block (uniform across the warp: broadcast loads)
-        float xs[kChunk];
-        {
-          const float* src = p.xs_t + (size_t)kb * p.rows_pad + wk.row0;
-#pragma unroll
-          for (int q = 0; q < kChunk; ++q) xs[q] = (q < wk.rows) ? __ldg(src + q) : 0.0f;
-        }
+        const int s = i % S;
         mbar_wait(&acc_full[a], na & 1);
+        mbar_wait(&full[s], (i / S) & 1);  // row scales staged (complete; stage held until we arrive)
         tc_fence_after();
+        const float* xs = xs_ring + s * kChunk;
         const float swg = __ldg(sw + (size_t)mt * p.kblocks + kb);
         const float swu = kGLU ? __ldg(sw + (size_t)(mt + p.up_offset / 128) * p.kblocks + kb) : 0.0f;
 #pragma unroll
@@ -200,7 +205,10 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[a]);
+        if (lane == 0) {
+          mbar_arrive(&acc_empty[a]);
+          mbar_arrive(&empty[s]);
+        }
       }
       if (kGLU) {
         // h = SiLU(gate) * up; per dispatched row, quantise the tile's 128
@@ -291,7 +299,7 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
   p.stage_bytes = (int)align_up((size_t)a_bytes + kChunk * 128, 1024);
   p.stages = (200 * 1024) / p.stage_bytes;
   if (p.stages > 8) p.stages = 8;
-  const size_t smem = (size_t)p.stages * p.stage_bytes + 1024 + 512;
+  const size_t smem = (size_t)p.stages * (p.stage_bytes + kChunk * 4) + 1024 + 512;
   cudaError_t e;
   if (glu) {
     static size_t attr = 0;

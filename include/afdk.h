@@ -182,6 +182,28 @@ typedef struct afdk_moe_args {
 
 afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a, afdk_stream stream);
 
+/* ------------------------------------------- C1/C2 AFD exchange (NVLink)
+ * Zero-SM point-to-point transport between attention and FFN GPUs of one
+ * box (the StepMesh pattern of PAPER.md:701-724 on NVLink 5 / NVSwitch):
+ * buffers are registered once through CUDA IPC, data moves as copy-engine
+ * DMA (afdk_copy: cudaMemcpyAsync on the stream; src/dst may be peer-mapped),
+ * readiness travels as monotonically increasing 32-bit sequence flags
+ * (afdk_signal writes a flag word, typically on a peer, after all prior work
+ * of the stream; afdk_wait blocks the stream until a local flag >= value).
+ * Together they carry ffn_net_bytes = (dispatch+combine)*H*T per layer
+ * (moeplan.cpp:17-20).  IPC handles are 64 opaque bytes.                 */
+afdk_status afdk_ipc_handle(afdk_ctx* ctx, const void* dev_ptr, void* handle64);
+afdk_status afdk_ipc_open(afdk_ctx* ctx, const void* handle64, void** dev_ptr);
+afdk_status afdk_ipc_close(afdk_ctx* ctx, void* dev_ptr);
+afdk_status afdk_copy(afdk_ctx* ctx, void* dst, const void* src, size_t bytes, afdk_stream stream);
+afdk_status afdk_signal(afdk_ctx* ctx, uint32_t* flag, uint32_t value, afdk_stream stream);
+afdk_status afdk_wait(afdk_ctx* ctx, const uint32_t* flag, uint32_t value, afdk_stream stream);
+/* EP reduction on the attention side: out = base + sum_i parts[i] (bf16, fp32
+ * sum in index order); parts_dev is a DEVICE array of n device pointers;
+ * base may be NULL; count % 8 == 0.                                        */
+afdk_status afdk_add_partials(afdk_ctx* ctx, const void* base, const void* const* parts_dev, int n, size_t count,
+                              void* out, afdk_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,6 +88,13 @@ SIGNATURES = {
                                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_permute": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_ffn": (c_int, [c_void_p, POINTER(MoeWeights), POINTER(MoeArgs), c_void_p]),
+    "afdk_ipc_handle": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "afdk_ipc_open": (c_int, [c_void_p, c_void_p, POINTER(c_void_p)]),
+    "afdk_ipc_close": (c_int, [c_void_p, c_void_p]),
+    "afdk_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "afdk_signal": (c_int, [c_void_p, c_void_p, ctypes.c_uint32, c_void_p]),
+    "afdk_wait": (c_int, [c_void_p, c_void_p, ctypes.c_uint32, c_void_p]),
+    "afdk_add_partials": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_size_t, c_void_p, c_void_p]),
 }
 
 _lib = None
@@ -200,3 +207,30 @@ class Context:
         mw = MoeWeights(Hd, inter, E, k, expert_lo, hi, ptr(w["w13"]), ptr(w["s13"]), ptr(w["w2"]), ptr(w["s2"]))
         a = MoeArgs(T, ptr(xq), ptr(xs), ptr(ids), ptr(weights), sh_lo, sh_hi, ptr(out))
         check(self.lib.afdk_moe_ffn(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+
+    # ------------------------------------------------------- C1/C2 exchange
+    def ipc_handle(self, t) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        check(self.lib.afdk_ipc_handle(self.handle, ptr(t), buf))
+        return buf.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        out = c_void_p()
+        check(self.lib.afdk_ipc_open(self.handle, ctypes.create_string_buffer(handle, 64), ctypes.byref(out)))
+        return out.value
+
+    def ipc_close(self, dev_ptr: int) -> None:
+        check(self.lib.afdk_ipc_close(self.handle, c_void_p(dev_ptr)))
+
+    def copy(self, dst: int, src: int, nbytes: int, stream: int = 0) -> None:
+        check(self.lib.afdk_copy(self.handle, c_void_p(dst), c_void_p(src), nbytes, c_void_p(stream)))
+
+    def signal(self, flag_ptr: int, value: int, stream: int = 0) -> None:
+        check(self.lib.afdk_signal(self.handle, c_void_p(flag_ptr), value, c_void_p(stream)))
+
+    def wait(self, flag_ptr: int, value: int, stream: int = 0) -> None:
+        check(self.lib.afdk_wait(self.handle, c_void_p(flag_ptr), value, c_void_p(stream)))
+
+    def add_partials(self, base, parts_dev, n: int, out, stream: int = 0) -> None:
+        check(self.lib.afdk_add_partials(self.handle, ptr(base), ptr(parts_dev), n, out.numel(), ptr(out),
+                                         c_void_p(stream)))

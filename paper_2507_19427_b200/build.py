@@ -24,6 +24,7 @@ CU_SOURCES = [
     "moe_route.cu",
     "moe_gemm.cu",
     "moe_ffn.cu",
+    "exchange.cu",
 ]
 CXX_SOURCES: list[str] = []
 

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstring>
 #include <string>
 
 #include "../../include/afdk.h"
@@ -268,6 +269,65 @@ afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_mo
   if (!ws) { set_error("afdk_moe_ffn: workspace allocation failed"); return AFDK_ERR_CUDA; }
   const cudaError_t e = afdk::moe_ffn_launch(c, m, ws, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return AFDK_ERR_CUDA;  // message set by moe_ffn_launch
+  return AFDK_OK;
+}
+
+afdk_status afdk_ipc_handle(afdk_ctx* ctx, const void* dev_ptr, void* handle64) {
+  if (!ctx || !dev_ptr || !handle64) { set_error("afdk_ipc_handle: NULL argument"); return AFDK_ERR_INVALID; }
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
+  cudaSetDevice(ctx->c.device);
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  if (e != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle", e);
+  std::memcpy(handle64, &h, 64);
+  return AFDK_OK;
+}
+
+afdk_status afdk_ipc_open(afdk_ctx* ctx, const void* handle64, void** dev_ptr) {
+  if (!ctx || !handle64 || !dev_ptr) { set_error("afdk_ipc_open: NULL argument"); return AFDK_ERR_INVALID; }
+  cudaSetDevice(ctx->c.device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail("cudaIpcOpenMemHandle", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_ipc_close(afdk_ctx* ctx, void* dev_ptr) {
+  if (!ctx || !dev_ptr) { set_error("afdk_ipc_close: NULL argument"); return AFDK_ERR_INVALID; }
+  cudaSetDevice(ctx->c.device);
+  const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail("cudaIpcCloseMemHandle", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_copy(afdk_ctx* ctx, void* dst, const void* src, size_t bytes, afdk_stream stream) {
+  if (!ctx || !dst || !src) { set_error("afdk_copy: NULL argument"); return AFDK_ERR_INVALID; }
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("afdk_copy", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_signal(afdk_ctx* ctx, uint32_t* flag, uint32_t value, afdk_stream stream) {
+  if (!ctx || !flag) { set_error("afdk_signal: NULL argument"); return AFDK_ERR_INVALID; }
+  const cudaError_t e = afdk::exchange_signal(flag, value, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("afdk_signal (cuStreamWriteValue32)", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_wait(afdk_ctx* ctx, const uint32_t* flag, uint32_t value, afdk_stream stream) {
+  if (!ctx || !flag) { set_error("afdk_wait: NULL argument"); return AFDK_ERR_INVALID; }
+  const cudaError_t e = afdk::exchange_wait(flag, value, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("afdk_wait (cuStreamWaitValue32)", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_add_partials(afdk_ctx* ctx, const void* base, const void* const* parts_dev, int n, size_t count,
+                              void* out, afdk_stream stream) {
+  if (!ctx || !out || (n > 0 && !parts_dev) || n < 0) { set_error("afdk_add_partials: bad argument"); return AFDK_ERR_INVALID; }
+  if (count % 8) { set_error("afdk_add_partials: count must be a multiple of 8"); return AFDK_ERR_INVALID; }
+  const cudaError_t e = afdk::add_partials_launch(base, parts_dev, n, count, out, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("afdk_add_partials", e);
   return AFDK_OK;
 }
 

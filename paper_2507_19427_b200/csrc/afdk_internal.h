@@ -127,4 +127,11 @@ struct MoeFfnArgs {
 size_t moe_ffn_workspace_bytes(int T, int k, int E, int H, int I);
 cudaError_t moe_ffn_launch(Ctx& ctx, const MoeFfnArgs& a, void* ws, cudaStream_t stream);
 
+// ---------------------------------------------------------- AFD exchange
+bool exchange_available();
+cudaError_t exchange_signal(uint32_t* flag, uint32_t value, cudaStream_t s);
+cudaError_t exchange_wait(const uint32_t* flag, uint32_t value, cudaStream_t s);
+cudaError_t add_partials_launch(const void* base, const void* const* parts_dev, int n, size_t count, void* out,
+                                cudaStream_t s);
+
 }  // namespace afdk

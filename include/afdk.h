@@ -191,9 +191,11 @@ afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_mo
  * (afdk_signal writes a flag word, typically on a peer, after all prior work
  * of the stream; afdk_wait blocks the stream until a local flag >= value).
  * Together they carry ffn_net_bytes = (dispatch+combine)*H*T per layer
- * (moeplan.cpp:17-20).  IPC handles are 64 opaque bytes.                 */
-afdk_status afdk_ipc_handle(afdk_ctx* ctx, const void* dev_ptr, void* handle64);
-afdk_status afdk_ipc_open(afdk_ctx* ctx, const void* handle64, void** dev_ptr);
+ * (moeplan.cpp:17-20).  IPC handles are 72 opaque bytes (the allocation's
+ * CUDA IPC handle + the pointer's offset inside it); afdk_ipc_close takes
+ * the pointer afdk_ipc_open returned.                                      */
+afdk_status afdk_ipc_handle(afdk_ctx* ctx, const void* dev_ptr, void* handle72);
+afdk_status afdk_ipc_open(afdk_ctx* ctx, const void* handle72, void** dev_ptr);
 afdk_status afdk_ipc_close(afdk_ctx* ctx, void* dev_ptr);
 afdk_status afdk_copy(afdk_ctx* ctx, void* dst, const void* src, size_t bytes, afdk_stream stream);
 afdk_status afdk_signal(afdk_ctx* ctx, uint32_t* flag, uint32_t value, afdk_stream stream);

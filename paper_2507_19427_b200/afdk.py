@@ -210,13 +210,13 @@ class Context:
 
     # ------------------------------------------------------- C1/C2 exchange
     def ipc_handle(self, t) -> bytes:
-        buf = ctypes.create_string_buffer(64)
+        buf = ctypes.create_string_buffer(72)
         check(self.lib.afdk_ipc_handle(self.handle, ptr(t), buf))
         return buf.raw
 
     def ipc_open(self, handle: bytes) -> int:
         out = c_void_p()
-        check(self.lib.afdk_ipc_open(self.handle, ctypes.create_string_buffer(handle, 64), ctypes.byref(out)))
+        check(self.lib.afdk_ipc_open(self.handle, ctypes.create_string_buffer(handle, 72), ctypes.byref(out)))
         return out.value
 
     def ipc_close(self, dev_ptr: int) -> None:

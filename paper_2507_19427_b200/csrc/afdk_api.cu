@@ -272,31 +272,63 @@ afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_mo
   return AFDK_OK;
 }
 
-afdk_status afdk_ipc_handle(afdk_ctx* ctx, const void* dev_ptr, void* handle64) {
-  if (!ctx || !dev_ptr || !handle64) { set_error("afdk_ipc_handle: NULL argument"); return AFDK_ERR_INVALID; }
+// The handle names the whole allocation containing dev_ptr (allocators
+// sub-allocate); bytes [64,72) carry dev_ptr's offset from that base.
+afdk_status afdk_ipc_handle(afdk_ctx* ctx, const void* dev_ptr, void* handle72) {
+  if (!ctx || !dev_ptr || !handle72) { set_error("afdk_ipc_handle: NULL argument"); return AFDK_ERR_INVALID; }
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
+  using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      set_error("afdk_ipc_handle: cuMemGetAddressRange unavailable");
+      return AFDK_ERR_CUDA;
+    }
+    range = reinterpret_cast<RangeFn>(fn);
+  }
   cudaSetDevice(ctx->c.device);
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) {
+    set_error("afdk_ipc_handle: pointer is not a device allocation");
+    return AFDK_ERR_INVALID;
+  }
   cudaIpcMemHandle_t h;
-  const cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  const cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
   if (e != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle", e);
-  std::memcpy(handle64, &h, 64);
+  const uint64_t off = reinterpret_cast<uint64_t>(dev_ptr) - static_cast<uint64_t>(base);
+  std::memcpy(handle72, &h, 64);
+  std::memcpy(static_cast<uint8_t*>(handle72) + 64, &off, 8);
   return AFDK_OK;
 }
 
-afdk_status afdk_ipc_open(afdk_ctx* ctx, const void* handle64, void** dev_ptr) {
-  if (!ctx || !handle64 || !dev_ptr) { set_error("afdk_ipc_open: NULL argument"); return AFDK_ERR_INVALID; }
+afdk_status afdk_ipc_open(afdk_ctx* ctx, const void* handle72, void** dev_ptr) {
+  if (!ctx || !handle72 || !dev_ptr) { set_error("afdk_ipc_open: NULL argument"); return AFDK_ERR_INVALID; }
   cudaSetDevice(ctx->c.device);
   cudaIpcMemHandle_t h;
-  std::memcpy(&h, handle64, 64);
-  const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  uint64_t off = 0;
+  std::memcpy(&h, handle72, 64);
+  std::memcpy(&off, static_cast<const uint8_t*>(handle72) + 64, 8);
+  void* base = nullptr;
+  const cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return cuda_fail("cudaIpcOpenMemHandle", e);
+  *dev_ptr = static_cast<uint8_t*>(base) + off;
   return AFDK_OK;
 }
 
 afdk_status afdk_ipc_close(afdk_ctx* ctx, void* dev_ptr) {
   if (!ctx || !dev_ptr) { set_error("afdk_ipc_close: NULL argument"); return AFDK_ERR_INVALID; }
   cudaSetDevice(ctx->c.device);
-  const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUdeviceptr base = reinterpret_cast<CUdeviceptr>(dev_ptr);
+  size_t size = 0;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess && fn)
+    reinterpret_cast<RangeFn>(fn)(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr));
+  const cudaError_t e = cudaIpcCloseMemHandle(reinterpret_cast<void*>(base));
   if (e != cudaSuccess) return cuda_fail("cudaIpcCloseMemHandle", e);
   return AFDK_OK;
 }

@@ -89,6 +89,13 @@ def main():
                 torch.cuda.synchronize()
                 ref = (h_res.float() + part.float())
                 errs.append(rel_err(r.x[mb].float().cpu().numpy(), ref.cpu().numpy()))
+                L = r.lay
+                sb = r.send[mb]
+                sent_xq = sb[L.off["xq"]:L.off["xq"] + L.size("xq")].view(c.T_mb, c.hidden)
+                sent_ids = sb[L.off["ids"]:L.off["ids"] + L.size("ids")].view(torch.int32).view(c.T_mb, c.top_k)
+                print("mb", mb, "x err", errs[-1], "h_res err", rel_err(r.h_res[mb].float().cpu().numpy(), h_res.float().cpu().numpy()),
+                      "part err", rel_err(r.recv_part[mb][0].float().cpu().numpy(), part.float().cpu().numpy()),
+                      "xq eq", bool(torch.equal(sent_xq, xq)), "ids eq", bool(torch.equal(sent_ids, ids)), flush=True)
             ok = max(errs) <= 2e-2
             print(json.dumps({"afd_check": "ok" if ok else "FAIL", "rel_err": errs, "world": world,
                               "n_attn": cfg.n_attn}), flush=True)

@@ -206,6 +206,54 @@ afdk_status afdk_wait(afdk_ctx* ctx, const uint32_t* flag, uint32_t value, afdk_
 afdk_status afdk_add_partials(afdk_ctx* ctx, const void* base, const void* const* parts_dev, int n, size_t count,
                               void* out, afdk_stream stream);
 
+/* ------------------------------------------------ measured stage times
+ * The measured counterpart of derive_stage_times (pipesim.cpp:59-127): runs
+ * one attention-tier layer (afdk_mfa_layer + router/dispatch) at
+ * ceil(micro_batch / attn_gpus) requests and avg_ctx tokens, one FFN-tier MoE
+ * layer (48/ffn_gpus local experts + the shared expert's token share) and one
+ * dense FFN layer at micro_batch tokens, and the NVLink transfers, then fills
+ * per-layer seconds for n_layers Step-3 layers (layers 0-3 and n_layers-1
+ * dense, builtin_catalog.cpp:248-250).  link_gbs <= 0 measures a peer copy
+ * when a second GPU is visible, else uses the pool's measured 770 GB/s.   */
+typedef struct afdk_stage_plan {
+  int attn_gpus, ffn_gpus;
+  long long micro_batch;
+  long long avg_ctx;
+  int n_layers;
+  int hidden;
+  double link_gbs;
+} afdk_stage_plan;
+
+typedef struct afdk_layer_times {
+  double attn_s, moe_ffn_s, dense_ffn_s, comm_fwd_s, comm_bwd_s, link_gbs;
+  long long attn_batch, ffn_tokens;
+  int local_experts, link_measured;
+} afdk_layer_times;
+
+afdk_status afdk_measure_stage_times(afdk_ctx* ctx, const afdk_stage_plan* plan, double* attn, double* comm_fwd,
+                                     double* ffn, double* comm_bwd, afdk_layer_times* detail);
+
+/* ------------------------------------------------- pipeline model (host)
+ * simulate() of pipesim.cpp:155-237 evaluated on any StageTimes (typically
+ * measured ones): tpot, tgs = total_batch / (tpot * total_gpus), per-resource
+ * utilisation and bubbles (attention, fwd link, ffn, bwd link).  CPU only. */
+typedef struct afdk_sim_plan {
+  int n_micro;
+  long long total_batch;
+  int total_gpus;
+  int token_steps;
+  int shared_link;
+} afdk_sim_plan;
+
+typedef struct afdk_sim_result {
+  double tpot, tgs;
+  double utilization[4];
+  double bubble_fraction[4];
+} afdk_sim_result;
+
+afdk_status afdk_simulate(const double* attn, const double* comm_fwd, const double* ffn, const double* comm_bwd,
+                          int layers, const afdk_sim_plan* plan, afdk_sim_result* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,28 @@ class MoeArgs(Structure):
     ]
 
 
+class StagePlan(Structure):
+    _fields_ = [("attn_gpus", c_int), ("ffn_gpus", c_int), ("micro_batch", ctypes.c_longlong),
+                ("avg_ctx", ctypes.c_longlong), ("n_layers", c_int), ("hidden", c_int), ("link_gbs", ctypes.c_double)]
+
+
+class LayerTimes(Structure):
+    _fields_ = [("attn_s", ctypes.c_double), ("moe_ffn_s", ctypes.c_double), ("dense_ffn_s", ctypes.c_double),
+                ("comm_fwd_s", ctypes.c_double), ("comm_bwd_s", ctypes.c_double), ("link_gbs", ctypes.c_double),
+                ("attn_batch", ctypes.c_longlong), ("ffn_tokens", ctypes.c_longlong), ("local_experts", c_int),
+                ("link_measured", c_int)]
+
+
+class SimPlan(Structure):
+    _fields_ = [("n_micro", c_int), ("total_batch", ctypes.c_longlong), ("total_gpus", c_int),
+                ("token_steps", c_int), ("shared_link", c_int)]
+
+
+class SimResult(Structure):
+    _fields_ = [("tpot", ctypes.c_double), ("tgs", ctypes.c_double), ("utilization", ctypes.c_double * 4),
+                ("bubble_fraction", ctypes.c_double * 4)]
+
+
 # exported symbol -> (restype, argtypes); the CPU test checks every symbol of
 # include/afdk.h is present in the built library
 SIGNATURES = {
@@ -95,6 +117,9 @@ SIGNATURES = {
     "afdk_signal": (c_int, [c_void_p, c_void_p, ctypes.c_uint32, c_void_p]),
     "afdk_wait": (c_int, [c_void_p, c_void_p, ctypes.c_uint32, c_void_p]),
     "afdk_add_partials": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_size_t, c_void_p, c_void_p]),
+    "afdk_measure_stage_times": (c_int, [c_void_p, POINTER(StagePlan), c_void_p, c_void_p, c_void_p, c_void_p,
+                                         POINTER(LayerTimes)]),
+    "afdk_simulate": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, POINTER(SimPlan), POINTER(SimResult)]),
 }
 
 _lib = None
@@ -123,6 +148,17 @@ def check(status: int) -> None:
 def ptr(t) -> int:
     """Raw device pointer of a torch tensor (None -> NULL)."""
     return 0 if t is None else int(t.data_ptr())
+
+
+def simulate(attn, fwd, ffn, bwd, n_micro, total_batch, total_gpus, token_steps=3, shared_link=False) -> dict:
+    """Pipeline model (pipesim.cpp:155-237 semantics) on given per-layer stage times; CPU only."""
+    L = len(attn)
+    arrs = [(ctypes.c_double * L)(*map(float, v)) for v in (attn, fwd, ffn, bwd)]
+    out = SimResult()
+    check(load().afdk_simulate(*[ctypes.cast(a, c_void_p) for a in arrs], L,
+                               ctypes.byref(SimPlan(n_micro, total_batch, total_gpus, token_steps, int(shared_link))),
+                               ctypes.byref(out)))
+    return dict(tpot=out.tpot, tgs=out.tgs, utilization=list(out.utilization), bubble=list(out.bubble_fraction))
 
 
 class Context:
@@ -234,3 +270,17 @@ class Context:
     def add_partials(self, base, parts_dev, n: int, out, stream: int = 0) -> None:
         check(self.lib.afdk_add_partials(self.handle, ptr(base), ptr(parts_dev), n, out.numel(), ptr(out),
                                          c_void_p(stream)))
+
+    # -------------------------------------------------- measured stage times
+    def measure_stage_times(self, attn_gpus, ffn_gpus, micro_batch, avg_ctx, n_layers=61, hidden=7168,
+                            link_gbs=0.0) -> dict:
+        L = n_layers
+        arrs = [(ctypes.c_double * L)() for _ in range(4)]
+        det = LayerTimes()
+        check(self.lib.afdk_measure_stage_times(
+            self.handle, ctypes.byref(StagePlan(attn_gpus, ffn_gpus, micro_batch, avg_ctx, L, hidden, link_gbs)),
+            *[ctypes.cast(a, c_void_p) for a in arrs], ctypes.byref(det)))
+        names = ["attn", "comm_fwd", "ffn", "comm_bwd"]
+        res = {n: list(a) for n, a in zip(names, arrs)}
+        res["detail"] = {f: getattr(det, f) for f, _ in LayerTimes._fields_}
+        return res

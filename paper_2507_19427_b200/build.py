@@ -25,6 +25,8 @@ CU_SOURCES = [
     "moe_gemm.cu",
     "moe_ffn.cu",
     "exchange.cu",
+    "afd_measured.cu",
+    "pipeline_model.cpp",
 ]
 CXX_SOURCES: list[str] = []
 
@@ -50,7 +52,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objdir = os.path.join(HERE, "_obj")
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh", ".hpp"))]
-    headers.append(os.path.join(ROOT, "include", "afdk.h"))
+    headers += [os.path.join(ROOT, "include", h) for h in ("afdk.h", "afd_b200.hpp", "afd_compat.hpp")]
     objs = []
     for src in CU_SOURCES + CXX_SOURCES:
         path = os.path.join(CSRC, src)
@@ -70,7 +72,25 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if res.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
             raise RuntimeError("link failed")
+    build_demo(force)
     return OUT
+
+
+DEMO_SRC = os.path.join(ROOT, "tests", "cpp", "stage_times_demo.cpp")
+DEMO_OUT = os.path.join(ROOT, "tests", "cpp", "stage_times_demo")
+
+
+def build_demo(force: bool = False) -> str:
+    """C++ consumer of the host API (afd_b200.hpp), linked against libafdk.so."""
+    deps = [DEMO_SRC, OUT, os.path.join(ROOT, "include", "afd_b200.hpp")]
+    if force or _stale(DEMO_OUT, deps):
+        cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), DEMO_SRC, "-o", DEMO_OUT,
+               "-L", HERE, "-lafdk", f"-Wl,-rpath,{HERE}", "-Wl,-rpath,$ORIGIN/../../paper_2507_19427_b200"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+            raise RuntimeError("demo build failed")
+    return DEMO_OUT
 
 
 if __name__ == "__main__":

@@ -125,7 +125,6 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   int32_t* prefix = reinterpret_cast<int32_t*>(&sm + 1);  // [B+1] after the Smem block
-  __shared__ int s_scan[kThreads];
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;

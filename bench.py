@@ -40,6 +40,7 @@ def parse():
     p.add_argument("--ctx", type=int, default=CTX)
     p.add_argument("--workload", default="layer", choices=["layer", "attn"])
     p.add_argument("--no-moe", action="store_true", help="skip the config-3 MoE FFN sub-measurement")
+    p.add_argument("--no-afd", action="store_true", help="skip the config-5 AFD measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -195,6 +196,80 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0):
             "gpu_launches_per_layer": 5}
 
 
+# --------------------------------------------- config 5: AFD layer pipeline
+def afd_roles(world):
+    """2A6F at 8 GPUs (config 5); the same 1:3 attention:FFN ratio below it."""
+    return {2: (1, 1), 3: (1, 2), 4: (1, 3), 8: (2, 6)}.get(world, (max(1, world // 4), world - max(1, world // 4)))
+
+
+def run_afd_measured(torch, dist, dev, world, rank, local, steps):
+    """Real pipeline on all ranks: nA attention GPUs + nF FFN GPUs, 2 ping-pong
+    micro-batches, 2 layers per step (distinct KV caches), copy-engine NVLink."""
+    from paper_2507_19427_b200 import Context
+    from paper_2507_19427_b200.afd import AfdConfig, AfdRank, wire_bytes
+
+    na, nf = afd_roles(world)
+    cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=192, n_micro=2, layers=2, ctx_len=CTX)
+    ctxs = [Context(local) for _ in range(cfg.n_micro)]
+    r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
+    r.setup()
+
+    def run(n):
+        dist.barrier()
+        torch.cuda.synchronize()
+        start = torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        start.record(cur)
+        for st in r.streams_all():
+            st.wait_event(start)
+        for _ in range(n):
+            r.step()
+        for st in r.streams_all():
+            ev = torch.cuda.Event()
+            ev.record(st)
+            cur.wait_event(ev)
+        end = torch.cuda.Event(enable_timing=True)
+        end.record(cur)
+        torch.cuda.synchronize()
+        t = torch.tensor([start.elapsed_time(end)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    run(2)
+    ms = run(steps)
+    period = ms / (steps * cfg.layers)
+    tokens = na * cfg.n_micro * cfg.T_mb
+    wb = wire_bytes(cfg)
+    r.close()
+    for c in ctxs:
+        c.close()
+    return {"plan": f"{na}A{nf}F", "T_mb": cfg.T_mb, "n_micro": cfg.n_micro, "ctx": cfg.ctx_len,
+            "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
+            "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
+            "nvlink_bytes_per_layer": {k: v * cfg.n_micro for k, v in wb.items()},
+            "transport": "copy-engine DMA pulls + cuStreamWaitValue32 flags (zero SM)", "measured": True}
+
+
+def run_afd_modeled(ctx):
+    """Config 5 (2A6F @ 4K) on 1 GPU: measured per-layer stage times
+    (afdk_measure_stage_times: attention-tier layer at 192 requests, FFN tier at
+    8 local experts + shared share over 384 tokens) fed to the pipeline model
+    (afdk_simulate, pipesim.cpp:155 semantics) -> modeled 8-GPU TPOT/TGS."""
+    from paper_2507_19427_b200 import afdk
+
+    mb, n_micro = 384, 3
+    st = ctx.measure_stage_times(attn_gpus=2, ffn_gpus=6, micro_batch=mb, avg_ctx=CTX)
+    sim = afdk.simulate(st["attn"], st["comm_fwd"], st["ffn"], st["comm_bwd"], n_micro=n_micro,
+                        total_batch=mb * n_micro, total_gpus=8)
+    d = st["detail"]
+    return {"plan": "2A6F", "micro_batch": mb, "n_micro": n_micro, "ctx": CTX, "modeled": True,
+            "stage_us": {"attn": 1e6 * d["attn_s"], "moe_ffn": 1e6 * d["moe_ffn_s"], "dense_ffn": 1e6 * d["dense_ffn_s"],
+                         "comm_fwd": 1e6 * d["comm_fwd_s"], "comm_bwd": 1e6 * d["comm_bwd_s"]},
+            "link": {"gbs": d["link_gbs"], "measured": bool(d["link_measured"])},
+            "tpot_ms": 1e3 * sim["tpot"], "tgs_tok_per_gpu_s": sim["tgs"],
+            "tokens_per_s_per_gpu_per_layer": sim["tgs"] * 61, "utilization": sim["utilization"]}
+
+
 # ------------------------------------------------- CPU port (oracle) legs
 def cpu_layer_sample(n_req, ctx_len, seed=0):
     """Times the CPU oracle port of the same layer (all host threads)."""
@@ -337,6 +412,15 @@ def main():
     moe = None
     if not args.no_moe:
         moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=rank) for T in (256, 4096)]
+    afd = None
+    if not args.no_afd:
+        try:
+            if world == 1:
+                afd = run_afd_modeled(ctx)
+            else:
+                afd = run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4))
+        except Exception as e:  # reported, never silently replaced
+            afd = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         cpu = None
@@ -369,6 +453,7 @@ def main():
                     "h2d_bytes_per_step": in_host.numel() * in_host.element_size(),
                     "d2h_bytes_per_step": out_host.numel() * out_host.element_size()},
             "moe_ffn": moe,
+            "afd": afd,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }

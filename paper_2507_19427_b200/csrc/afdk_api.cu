@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -110,6 +111,7 @@ afdk_status afdk_create(afdk_ctx** out, const afdk_cfg* cfg) {
     return AFDK_ERR_CUDA;
   }
   ctx->c.encode = reinterpret_cast<afdk::EncodeTiledFn>(fn);
+  ctx->c.pdl = std::getenv("AFDK_NO_PDL") == nullptr;
   if ((e = cudaMalloc(&ctx->c.counters, afdk::kCounterSlots * sizeof(int))) != cudaSuccess ||
       (e = cudaMemset(ctx->c.counters, 0, afdk::kCounterSlots * sizeof(int))) != cudaSuccess) {
     delete ctx;

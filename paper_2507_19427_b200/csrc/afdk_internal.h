@@ -6,6 +6,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <utility>
 
 #include "linear.cuh"
 #include "moe.cuh"
@@ -29,6 +30,7 @@ struct Ctx {
   void* ws = nullptr;  // grow-only device workspace
   size_t ws_bytes = 0;
   int* counters = nullptr;      // zeroed arrival counters (self-resetting kernels)
+  bool pdl = true;               // launch chained kernels with programmatic dependent launch
   double* rope_freq = nullptr;  // NeoX inv_freq table (host-computed in double)
   int rope_dim = 0;
   float rope_theta = 0.0f;
@@ -44,6 +46,23 @@ bool encode_tma(Ctx& ctx, CUtensorMap* map, CUtensorMapDataType dt, int rank, vo
                 CUtensorMapSwizzle swizzle);
 
 void set_error(const std::string& msg);
+
+// cudaLaunchKernelEx with optional programmatic stream serialization (PDL).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 struct MfaDecodeArgs {
   int batch;

@@ -75,6 +75,7 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  griddep_launch();
   const uint32_t tmem = *tmem_slot;
   const int n_mma = P.n_mma;
 
@@ -83,7 +84,20 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       const uint32_t bytes = kABytes + n_mma * 128;
-      for (int u = u_lo, i = 0; u < u_hi; ++u, ++i) {
+      // weights never depend on the previous kernel: fill the first S stages'
+      // weight panels before waiting for the predecessor (PDL), then the X panels
+      const int pro = min(S, u_hi - u_lo);
+      for (int i = 0; i < pro; ++i) {
+        const int u = u_lo + i, tile = u / P.kblocks, kb = u % P.kblocks;
+        mbar_expect_tx(&full[i], bytes);
+        tma_load_2d(smem + i * kp.stage_bytes, &tm_w, &full[i], kb * 64, tile * kBM, pol_w);
+      }
+      griddep_wait();
+      for (int i = 0; i < pro; ++i) {
+        const int u = u_lo + i, kb = u % P.kblocks;
+        tma_load_2d(smem + i * kp.stage_bytes + kABytes, &tm_x, &full[i], kb * 64, 0, pol_x);
+      }
+      for (int u = u_lo + pro, i = pro; u < u_hi; ++u, ++i) {
         const int s = i % S, n = i / S;
         if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
         const int tile = u / P.kblocks, kb = u % P.kblocks;
@@ -162,6 +176,8 @@ __global__ void __launch_bounds__(256) linear_store_kernel(const LinearPlan P, c
                                                            int G, void* __restrict__ out, int out_fp32) {
   __shared__ SlotTable tab;
   build_slot_table(P, G, tab);
+  griddep_wait();
+  griddep_launch();
   const int row = blockIdx.x;
   for (int f = blockIdx.y * 256 + threadIdx.x; f < P.n_out; f += 256 * gridDim.y) {
     const float v = tab.sum(P, part, row, f);
@@ -183,9 +199,9 @@ int linear_grid(const Ctx& ctx, const LinearPlan& p) {
 
 cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,
                                 cudaStream_t stream) {
-  lin::linear_store_kernel<<<dim3(p.m_tok, (p.n_out + 255) / 256 > 8 ? 8 : (p.n_out + 255) / 256), 256, 0, stream>>>(
-      p, part, linear_grid(ctx, p), out, out_fp32 ? 1 : 0);
-  return cudaGetLastError();
+  const int gy = (p.n_out + 255) / 256 > 8 ? 8 : (p.n_out + 255) / 256;
+  return launch_k(ctx.pdl, lin::linear_store_kernel, dim3(p.m_tok, gy), dim3(256), 0, stream, p, part,
+                  linear_grid(ctx, p), out, out_fp32 ? 1 : 0);
 }
 
 LinearPlan make_linear_plan(int m_tok, int n_out, int k) {
@@ -238,8 +254,7 @@ cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, con
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  linear_bf16_kernel<<<linear_grid(ctx, p), kThreads, smem, stream>>>(tw, tx, kp);
-  return cudaGetLastError();
+  return launch_k(ctx.pdl, linear_bf16_kernel, dim3(linear_grid(ctx, p)), dim3(kThreads), smem, stream, tw, tx, kp);
 }
 
 

@@ -48,6 +48,7 @@ constexpr int kThreads = 224;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColO = 0, kColS = 256;    // O: 256 cols, S: 2 x 64 cols
 constexpr float kRescaleThresh = 8.0f;        // lazy O rescale (log2 units)
+constexpr int kPrefetch = 0;                  // pages prefetched into L2 ahead of the rings
 
 struct __align__(1024) Smem {
   uint8_t q[4 * kChunkBytes];       // 32 KB  Q of the current request
@@ -125,6 +126,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   int32_t* prefix = reinterpret_cast<int32_t*>(&sm + 1);  // [B+1] after the Smem block
+  // (seq_lens is a caller input: no kernel of this library writes it, so it may be read before griddep_wait)
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -158,8 +160,6 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     }
   }
   __syncthreads();
-  if (cta == 0)
-    for (int i = threadIdx.x; i <= prm.batch; i += kThreads) prm.prefix_out[i] = prefix[i];
   const int T = prefix[prm.batch];
   int range_lo, range_hi;
   cta_range(cta, G, T, range_lo, range_hi);
@@ -186,6 +186,10 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  griddep_wait();  // q, the appended K/V row and the reused workspace belong to the predecessors
+  griddep_launch();
+  if (cta == 0)
+    for (int i = threadIdx.x; i <= prm.batch; i += kThreads) prm.prefix_out[i] = prefix[i];
 
   if (warp == 0) {
     // ------------------------------------------------ Q + K TMA producer
@@ -193,6 +197,20 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
       SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      // L2 prefetch kPrefetch pages ahead of the smem rings (K and V): more
+      // bytes in flight per SM than the 5 x 32 KB of smem slots allow
+      int pf_pos = range_lo, pf_r = (range_lo < range_hi) ? find_request(prefix, prm.batch, range_lo) : 0;
+      auto prefetch_next = [&]() {
+        if (pf_pos >= range_hi) return;
+        while (prefix[pf_r + 1] <= pf_pos) ++pf_r;
+        const int pg = __ldg(prm.block_table + (size_t)pf_r * prm.max_pages + (pf_pos - prefix[pf_r]));
+        for (int c = 0; c < 4; ++c) {
+          tma_prefetch_l2_3d(&tm_k, c * 64, 0, pg);
+          tma_prefetch_l2_3d(&tm_v, c * 64, 0, pg);
+        }
+        ++pf_pos;
+      };
+      for (int i = 0; i < kPrefetch; ++i) prefetch_next();
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -201,6 +219,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
         for (int c = 0; c < 4; ++c)
           tma_load_2d(sm.q + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, req * kHeads, pol_keep);
         for (int t = lo; t < hi; ++t, ++g) {
+          prefetch_next();
           const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
           const int s = g % kNK, n = g / kNK;
           if (n > 0) mbar_wait(&sm.k_empty[s], (n & 1) ^ 1);
@@ -441,6 +460,8 @@ __global__ void __launch_bounds__(256) mfa_combine_kernel(const Params prm, int 
   __shared__ int s_slot[kMaxSplit];
   __shared__ float s_w[4][kMaxSplit];
   __shared__ int s_n;
+  griddep_wait();
+  griddep_launch();
   const int req = blockIdx.x;
   const int T = prm.prefix_out[prm.batch];
   const int p0 = prm.prefix_out[req], p1 = prm.prefix_out[req + 1];
@@ -547,9 +568,9 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  mfa_decode_kernel<<<G, kThreads, smem, stream>>>(tq, tk, tv, prm);
-  mfa_combine_kernel<<<dim3(a.batch, kHeads / 4), 256, 0, stream>>>(prm, G);
-  return cudaGetLastError();
+  cudaError_t e = launch_k(ctx.pdl, mfa_decode_kernel, dim3(G), dim3(kThreads), smem, stream, tq, tk, tv, prm);
+  if (e != cudaSuccess) return e;
+  return launch_k(ctx.pdl, mfa_combine_kernel, dim3(a.batch, kHeads / 4), dim3(256), 0, stream, prm, G);
 }
 
 }  // namespace afdk

@@ -42,6 +42,8 @@ __global__ void __launch_bounds__(1024) rmsnorm_kernel(const __nv_bfloat16* __re
                                                        const __nv_bfloat16* __restrict__ w,
                                                        __nv_bfloat16* __restrict__ out, int dim, float eps) {
   __shared__ float red[32];
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const size_t row = blockIdx.x;
   const __nv_bfloat16* xr = x + row * dim;
   float ss = 0.0f;
@@ -87,6 +89,8 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
   __shared__ float red[32];
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const int row = blockIdx.x;
   float ss = 0.0f;
   for (int f = threadIdx.x; f < e.n_out; f += blockDim.x) {
@@ -125,6 +129,8 @@ __global__ void __launch_bounds__(1024) qup_epilogue_kernel(const LinearPlan P, 
                                                             __nv_bfloat16* __restrict__ q) {
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const int row = blockIdx.x;
   const int half = head_dim / 2;
   const int pos = max(__ldg(seq_lens + row) - 1, 0);
@@ -151,6 +157,8 @@ __global__ void __launch_bounds__(1024) o_epilogue_kernel(const LinearPlan P, co
   __shared__ float red[32];
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const size_t row = blockIdx.x;
   float ss = 0.0f;
   for (int f = threadIdx.x * 4; f < n; f += blockDim.x * 4) {
@@ -231,20 +239,24 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   cudaError_t e;
 
   // K1a: input RMSNorm
-  rmsnorm_kernel<<<B, 1024, 0, stream>>>(static_cast<const __nv_bfloat16*>(a.x),
-                                          static_cast<const __nv_bfloat16*>(a.w_in_norm), xn, Hd, a.rms_eps);
+  if ((e = launch_k(ctx.pdl, rmsnorm_kernel, dim3(B), dim3(1024), 0, stream, static_cast<const __nv_bfloat16*>(a.x),
+                    static_cast<const __nv_bfloat16*>(a.w_in_norm), xn, Hd, a.rms_eps)) != cudaSuccess)
+    return e;
   // K1b: [q_down | k | v] projection, then q RMSNorm + RoPE(k) + paged KV append
   const LinearPlan p1 = make_linear_plan(B, QL + 2 * D, Hd);
   if ((e = linear_bf16_launch(ctx, p1, xn, a.w_qkv, part, stream)) != cudaSuccess) return e;
   QkvEpi qe{QL, D, a.page_size, a.max_pages, p1.n_out, a.rms_eps,
             static_cast<const __nv_bfloat16*>(a.w_q_norm), qa, static_cast<__nv_bfloat16*>(a.k_cache),
             static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq};
-  qkv_epilogue_kernel<<<B, 512, p1.n_out * sizeof(float), stream>>>(p1, part, linear_grid(ctx, p1), qe);
+  if ((e = launch_k(ctx.pdl, qkv_epilogue_kernel, dim3(B), dim3(512), p1.n_out * sizeof(float), stream, p1,
+                    (const float*)part, linear_grid(ctx, p1), qe)) != cudaSuccess)
+    return e;
   // K1c: q_up projection + RoPE(q)
   const LinearPlan p2 = make_linear_plan(B, NQ, QL);
   if ((e = linear_bf16_launch(ctx, p2, qa, a.w_q_up, part, stream)) != cudaSuccess) return e;
-  qup_epilogue_kernel<<<dim3(B, (NQ / 2 + 1023) / 1024), 1024, 0, stream>>>(p2, part, linear_grid(ctx, p2), NQ, D,
-                                                                           a.seq_lens, inv_freq, q);
+  if ((e = launch_k(ctx.pdl, qup_epilogue_kernel, dim3(B, (NQ / 2 + 1023) / 1024), dim3(1024), 0, stream, p2,
+                    (const float*)part, linear_grid(ctx, p2), NQ, D, a.seq_lens, inv_freq, q)) != cudaSuccess)
+    return e;
   // K2/K3: MFA decode core over the paged cache (now including this token)
   MfaDecodeArgs md{B, q, a.k_cache, a.v_cache, a.num_pages, a.block_table, a.max_pages, a.seq_lens,
                    a.softmax_scale, attn, nullptr, part};
@@ -252,11 +264,11 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   // K4: o_proj, then residual + post-attention RMSNorm
   const LinearPlan p3 = make_linear_plan(B, Hd, NQ);
   if ((e = linear_bf16_launch(ctx, p3, attn, a.w_o, part, stream)) != cudaSuccess) return e;
-  o_epilogue_kernel<<<B, 1024, Hd * sizeof(float), stream>>>(p3, part, linear_grid(ctx, p3), Hd,
-                                                             static_cast<const __nv_bfloat16*>(a.x),
-                                                             static_cast<const __nv_bfloat16*>(a.w_post_norm),
-                                                             a.rms_eps, static_cast<__nv_bfloat16*>(a.h_res),
-                                                             static_cast<__nv_bfloat16*>(a.h_norm));
+  if ((e = launch_k(ctx.pdl, o_epilogue_kernel, dim3(B), dim3(1024), Hd * sizeof(float), stream, p3,
+                    (const float*)part, linear_grid(ctx, p3), Hd, static_cast<const __nv_bfloat16*>(a.x),
+                    static_cast<const __nv_bfloat16*>(a.w_post_norm), a.rms_eps,
+                    static_cast<__nv_bfloat16*>(a.h_res), static_cast<__nv_bfloat16*>(a.h_norm))) != cudaSuccess)
+    return e;
   return cudaGetLastError();
 }
 

@@ -55,6 +55,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ------------------------------------------- programmatic dependent launch
+// Every kernel waits for its stream predecessor (griddepcontrol.wait, a no-op
+// when launched without the PDL attribute) before touching data it may have
+// produced, and lets its own successor launch early so the successor's
+// prologue (barrier init, TMEM alloc, weight prefetch) overlaps this tail.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ----------------------------------------------------------------- fences
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

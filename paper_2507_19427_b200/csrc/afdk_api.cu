@@ -217,7 +217,7 @@ afdk_status afdk_router_topk(afdk_ctx* ctx, const void* h, const void* gate_w, i
   cudaSetDevice(ctx->c.device);
   afdk::moe::RouterArgs a{static_cast<const __nv_bfloat16*>(h), static_cast<const __nv_bfloat16*>(gate_w), T, H, E, k,
                           renormalize, logits, ids, weights, static_cast<uint8_t*>(xq), xs};
-  const cudaError_t e = afdk::router_launch(a, static_cast<cudaStream_t>(stream));
+  const cudaError_t e = afdk::router_launch(a, static_cast<cudaStream_t>(stream), ctx->c.pdl);
   if (e != cudaSuccess) return cuda_fail("afdk_router_topk", e);
   return AFDK_OK;
 }
@@ -236,7 +236,7 @@ afdk_status afdk_moe_permute(afdk_ctx* ctx, const int32_t* ids, int T, int k, in
   if (!ws) { set_error("afdk_moe_permute: workspace allocation failed"); return AFDK_ERR_CUDA; }
   afdk::moe::PermuteArgs a{ids, T, k, E, 0, E, 0, 0, 0, offsets, perm, inv,
                            reinterpret_cast<afdk::moe::Work*>(ws), reinterpret_cast<int*>(ws + wbytes - 256)};
-  const cudaError_t e = afdk::permute_launch(a, static_cast<cudaStream_t>(stream));
+  const cudaError_t e = afdk::permute_launch(a, static_cast<cudaStream_t>(stream), ctx->c.pdl);
   if (e != cudaSuccess) return cuda_fail("afdk_moe_permute", e);
   return AFDK_OK;
 }

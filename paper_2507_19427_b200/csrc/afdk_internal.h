@@ -110,10 +110,10 @@ size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms);
 cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws, cudaStream_t stream);
 
 // ---------------------------------------------------------------- MoE FFN
-cudaError_t router_launch(const moe::RouterArgs& a, cudaStream_t stream);
-cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream);
-cudaError_t gather_launch(const moe::GatherArgs& a, cudaStream_t stream);
-cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream);
+cudaError_t router_launch(const moe::RouterArgs& a, cudaStream_t stream, bool pdl);
+cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream, bool pdl);
+cudaError_t gather_launch(const moe::GatherArgs& a, cudaStream_t stream, bool pdl);
+cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream, bool pdl);
 
 struct MoeGemmArgs {
   const void* w;         // e4m3 [(n_local+1) * w_rows, K]

@@ -54,9 +54,9 @@ cudaError_t moe_ffn_launch(Ctx& ctx, const MoeFfnArgs& a, void* ws_base, cudaStr
 
   moe::PermuteArgs pa{a.ids, T, k, E, a.expert_lo, a.expert_hi, shared_local ? 1 : 0, a.shared_lo, a.shared_hi,
                       offsets, perm, inv, work, n_work};
-  if ((e = chk(permute_launch(pa, stream), "permute")) != cudaSuccess) return e;
+  if ((e = chk(permute_launch(pa, stream, ctx.pdl), "permute")) != cudaSuccess) return e;
   moe::GatherArgs ga{a.xq, a.xs, perm, T, k, H, rp, xp, xs_t};
-  if ((e = chk(gather_launch(ga, stream), "gather")) != cudaSuccess) return e;
+  if ((e = chk(gather_launch(ga, stream, ctx.pdl), "gather")) != cudaSuccess) return e;
   const int n_local = a.expert_hi - a.expert_lo;
   MoeGemmArgs g13{a.w13, a.s13, xp, xs_t, work, n_work, H, I, E, a.expert_lo, n_local, rp, hq, hs_t, nullptr};
   if ((e = chk(moe_gemm_launch(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
@@ -64,7 +64,7 @@ cudaError_t moe_ffn_launch(Ctx& ctx, const MoeFfnArgs& a, void* ws_base, cudaStr
   if ((e = chk(moe_gemm_launch(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
   moe::CombineArgs ca{y, a.ids, a.weights, inv, T, k, H, a.expert_lo, a.expert_hi, shared_local ? 1 : 0,
                       a.shared_lo, a.shared_hi, static_cast<__nv_bfloat16*>(a.out)};
-  return chk(combine_launch(ca, stream), "combine");
+  return chk(combine_launch(ca, stream, ctx.pdl), "combine");
 }
 
 }  // namespace afdk

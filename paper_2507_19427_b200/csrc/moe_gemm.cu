@@ -19,7 +19,8 @@
 // take chunks of the same group for one m-tile so a weight tile re-read by
 // several chunks hits L2.
 //
-// Roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2-5 epilogue.
+// Roles (224 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2-5 epilogue,
+// w6 activation-scale stager.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp8.h>
@@ -37,7 +38,7 @@ namespace moe {
 
 using namespace sm100;
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;  // w0 TMA, w1 MMA, w2-5 epilogue, w6 scale stager
 constexpr int kAccSlots = 4;  // TMEM ring: 4 x 128 columns
 
 struct GemmParams {
@@ -76,8 +77,11 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
   constexpr int kAOps = kGLU ? 2 : 1;
   constexpr int kB = kChunk * 128;              // 8 KB activation panel
   const int S = p.stages;
-  float* xs_ring = reinterpret_cast<float*>(smem + S * p.stage_bytes);  // [S][kChunk] row scales
-  uint64_t* full = reinterpret_cast<uint64_t*>(xs_ring + S * kChunk);
+  // per stage: the chunk's kChunk activation row scales + the weight tile's
+  // gate/up block scales of this k-block (staged by warp 6, read by the epilogue)
+  constexpr int kRing = kChunk + 4;
+  float* xs_ring = reinterpret_cast<float*>(smem + S * p.stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xs_ring + S * kRing);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;
   uint64_t* acc_empty = acc_full + kAccSlots;
@@ -86,12 +90,11 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
 
   const int warp = warp_id(), lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
-  const int n_items = (*p.n_work) * p.m_tiles;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1 + 32); mbar_init(&empty[i], 1 + 4); }
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1 + 32); mbar_init(&empty[i], 1 + 4); }  // TMA + stager lanes; MMA + epilogue warps
     for (int i = 0; i < kAccSlots; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
     fence_barrier_init();
   }
@@ -99,34 +102,51 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  griddep_wait();  // work list, dispatch rows and scales come from the predecessors
+  griddep_launch();
   const uint32_t tmem = *tmem_slot;
   const int n_work = *p.n_work;
+  const int n_items = n_work * p.m_tiles;
 
   if (warp == 0) {
-    // whole warp: lane 0 issues the TMA loads, every lane stages two of the
-    // chunk's activation row scales for this k-block into the stage (plain
-    // loads: dispatch rows start at arbitrary offsets) and arrives on full[s]
-    const uint64_t pol_w = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();
-    int i = 0;
-    for (int it = cta; it < n_items; it += G) {
-      const int mt = it / n_work, gc = it % n_work;
-      const Work wk = p.work[gc];
-      const int wrow = weight_index(p, wk.group) * p.w_rows + mt * 128;
-      for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
-        const int s = i % S, n = i / S;
-        if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
-        uint8_t* st = smem + s * p.stage_bytes;
-        if (lane == 0) {
+    // TMA producer: weight panel(s) + activation panel of every k-block
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int i = 0;
+      for (int it = cta; it < n_items; it += G) {
+        const int mt = it / n_work, gc = it % n_work;
+        const Work wk = p.work[gc];
+        const int wrow = weight_index(p, wk.group) * p.w_rows + mt * 128;
+        for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
+          const int s = i % S, n = i / S;
+          if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
+          uint8_t* st = smem + s * p.stage_bytes;
           mbar_expect_tx(&full[s], kAOps * kA + kB);
           tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol_w);
           if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol_w);
           tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, wk.row0, pol_x);
         }
+      }
+    }
+  } else if (warp == 6) {
+    // row-scale stager: the chunk's activation scales of each k-block (plain
+    // loads: dispatch rows start at arbitrary offsets), off the TMA issue path
+    int i = 0;
+    const int nb_rows = p.w_rows / 128;
+    for (int it = cta; it < n_items; it += G) {
+      const int mt = it / n_work;
+      const Work wk = p.work[it % n_work];
+      const float* sw = p.w_scale + (size_t)weight_index(p, wk.group) * nb_rows * p.kblocks;
+      for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
+        const int s = i % S, n = i / S;
+        if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
         const float* src = p.xs_t + (size_t)kb * p.rows_pad + wk.row0;
-        float* dst = xs_ring + s * kChunk;
+        float* dst = xs_ring + s * kRing;
         dst[lane] = (lane < wk.rows) ? __ldg(src + lane) : 0.0f;
         dst[lane + 32] = (lane + 32 < wk.rows) ? __ldg(src + lane + 32) : 0.0f;
+        if (lane == 0) dst[kChunk] = __ldg(sw + (size_t)mt * p.kblocks + kb);
+        if (lane == 1 && kGLU) dst[kChunk + 1] = __ldg(sw + (size_t)(mt + p.up_offset / 128) * p.kblocks + kb);
         mbar_arrive(&full[s]);
       }
     }
@@ -159,7 +179,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
         }
       }
     }
-  } else {
+  } else if (warp >= 2 && warp <= 5) {
     // ----------------------------------------------------------- epilogue
     const int sub = warp & 3, et = sub * 32 + lane;  // et = feature row in the tile
     const uint32_t t_lane = tmem + ((uint32_t)(sub * 32) << 16);
@@ -167,9 +187,6 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
     for (int it = cta; it < n_items; it += G) {
       const int mt = it / n_work;
       const Work wk = p.work[it % n_work];
-      const int widx = weight_index(p, wk.group);
-      const int nb_rows = p.w_rows / 128;
-      const float* sw = p.w_scale + (size_t)widx * nb_rows * p.kblocks;
       float accg[kChunk], accu[kGLU ? kChunk : 1];
 #pragma unroll
       for (int n = 0; n < kChunk; ++n) accg[n] = 0.0f;
@@ -184,9 +201,9 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
         mbar_wait(&acc_full[a], na & 1);
         mbar_wait(&full[s], (i / S) & 1);  // row scales staged (complete; stage held until we arrive)
         tc_fence_after();
-        const float* xs = xs_ring + s * kChunk;
-        const float swg = __ldg(sw + (size_t)mt * p.kblocks + kb);
-        const float swu = kGLU ? __ldg(sw + (size_t)(mt + p.up_offset / 128) * p.kblocks + kb) : 0.0f;
+        const float* xs = xs_ring + s * kRing;
+        const float swg = xs[kChunk];
+        const float swu = kGLU ? xs[kChunk + 1] : 0.0f;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           if (c < n_ld) {
@@ -212,30 +229,40 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
       }
       if (kGLU) {
         // h = SiLU(gate) * up; per dispatched row, quantise the tile's 128
-        // features (one 1x128 block) to e4m3
+        // features (one 1x128 block) to e4m3.  Work in groups of 16 rows and
+        // skip the groups beyond this chunk's rows (warp-uniform).
         float h[kChunk];
 #pragma unroll
-        for (int n = 0; n < kChunk; ++n) {
-          const float g = accg[n];
-          h[n] = (g / (1.0f + expf(-g))) * accu[kGLU ? n : 0];
-        }
+        for (int g16 = 0; g16 < kChunk / 16; ++g16) {
+          if (g16 * 16 < wk.rows) {
 #pragma unroll
-        for (int n = 0; n < kChunk; ++n) {
-          float m = fabsf(h[n]);
+            for (int j = 0; j < 16; ++j) {
+              const int n = g16 * 16 + j;
+              const float g = accg[n];
+              h[n] = (g / (1.0f + __expf(-g))) * accu[kGLU ? n : 0];
+              float m = fabsf(h[n]);
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
-          if (lane == 0) s_red[sub][n] = m;
+              for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+              if (lane == 0) s_red[sub][n] = m;
+            }
+          }
         }
         named_bar(1, 128);
 #pragma unroll
-        for (int n = 0; n < kChunk; ++n) {
-          if (n < wk.rows) {
-            const float amax = fmaxf(fmaxf(s_red[0][n], s_red[1][n]), fmaxf(s_red[2][n], s_red[3][n]));
-            const float sc = __fdiv_rn(fmaxf(amax, 1e-10f), 448.0f);
-            const size_t row = (size_t)wk.row0 + n;
-            p.hq[row * p.out_cols + mt * 128 + et] =
-                (uint8_t)__nv_cvt_float_to_fp8(__fdiv_rn(h[n], sc), __NV_SATFINITE, __NV_E4M3);
-            if (et == 0) p.hs_t[(size_t)mt * p.rows_pad + row] = sc;
+        for (int g16 = 0; g16 < kChunk / 16; ++g16) {
+          if (g16 * 16 < wk.rows) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int n = g16 * 16 + j;
+              if (n < wk.rows) {
+                const float amax = fmaxf(fmaxf(s_red[0][n], s_red[1][n]), fmaxf(s_red[2][n], s_red[3][n]));
+                const float sc = __fdiv_rn(fmaxf(amax, 1e-10f), 448.0f);
+                const size_t row = (size_t)wk.row0 + n;
+                p.hq[row * p.out_cols + mt * 128 + et] =
+                    (uint8_t)__nv_cvt_float_to_fp8(__fdiv_rn(h[n], sc), __NV_SATFINITE, __NV_E4M3);
+                if (et == 0) p.hs_t[(size_t)mt * p.rows_pad + row] = sc;
+              }
+            }
           }
         }
         named_bar(1, 128);
@@ -299,7 +326,7 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
   p.stage_bytes = (int)align_up((size_t)a_bytes + kChunk * 128, 1024);
   p.stages = (200 * 1024) / p.stage_bytes;
   if (p.stages > 8) p.stages = 8;
-  const size_t smem = (size_t)p.stages * (p.stage_bytes + kChunk * 4) + 1024 + 512;
+  const size_t smem = (size_t)p.stages * (p.stage_bytes + (kChunk + 4) * 4) + 1024 + 512;
   cudaError_t e;
   if (glu) {
     static size_t attr = 0;
@@ -308,7 +335,7 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
         return e;
       attr = smem;
     }
-    moe_gemm_kernel<true><<<ctx.num_sms, kThreads, smem, stream>>>(tw, tx, p);
+    return launch_k(ctx.pdl, moe_gemm_kernel<true>, dim3(ctx.num_sms), dim3(kThreads), smem, stream, tw, tx, p);
   } else {
     static size_t attr = 0;
     if (smem > attr) {
@@ -316,7 +343,7 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
         return e;
       attr = smem;
     }
-    moe_gemm_kernel<false><<<ctx.num_sms, kThreads, smem, stream>>>(tw, tx, p);
+    return launch_k(ctx.pdl, moe_gemm_kernel<false>, dim3(ctx.num_sms), dim3(kThreads), smem, stream, tw, tx, p);
   }
   return cudaGetLastError();
 }

@@ -22,6 +22,7 @@
 
 #include "afdk_internal.h"
 #include "moe.cuh"
+#include "sm100.cuh"
 
 namespace afdk {
 namespace moe {
@@ -38,6 +39,8 @@ __device__ __forceinline__ uint8_t to_e4m3(float v) {
 // the logits are bitwise reproducible run to run.
 __global__ void __launch_bounds__(256) router_kernel(RouterArgs a) {
   __shared__ float s_logit[kRouterTok][kMaxExperts];
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * kRouterTok;
   const int nt = min(kRouterTok, a.T - t0);
@@ -146,6 +149,8 @@ __global__ void __launch_bounds__(256) router_kernel(RouterArgs a) {
 __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
   extern __shared__ uint8_t s_ids[];
   __shared__ int s_cnt[kMaxExperts], s_off[kMaxExperts + 1];
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const int n = a.T * a.k;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s_ids[i] = (uint8_t)a.ids[i];
@@ -203,6 +208,8 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
 // shared expert's tokens in order.  Scales are written transposed
 // [H/128][rows] so the GEMM fetches one k-block's row scales with a TMA box.
 __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const int s = blockIdx.x;
   const int n_routed = a.T * a.k;
   const int src = (s < n_routed) ? __ldg(a.perm + s) / a.k : s - n_routed;
@@ -216,6 +223,8 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
 // --------------------------------------------------------------- K9 combine
 // out[t] = sum_j w[t,j] y[inv[t,j]] (local experts only) + y[shared row of t]
 __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const int t = blockIdx.x;
   const int n_routed = a.T * a.k;
   float w[kMaxTopK];
@@ -249,24 +258,20 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
 
 }  // namespace moe
 
-cudaError_t router_launch(const moe::RouterArgs& a, cudaStream_t stream) {
-  moe::router_kernel<<<(a.T + moe::kRouterTok - 1) / moe::kRouterTok, 256, 0, stream>>>(a);
-  return cudaGetLastError();
+cudaError_t router_launch(const moe::RouterArgs& a, cudaStream_t stream, bool pdl) {
+  return launch_k(pdl, moe::router_kernel, dim3((a.T + moe::kRouterTok - 1) / moe::kRouterTok), dim3(256), 0, stream, a);
 }
 
-cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream) {
-  moe::permute_kernel<<<1, 1024, (size_t)a.T * a.k, stream>>>(a);
-  return cudaGetLastError();
+cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream, bool pdl) {
+  return launch_k(pdl, moe::permute_kernel, dim3(1), dim3(1024), (size_t)a.T * a.k, stream, a);
 }
 
-cudaError_t gather_launch(const moe::GatherArgs& a, cudaStream_t stream) {
-  moe::gather_kernel<<<a.T * a.k + a.T, 256, 0, stream>>>(a);
-  return cudaGetLastError();
+cudaError_t gather_launch(const moe::GatherArgs& a, cudaStream_t stream, bool pdl) {
+  return launch_k(pdl, moe::gather_kernel, dim3(a.T * a.k + a.T), dim3(256), 0, stream, a);
 }
 
-cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream) {
-  moe::combine_kernel<<<a.T, 256, 0, stream>>>(a);
-  return cudaGetLastError();
+cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream, bool pdl) {
+  return launch_k(pdl, moe::combine_kernel, dim3(a.T), dim3(256), 0, stream, a);
 }
 
 }  // namespace afdk

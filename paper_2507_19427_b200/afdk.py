@@ -12,7 +12,7 @@ import os
 from ctypes import POINTER, Structure, c_char_p, c_float, c_int, c_int32, c_size_t, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libafdk.so")
+LIB_PATH = os.environ.get("AFDK_LIB") or os.path.join(HERE, "libafdk.so")
 
 AFDK_OK = 0
 _STATUS = {1: "AFDK_ERR_INVALID", 2: "AFDK_ERR_CUDA", 3: "AFDK_ERR_UNSUPPORTED", 4: "AFDK_ERR_NO_DEVICE"}

@@ -19,9 +19,11 @@
 // slot (request + cta), and mfa_combine (K3) merges the partials.  Each CTA
 // derives the page prefix of the batch itself (no planning launch).
 //
-// Warp roles (224 threads):  w0 = Q/K TMA producer, w1 = MMA issuer + TMEM
-// owner, w2..w5 = softmax / O-correction / epilogue (TMEM lanes 0-15 of each
-// 32-lane sub-partition hold the M=64 accumulator rows), w6 = V TMA producer.
+// Warp roles (256 threads):  w0 = Q/K TMA producer, w1 = QK^T MMA issuer +
+// TMEM owner, w2..w5 = softmax / O-correction / epilogue (TMEM lanes 0-15 of
+// each 32-lane sub-partition hold the M=64 accumulator rows), w6 = V TMA
+// producer, w7 = P.V MMA issuer.  QK^T and P.V are issued by different
+// threads so K slots recycle at QK^T completion whatever the softmax does.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -42,13 +44,22 @@ constexpr int kDim = 256;
 constexpr int kPage = 64;                    // tokens per KV page == one tile
 constexpr int kTileBytes = kPage * kDim * 2;  // 32 KB (K or V of one page, bf16)
 constexpr int kChunkBytes = 64 * 128;         // one 64-row x 128B swizzle panel
-constexpr int kNK = 2;                        // K ring depth
-constexpr int kNV = 3;                        // V ring depth
-constexpr int kThreads = 224;
+#ifndef AFDK_MFA_NK
+#define AFDK_MFA_NK 2
+#endif
+#ifndef AFDK_MFA_NV
+#define AFDK_MFA_NV 3
+#endif
+#ifndef AFDK_MFA_PREFETCH
+#define AFDK_MFA_PREFETCH 0
+#endif
+constexpr int kNK = AFDK_MFA_NK;              // K ring depth
+constexpr int kNV = AFDK_MFA_NV;              // V ring depth
+constexpr int kThreads = 256;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColO = 0, kColS = 256;    // O: 256 cols, S: 2 x 64 cols
 constexpr float kRescaleThresh = 8.0f;        // lazy O rescale (log2 units)
-constexpr int kPrefetch = 0;                  // pages prefetched into L2 ahead of the rings
+constexpr int kPrefetch = AFDK_MFA_PREFETCH;  // pages prefetched into L2 ahead of the rings (0: off)
 
 struct __align__(1024) Smem {
   uint8_t q[4 * kChunkBytes];       // 32 KB  Q of the current request
@@ -65,7 +76,7 @@ struct __align__(1024) Smem {
 };
 
 constexpr int kMaxBatch = 2048;  // prefix of pages per request lives in smem
-constexpr int kMaxSplit = 160;   // >= #SMs + 1: CTAs one request may span
+
 
 struct Params {
   const int32_t* block_table;  // [B, max_pages]
@@ -249,31 +260,15 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------ MMA issuer
+    // --------------------------------------------------- QK^T MMA issuer
+    // Runs ahead of the softmax by the S double buffer only: K slots are
+    // released as soon as their QK completes, independent of PV progress.
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16(64, 64, false, false);
-      constexpr uint32_t idesc_pv = idesc_bf16(64, 256, false, true);
       const uint32_t q_base = smem_u32(sm.q);
       SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
-      auto issue_pv = [&](int gg, bool first_in_seg, int seg_idx) {
-        const int vs = gg % kNV, pb = gg & 1;
-        mbar_wait(&sm.v_full[vs], (gg / kNV) & 1);
-        mbar_wait(&sm.p_full[pb], (gg >> 1) & 1);
-        if (first_in_seg && seg_idx > 0) mbar_wait(&sm.o_free, (seg_idx - 1) & 1);
-        tc_fence_after();
-        const uint32_t p_base = smem_u32(sm.p[pb]);
-        const uint32_t v_base = smem_u32(sm.v[vs]);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t a = sdesc_sw128(p_base + kk * 32, 0, 1024);
-          const uint64_t b = sdesc_sw128(v_base + kk * 2048, kChunkBytes, 1024);
-          mma_bf16(tmem + kColO, a, b, idesc_pv, (first_in_seg && kk == 0) ? 0u : 1u);
-        }
-        mma_commit(&sm.v_empty[vs]);
-        mma_commit(&sm.p_empty[pb]);
-      };
       while (walk.next(req, lo, hi, whole)) {
         const int n = hi - lo;
         mbar_wait(&sm.q_full, seg & 1);
@@ -295,14 +290,43 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
           mma_commit(&sm.s_full[sb]);
           mma_commit(&sm.k_empty[ks]);
           if (j == n - 1) mma_commit(&sm.q_empty);
-          if (j >= 1) issue_pv(gg - 1, j == 1, seg);
         }
-        issue_pv(g + n - 1, n == 1, seg);
         g += n;
         ++seg;
       }
     }
-  } else {
+  } else if (warp == 7) {
+    // ------------------------------------------------------ P.V MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_pv = idesc_bf16(64, 256, false, true);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      int req, lo, hi, seg = 0, g = 0;
+      bool whole;
+      while (walk.next(req, lo, hi, whole)) {
+        const int n = hi - lo;
+        for (int j = 0; j < n; ++j) {
+          const int gg = g + j;
+          const int vs = gg % kNV, pb = gg & 1;
+          mbar_wait(&sm.v_full[vs], (gg / kNV) & 1);
+          mbar_wait(&sm.p_full[pb], (gg >> 1) & 1);
+          if (j == 0 && seg > 0) mbar_wait(&sm.o_free, (seg - 1) & 1);
+          tc_fence_after();
+          const uint32_t p_base = smem_u32(sm.p[pb]);
+          const uint32_t v_base = smem_u32(sm.v[vs]);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t a = sdesc_sw128(p_base + kk * 32, 0, 1024);
+            const uint64_t b = sdesc_sw128(v_base + kk * 2048, kChunkBytes, 1024);
+            mma_bf16(tmem + kColO, a, b, idesc_pv, (j == 0 && kk == 0) ? 0u : 1u);
+          }
+          mma_commit(&sm.v_empty[vs]);
+          mma_commit(&sm.p_empty[pb]);
+        }
+        g += n;
+        ++seg;
+      }
+    }
+  } else if (warp >= 2 && warp <= 5) {
     // ------------------------------- softmax / correction / epilogue (w2-5)
     const int sub = warp & 3;                 // TMEM sub-partition of this warp
     const bool active = lane < 16;            // M=64: lanes 0-15 hold rows
@@ -453,6 +477,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   }
 }
 
+constexpr int kMaxSplit = 160;  // CTAs one request may span (>= #SMs + 1)
 // K3: merge the split partials of requests that spanned several CTAs (fixed
 // CTA order => deterministic), zero-fill empty requests.  grid (B, 16): 4
 // heads per CTA, 64 threads per head, 4 dims (one float4) per thread.

@@ -220,6 +220,17 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe (x <= ~0; -inf -> 0): Cody-Waite split + degree-3
+// minimax for 2^f on [0,1) (max rel err ~1.7e-4, far below the bf16 rounding
+// P is stored with).  Used for part of the softmax exponentials so the MUFU
+// pipe (8 ex2/clk/SM on B200) is not the only exp unit.
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -127.0f);
+  const float fi = floorf(x);
+  const float f = x - fi;
+  const float p = fmaf(fmaf(fmaf(0.0786326f, f, 0.2261887f), f, 0.6951786f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (static_cast<int>(fi) << 23));
+}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),

@@ -13,9 +13,14 @@ attention is "replicas only": the attention tier has no cross-GPU exchange).
 """
 from __future__ import annotations
 
+import os
+
+# the CPU-port legs use OpenMP: workers must sleep between parallel regions or
+# they fight torch's thread pools (every region cost ~60 ms with spinning workers)
+os.environ.setdefault("OMP_WAIT_POLICY", "passive")
+
 import argparse
 import json
-import os
 import subprocess
 import sys
 import threading
@@ -41,6 +46,7 @@ def parse():
     p.add_argument("--workload", default="layer", choices=["layer", "attn"])
     p.add_argument("--no-moe", action="store_true", help="skip the config-3 MoE FFN sub-measurement")
     p.add_argument("--no-afd", action="store_true", help="skip the config-5 AFD measurement")
+    p.add_argument("--no-long", action="store_true", help="skip the config-4 32K measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -194,6 +200,76 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0):
                        "peak": 2 * tf_peak, "peak_kind": f"fp8 = 2 x {kind} bf16 cuBLAS",
                        "frac": flops / (ms * 1e-3) / 1e12 / (2 * tf_peak)},
             "gpu_launches_per_layer": 5}
+
+
+# ------------------------------------------- config 4: 32K split-KV attention
+def run_long_context(ctx, torch, dev, steps, batch=32, ctx_len=32768):
+    """MFA decode core at B=32, 32K context (1.07 GB of bf16 KV per layer)."""
+    w = make_workload_attn(torch, dev, batch, ctx_len)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step(i):
+        k, v = w["kv"][i % 2]
+        ctx.mfa_decode_attention(w["q"], k, v, w["block_table"], w["seq_lens"], w["out"], D ** -0.5, stream=sp)
+
+    for i in range(3):
+        step(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(steps):
+        step(i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    hbm_peak, _, kind = peaks()
+    nbytes = kv_bytes(batch, ctx_len) + 2 * batch * H * D * 2
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    del w
+    return {"workload": "config4-mfa-decode-core 32K split-KV", "batch": batch, "ctx": ctx_len, "ms": ms,
+            "tokens_per_s": batch / (ms * 1e-3), "hbm": {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                                                       "frac": gbs / hbm_peak, "alg_bytes": nbytes}}
+
+
+def make_workload_attn(torch, dev, batch, ctx_len, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    pages_per_req = (ctx_len + PAGE - 1) // PAGE
+    num_pages = batch * pages_per_req
+    perm = torch.randperm(num_pages, generator=g).to(torch.int32)
+    return {"q": torch.randn(batch, H, D, generator=g).to(torch.bfloat16).to(dev),
+            "block_table": perm.view(batch, pages_per_req).contiguous().to(dev),
+            "seq_lens": torch.full((batch,), ctx_len, dtype=torch.int32, device=dev),
+            "kv": [(torch.empty(num_pages, PAGE, D, dtype=torch.bfloat16, device=dev).normal_(),
+                    torch.empty(num_pages, PAGE, D, dtype=torch.bfloat16, device=dev).normal_()) for _ in range(2)],
+            "out": torch.empty(batch, H, D, dtype=torch.bfloat16, device=dev)}
+
+
+def config1_cpu():
+    """Config 1: MFA at the reference's small dims (kTinyCatalog geometry,
+    test_catalog.cpp:16-51: hidden 64, 4 heads x 32, one K/V head), batch 4,
+    4K context, fp32 — CPU oracle only (no GPU, no roofline)."""
+    import numpy as np
+
+    from oracle import oracle as orc
+
+    dims = dict(hidden=64, q_lora=32, n_heads=4, head_dim=32, page=16)
+    rng = np.random.default_rng(1)
+    B, L = 4, 4096
+    pages = L // 16
+    w = {"in_norm": np.ones(64, np.float32), "qkv": rng.standard_normal((32 + 64, 64), dtype=np.float32) / 8,
+         "q_norm": np.ones(32, np.float32), "q_up": rng.standard_normal((128, 32), dtype=np.float32) / 6,
+         "o": rng.standard_normal((64, 128), dtype=np.float32) / 11, "post_norm": np.ones(64, np.float32)}
+    x = rng.standard_normal((B, 64), dtype=np.float32)
+    kc = rng.standard_normal((B * pages, 16, 32), dtype=np.float32)
+    vc = rng.standard_normal((B * pages, 16, 32), dtype=np.float32)
+    bt = np.arange(B * pages, dtype=np.int32).reshape(B, pages)
+    sl = np.full(B, L, np.int32)
+    t0 = time.perf_counter()
+    orc.mfa_layer(dims, x, w, kc, vc, bt, sl, round_bf16=False)
+    dt = time.perf_counter() - t0
+    return {"workload": "config1-mfa-small-dims fp32 (CPU oracle)", "batch": B, "ctx": L, "seconds": dt,
+            "tokens_per_s": B / dt, "threads": orc.num_threads()}
 
 
 # --------------------------------------------- config 5: AFD layer pipeline
@@ -466,6 +542,9 @@ def main():
     e2e_value = world * args.batch / (e2e_ms * 1e-3)
     in_host, out_host = in_host[0], out_host[0]
 
+    long_ctx = None
+    if not args.no_long:
+        long_ctx = run_long_context(ctx, torch, dev, max(3, args.steps // 4))
     moe = None
     if not args.no_moe:
         moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=rank) for T in (256, 4096)]
@@ -509,6 +588,8 @@ def main():
             "e2e": {"value": e2e_value, "unit": "tokens/s",
                     "h2d_bytes_per_step": in_host.numel() * in_host.element_size(),
                     "d2h_bytes_per_step": out_host.numel() * out_host.element_size()},
+            "config4_long_context": long_ctx,
+            "config1_cpu": config1_cpu() if (world == 1 and not args.no_cpu_baseline) else None,
             "moe_ffn": moe,
             "afd": afd,
             "gpu_launches": launches_per_step * args.steps,

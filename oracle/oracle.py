@@ -27,6 +27,10 @@ def _p(a, ct):
 def orc() -> ctypes.CDLL:
     global _orc
     if _orc is None:
+        # OpenMP workers must sleep between parallel regions: spinning workers
+        # fight the other thread pools of the process (torch, OpenBLAS) and made
+        # every small parallel region cost ~60 ms here.  Read by libgomp at load.
+        os.environ.setdefault("OMP_WAIT_POLICY", "passive")
         if not os.path.exists(ORC_PATH):
             raise ImportError("oracle/liborc.so not built (make -C oracle)")
         _orc = ctypes.CDLL(ORC_PATH)

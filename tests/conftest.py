@@ -1,6 +1,8 @@
 import os
 import sys
 
+os.environ.setdefault("OMP_WAIT_POLICY", "passive")  # see oracle/oracle.py
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

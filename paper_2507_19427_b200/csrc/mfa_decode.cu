@@ -50,6 +50,9 @@ constexpr int kChunkBytes = 64 * 128;         // one 64-row x 128B swizzle panel
 #ifndef AFDK_MFA_NV
 #define AFDK_MFA_NV 3
 #endif
+#ifndef AFDK_MFA_BF16_PART
+#define AFDK_MFA_BF16_PART 1
+#endif
 #ifndef AFDK_MFA_PREFETCH
 #define AFDK_MFA_PREFETCH 0
 #endif
@@ -84,7 +87,7 @@ struct Params {
   int32_t* prefix_out;         // [B+1] pages-per-request prefix, written by CTA 0 for K3
   __nv_bfloat16* out;          // [B, 64, 256]
   float* lse;                  // [B, 64] natural log, optional
-  float* part_o;               // [(B+G), 64, 256]
+  float* part_o;               // [(B+G), 64, 256] split partials (bf16 when AFDK_MFA_BF16_PART)
   float* part_lse;             // [(B+G), 64] log2 domain
   int batch, max_pages;
   float scale_log2;            // softmax scale * log2(e)
@@ -446,11 +449,25 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
               dst[q4] = v;
             }
           } else {
+#if AFDK_MFA_BF16_PART
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.part_o) +
+                                                  ((size_t)slot * kHeads + head) * kDim + c * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint4 v;
+              v.x = pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv_l, __uint_as_float(o[8 * q4 + 1]) * inv_l);
+              v.y = pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv_l, __uint_as_float(o[8 * q4 + 3]) * inv_l);
+              v.z = pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv_l, __uint_as_float(o[8 * q4 + 5]) * inv_l);
+              v.w = pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv_l, __uint_as_float(o[8 * q4 + 7]) * inv_l);
+              dst[q4] = v;
+            }
+#else
             float4* dst = reinterpret_cast<float4*>(prm.part_o + ((size_t)slot * kHeads + head) * kDim + c * 32);
 #pragma unroll
             for (int q4 = 0; q4 < 8; ++q4)
               dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv_l, __uint_as_float(o[4 * q4 + 1]) * inv_l,
                                     __uint_as_float(o[4 * q4 + 2]) * inv_l, __uint_as_float(o[4 * q4 + 3]) * inv_l);
+#endif
           }
         }
       }
@@ -523,7 +540,15 @@ __global__ void __launch_bounds__(256) mfa_combine_kernel(const Params prm, int 
   for (int k = 0; k < n; ++k) {
     const float w = exp2f(s_w[hl][k] - m);
     wsum += w;
+#if AFDK_MFA_BF16_PART
+    const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(prm.part_o) +
+                                                            ((size_t)s_slot[k] * kHeads + head) * kDim + d));
+    const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+    const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+    const float4 v = make_float4(v01.x, v01.y, v23.x, v23.y);
+#else
     const float4 v = __ldcg(reinterpret_cast<const float4*>(prm.part_o + ((size_t)s_slot[k] * kHeads + head) * kDim + d));
+#endif
     acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
   }
   const float inv = 1.0f / wsum;

@@ -149,9 +149,11 @@ def moe_weight_bytes(n_experts):
     return n_experts * (3 * HIDDEN * INTER + 4 * (2 * INTER // 128 * HIDDEN // 128 + HIDDEN // 128 * INTER // 128))
 
 
-def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0):
+def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8"):
     """One FFN-side MoE layer (permute, gather, W13+SwiGLU+requant, W2, combine)
-    over T dispatched tokens, all 48 routed experts + the shared one on this GPU."""
+    over T dispatched tokens, all 48 routed experts + the shared one on this GPU.
+    fmt "fp8": e4m3 with 1x128 / 128x128 fp32 block scales (software-scaled
+    MMA); "mx": MXFP8 (UE8M0 per 32, hardware block-scaled MMA)."""
     g = torch.Generator(device="cpu").manual_seed(seed)
     n = E_ROUTED + 1
 
@@ -166,6 +168,11 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0):
          "s2": torch.full((n, HIDDEN // 128, INTER // 128), 0.5 / INTER ** 0.5, device=dev)}
     xq = e4m3((T, HIDDEN))
     xs = torch.full((T, HIDDEN // 128), 0.01, device=dev)
+    if fmt == "mx":
+        w = {"n_experts": E_ROUTED, "w13": w["w13"], "w2": w["w2"],
+             "sf13": torch.full((n, 2 * INTER, HIDDEN // 32), 120, dtype=torch.uint8, device=dev),
+             "sf2": torch.full((n, HIDDEN, INTER // 32), 120, dtype=torch.uint8, device=dev)}
+        xs = torch.full((T, HIDDEN // 32), 121, dtype=torch.uint8, device=dev)
     logits = torch.randn(T, E_ROUTED, generator=g).to(dev)
     top = torch.topk(logits, TOPK, dim=1)
     ids = top.indices.to(torch.int32).contiguous()
@@ -175,7 +182,10 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0):
     sp = stream.cuda_stream
 
     def step(i):
-        ctx.moe_ffn(w, xq, xs, ids, wts, out, stream=sp)
+        if fmt == "mx":
+            ctx.moe_ffn_mx(w, xq, xs, ids, wts, out, stream=sp)
+        else:
+            ctx.moe_ffn(w, xq, xs, ids, wts, out, stream=sp)
 
     for i in range(warmup):
         step(i)
@@ -192,7 +202,8 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0):
     flops = 2.0 * 3 * HIDDEN * INTER * (TOPK + 1) * T
     hbm_peak, tf_peak, kind = peaks()
     del w
-    return {"T": T, "ms_per_layer": ms, "tokens_per_s": T / (ms * 1e-3),
+    return {"T": T, "format": "mxfp8" if fmt == "mx" else "fp8_block128", "ms_per_layer": ms,
+            "tokens_per_s": T / (ms * 1e-3),
             "hbm": {"achieved": wbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": wbytes / (ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": wbytes,
                     "experts_touched": touched},

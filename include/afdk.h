@@ -182,6 +182,43 @@ typedef struct afdk_moe_args {
 
 afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a, afdk_stream stream);
 
+/* ------------------------------------- K5'/K7/K8/K9 MoE FFN (MXFP8 path)
+ * The large-batch variant of afdk_moe_ffn: all GEMM operands in OCP MXFP8
+ * (e4m3 + one UE8M0 scale per 32 elements along K), run on the hardware
+ * block-scaled tensor-core MMA.  Same routing, shared-expert and partial-sum
+ * semantics as afdk_moe_ffn (replaces the same ffn_flops accounting,
+ * costmodel.cpp:68-74); the SiLU(gate)*up intermediate is re-quantised to
+ * MXFP8.  Scale tensors are row-major with K/32 bytes per row:
+ *   sf13 [(n_local+1), 2*inter, hidden/32], sf2 [(n_local+1), hidden, inter/32].
+ * Limits: hidden % 512 == 0, inter % 512 == 0, E <= 64, k <= 8, T*k <= 65536. */
+typedef struct afdk_moe_mx_weights {
+  int hidden, inter, n_experts, top_k;
+  int expert_lo, expert_hi;
+  const void* w13;
+  const uint8_t* sf13;
+  const void* w2;
+  const uint8_t* sf2;
+} afdk_moe_mx_weights;
+
+typedef struct afdk_moe_mx_args {
+  int T;
+  const void* xq;        /* e4m3 [T, hidden]                         */
+  const uint8_t* xsf;    /* UE8M0 [T, hidden/32]                     */
+  const int32_t* ids;    /* [T, top_k]                               */
+  const float* weights;  /* [T, top_k]                               */
+  int shared_lo, shared_hi;
+  void* out;             /* bf16 [T, hidden] this rank's partial     */
+} afdk_moe_mx_args;
+
+afdk_status afdk_moe_ffn_mx(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
+                            afdk_stream stream);
+
+/* MXFP8 quantisation of the dispatch payload: x bf16 [T, H] -> q e4m3 [T, H]
+ * + sf UE8M0 [T, H/32].  Per 32 elements: e = smallest integer with
+ * amax <= 448 * 2^e (e = -127 for an all-zero block), sf = e + 127,
+ * q = e4m3_rn_satfinite(x * 2^-e).  H % 32 == 0. */
+afdk_status afdk_quant_mx(afdk_ctx* ctx, const void* x, int T, int H, void* q, uint8_t* sf, afdk_stream stream);
+
 /* ------------------------------------------- C1/C2 AFD exchange (NVLink)
  * Zero-SM point-to-point transport between attention and FFN GPUs of one
  * box (the StepMesh pattern of PAPER.md:701-724 on NVLink 5 / NVSwitch):

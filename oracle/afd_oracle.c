@@ -378,6 +378,116 @@ void orc_moe_layer_fp8(const uint8_t* xq, const float* xs, int T, int H, int I, 
   free(acc); free(y); free(gx); free(gs); free(rows_tok); free(rows_w);
 }
 
+/* ------------------------------------------------------------------ MXFP8 */
+/* smallest e with amax <= 448 * 2^e, from the exact binary exponent/mantissa
+ * of amax (448 = 1.75 * 2^8) */
+int orc_mx_exponent(float amax) {
+  if (!(amax > 0.0f)) return -127;
+  uint32_t u;
+  memcpy(&u, &amax, 4);
+  const int E = (int)((u >> 23) & 0xff);
+  const uint32_t M = u & 0x7fffffu;
+  if (E == 0) return -127; /* subnormal amax */
+  const int k = E - 127;
+  int e = (M <= 6291456u) ? k - 8 : k - 7; /* mantissa 1.M <= 1.75 */
+  if (e < -127) e = -127;
+  if (e > 127) e = 127;
+  return e;
+}
+
+float orc_mx_scale(uint8_t sf) { return ldexpf(1.0f, (int)sf - 127); }
+
+void orc_quant_mx(const float* x, int rows, int cols, uint8_t* q, uint8_t* sf) {
+  const int nb = cols / 32;
+  for (int r = 0; r < rows; ++r)
+    for (int b = 0; b < nb; ++b) {
+      const float* xb = x + (size_t)r * cols + (size_t)b * 32;
+      float amax = 0.0f;
+      for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(xb[i]));
+      const int e = orc_mx_exponent(amax);
+      sf[(size_t)r * nb + b] = (uint8_t)(e + 127);
+      const float inv = ldexpf(1.0f, -e);
+      for (int i = 0; i < 32; ++i) q[(size_t)r * cols + (size_t)b * 32 + i] = orc_f32_to_e4m3(xb[i] * inv);
+    }
+}
+
+void orc_expert_ffn_mx(const uint8_t* xq, const uint8_t* xsf, int rows, int H, int I,
+                       const uint8_t* w13, const uint8_t* sf13, const uint8_t* w2,
+                       const uint8_t* sf2, float* y) {
+  float lut[256];
+  for (int i = 0; i < 256; ++i) lut[i] = orc_e4m3_to_f32((uint8_t)i);
+  const int nbH = H / 32, nbI = I / 32;
+  float* hbuf = (float*)malloc(sizeof(float) * (size_t)rows * I);
+  uint8_t* hq = (uint8_t*)malloc((size_t)rows * I);
+  uint8_t* hsf = (uint8_t*)malloc((size_t)rows * nbI);
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int r = 0; r < rows; ++r)
+    for (int n = 0; n < I; ++n) {
+      double g = 0.0, u = 0.0;
+      for (int kb = 0; kb < nbH; ++kb) {
+        double ag = 0.0, au = 0.0;
+        for (int c = kb * 32; c < kb * 32 + 32; ++c) {
+          const double xv = lut[xq[(size_t)r * H + c]];
+          ag += xv * lut[w13[(size_t)n * H + c]];
+          au += xv * lut[w13[(size_t)(n + I) * H + c]];
+        }
+        const double sx = orc_mx_scale(xsf[(size_t)r * nbH + kb]);
+        g += ag * sx * orc_mx_scale(sf13[(size_t)n * nbH + kb]);
+        u += au * sx * orc_mx_scale(sf13[(size_t)(n + I) * nbH + kb]);
+      }
+      hbuf[(size_t)r * I + n] = silu((float)g) * (float)u;
+    }
+  orc_quant_mx(hbuf, rows, I, hq, hsf);
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int r = 0; r < rows; ++r)
+    for (int n = 0; n < H; ++n) {
+      double acc = 0.0;
+      for (int kb = 0; kb < nbI; ++kb) {
+        double a = 0.0;
+        for (int c = kb * 32; c < kb * 32 + 32; ++c)
+          a += (double)lut[hq[(size_t)r * I + c]] * lut[w2[(size_t)n * I + c]];
+        acc += a * orc_mx_scale(hsf[(size_t)r * nbI + kb]) * orc_mx_scale(sf2[(size_t)n * nbI + kb]);
+      }
+      y[(size_t)r * H + n] = (float)acc;
+    }
+  free(hbuf); free(hq); free(hsf);
+}
+
+void orc_moe_layer_mx(const uint8_t* xq, const uint8_t* xsf, int T, int H, int I, int E, int k,
+                      const int32_t* ids, const float* weights, const uint8_t* w13_all,
+                      const uint8_t* sf13_all, const uint8_t* w2_all, const uint8_t* sf2_all,
+                      int round_bf16, float* out) {
+  const int nbH = H / 32;
+  const size_t w13_sz = (size_t)2 * I * H, w2_sz = (size_t)H * I;
+  const size_t sf13_sz = (size_t)2 * I * nbH, sf2_sz = (size_t)H * (I / 32);
+  double* acc = (double*)calloc((size_t)T * H, sizeof(double));
+  float* y = (float*)malloc(sizeof(float) * (size_t)T * H);
+  uint8_t* gx = (uint8_t*)malloc((size_t)T * H);
+  uint8_t* gs = (uint8_t*)malloc((size_t)T * nbH);
+  int32_t* rows_tok = (int32_t*)malloc(sizeof(int32_t) * (size_t)T);
+  float* rows_w = (float*)malloc(sizeof(float) * (size_t)T);
+  for (int e = 0; e <= E; ++e) {
+    int n = 0;
+    for (int t = 0; t < T; ++t) {
+      if (e == E) { rows_tok[n] = t; rows_w[n] = 1.0f; ++n; continue; }
+      for (int j = 0; j < k; ++j)
+        if (ids[(size_t)t * k + j] == e) { rows_tok[n] = t; rows_w[n] = weights[(size_t)t * k + j]; ++n; }
+    }
+    if (n == 0) continue;
+    for (int r = 0; r < n; ++r) {
+      memcpy(gx + (size_t)r * H, xq + (size_t)rows_tok[r] * H, (size_t)H);
+      memcpy(gs + (size_t)r * nbH, xsf + (size_t)rows_tok[r] * nbH, (size_t)nbH);
+    }
+    orc_expert_ffn_mx(gx, gs, n, H, I, w13_all + e * w13_sz, sf13_all + e * sf13_sz, w2_all + e * w2_sz,
+                      sf2_all + e * sf2_sz, y);
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < H; ++c)
+        acc[(size_t)rows_tok[r] * H + c] += (double)rows_w[r] * y[(size_t)r * H + c];
+  }
+  for (size_t i = 0; i < (size_t)T * H; ++i) out[i] = maybe_bf16((float)acc[i], round_bf16);
+  free(acc); free(y); free(gx); free(gs); free(rows_tok); free(rows_w);
+}
+
 /* -------------------------------------------------------------- accounting */
 /* costmodel.cpp:26-44 (full attention): 2 * n_q * (qk + v) * ctx */
 double orc_mfa_core_flops(int n_heads, int head_dim, int64_t ctx) {

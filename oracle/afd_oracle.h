@@ -138,6 +138,26 @@ void orc_moe_layer_fp8(const uint8_t* xq, const float* xs, int T, int H, int I, 
                        const uint8_t* w2_all, const float* s2_all, int round_bf16,
                        float* out);
 
+/* ---- MXFP8 (OCP MX, e4m3 elements + one UE8M0 scale per 32) ----------- */
+/* Tensor-core block-scaled format used by the large-batch expert GEMMs.
+ * Per 32-element block: e = smallest integer with amax <= 448 * 2^e
+ * (amax == 0 -> e = -127), clamped to [-127, 127]; sf = e + 127 (UE8M0);
+ * q = e4m3_rn_satfinite(x * 2^-e) (exact power-of-two scaling). */
+int orc_mx_exponent(float amax);
+void orc_quant_mx(const float* x, int rows, int cols, uint8_t* q, uint8_t* sf);
+float orc_mx_scale(uint8_t sf); /* 2^(sf-127) */
+/* One gated expert, all operands MXFP8: xq [rows,H] + xsf [rows,H/32],
+ * w13 [2I,H] + sf13 [2I,H/32], w2 [H,I] + sf2 [H,I/32]; the SiLU(gate)*up
+ * intermediate is re-quantised to MXFP8 before W2. y [rows,H] fp32. */
+void orc_expert_ffn_mx(const uint8_t* xq, const uint8_t* xsf, int rows, int H, int I,
+                       const uint8_t* w13, const uint8_t* sf13, const uint8_t* w2,
+                       const uint8_t* sf2, float* y);
+/* Whole MoE layer in MXFP8 (weights of E routed + 1 shared expert stacked). */
+void orc_moe_layer_mx(const uint8_t* xq, const uint8_t* xsf, int T, int H, int I, int E, int k,
+                      const int32_t* ids, const float* weights, const uint8_t* w13_all,
+                      const uint8_t* sf13_all, const uint8_t* w2_all, const uint8_t* sf2_all,
+                      int round_bf16, float* out);
+
 /* ---- accounting (must equal the reference's analytic model) ------------- */
 /* attention-core FLOPs of one decode step for one request at ctx tokens */
 double orc_mfa_core_flops(int n_heads, int head_dim, int64_t ctx);

@@ -228,6 +228,49 @@ def moe_layer_fp8(xq, xs, ids, weights, w13_all, s13_all, w2_all, s2_all, round_
     return out
 
 
+def mx_exponent(amax: float) -> int:
+    orc().orc_mx_exponent.argtypes = [c_float]
+    return orc().orc_mx_exponent(c_float(amax))
+
+
+def quant_mx(x):
+    """MXFP8: e4m3 codes [rows, cols] + UE8M0 scales [rows, cols/32]."""
+    x = _f32(x)
+    rows, cols = x.shape
+    q = np.empty((rows, cols), np.uint8)
+    sf = np.empty((rows, cols // 32), np.uint8)
+    orc().orc_quant_mx(_p(x, c_float), c_int(rows), c_int(cols), _p(q, c_uint8), _p(sf, c_uint8))
+    return q, sf
+
+
+def mx_dequant(q, sf):
+    q = np.asarray(q, np.uint8)
+    return e4m3_to_f32(q) * np.exp2(np.repeat(np.asarray(sf, np.float64) - 127.0, 32, axis=-1)).astype(np.float32)
+
+
+def expert_ffn_mx(xq, xsf, w13, sf13, w2, sf2):
+    rows, H = xq.shape
+    I = w2.shape[1]
+    y = np.empty((rows, H), np.float32)
+    c8 = lambda a: _p(np.ascontiguousarray(a, dtype=np.uint8), c_uint8)
+    orc().orc_expert_ffn_mx(c8(xq), c8(xsf), c_int(rows), c_int(H), c_int(I), c8(w13), c8(sf13), c8(w2), c8(sf2),
+                            _p(y, c_float))
+    return y
+
+
+def moe_layer_mx(xq, xsf, ids, weights, w13_all, sf13_all, w2_all, sf2_all, round_bf16=True):
+    T, H = xq.shape
+    E = w13_all.shape[0] - 1
+    I = w2_all.shape[2]
+    k = ids.shape[1]
+    out = np.empty((T, H), np.float32)
+    c8 = lambda a: _p(np.ascontiguousarray(a, dtype=np.uint8), c_uint8)
+    orc().orc_moe_layer_mx(c8(xq), c8(xsf), c_int(T), c_int(H), c_int(I), c_int(E), c_int(k), _p(_i32(ids), c_int32),
+                           _p(_f32(weights), c_float), c8(w13_all), c8(sf13_all), c8(w2_all), c8(sf2_all),
+                           c_int(int(round_bf16)), _p(out, c_float))
+    return out
+
+
 def num_threads() -> int:
     return orc().orc_num_threads()
 

@@ -73,6 +73,21 @@ class MoeArgs(Structure):
     ]
 
 
+class MoeMxWeights(Structure):
+    _fields_ = [
+        ("hidden", c_int), ("inter", c_int), ("n_experts", c_int), ("top_k", c_int),
+        ("expert_lo", c_int), ("expert_hi", c_int),
+        ("w13", c_void_p), ("sf13", c_void_p), ("w2", c_void_p), ("sf2", c_void_p),
+    ]
+
+
+class MoeMxArgs(Structure):
+    _fields_ = [
+        ("T", c_int), ("xq", c_void_p), ("xsf", c_void_p), ("ids", c_void_p), ("weights", c_void_p),
+        ("shared_lo", c_int), ("shared_hi", c_int), ("out", c_void_p),
+    ]
+
+
 class StagePlan(Structure):
     _fields_ = [("attn_gpus", c_int), ("ffn_gpus", c_int), ("micro_batch", ctypes.c_longlong),
                 ("avg_ctx", ctypes.c_longlong), ("n_layers", c_int), ("hidden", c_int), ("link_gbs", ctypes.c_double)]
@@ -110,6 +125,8 @@ SIGNATURES = {
                                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_permute": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_ffn": (c_int, [c_void_p, POINTER(MoeWeights), POINTER(MoeArgs), c_void_p]),
+    "afdk_moe_ffn_mx": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), c_void_p]),
+    "afdk_quant_mx": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "afdk_ipc_handle": (c_int, [c_void_p, c_void_p, c_void_p]),
     "afdk_ipc_open": (c_int, [c_void_p, c_void_p, POINTER(c_void_p)]),
     "afdk_ipc_close": (c_int, [c_void_p, c_void_p]),
@@ -243,6 +260,23 @@ class Context:
         mw = MoeWeights(Hd, inter, E, k, expert_lo, hi, ptr(w["w13"]), ptr(w["s13"]), ptr(w["w2"]), ptr(w["s2"]))
         a = MoeArgs(T, ptr(xq), ptr(xs), ptr(ids), ptr(weights), sh_lo, sh_hi, ptr(out))
         check(self.lib.afdk_moe_ffn(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+
+    def moe_ffn_mx(self, w: dict, xq, xsf, ids, weights, out, expert_lo=0, expert_hi=None, shared=(0, None),
+                   stream: int = 0) -> None:
+        """MXFP8 path. w: n_experts, w13, sf13, w2, sf2 (local experts then the shared one)."""
+        T, Hd = xq.shape
+        k = ids.shape[1]
+        inter = w["w2"].shape[2]
+        E = w["n_experts"]
+        hi = E if expert_hi is None else expert_hi
+        sh_lo, sh_hi = shared[0], (T if shared[1] is None else shared[1])
+        mw = MoeMxWeights(Hd, inter, E, k, expert_lo, hi, ptr(w["w13"]), ptr(w["sf13"]), ptr(w["w2"]), ptr(w["sf2"]))
+        a = MoeMxArgs(T, ptr(xq), ptr(xsf), ptr(ids), ptr(weights), sh_lo, sh_hi, ptr(out))
+        check(self.lib.afdk_moe_ffn_mx(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+
+    def quant_mx(self, x, q, sf, stream: int = 0) -> None:
+        T, Hd = x.shape
+        check(self.lib.afdk_quant_mx(self.handle, ptr(x), T, Hd, ptr(q), ptr(sf), c_void_p(stream)))
 
     # ------------------------------------------------------- C1/C2 exchange
     def ipc_handle(self, t) -> bytes:

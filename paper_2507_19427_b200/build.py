@@ -20,6 +20,7 @@ CU_SOURCES = [
     "afdk_api.cu",
     "mfa_decode.cu",
     "linear.cu",
+    "moe_gemm_mx.cu",
     "mfa_layer.cu",
     "moe_route.cu",
     "moe_gemm.cu",

@@ -235,7 +235,8 @@ afdk_status afdk_moe_permute(afdk_ctx* ctx, const int32_t* ids, int T, int k, in
   uint8_t* ws = static_cast<uint8_t*>(afdk::workspace(c, wbytes));
   if (!ws) { set_error("afdk_moe_permute: workspace allocation failed"); return AFDK_ERR_CUDA; }
   afdk::moe::PermuteArgs a{ids, T, k, E, 0, E, 0, 0, 0, offsets, perm, inv,
-                           reinterpret_cast<afdk::moe::Work*>(ws), reinterpret_cast<int*>(ws + wbytes - 256)};
+                           reinterpret_cast<afdk::moe::Work*>(ws), reinterpret_cast<int*>(ws + wbytes - 256),
+                           afdk::moe::kChunk};
   const cudaError_t e = afdk::permute_launch(a, static_cast<cudaStream_t>(stream), ctx->c.pdl);
   if (e != cudaSuccess) return cuda_fail("afdk_moe_permute", e);
   return AFDK_OK;
@@ -271,6 +272,51 @@ afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_mo
   if (!ws) { set_error("afdk_moe_ffn: workspace allocation failed"); return AFDK_ERR_CUDA; }
   const cudaError_t e = afdk::moe_ffn_launch(c, m, ws, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return AFDK_ERR_CUDA;  // message set by moe_ffn_launch
+  return AFDK_OK;
+}
+
+afdk_status afdk_moe_ffn_mx(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
+                            afdk_stream stream) {
+  if (!ctx || !w || !a) { set_error("afdk_moe_ffn_mx: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }
+  if (w->hidden % 512 || w->inter % 512 || w->hidden < 512 || w->inter < 512) {
+    set_error("afdk_moe_ffn_mx: hidden and inter must be positive multiples of 512");
+    return AFDK_ERR_INVALID;
+  }
+  if (w->n_experts < 1 || w->n_experts > afdk::moe::kMaxExperts || w->top_k < 1 || w->top_k > afdk::moe::kMaxTopK) {
+    set_error("afdk_moe_ffn_mx: need 1 <= n_experts <= 64 and 1 <= top_k <= 8");
+    return AFDK_ERR_INVALID;
+  }
+  if (w->expert_lo < 0 || w->expert_hi > w->n_experts || w->expert_lo > w->expert_hi) {
+    set_error("afdk_moe_ffn_mx: expert range out of bounds");
+    return AFDK_ERR_INVALID;
+  }
+  if (a->T < 1 || a->T * w->top_k > 65536) { set_error("afdk_moe_ffn_mx: T out of range"); return AFDK_ERR_INVALID; }
+  if (!a->xq || !a->xsf || !a->ids || !a->weights || !a->out || !w->w13 || !w->sf13 || !w->w2 || !w->sf2) {
+    set_error("afdk_moe_ffn_mx: NULL tensor pointer");
+    return AFDK_ERR_INVALID;
+  }
+  afdk::Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  const int sh_lo = a->shared_lo < 0 ? 0 : a->shared_lo;
+  const int sh_hi = a->shared_hi > a->T ? a->T : a->shared_hi;
+  afdk::MoeFfnMxArgs m{a->T, w->top_k, w->n_experts, w->hidden, w->inter, w->expert_lo, w->expert_hi,
+                       w->w13, w->sf13, w->w2, w->sf2, static_cast<const uint8_t*>(a->xq), a->xsf, a->ids,
+                       a->weights, sh_lo, sh_hi, a->out};
+  void* ws = afdk::workspace(c, afdk::moe_ffn_mx_workspace_bytes(a->T, w->top_k, w->n_experts, w->hidden, w->inter));
+  if (!ws) { set_error("afdk_moe_ffn_mx: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  const cudaError_t e = afdk::moe_ffn_mx_launch(c, m, ws, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return AFDK_ERR_CUDA;
+  return AFDK_OK;
+}
+
+afdk_status afdk_quant_mx(afdk_ctx* ctx, const void* x, int T, int H, void* q, uint8_t* sf, afdk_stream stream) {
+  if (!ctx || !x || !q || !sf) { set_error("afdk_quant_mx: NULL argument"); return AFDK_ERR_INVALID; }
+  if (T < 0 || H <= 0 || H % 32) { set_error("afdk_quant_mx: need T >= 0 and H % 32 == 0"); return AFDK_ERR_INVALID; }
+  if (T == 0) return AFDK_OK;
+  cudaSetDevice(ctx->c.device);
+  afdk::moe::QuantMxArgs a{static_cast<const __nv_bfloat16*>(x), T, H, static_cast<uint8_t*>(q), sf};
+  const cudaError_t e = afdk::quant_mx_launch(a, static_cast<cudaStream_t>(stream), ctx->c.pdl);
+  if (e != cudaSuccess) return cuda_fail("afdk_quant_mx", e);
   return AFDK_OK;
 }
 

@@ -146,6 +146,38 @@ struct MoeFfnArgs {
 size_t moe_ffn_workspace_bytes(int T, int k, int E, int H, int I);
 cudaError_t moe_ffn_launch(Ctx& ctx, const MoeFfnArgs& a, void* ws, cudaStream_t stream);
 
+// MXFP8 path (hardware block-scaled MMA; moe_gemm_mx.cu)
+cudaError_t quant_mx_launch(const moe::QuantMxArgs& a, cudaStream_t stream, bool pdl);
+struct MoeGemmMxArgs {
+  const void* w;         // e4m3 [(n_local+1) * w_rows, K]
+  const uint8_t* w_sf;   // UE8M0 [(n_local+1) * w_rows, K/32]
+  const void* x;         // e4m3 [rows_pad, K]
+  const uint8_t* x_sf;   // UE8M0 [rows_pad, K/32]
+  const moe::Work* work;
+  const int* n_work;
+  int H, I, E, expert_lo, n_local, rows_pad;
+  uint8_t* hq;           // W13 outputs [rows_pad, I] + [rows_pad, I/32]
+  uint8_t* hsf;
+  float* y;              // W2 output [rows_pad, H]
+};
+cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream);
+struct MoeFfnMxArgs {
+  int T, k, E, H, I;
+  int expert_lo, expert_hi;
+  const void* w13;
+  const uint8_t* sf13;
+  const void* w2;
+  const uint8_t* sf2;
+  const uint8_t* xq;
+  const uint8_t* xsf;
+  const int32_t* ids;
+  const float* weights;
+  int shared_lo, shared_hi;
+  void* out;
+};
+size_t moe_ffn_mx_workspace_bytes(int T, int k, int E, int H, int I);
+cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws, cudaStream_t stream);
+
 // ---------------------------------------------------------- AFD exchange
 bool exchange_available();
 cudaError_t exchange_signal(uint32_t* flag, uint32_t value, cudaStream_t s);

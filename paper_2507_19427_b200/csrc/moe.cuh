@@ -10,6 +10,7 @@ namespace moe {
 constexpr int kMaxExperts = 64;  // routed experts (Step-3: 48)
 constexpr int kMaxTopK = 8;      // Step-3: 3
 constexpr int kChunk = 64;       // dispatched rows per GEMM work item (MMA N <= 64)
+constexpr int kChunkMX = 128;    // rows per work item of the MXFP8 (block-scaled MMA) GEMMs
 
 struct RouterArgs {
   const __nv_bfloat16* h;       // [T, H] post-attention RMSNorm output
@@ -38,6 +39,7 @@ struct PermuteArgs {
   int32_t* inv;        // [T*k] t*k+j -> slot
   Work* work;          // [max work]
   int* n_work;
+  int chunk;           // rows per work item (kChunk or kChunkMX)
 };
 
 struct GatherArgs {
@@ -47,6 +49,8 @@ struct GatherArgs {
   int T, k, H, rows_pad;
   uint8_t* xp;         // [rows_pad, H]  routed rows then shared rows
   float* xs_t;         // [H/128, rows_pad]
+  const uint8_t* xsf;  // MXFP8 mode (xs == nullptr): [T, H/32] UE8M0 scales
+  uint8_t* xsf_p;      //   gathered [rows_pad, H/32]
 };
 
 struct CombineArgs {
@@ -61,6 +65,16 @@ struct CombineArgs {
 
 inline int max_work(int T, int k, int E) { return E + (T * k) / kChunk + 1 + T / kChunk + 1; }
 inline int rows_pad(int T, int k) { return ((T * k + T + 127) / 128) * 128; }
+// MX work items read a full 128-row panel (scale rows by plain loads): keep
+// one spare panel so the last chunk never runs off the buffer
+inline int rows_pad_mx(int T, int k) { return rows_pad(T, k) + kChunkMX; }
+
+struct QuantMxArgs {
+  const __nv_bfloat16* x;  // [T, H]
+  int T, H;
+  uint8_t* q;              // [T, H] e4m3
+  uint8_t* sf;             // [T, H/32] UE8M0
+};
 
 }  // namespace moe
 }  // namespace afdk

@@ -1,0 +1,345 @@
+// moe_gemm_mx.cu — K7/K8 for large FFN batches: grouped MXFP8 expert GEMMs on
+// the hardware block-scaled tensor-core path (tcgen05.mma kind::mxf8f6f4
+// .block_scale).
+//
+// Same two GEMMs per gated expert as moe_gemm.cu (builtin_catalog.cpp:248-251,
+// 3*h*inter params per expert) and the same swap-AB orientation (a 128-row
+// weight tile is MMA M, up to 128 dispatched rows are N), but the operands carry
+// one UE8M0 scale per 32 K elements (OCP MX) and the tensor core applies them
+// inside the MMA.  The accumulator therefore spans the whole K loop in TMEM:
+// no per-k-block promotion by the epilogue warps, which is what bounds the
+// 1x128/128x128 software-scaled kernel once batches are large (PAPER.md:651,
+// the FFN side at hundreds of tokens per expert).
+//
+// Scale factors reach the tensor core through TMEM.  Per pipeline stage (one
+// 128-wide k-block) a ring slot holds 4 columns per operand; column j, lane i
+// of every 32-lane subpartition holds the 4 packed UE8M0 bytes (k sub-blocks
+// 0..3) of row 32j+i, and the k-step kk of the MMA selects byte kk through
+// the instruction descriptor's sf ids.  Four stager warps (one per
+// subpartition) load the packed scales with 16-byte loads (4 k-blocks at a
+// time, double-buffered in registers) and write them with tcgen05.st.
+//
+// Roles (320 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2-5
+// epilogue, w6-9 scale stagers.  TMEM: accumulators in columns [0,256) (W13:
+// gate | up of one item; W2: two 128-column buffers so the epilogue of item i
+// overlaps the MMAs of item i+1), scale ring from column 256.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp8.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "afdk_internal.h"
+#include "moe.cuh"
+#include "sm100.cuh"
+
+namespace afdk {
+namespace moe {
+
+using namespace sm100;
+
+constexpr int kMxThreads = 320;
+constexpr uint32_t kSfCol0 = 256;
+
+struct MxGemmParams {
+  const Work* work;
+  const int* n_work;
+  int m_tiles;          // output features / 128 (W13: per half)
+  int kblocks;          // K / 128 (multiple of 4)
+  int w_rows;           // weight rows per expert (W13: 2I, W2: H)
+  int up_offset;        // W13: row offset of the up half (= I)
+  const uint8_t* w_sf;  // [(n_local+1) * w_rows, K/32]
+  const uint8_t* x_sf;  // [rows_pad, K/32]
+  int E, expert_lo, n_local;
+  int out_cols;         // W13: I, W2: H
+  uint8_t* hq;          // W13 out: [rows_pad, I] e4m3
+  uint8_t* hsf;         // W13 out: [rows_pad, I/32] UE8M0
+  float* y;             // W2 out:  [rows_pad, H] fp32
+  int stage_bytes, stages;
+};
+
+__device__ __forceinline__ int mx_weight_index(const MxGemmParams& p, int group) {
+  return group == p.E ? p.n_local : group - p.expert_lo;
+}
+
+__device__ __forceinline__ int mx_exp(float amax) {
+  const uint32_t u = __float_as_uint(amax);
+  const int E = (int)((u >> 23) & 0xff);
+  if (!(amax > 0.0f) || E == 0) return -127;
+  const int e = ((u & 0x7fffffu) <= 6291456u) ? E - 135 : E - 134;
+  return max(-127, min(127, e));
+}
+
+__device__ __forceinline__ uint32_t u4_get(const uint4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+template <bool kGLU>
+__global__ void __launch_bounds__(kMxThreads, 1)
+moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                   const MxGemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kA = 128 * 128;
+  constexpr int kAOps = kGLU ? 2 : 1;
+  constexpr int kB = kChunkMX * 128;
+  constexpr int kAcc = kGLU ? 1 : 2;           // accumulator buffers
+  constexpr int kSfCols = 4 * kAOps + 4;       // scale columns per ring slot
+  const int S = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * p.stage_bytes);
+  uint64_t* sf_full = full + S;
+  uint64_t* empty = sf_full + S;
+  uint64_t* acc_full = empty + S;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = warp_id(), lane = threadIdx.x & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_w);
+    tma_prefetch_desc(&tm_x);
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&sf_full[i], 4); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  griddep_wait();
+  griddep_launch();
+  const uint32_t tmem = *tmem_slot;
+  const int n_work = *p.n_work;
+  const int n_items = n_work * p.m_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int i = 0;
+      for (int it = cta; it < n_items; it += G) {
+        const int mt = it / n_work;
+        const Work wk = p.work[it % n_work];
+        const int wrow = mx_weight_index(p, wk.group) * p.w_rows + mt * 128;
+        for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
+          const int s = i % S, n = i / S;
+          if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
+          uint8_t* st = smem + s * p.stage_bytes;
+          mbar_expect_tx(&full[s], kAOps * kA + kB);
+          tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol_w);
+          if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol_w);
+          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, wk.row0, pol_x);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int i = 0, li = 0;
+      for (int it = cta; it < n_items; it += G, ++li) {
+        const Work wk = p.work[it % n_work];
+        const int b = kGLU ? 0 : (li & 1);
+        const int nb = kGLU ? li : (li >> 1);
+        if (nb > 0) mbar_wait(&acc_empty[b], (nb & 1) ^ 1);
+        const uint32_t n_mma = (uint32_t)((wk.rows + 15) & ~15);
+        const uint32_t idesc = idesc_mxf8(128, n_mma);
+        for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
+          const int s = i % S, n = i / S;
+          mbar_wait(&full[s], n & 1);
+          mbar_wait(&sf_full[s], n & 1);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + s * p.stage_bytes);
+          const uint32_t b_base = base + kAOps * kA;
+          const uint32_t sf = tmem + kSfCol0 + (uint32_t)(s * kSfCols);
+#pragma unroll
+          for (int op = 0; op < kAOps; ++op) {
+            const uint32_t d = tmem + (kGLU ? op * 128 : b * 128);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t da = sdesc_sw128(base + op * kA + kk * 32, 0, 1024);
+              const uint64_t db = sdesc_sw128(b_base + kk * 32, 0, 1024);
+              const uint32_t sel = (uint32_t)kk << 30;
+              mma_mxf8(d, da, db, idesc | idesc_sf_ids(kk, kk), (sf + op * 4) | sel, (sf + kAOps * 4) | sel,
+                       (kb > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[s]);
+          if (kb == p.kblocks - 1) mma_commit(&acc_full[b]);
+        }
+      }
+    }
+  } else if (warp >= 6) {
+    // ------------------------------------------------------ scale stagers
+    const int sp = warp & 3;
+    const uint32_t t_lane = tmem + ((uint32_t)(sp * 32) << 16);
+    const int kq = p.kblocks * 4;  // scale bytes per row
+    int i = 0;
+    for (int it = cta; it < n_items; it += G) {
+      const int mt = it / n_work;
+      const Work wk = p.work[it % n_work];
+      const int wrow = mx_weight_index(p, wk.group) * p.w_rows + mt * 128;
+      const uint8_t* sa = p.w_sf + (size_t)(wrow + lane) * kq;
+      const uint8_t* su = p.w_sf + (size_t)(wrow + p.up_offset + lane) * kq;
+      const uint8_t* sb = p.x_sf + (size_t)(wk.row0 + lane) * kq;
+      // 16-byte loads cover 4 k-blocks of one row; rows 32j+lane, j = 0..3
+      uint4 ca[4], cu[4], cb[4];
+      auto load = [&](int g, uint4* la, uint4* lu, uint4* lb) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          la[j] = __ldg(reinterpret_cast<const uint4*>(sa + (size_t)32 * j * kq + g * 4));
+          if (kGLU) lu[j] = __ldg(reinterpret_cast<const uint4*>(su + (size_t)32 * j * kq + g * 4));
+          lb[j] = __ldg(reinterpret_cast<const uint4*>(sb + (size_t)32 * j * kq + g * 4));
+        }
+      };
+      load(0, ca, cu, cb);
+      for (int g = 0; g < p.kblocks; g += 4) {
+        uint4 na[4], nu[4], nb4[4];
+        const bool more = g + 4 < p.kblocks;
+        if (more) load(g + 4, na, nu, nb4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u, ++i) {
+          const int s = i % S, n = i / S;
+          if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
+          const uint32_t col = t_lane + kSfCol0 + (uint32_t)(s * kSfCols);
+          tmem_st4(col, u4_get(ca[0], u), u4_get(ca[1], u), u4_get(ca[2], u), u4_get(ca[3], u));
+          if (kGLU) tmem_st4(col + 4, u4_get(cu[0], u), u4_get(cu[1], u), u4_get(cu[2], u), u4_get(cu[3], u));
+          tmem_st4(col + kAOps * 4, u4_get(cb[0], u), u4_get(cb[1], u), u4_get(cb[2], u), u4_get(cb[3], u));
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sf_full[s]);
+        }
+        if (more) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) { ca[j] = na[j]; cu[j] = nu[j]; cb[j] = nb4[j]; }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int sub = warp & 3, feat = sub * 32 + lane;  // feature row within the tile
+    const uint32_t t_lane = tmem + ((uint32_t)(sub * 32) << 16);
+    int li = 0;
+    for (int it = cta; it < n_items; it += G, ++li) {
+      const int mt = it / n_work;
+      const Work wk = p.work[it % n_work];
+      const int b = kGLU ? 0 : (li & 1);
+      const int nb = kGLU ? li : (li >> 1);
+      mbar_wait(&acc_full[b], nb & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < kChunkMX / 32; ++c) {
+        if (c * 32 >= wk.rows) break;
+        uint32_t v[32];
+        tmem_ld32(t_lane + b * 128 + c * 32, v);
+        if (kGLU) {
+          uint32_t u[32];
+          tmem_ld32(t_lane + 128 + c * 32, u);
+          tmem_wait_ld();
+          // h = SiLU(gate) * up, re-quantised to MXFP8 over 32-feature blocks
+          // (this warp's 32 lanes = one block of the tile)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float g = __uint_as_float(v[j]);
+            const float h = (g / (1.0f + __expf(-g))) * __uint_as_float(u[j]);
+            float m = fabsf(h);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+            const int e = mx_exp(m);
+            const float inv = e < 127 ? __uint_as_float((uint32_t)(127 - e) << 23) : __uint_as_float(1u << 22);
+            const int r = c * 32 + j;
+            if (r < wk.rows) {
+              const size_t row = (size_t)wk.row0 + r;
+              p.hq[row * p.out_cols + mt * 128 + feat] =
+                  (uint8_t)__nv_cvt_float_to_fp8(h * inv, __NV_SATFINITE, __NV_E4M3);
+              if (lane == 0) p.hsf[row * (p.out_cols / 32) + mt * 4 + sub] = (uint8_t)(e + 127);
+            }
+          }
+        } else {
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int r = c * 32 + j;
+            if (r < wk.rows) p.y[((size_t)wk.row0 + r) * p.out_cols + mt * 128 + feat] = __uint_as_float(v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace moe
+
+cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream) {
+  using namespace moe;
+  CUtensorMap tw, tx;
+  const int K = glu ? a.H : a.I;
+  const int w_rows = glu ? 2 * a.I : a.H;
+  {
+    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)(a.n_local + 1) * w_rows};
+    const uint64_t strides[1] = {(uint64_t)K};
+    const uint32_t box[2] = {128, 128};
+    if (!encode_tma(ctx, &tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(a.w), dims, strides, box,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)a.rows_pad};
+    const uint64_t strides[1] = {(uint64_t)K};
+    const uint32_t box[2] = {128, kChunkMX};
+    if (!encode_tma(ctx, &tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(a.x), dims, strides, box,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  }
+  MxGemmParams p{};
+  p.work = a.work;
+  p.n_work = a.n_work;
+  p.m_tiles = glu ? a.I / 128 : a.H / 128;
+  p.kblocks = K / 128;
+  p.w_rows = w_rows;
+  p.up_offset = glu ? a.I : 0;
+  p.w_sf = a.w_sf;
+  p.x_sf = a.x_sf;
+  p.E = a.E;
+  p.expert_lo = a.expert_lo;
+  p.n_local = a.n_local;
+  p.out_cols = glu ? a.I : a.H;
+  p.hq = a.hq;
+  p.hsf = a.hsf;
+  p.y = a.y;
+  p.stage_bytes = (glu ? 2 : 1) * 128 * 128 + kChunkMX * 128;
+  p.stages = (200 * 1024) / p.stage_bytes;
+  if (p.stages > 6) p.stages = 6;
+  const size_t smem = (size_t)p.stages * p.stage_bytes + 1024 + 512;
+  cudaError_t e;
+  if (glu) {
+    static size_t attr = 0;
+    if (smem > attr) {
+      if ((e = cudaFuncSetAttribute(moe_gemm_mx_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess)
+        return e;
+      attr = smem;
+    }
+    return launch_k(ctx.pdl, moe_gemm_mx_kernel<true>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, p);
+  }
+  static size_t attr = 0;
+  if (smem > attr) {
+    if ((e = cudaFuncSetAttribute(moe_gemm_mx_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem)) != cudaSuccess)
+      return e;
+    attr = smem;
+  }
+  return launch_k(ctx.pdl, moe_gemm_mx_kernel<false>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, p);
+}
+
+}  // namespace afdk

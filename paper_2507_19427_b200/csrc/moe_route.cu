@@ -176,10 +176,10 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
       if (!local) continue;
       const int row0 = (e == a.E) ? n + a.shared_lo : s_off[e];
       const int rows = (e == a.E) ? a.shared_hi - a.shared_lo : s_cnt[e];
-      for (int r = 0; r < rows; r += kChunk) {
+      for (int r = 0; r < rows; r += a.chunk) {
         a.work[g].group = e;
         a.work[g].row0 = row0 + r;
-        a.work[g].rows = min(kChunk, rows - r);
+        a.work[g].rows = min(a.chunk, rows - r);
         ++g;
       }
     }
@@ -216,8 +216,65 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
   const uint4* in = reinterpret_cast<const uint4*>(a.xq + (size_t)src * a.H);
   uint4* out = reinterpret_cast<uint4*>(a.xp + (size_t)s * a.H);
   for (int i = threadIdx.x; i < a.H / 16; i += blockDim.x) out[i] = __ldg(in + i);
-  const int nb = a.H / 128;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) a.xs_t[(size_t)b * a.rows_pad + s] = __ldg(a.xs + (size_t)src * nb + b);
+  if (a.xs) {
+    const int nb = a.H / 128;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) a.xs_t[(size_t)b * a.rows_pad + s] = __ldg(a.xs + (size_t)src * nb + b);
+  } else {
+    const int nb = a.H / 32;  // MXFP8: copy the row's UE8M0 scales
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) a.xsf_p[(size_t)s * nb + b] = __ldg(a.xsf + (size_t)src * nb + b);
+  }
+}
+
+// ------------------------------------------------------- MXFP8 quantisation
+// One thread per 32-element block: e = smallest exponent with amax <= 448*2^e
+// (exact, from amax's exponent/mantissa bits), q = e4m3(x * 2^-e).
+__device__ __forceinline__ int mx_exponent(float amax) {
+  const uint32_t u = __float_as_uint(amax);
+  const int E = (int)((u >> 23) & 0xff);
+  if (!(amax > 0.0f) || E == 0) return -127;
+  const int e = ((u & 0x7fffffu) <= 6291456u) ? E - 135 : E - 134;
+  return max(-127, min(127, e));
+}
+__device__ __forceinline__ float mx_inv_scale(int e) {
+  return e < 127 ? __uint_as_float((uint32_t)(127 - e) << 23) : __uint_as_float(1u << 22);
+}
+
+__global__ void __launch_bounds__(256) quant_mx_kernel(QuantMxArgs a) {
+  sm100::griddep_wait();
+  sm100::griddep_launch();
+  const int nb = a.H / 32;
+  const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blk >= a.T * nb) return;
+  const uint4* src = reinterpret_cast<const uint4*>(a.x + (size_t)blk * 32);
+  float v[32];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 w = __ldg(src + c);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[c * 8 + 2 * j] = __uint_as_float(ws[j] << 16);
+      v[c * 8 + 2 * j + 1] = __uint_as_float(ws[j] & 0xffff0000u);
+    }
+  }
+  float amax = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) amax = fmaxf(amax, fabsf(v[j]));
+  const int e = mx_exponent(amax);
+  const float inv = mx_inv_scale(e);
+  uint32_t out[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      w |= (uint32_t)__nv_cvt_float_to_fp8(v[4 * j + b] * inv, __NV_SATFINITE, __NV_E4M3) << (8 * b);
+    out[j] = w;
+  }
+  uint4* dst = reinterpret_cast<uint4*>(a.q + (size_t)blk * 32);
+  dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+  dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+  a.sf[blk] = (uint8_t)(e + 127);
 }
 
 // --------------------------------------------------------------- K9 combine
@@ -268,6 +325,11 @@ cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream, bool 
 
 cudaError_t gather_launch(const moe::GatherArgs& a, cudaStream_t stream, bool pdl) {
   return launch_k(pdl, moe::gather_kernel, dim3(a.T * a.k + a.T), dim3(256), 0, stream, a);
+}
+
+cudaError_t quant_mx_launch(const moe::QuantMxArgs& a, cudaStream_t stream, bool pdl) {
+  const int n = a.T * (a.H / 32);
+  return launch_k(pdl, moe::quant_mx_kernel, dim3((n + 255) / 256), dim3(256), 0, stream, a);
 }
 
 cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream, bool pdl) {

@@ -148,6 +148,77 @@ def test_moe_layer_matches_per_expert_sum():
     np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-5)
 
 
+# ----------------------------------------------------------------- MXFP8
+def _np_mx_quant(x):
+    """independent restatement: smallest e with amax <= 448*2^e by search"""
+    rows, cols = x.shape
+    xb = x.reshape(rows, cols // 32, 32).astype(np.float64)
+    amax = np.abs(xb).max(axis=2)
+    e = np.full(amax.shape, -127, np.int64)
+    nz = amax > 0
+    e0 = np.floor(np.log2(np.where(nz, amax, 1.0))).astype(np.int64) - 10
+    for _ in range(4):
+        bump = nz & (amax > 448.0 * np.exp2(e0.astype(np.float64)))
+        e0 = e0 + bump
+    e = np.where(nz, np.clip(e0, -127, 127), -127)
+    scaled = (xb * np.exp2(-e.astype(np.float64))[..., None]).astype(np.float32).reshape(rows, cols)
+    return npr.quant_e4m3(scaled).reshape(rows, cols), (e + 127).astype(np.uint8)
+
+
+def test_mx_quant_vs_independent_numpy():
+    rng = np.random.default_rng(11)
+    x = (rng.standard_normal((64, 512)) * np.exp2(rng.integers(-30, 30, (64, 1)))).astype(np.float32)
+    x[0, :32] = 0.0
+    x[1, :32] = 448.0
+    x[2, 5] = 448.0 * 1.0000001
+    q, sf = orc.quant_mx(x)
+    nq, nsf = _np_mx_quant(x)
+    np.testing.assert_array_equal(sf, nsf)
+    np.testing.assert_array_equal(q, nq)
+    assert sf[0, 0] == 0 and sf[1, 0] == 127 and sf[2, 0] == 128
+    d = orc.mx_dequant(q, sf)
+    blk = np.abs(x).reshape(64, 16, 32).max(axis=2, keepdims=True)
+    assert np.all(np.abs(d - x).reshape(64, 16, 32) <= blk * 2.0 ** -4 + 1e-30)
+
+
+def test_expert_mx_vs_numpy_dequant():
+    rng = np.random.default_rng(12)
+    rows, H, I = 6, 256, 128
+    xq, xsf = orc.quant_mx(rng.standard_normal((rows, H)).astype(np.float32))
+    w13, sf13 = orc.quant_mx((rng.standard_normal((2 * I, H)) / 16).astype(np.float32))
+    w2, sf2 = orc.quant_mx((rng.standard_normal((H, I)) / 11).astype(np.float32))
+    y = orc.expert_ffn_mx(xq, xsf, w13, sf13, w2, sf2)
+    xd = orc.mx_dequant(xq, xsf).astype(np.float64)
+    gu = xd @ orc.mx_dequant(w13, sf13).astype(np.float64).T
+    g, u = gu[:, :I], gu[:, I:]
+    h = (g / (1 + np.exp(-g)) * u).astype(np.float32)
+    hq, hsf = _np_mx_quant(h)
+    ny = orc.mx_dequant(hq, hsf).astype(np.float64) @ orc.mx_dequant(w2, sf2).astype(np.float64).T
+    assert np.max(np.abs(ny - y)) <= 1e-2 * np.max(np.abs(ny))
+
+
+def test_moe_layer_mx_matches_per_expert_sum():
+    H, I, E, k, T = 256, 128, 4, 2, 9
+    rng = np.random.default_rng(13)
+    xq, xsf = orc.quant_mx(rng.standard_normal((T, H)).astype(np.float32))
+    w13 = np.zeros((E + 1, 2 * I, H), np.uint8)
+    sf13 = np.zeros((E + 1, 2 * I, H // 32), np.uint8)
+    w2 = np.zeros((E + 1, H, I), np.uint8)
+    sf2 = np.zeros((E + 1, H, I // 32), np.uint8)
+    for e in range(E + 1):
+        w13[e], sf13[e] = orc.quant_mx((rng.standard_normal((2 * I, H)) / 16).astype(np.float32))
+        w2[e], sf2[e] = orc.quant_mx((rng.standard_normal((H, I)) / 11).astype(np.float32))
+    ids, wts = orc.router_topk(rng.standard_normal((T, E)).astype(np.float32), k)
+    out = orc.moe_layer_mx(xq, xsf, ids, wts, w13, sf13, w2, sf2, round_bf16=False)
+    ref = np.zeros((T, H))
+    for t in range(T):
+        one = lambda e: orc.expert_ffn_mx(xq[t:t + 1], xsf[t:t + 1], w13[e], sf13[e], w2[e], sf2[e])[0]
+        ref[t] += one(E)
+        for j in range(k):
+            ref[t] += wts[t, j] * one(ids[t, j])
+    np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-5)
+
+
 # ------------------------------------------------------ accounting parity
 STEP3 = dict(hidden=7168, q_lora=2048, n_heads=64, head_dim=256, inter=5120, dense_inter=18432,
              layers=61, moe_layers=56, experts=48, topk=3)

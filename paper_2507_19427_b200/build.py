@@ -21,6 +21,7 @@ CU_SOURCES = [
     "mfa_decode.cu",
     "linear.cu",
     "moe_gemm_mx.cu",
+    "moe_gemm_mx2.cu",
     "mfa_layer.cu",
     "moe_route.cu",
     "moe_gemm.cu",

@@ -64,6 +64,28 @@ cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, 
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Same, launched as thread-block clusters of `cluster_x` CTAs (CTA pairs for
+// cta_group::2 tensor-core kernels).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_cluster_k(bool pdl, int cluster_x, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster_x;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 struct MfaDecodeArgs {
   int batch;
   const void* q;
@@ -161,6 +183,9 @@ struct MoeGemmMxArgs {
   float* y;              // W2 output [rows_pad, H]
 };
 cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream);
+cudaError_t moe_gemm_mx2_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream);
+// CTA-pair kernels once experts see enough rows (AFDK_MX_PAIR=0/1 forces)
+bool moe_mx_use_pair(int T, int k, int E);
 struct MoeFfnMxArgs {
   int T, k, E, H, I;
   int expert_lo, expert_hi;

@@ -11,6 +11,7 @@ constexpr int kMaxExperts = 64;  // routed experts (Step-3: 48)
 constexpr int kMaxTopK = 8;      // Step-3: 3
 constexpr int kChunk = 64;       // dispatched rows per GEMM work item (MMA N <= 64)
 constexpr int kChunkMX = 128;    // rows per work item of the MXFP8 (block-scaled MMA) GEMMs
+constexpr int kChunkMX2 = 256;   // rows per work item of the CTA-pair MXFP8 GEMMs
 
 struct RouterArgs {
   const __nv_bfloat16* h;       // [T, H] post-attention RMSNorm output

@@ -15,9 +15,17 @@
 // 128-wide k-block) a ring slot holds 4 columns per operand; column j, lane i
 // of every 32-lane subpartition holds the 4 packed UE8M0 bytes (k sub-blocks
 // 0..3) of row 32j+i, and the k-step kk of the MMA selects byte kk through
-// the instruction descriptor's sf ids.  Four stager warps (one per
-// subpartition) load the packed scales with 16-byte loads (4 k-blocks at a
-// time, double-buffered in registers) and write them with tcgen05.st.
+// the instruction descriptor's sf ids.  The producer TMA-loads the packed
+// scales of 4 k-blocks at a time (one 16 B x 128-row box per operand, from the
+// row-major [rows, K/32] UE8M0 arrays) into a 2-slot smem ring; four stager
+// warps (one per TMEM subpartition) read them from smem and write the TMEM
+// slot with tcgen05.st.
+//
+// Items are ordered chunk-major (all m-tiles of a chunk, then the next chunk;
+// an expert's chunks are adjacent), so the ~148 concurrently running items
+// cover a few chunks of one or two experts: each weight tile is fetched from
+// HBM about once and shared in L2 by the expert's chunks, each activation
+// panel by the m-tiles of its chunk.
 //
 // Roles (320 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2-5
 // epilogue, w6-9 scale stagers.  TMEM: accumulators in columns [0,256) (W13:
@@ -78,6 +86,7 @@ __device__ __forceinline__ uint32_t u4_get(const uint4& v, int i) {
 template <bool kGLU>
 __global__ void __launch_bounds__(kMxThreads, 1)
 moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                   const __grid_constant__ CUtensorMap tm_wsf, const __grid_constant__ CUtensorMap tm_xsf,
                    const MxGemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -86,13 +95,18 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
   constexpr int kB = kChunkMX * 128;
   constexpr int kAcc = kGLU ? 1 : 2;           // accumulator buffers
   constexpr int kSfCols = 4 * kAOps + 4;       // scale columns per ring slot
+  constexpr int kSfOp = 128 * 16;              // one operand's scales for 4 k-blocks
+  constexpr int kSfGrp = (kAOps + 1) * kSfOp;  // smem scale group (4 k-blocks)
   const int S = p.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * p.stage_bytes);
+  uint8_t* sfbuf = smem + S * p.stage_bytes;   // 2 x kSfGrp
+  uint64_t* full = reinterpret_cast<uint64_t*>(sfbuf + 2 * kSfGrp);
   uint64_t* sf_full = full + S;
   uint64_t* empty = sf_full + S;
   uint64_t* acc_full = empty + S;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* sfg_full = acc_empty + 2;
+  uint64_t* sfg_empty = sfg_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfg_empty + 2);
 
   const int warp = warp_id(), lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -100,8 +114,15 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_wsf);
+    tma_prefetch_desc(&tm_xsf);
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&sf_full[i], 4); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);
+      mbar_init(&sfg_full[i], 1);
+      mbar_init(&sfg_empty[i], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -116,21 +137,32 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
-      int i = 0;
+      // weight tiles are shared by the expert's concurrently running chunks and
+      // activation panels by the m-tiles of the same chunk: no eviction hints
+      const uint64_t pol = policy_evict_normal();
+      int i = 0, gi = 0;
       for (int it = cta; it < n_items; it += G) {
-        const int mt = it / n_work;
-        const Work wk = p.work[it % n_work];
+        const int mt = it % p.m_tiles;
+        const Work wk = p.work[it / p.m_tiles];
         const int wrow = mx_weight_index(p, wk.group) * p.w_rows + mt * 128;
         for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
+          if ((kb & 3) == 0) {  // scale group of k-blocks kb..kb+3
+            const int g = gi & 1, ng = gi >> 1;
+            ++gi;
+            if (ng > 0) mbar_wait(&sfg_empty[g], (ng & 1) ^ 1);
+            uint8_t* dst = sfbuf + g * kSfGrp;
+            mbar_expect_tx(&sfg_full[g], kSfGrp);
+            tma_load_2d(dst, &tm_wsf, &sfg_full[g], kb * 4, wrow, pol);
+            if (kGLU) tma_load_2d(dst + kSfOp, &tm_wsf, &sfg_full[g], kb * 4, wrow + p.up_offset, pol);
+            tma_load_2d(dst + kAOps * kSfOp, &tm_xsf, &sfg_full[g], kb * 4, wk.row0, pol);
+          }
           const int s = i % S, n = i / S;
           if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
           uint8_t* st = smem + s * p.stage_bytes;
           mbar_expect_tx(&full[s], kAOps * kA + kB);
-          tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol_w);
-          if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol_w);
-          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, wk.row0, pol_x);
+          tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol);
+          if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol);
+          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, wk.row0, pol);
         }
       }
     }
@@ -138,7 +170,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     if (lane == 0) {
       int i = 0, li = 0;
       for (int it = cta; it < n_items; it += G, ++li) {
-        const Work wk = p.work[it % n_work];
+        const Work wk = p.work[it / p.m_tiles];
         const int b = kGLU ? 0 : (li & 1);
         const int nb = kGLU ? li : (li >> 1);
         if (nb > 0) mbar_wait(&acc_empty[b], (nb & 1) ^ 1);
@@ -173,47 +205,28 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     // ------------------------------------------------------ scale stagers
     const int sp = warp & 3;
     const uint32_t t_lane = tmem + ((uint32_t)(sp * 32) << 16);
-    const int kq = p.kblocks * 4;  // scale bytes per row
-    int i = 0;
+    int i = 0, gi = 0;
     for (int it = cta; it < n_items; it += G) {
-      const int mt = it / n_work;
-      const Work wk = p.work[it % n_work];
-      const int wrow = mx_weight_index(p, wk.group) * p.w_rows + mt * 128;
-      const uint8_t* sa = p.w_sf + (size_t)(wrow + lane) * kq;
-      const uint8_t* su = p.w_sf + (size_t)(wrow + p.up_offset + lane) * kq;
-      const uint8_t* sb = p.x_sf + (size_t)(wk.row0 + lane) * kq;
-      // 16-byte loads cover 4 k-blocks of one row; rows 32j+lane, j = 0..3
-      uint4 ca[4], cu[4], cb[4];
-      auto load = [&](int g, uint4* la, uint4* lu, uint4* lb) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          la[j] = __ldg(reinterpret_cast<const uint4*>(sa + (size_t)32 * j * kq + g * 4));
-          if (kGLU) lu[j] = __ldg(reinterpret_cast<const uint4*>(su + (size_t)32 * j * kq + g * 4));
-          lb[j] = __ldg(reinterpret_cast<const uint4*>(sb + (size_t)32 * j * kq + g * 4));
+      for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
+        const int g = gi & 1;
+        if ((kb & 3) == 0) mbar_wait(&sfg_full[g], (gi >> 1) & 1);
+        const int s = i % S, n = i / S;
+        if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
+        // row r's 4 packed k-block scales sit at r*16 bytes of the operand's box
+        const uint32_t* grp = reinterpret_cast<const uint32_t*>(sfbuf + g * kSfGrp) + (kb & 3) + lane * 4;
+        const uint32_t col = t_lane + kSfCol0 + (uint32_t)(s * kSfCols);
+        tmem_st4(col, grp[0], grp[128], grp[256], grp[384]);
+        if (kGLU) tmem_st4(col + 4, grp[512], grp[512 + 128], grp[512 + 256], grp[512 + 384]);
+        const uint32_t* gb = grp + kAOps * 512;
+        tmem_st4(col + kAOps * 4, gb[0], gb[128], gb[256], gb[384]);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&sf_full[s]);
+          if ((kb & 3) == 3 || kb == p.kblocks - 1) mbar_arrive(&sfg_empty[g]);
         }
-      };
-      load(0, ca, cu, cb);
-      for (int g = 0; g < p.kblocks; g += 4) {
-        uint4 na[4], nu[4], nb4[4];
-        const bool more = g + 4 < p.kblocks;
-        if (more) load(g + 4, na, nu, nb4);
-#pragma unroll
-        for (int u = 0; u < 4; ++u, ++i) {
-          const int s = i % S, n = i / S;
-          if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
-          const uint32_t col = t_lane + kSfCol0 + (uint32_t)(s * kSfCols);
-          tmem_st4(col, u4_get(ca[0], u), u4_get(ca[1], u), u4_get(ca[2], u), u4_get(ca[3], u));
-          if (kGLU) tmem_st4(col + 4, u4_get(cu[0], u), u4_get(cu[1], u), u4_get(cu[2], u), u4_get(cu[3], u));
-          tmem_st4(col + kAOps * 4, u4_get(cb[0], u), u4_get(cb[1], u), u4_get(cb[2], u), u4_get(cb[3], u));
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sf_full[s]);
-        }
-        if (more) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) { ca[j] = na[j]; cu[j] = nu[j]; cb[j] = nb4[j]; }
-        }
+        if ((kb & 3) == 3 || kb == p.kblocks - 1) ++gi;
       }
     }
   } else {
@@ -222,8 +235,8 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     const uint32_t t_lane = tmem + ((uint32_t)(sub * 32) << 16);
     int li = 0;
     for (int it = cta; it < n_items; it += G, ++li) {
-      const int mt = it / n_work;
-      const Work wk = p.work[it % n_work];
+      const int mt = it % p.m_tiles;
+      const Work wk = p.work[it / p.m_tiles];
       const int b = kGLU ? 0 : (li & 1);
       const int nb = kGLU ? li : (li >> 1);
       mbar_wait(&acc_full[b], nb & 1);
@@ -301,6 +314,23 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
                     CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
+  CUtensorMap twsf, txsf;
+  {
+    const uint64_t dims[2] = {(uint64_t)(K / 32), (uint64_t)(a.n_local + 1) * w_rows};
+    const uint64_t strides[1] = {(uint64_t)(K / 32)};
+    const uint32_t box[2] = {16, 128};
+    if (!encode_tma(ctx, &twsf, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.w_sf), dims, strides, box,
+                    CU_TENSOR_MAP_SWIZZLE_NONE))
+      return cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)(K / 32), (uint64_t)a.rows_pad};
+    const uint64_t strides[1] = {(uint64_t)(K / 32)};
+    const uint32_t box[2] = {16, 128};
+    if (!encode_tma(ctx, &txsf, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.x_sf), dims, strides, box,
+                    CU_TENSOR_MAP_SWIZZLE_NONE))
+      return cudaErrorInvalidValue;
+  }
   MxGemmParams p{};
   p.work = a.work;
   p.n_work = a.n_work;
@@ -318,9 +348,9 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
   p.hsf = a.hsf;
   p.y = a.y;
   p.stage_bytes = (glu ? 2 : 1) * 128 * 128 + kChunkMX * 128;
-  p.stages = (200 * 1024) / p.stage_bytes;
+  p.stages = (196 * 1024) / p.stage_bytes;
   if (p.stages > 6) p.stages = 6;
-  const size_t smem = (size_t)p.stages * p.stage_bytes + 1024 + 512;
+  const size_t smem = (size_t)p.stages * p.stage_bytes + 2 * (glu ? 3 : 2) * 2048 + 1024 + 512;
   cudaError_t e;
   if (glu) {
     static size_t attr = 0;
@@ -330,7 +360,7 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
         return e;
       attr = smem;
     }
-    return launch_k(ctx.pdl, moe_gemm_mx_kernel<true>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, p);
+    return launch_k(ctx.pdl, moe_gemm_mx_kernel<true>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, twsf, txsf, p);
   }
   static size_t attr = 0;
   if (smem > attr) {
@@ -339,7 +369,7 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
       return e;
     attr = smem;
   }
-  return launch_k(ctx.pdl, moe_gemm_mx_kernel<false>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, p);
+  return launch_k(ctx.pdl, moe_gemm_mx_kernel<false>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, twsf, txsf, p);
 }
 
 }  // namespace afdk

@@ -78,29 +78,46 @@ def run_moe_mx(ctx, T, H, I, E, k, seed, ranges=None):
     return got, ref
 
 
+# "0": single-CTA kernels (128-row items), "1": CTA-pair kernels (256-row items)
+KERNELS = ["0", "1"]
+
+
+@pytest.fixture(params=KERNELS, ids=["cta", "pair"])
+def mx_kernel(request, monkeypatch):
+    monkeypatch.setenv("AFDK_MX_PAIR", request.param)
+    return request.param
+
+
 @pytest.mark.gpu
-def test_moe_ffn_mx_small(ctx):
+def test_moe_ffn_mx_small(ctx, mx_kernel):
     got, ref = run_moe_mx(ctx, 33, 512, 512, 8, 2, 1)
     assert np.isfinite(got).all()
     assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu
-def test_moe_ffn_mx_many_rows_per_expert(ctx):
-    """> 128 rows for one expert (several work chunks) and a ragged last chunk."""
+def test_moe_ffn_mx_many_rows_per_expert(ctx, mx_kernel):
+    """> 256 rows for one expert (several work chunks) and a ragged last chunk."""
     got, ref = run_moe_mx(ctx, 300, 512, 1024, 4, 2, 3)
     assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu
-def test_moe_ffn_mx_step3_dims_reduced_experts(ctx):
+def test_moe_ffn_mx_step3_dims_reduced_experts(ctx, mx_kernel):
     """hidden 7168 / inter 5120 (Step-3 expert shape), 8 routed + shared, top-3."""
     got, ref = run_moe_mx(ctx, 40, 7168, 5120, 8, 3, 2)
     assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu
-def test_moe_ffn_mx_expert_parallel_partials(ctx):
+def test_moe_ffn_mx_step3_dims_large_batch(ctx, mx_kernel):
+    """Step-3 expert shape at ~200 rows per expert (the tensor-bound regime)."""
+    got, ref = run_moe_mx(ctx, 400, 7168, 5120, 4, 2, 5)
+    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+
+
+@pytest.mark.gpu
+def test_moe_ffn_mx_expert_parallel_partials(ctx, mx_kernel):
     T = 50
     got, ref = run_moe_mx(ctx, T, 512, 512, 8, 3, 4, ranges=[((0, 4), (0, 20)), ((4, 8), (20, T))])
     assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)

@@ -558,7 +558,10 @@ def main():
         long_ctx = run_long_context(ctx, torch, dev, max(3, args.steps // 4))
     moe = None
     if not args.no_moe:
-        moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=rank) for T in (256, 4096)]
+        # config 3 FFN layer: 1x128/128x128 fp8 (software-scaled) and MXFP8
+        # (hardware block-scaled; CTA-pair kernels at >= 64 rows/expert)
+        moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=rank, fmt=f)
+               for f, T in (("fp8", 256), ("fp8", 4096), ("mx", 256), ("mx", 4096), ("mx", 8192))]
     afd = None
     if not args.no_afd:
         try:

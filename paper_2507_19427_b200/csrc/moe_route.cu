@@ -141,41 +141,56 @@ __global__ void __launch_bounds__(256) router_kernel(RouterArgs a) {
 }
 
 // ------------------------------------------------------------- K6 permute
-// One CTA.  ids staged in smem; warp w owns experts w and w+32.  Two ballot
-// passes (count, scatter) give the stable (expert, token, j) order exactly.
-// Also emits the grouped-GEMM work list: chunks of <= kChunk rows per group,
-// groups 0..E-1 routed (rows at offsets[e]) and group E = shared expert over
-// all T tokens (rows 3T.. of the dispatch buffer).
+// One CTA of 32 warps; warp w owns the contiguous entry segment w of the
+// [T*k] routing.  Pass 1 counts each expert per segment (__match_any_sync
+// groups equal experts within a 32-entry batch); the per-(segment, expert)
+// counts are scanned into slot bases in expert-major, segment-minor order;
+// pass 2 repeats the batches and places every entry at base + running count
+// + rank within its batch.  Segments are in entry order, so the result is the
+// stable (expert, token, j) permutation exactly.  Also emits the grouped-GEMM
+// work list: chunks of <= a.chunk rows per group, groups 0..E-1 routed (rows
+// at offsets[e]) and group E = shared expert over its token range.
 __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
   extern __shared__ uint8_t s_ids[];
-  __shared__ int s_cnt[kMaxExperts], s_off[kMaxExperts + 1];
+  __shared__ int s_cnt[32][kMaxExperts];
+  __shared__ int s_tot[kMaxExperts], s_off[kMaxExperts + 1];
   sm100::griddep_wait();
   sm100::griddep_launch();
   const int n = a.T * a.k;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s_ids[i] = (uint8_t)a.ids[i];
+  for (int i = threadIdx.x; i < 32 * kMaxExperts; i += blockDim.x) (&s_cnt[0][0])[i] = 0;
   __syncthreads();
-  for (int e = warp; e < a.E; e += 32) {
-    int c = 0;
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      c += __popc(__ballot_sync(0xffffffff, i < n && s_ids[i] == e));
-    }
-    if (lane == 0) s_cnt[e] = c;
+  const int seg = (n + 31) / 32;
+  const int lo = warp * seg, hi = min(n, lo + seg);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int base = lo; base < hi; base += 32) {
+    const int i = base + lane;
+    const bool valid = i < hi;
+    const int e = valid ? s_ids[i] : 255;
+    const unsigned m = __match_any_sync(0xffffffff, e);
+    if (valid && (m & lt) == 0) s_cnt[warp][e] += __popc(m);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x < a.E) {
+    const int e = threadIdx.x;
+    int run = 0;
+    for (int w = 0; w < 32; ++w) { const int c = s_cnt[w][e]; s_cnt[w][e] = run; run += c; }
+    s_tot[e] = run;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     int run = 0;
-    for (int e = 0; e < a.E; ++e) { s_off[e] = run; run += s_cnt[e]; }
+    for (int e = 0; e < a.E; ++e) { s_off[e] = run; run += s_tot[e]; }
     s_off[a.E] = run;
     for (int e = 0; e <= a.E; ++e) a.offsets[e] = s_off[e];
-    // work list (group, first row, rows)
     int g = 0;
     for (int e = 0; e <= a.E; ++e) {
       const bool local = (e == a.E) ? a.shared_local : (e >= a.expert_lo && e < a.expert_hi);
       if (!local) continue;
       const int row0 = (e == a.E) ? n + a.shared_lo : s_off[e];
-      const int rows = (e == a.E) ? a.shared_hi - a.shared_lo : s_cnt[e];
+      const int rows = (e == a.E) ? a.shared_hi - a.shared_lo : s_tot[e];
       for (int r = 0; r < rows; r += a.chunk) {
         a.work[g].group = e;
         a.work[g].row0 = row0 + r;
@@ -186,20 +201,22 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
     *a.n_work = g;
   }
   __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
-  for (int e = warp; e < a.E; e += 32) {
-    int run = s_off[e];
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      const bool hit = i < n && s_ids[i] == e;
-      const unsigned m = __ballot_sync(0xffffffff, hit);
-      if (hit) {
-        const int pos = run + __popc(m & lt);
-        a.perm[pos] = i;
-        a.inv[i] = pos;
-      }
-      run += __popc(m);
+  if (threadIdx.x < a.E)
+    for (int w = 0; w < 32; ++w) s_cnt[w][threadIdx.x] += s_off[threadIdx.x];
+  __syncthreads();
+  for (int base = lo; base < hi; base += 32) {
+    const int i = base + lane;
+    const bool valid = i < hi;
+    const int e = valid ? s_ids[i] : 255;
+    const unsigned m = __match_any_sync(0xffffffff, e);
+    if (valid) {
+      const int pos = s_cnt[warp][e] + __popc(m & lt);
+      a.perm[pos] = i;
+      a.inv[i] = pos;
     }
+    __syncwarp();
+    if (valid && (m & lt) == 0) s_cnt[warp][e] += __popc(m);
+    __syncwarp();
   }
 }
 

@@ -374,8 +374,10 @@ def cpu_layer_sample(n_req, ctx_len, seed=0):
          "q_norm": np.ones(QL, np.float32), "q_up": wt((H * D, QL), QL), "o": wt((HIDDEN, H * D), H * D),
          "post_norm": np.ones(HIDDEN, np.float32)}
     x = rng.standard_normal((n_req, HIDDEN), dtype=np.float32)
-    kc = rng.standard_normal((n_req * pages, PAGE, D), dtype=np.float32)
-    vc = rng.standard_normal((n_req * pages, PAGE, D), dtype=np.float32)
+    # KV contents do not change the op count: tile one random 4 MB block
+    pool = rng.standard_normal((2, 16, PAGE, D), dtype=np.float32)
+    kc = np.resize(pool[0], (n_req * pages, PAGE, D))
+    vc = np.resize(pool[1], (n_req * pages, PAGE, D))
     bt = np.arange(n_req * pages, dtype=np.int32).reshape(n_req, pages)
     sl = np.full(n_req, ctx_len, np.int32)
     dims = dict(hidden=HIDDEN, q_lora=QL, n_heads=H, head_dim=D, page=PAGE)
@@ -388,8 +390,8 @@ def cpu_layer_sample(n_req, ctx_len, seed=0):
 def run_reference(args):
     if int(os.environ.get("RANK", "0")) != 0:
         return  # rank 0 alone runs the CPU reference arm
-    sample = 2
-    for _ in range(args.warmup):
+    sample = args.batch  # the whole config-2 batch per step (~1-2 s of CPU work on 16 threads)
+    for _ in range(min(args.warmup, 1)):
         cpu_layer_sample(1, 256)
     vals, total = [], 0.0
     for s in range(args.steps):
@@ -575,9 +577,9 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            v, dt, cores = cpu_layer_sample(2, args.ctx)
+            v, dt, cores = cpu_layer_sample(args.batch, args.ctx)
             cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
-                   "sample": f"2 requests x {args.ctx} ctx, full attention-side layer "
+                   "sample": f"{args.batch} requests x {args.ctx} ctx (the whole config-2 batch), full attention-side layer "
                              f"(oracle/afd_oracle.c orc_mfa_layer, OpenMP), {dt:.2f} s"}
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")

@@ -91,6 +91,16 @@ typedef struct afdk_mfa_decode_args {
 afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args* a,
                                       afdk_stream stream);
 
+/* Same core over an e4m3 KV cache (512 B per token per layer: the
+ * kv_token_bytes the reference charges Step-3, builtin_catalog.cpp:11,242;
+ * the paper's FP8 attention).  k_cache / v_cache hold e4m3
+ * codes [num_pages, page_size, head_dim], dequantised by the per-tensor
+ * k_scale / v_scale (> 0).  q stays bf16; the kernel quantises it per
+ * (request, head) with scale = max(amax,1e-10)/448 and runs Q.K^T and P.V as
+ * FP8 tensor-core MMAs (P rounded to e4m3); out/lse as above.            */
+afdk_status afdk_mfa_decode_attention_fp8(afdk_ctx* ctx, const afdk_mfa_decode_args* a, float k_scale,
+                                          float v_scale, afdk_stream stream);
+
 /* ------------------------------------------------------------ K1/K4 GEMM
  * y[m, n] = x[m, k] . w[n, k]^T, bf16 inputs, fp32 accumulate, decode-shaped
  * (1 <= m <= 256, k % 64 == 0).  out is bf16 (out_fp32 = 0) or fp32.      */

@@ -134,6 +134,25 @@ def mfa_decode_attention(q, k_cache, v_cache, block_table, seq_lens, scale, roun
     return out, lse
 
 
+def mfa_decode_attention_fp8(q, kq, vq, k_scale, v_scale, block_table, seq_lens, scale, round_bf16=False):
+    """FP8-KV MFA decode (the paper's production setting).
+
+    Semantics: K = e4m3(kq)*k_scale, V = e4m3(vq)*v_scale (per-tensor scales,
+    512 B of KV per token, builtin_catalog.cpp:242); the query of every
+    (request, head) is quantised like the dispatch payload with one block of
+    256 (scale = max(amax,1e-10)/448, orc_quant_fp8_rowblock); attention is then
+    exact (double) on the dequantised Q/K/V.  The B200 kernel additionally
+    rounds the softmax probabilities to e4m3 for the P.V tensor-core MMA
+    (stated tolerance in tests/test_mfa_fp8_gpu.py)."""
+    q = _f32(q)
+    B, H, D = q.shape
+    qq, qs = quant_fp8_rowblock(q.reshape(B * H, D), block=D)
+    qd = (e4m3_to_f32(qq) * qs).reshape(B, H, D)
+    kd = e4m3_to_f32(kq) * np.float32(k_scale)
+    vd = e4m3_to_f32(vq) * np.float32(v_scale)
+    return mfa_decode_attention(qd, kd, vd, block_table, seq_lens, scale, round_bf16=round_bf16)
+
+
 class MfaDims(ctypes.Structure):
     _fields_ = [("hidden", c_int), ("q_lora", c_int), ("n_heads", c_int), ("head_dim", c_int),
                 ("page", c_int), ("rms_eps", c_float), ("rope_theta", c_float),

@@ -125,6 +125,7 @@ SIGNATURES = {
                                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_permute": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_ffn": (c_int, [c_void_p, POINTER(MoeWeights), POINTER(MoeArgs), c_void_p]),
+    "afdk_mfa_decode_attention_fp8": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_float, c_float, c_void_p]),
     "afdk_moe_ffn_mx": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), c_void_p]),
     "afdk_quant_mx": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "afdk_ipc_handle": (c_int, [c_void_p, c_void_p, c_void_p]),
@@ -210,6 +211,16 @@ class Context:
                           k_cache.shape[0], ptr(block_table), block_table.shape[1], ptr(seq_lens),
                           softmax_scale, ptr(out), ptr(lse))
         check(self.lib.afdk_mfa_decode_attention(self.handle, ctypes.byref(a), c_void_p(stream)))
+
+    def mfa_decode_attention_fp8(self, q, k_cache, v_cache, block_table, seq_lens, out, softmax_scale: float,
+                                 k_scale: float, v_scale: float, lse=None, stream: int = 0) -> None:
+        """e4m3 KV cache (uint8 codes) dequantised by per-tensor k_scale / v_scale."""
+        B, H, D = q.shape
+        a = MfaDecodeArgs(B, H, D, k_cache.shape[1], ptr(q), ptr(k_cache), ptr(v_cache),
+                          k_cache.shape[0], ptr(block_table), block_table.shape[1], ptr(seq_lens),
+                          softmax_scale, ptr(out), ptr(lse))
+        check(self.lib.afdk_mfa_decode_attention_fp8(self.handle, ctypes.byref(a), c_float(k_scale),
+                                                     c_float(v_scale), c_void_p(stream)))
 
     # ------------------------------------------------------------ K1/K4
     def linear(self, x, w, out, stream: int = 0) -> None:

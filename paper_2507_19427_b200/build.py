@@ -19,6 +19,7 @@ OUT = os.path.join(HERE, "libafdk.so")
 CU_SOURCES = [
     "afdk_api.cu",
     "mfa_decode.cu",
+    "mfa_decode_fp8.cu",
     "linear.cu",
     "moe_gemm_mx.cu",
     "moe_gemm_mx2.cu",

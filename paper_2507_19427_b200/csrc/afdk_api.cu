@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <string>
 
@@ -131,8 +132,8 @@ void afdk_destroy(afdk_ctx* ctx) {
 
 int afdk_num_sms(const afdk_ctx* ctx) { return ctx ? ctx->c.num_sms : 0; }
 
-afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args* a,
-                                      afdk_stream stream) {
+static afdk_status mfa_decode_entry(afdk_ctx* ctx, const afdk_mfa_decode_args* a, bool fp8, float k_scale,
+                                    float v_scale, afdk_stream stream) {
   if (!ctx || !a) { set_error("afdk_mfa_decode_attention: NULL ctx/args"); return AFDK_ERR_INVALID; }
   if (a->n_heads != 64) { set_error("mfa_decode: n_heads must be 64"); return AFDK_ERR_INVALID; }
   if (a->head_dim != 256) { set_error("mfa_decode: head_dim must be 256"); return AFDK_ERR_INVALID; }
@@ -153,10 +154,24 @@ afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args*
   void* ws = afdk::workspace(c, afdk::mfa_decode_workspace_bytes(a->batch, c.num_sms));
   if (!ws) { set_error("mfa_decode: workspace allocation failed"); return AFDK_ERR_CUDA; }
   afdk::MfaDecodeArgs m{a->batch, a->q, a->k_cache, a->v_cache, a->num_pages, a->block_table,
-                        a->max_pages, a->seq_lens, a->softmax_scale, a->out, a->lse, ws};
-  const cudaError_t e = afdk::mfa_decode_launch(c, m, static_cast<cudaStream_t>(stream));
+                        a->max_pages, a->seq_lens, a->softmax_scale, a->out, a->lse, ws, k_scale, v_scale};
+  const cudaError_t e = fp8 ? afdk::mfa_decode_fp8_launch(c, m, static_cast<cudaStream_t>(stream))
+                            : afdk::mfa_decode_launch(c, m, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail("mfa_decode launch", e);
   return AFDK_OK;
+}
+
+afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args* a, afdk_stream stream) {
+  return mfa_decode_entry(ctx, a, false, 1.0f, 1.0f, stream);
+}
+
+afdk_status afdk_mfa_decode_attention_fp8(afdk_ctx* ctx, const afdk_mfa_decode_args* a, float k_scale,
+                                          float v_scale, afdk_stream stream) {
+  if (!(k_scale > 0.0f) || !(v_scale > 0.0f) || !std::isfinite(k_scale) || !std::isfinite(v_scale)) {
+    set_error("mfa_decode_fp8: k_scale and v_scale must be positive and finite");
+    return AFDK_ERR_INVALID;
+  }
+  return mfa_decode_entry(ctx, a, true, k_scale, v_scale, stream);
 }
 
 afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, int m, int n, int k,

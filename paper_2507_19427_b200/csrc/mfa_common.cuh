@@ -1,0 +1,115 @@
+// mfa_common.cuh — pieces shared by the bf16 (mfa_decode.cu) and e4m3
+// (mfa_decode_fp8.cu) MFA decode kernels: work split, segment walker, the
+// split-KV partial layout consumed by K3 (mfa_combine_kernel).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace afdk {
+namespace mfa {
+
+constexpr int kHeads = 64;
+constexpr int kDim = 256;
+constexpr int kPage = 64;  // tokens per KV page == one tile
+#ifndef AFDK_MFA_BF16_PART
+#define AFDK_MFA_BF16_PART 1
+#endif
+
+constexpr int kMaxBatch = 2048;  // prefix of pages per request lives in smem
+
+
+struct Params {
+  const int32_t* block_table;  // [B, max_pages]
+  const int32_t* seq_lens;     // [B]
+  int32_t* prefix_out;         // [B+1] pages-per-request prefix, written by CTA 0 for K3
+  __nv_bfloat16* out;          // [B, 64, 256]
+  float* lse;                  // [B, 64] natural log, optional
+  float* part_o;               // [(B+G), 64, 256] split partials (bf16 when AFDK_MFA_BF16_PART)
+  float* part_lse;             // [(B+G), 64] log2 domain
+  int batch, max_pages;
+  float scale_log2;            // softmax scale * log2(e)
+  float k_scale, v_scale;      // e4m3 KV cache dequantisation scales (fp8 kernel)
+};
+
+// Contiguous page range of CTA c out of G over T total pages.
+__device__ __forceinline__ void cta_range(int c, int G, int T, int& lo, int& hi) {
+  lo = (int)(((long long)c * T) / G);
+  hi = (int)(((long long)(c + 1) * T) / G);
+}
+
+// First request whose page range contains global page index `t` (prefix is
+// non-decreasing; empty requests are skipped because prefix[r+1] > t fails).
+__device__ __forceinline__ int find_request(const int32_t* prefix, int B, int t) {
+  int lo = 0, hi = B - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (prefix[mid + 1] > t) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// Walks the segments (request, [lo,hi) local pages) of one CTA in order.
+struct SegmentWalker {
+  const int32_t* prefix;
+  int B, end, r, pos;
+  __device__ SegmentWalker(const int32_t* pf, int b, int start, int stop)
+      : prefix(pf), B(b), end(stop), r(0), pos(start) {
+    if (start < stop) r = find_request(pf, b, start);
+  }
+  // returns false when the range is exhausted
+  __device__ bool next(int& req, int& lo, int& hi, bool& whole) {
+    if (pos >= end) return false;
+    while (prefix[r + 1] <= pos) ++r;
+    const int p0 = prefix[r], p1 = prefix[r + 1];
+    const int seg_hi = p1 < end ? p1 : end;
+    req = r;
+    lo = pos - p0;
+    hi = seg_hi - p0;
+    whole = (pos == p0) && (seg_hi == p1);
+    pos = seg_hi;
+    return true;
+  }
+};
+
+// pages per request -> exclusive prefix in smem (every CTA; B <= kMaxBatch).
+// seq_lens is a caller input (no kernel of this library writes it), so this
+// may run before griddepcontrol.wait.
+template <int kThreads>
+__device__ __forceinline__ void build_page_prefix(int32_t* prefix, const int32_t* seq_lens, int batch) {
+  __shared__ int s_wsum[kThreads / 32];
+  __shared__ int s_carry;
+  constexpr int nw = kThreads / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) { s_carry = 0; prefix[0] = 0; }
+  for (int base = 0; base < batch; base += kThreads) {
+    const int i = base + threadIdx.x;
+    const int v = (i < batch) ? (max(__ldg(seq_lens + i), 0) + kPage - 1) / kPage : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffff, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    int off = s_carry;
+    for (int w = 0; w < warp; ++w) off += s_wsum[w];
+    if (i < batch) prefix[i + 1] = off + x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < nw; ++w) t += s_wsum[w];
+      s_carry += t;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace mfa
+
+// K3 launch (defined in mfa_decode.cu)
+cudaError_t mfa_combine_launch(bool pdl, const mfa::Params& prm, int G, cudaStream_t stream);
+
+}  // namespace afdk

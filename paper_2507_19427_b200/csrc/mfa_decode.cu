@@ -32,6 +32,7 @@
 #include <cstdint>
 
 #include "afdk_internal.h"
+#include "mfa_common.cuh"
 #include "sm100.cuh"
 
 namespace afdk {
@@ -39,9 +40,6 @@ namespace mfa {
 
 using namespace sm100;
 
-constexpr int kHeads = 64;
-constexpr int kDim = 256;
-constexpr int kPage = 64;                    // tokens per KV page == one tile
 constexpr int kTileBytes = kPage * kDim * 2;  // 32 KB (K or V of one page, bf16)
 constexpr int kChunkBytes = 64 * 128;         // one 64-row x 128B swizzle panel
 #ifndef AFDK_MFA_NK
@@ -49,9 +47,6 @@ constexpr int kChunkBytes = 64 * 128;         // one 64-row x 128B swizzle panel
 #endif
 #ifndef AFDK_MFA_NV
 #define AFDK_MFA_NV 3
-#endif
-#ifndef AFDK_MFA_BF16_PART
-#define AFDK_MFA_BF16_PART 1
 #endif
 #ifndef AFDK_MFA_PREFETCH
 #define AFDK_MFA_PREFETCH 0
@@ -78,61 +73,6 @@ struct __align__(1024) Smem {
   uint32_t tmem_base;
 };
 
-constexpr int kMaxBatch = 2048;  // prefix of pages per request lives in smem
-
-
-struct Params {
-  const int32_t* block_table;  // [B, max_pages]
-  const int32_t* seq_lens;     // [B]
-  int32_t* prefix_out;         // [B+1] pages-per-request prefix, written by CTA 0 for K3
-  __nv_bfloat16* out;          // [B, 64, 256]
-  float* lse;                  // [B, 64] natural log, optional
-  float* part_o;               // [(B+G), 64, 256] split partials (bf16 when AFDK_MFA_BF16_PART)
-  float* part_lse;             // [(B+G), 64] log2 domain
-  int batch, max_pages;
-  float scale_log2;            // softmax scale * log2(e)
-};
-
-// Contiguous page range of CTA c out of G over T total pages.
-__device__ __forceinline__ void cta_range(int c, int G, int T, int& lo, int& hi) {
-  lo = (int)(((long long)c * T) / G);
-  hi = (int)(((long long)(c + 1) * T) / G);
-}
-
-// First request whose page range contains global page index `t` (prefix is
-// non-decreasing; empty requests are skipped because prefix[r+1] > t fails).
-__device__ __forceinline__ int find_request(const int32_t* prefix, int B, int t) {
-  int lo = 0, hi = B - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (prefix[mid + 1] > t) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
-
-// Walks the segments (request, [lo,hi) local pages) of one CTA in order.
-struct SegmentWalker {
-  const int32_t* prefix;
-  int B, end, r, pos;
-  __device__ SegmentWalker(const int32_t* pf, int b, int start, int stop)
-      : prefix(pf), B(b), end(stop), r(0), pos(start) {
-    if (start < stop) r = find_request(pf, b, start);
-  }
-  // returns false when the range is exhausted
-  __device__ bool next(int& req, int& lo, int& hi, bool& whole) {
-    if (pos >= end) return false;
-    while (prefix[r + 1] <= pos) ++r;
-    const int p0 = prefix[r], p1 = prefix[r + 1];
-    const int seg_hi = p1 < end ? p1 : end;
-    req = r;
-    lo = pos - p0;
-    hi = seg_hi - p0;
-    whole = (pos == p0) && (seg_hi == p1);
-    pos = seg_hi;
-    return true;
-  }
-};
-
 __global__ void __launch_bounds__(kThreads, 1)
 mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
                   const __grid_constant__ CUtensorMap tm_k,
@@ -144,35 +84,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
-  {
-    // pages per request -> exclusive prefix in smem (every CTA; B <= kMaxBatch)
-    __shared__ int s_wsum[kThreads / 32];
-    __shared__ int s_carry;
-    const int nw = kThreads / 32;
-    if (threadIdx.x == 0) { s_carry = 0; prefix[0] = 0; }
-    for (int base = 0; base < prm.batch; base += kThreads) {
-      const int i = base + threadIdx.x;
-      const int v = (i < prm.batch) ? (max(__ldg(prm.seq_lens + i), 0) + kPage - 1) / kPage : 0;
-      int x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffff, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) s_wsum[warp] = x;
-      __syncthreads();
-      int off = s_carry;
-      for (int w = 0; w < warp; ++w) off += s_wsum[w];
-      if (i < prm.batch) prefix[i + 1] = off + x;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int t = 0;
-        for (int w = 0; w < nw; ++w) t += s_wsum[w];
-        s_carry += t;
-      }
-      __syncthreads();
-    }
-  }
+  build_page_prefix<kThreads>(prefix, prm.seq_lens, prm.batch);
   __syncthreads();
   const int T = prefix[prm.batch];
   int range_lo, range_hi;
@@ -620,7 +532,11 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
   }
   cudaError_t e = launch_k(ctx.pdl, mfa_decode_kernel, dim3(G), dim3(kThreads), smem, stream, tq, tk, tv, prm);
   if (e != cudaSuccess) return e;
-  return launch_k(ctx.pdl, mfa_combine_kernel, dim3(a.batch, kHeads / 4), dim3(256), 0, stream, prm, G);
+  return mfa_combine_launch(ctx.pdl, prm, G, stream);
+}
+
+cudaError_t mfa_combine_launch(bool pdl, const mfa::Params& prm, int G, cudaStream_t stream) {
+  return launch_k(pdl, mfa::mfa_combine_kernel, dim3(prm.batch, mfa::kHeads / 4), dim3(256), 0, stream, prm, G);
 }
 
 }  // namespace afdk

@@ -191,10 +191,15 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
       if (!local) continue;
       const int row0 = (e == a.E) ? n + a.shared_lo : s_off[e];
       const int rows = (e == a.E) ? a.shared_hi - a.shared_lo : s_tot[e];
-      for (int r = 0; r < rows; r += a.chunk) {
+      // ceil(rows/chunk) items of near-equal size (multiples of 32 rows), so
+      // an expert never ends in a tiny item that streams its weights for a
+      // handful of tokens
+      const int n_items = (rows + a.chunk - 1) / a.chunk;
+      const int per = n_items > 0 ? ((rows + n_items - 1) / n_items + 31) & ~31 : 0;
+      for (int r = 0; r < rows; r += per) {
         a.work[g].group = e;
         a.work[g].row0 = row0 + r;
-        a.work[g].rows = min(a.chunk, rows - r);
+        a.work[g].rows = min(per, rows - r);
         ++g;
       }
     }

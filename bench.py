@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--no-moe", action="store_true", help="skip the config-3 MoE FFN sub-measurement")
     p.add_argument("--no-afd", action="store_true", help="skip the config-5 AFD measurement")
     p.add_argument("--no-long", action="store_true", help="skip the config-4 32K measurement")
+    p.add_argument("--no-fp8kv", action="store_true", help="skip the config-2 e4m3 KV-cache measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -139,6 +140,55 @@ def make_workload(torch, dev, batch, ctx_len, seed=0):
     s["h_res"] = torch.empty(batch, HIDDEN, dtype=torch.bfloat16, device=dev)
     s["h_norm"] = torch.empty(batch, HIDDEN, dtype=torch.bfloat16, device=dev)
     return s
+
+
+def run_fp8_kv(ctx, torch, dev, s, batch, ctx_len, steps):
+    """Config 2 with the paper's FP8 KV cache (512 B/token/layer, e4m3 codes +
+    per-tensor scales): the attention-side layer and the MFA core alone."""
+    npages = s["kv"][0][0].shape[0]
+
+    def codes():
+        sign = torch.randint(0, 2, (npages, PAGE, D), dtype=torch.uint8, device=dev) * 0x80
+        return torch.randint(0x08, 0x58, (npages, PAGE, D), dtype=torch.uint8, device=dev) | sign
+
+    kv8 = [(codes(), codes()) for _ in range(N_ROT)]
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    ks, vs = 0.05, 0.05
+
+    def layer(i):
+        k, v = kv8[i % N_ROT]
+        ctx.mfa_layer(s["w"], s["x"], k, v, s["block_table"], s["seq_lens"], s["h_res"], s["h_norm"], stream=sp,
+                      kv_scales=(ks, vs))
+
+    def core(i):
+        k, v = kv8[i % N_ROT]
+        ctx.mfa_decode_attention_fp8(s["q"], k, v, s["block_table"], s["seq_lens"], s["attn_out"], D ** -0.5, ks, vs,
+                                     stream=sp)
+
+    def timed(fn):
+        for i in range(3):
+            fn(i)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(steps):
+            fn(i)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps
+
+    layer_ms, core_ms = timed(layer), timed(core)
+    hbm_peak = peaks()[0]
+    kv = kv_bytes(batch, ctx_len) // 2
+    core_bytes = kv + 2 * batch * H * D * 2
+    return {"workload": "config2 with e4m3 KV cache (512 B/token/layer)", "batch": batch, "ctx": ctx_len,
+            "layer_ms": layer_ms, "tokens_per_s": batch / (layer_ms * 1e-3),
+            "layer_hbm": {"achieved": (kv + weight_bytes()) / (layer_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                          "frac": (kv + weight_bytes()) / (layer_ms * 1e-3) / 1e9 / hbm_peak},
+            "core_ms": core_ms,
+            "core_hbm": {"achieved": core_bytes / (core_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": core_bytes / (core_ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": core_bytes}}
 
 
 # ------------------------------------------------- config 3: MoE FFN layer
@@ -558,6 +608,9 @@ def main():
     long_ctx = None
     if not args.no_long:
         long_ctx = run_long_context(ctx, torch, dev, max(3, args.steps // 4))
+    fp8kv = None
+    if not args.no_fp8kv:
+        fp8kv = run_fp8_kv(ctx, torch, dev, s, args.batch, args.ctx, max(5, args.steps // 2))
     moe = None
     if not args.no_moe:
         # config 3 FFN layer: 1x128/128x128 fp8 (software-scaled) and MXFP8
@@ -605,6 +658,7 @@ def main():
                     "h2d_bytes_per_step": in_host.numel() * in_host.element_size(),
                     "d2h_bytes_per_step": out_host.numel() * out_host.element_size()},
             "config4_long_context": long_ctx,
+            "config2_fp8_kv": fp8kv,
             "config1_cpu": config1_cpu() if (world == 1 and not args.no_cpu_baseline) else None,
             "moe_ffn": moe,
             "afd": afd,

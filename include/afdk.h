@@ -139,6 +139,12 @@ typedef struct afdk_mfa_layer_args {
 afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
                            afdk_stream stream);
 
+/* The same layer over e4m3 KV caches (see afdk_mfa_decode_attention_fp8):
+ * the appended token is stored as e4m3_rn_satfinite(bf16(k_rope)/k_scale),
+ * e4m3_rn_satfinite(bf16(v)/v_scale); the core runs on the FP8 path.      */
+afdk_status afdk_mfa_layer_fp8(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
+                               float k_scale, float v_scale, afdk_stream stream);
+
 /* ------------------------------------------------ K5 router + FP8 dispatch
  * Attention-side router: logits = h . gate_w^T (fp32), softmax,
  * top-k by logit (ties -> lower expert id), weights = softmax probability

@@ -203,8 +203,24 @@ void orc_mfa_layer(const orc_mfa_dims* d, int B, const float* x,
     const int pg = block_table[(size_t)b * max_pages + pos / d->page];
     float* kdst = k_cache + ((size_t)pg * d->page + pos % d->page) * D;
     float* vdst = v_cache + ((size_t)pg * d->page + pos % d->page) * D;
-    memcpy(kdst, kb, sizeof(float) * D);                               /* paged KV append */
-    memcpy(vdst, vb, sizeof(float) * D);
+    if (d->kv_k_scale > 0.0f) { /* e4m3 cache: store the dequantised e4m3 value */
+      for (int i = 0; i < D; ++i) {
+        kdst[i] = orc_e4m3_to_f32(orc_f32_to_e4m3(kb[i] / d->kv_k_scale)) * d->kv_k_scale;
+        vdst[i] = orc_e4m3_to_f32(orc_f32_to_e4m3(vb[i] / d->kv_v_scale)) * d->kv_v_scale;
+      }
+    } else {
+      memcpy(kdst, kb, sizeof(float) * D);                             /* paged KV append */
+      memcpy(vdst, vb, sizeof(float) * D);
+    }
+  }
+  if (d->kv_k_scale > 0.0f) { /* per-(request, head) e4m3 query, as the fp8 kernel */
+    for (size_t r = 0; r < (size_t)B * NH; ++r) {
+      float* qr = q + r * D;
+      float amax = 0.0f;
+      for (int i = 0; i < D; ++i) amax = fmaxf(amax, fabsf(qr[i]));
+      const float sc = fmaxf(amax, 1e-10f) / 448.0f;
+      for (int i = 0; i < D; ++i) qr[i] = orc_e4m3_to_f32(orc_f32_to_e4m3(qr[i] / sc)) * sc;
+    }
   }
   orc_mfa_decode_attention(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, NH, D,
                            d->page, d->softmax_scale, round_bf16, attn, NULL);

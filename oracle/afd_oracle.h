@@ -74,6 +74,11 @@ void orc_mfa_decode_attention(const float* q, const float* k_cache, const float*
 typedef struct {
   int hidden, q_lora, n_heads, head_dim, page;
   float rms_eps, rope_theta, softmax_scale;
+  /* e4m3 KV cache (0 = off): the caches hold DEQUANTISED values
+   * e4m3(code)*scale; the appended token is stored as e4m3(x/scale) (x the
+   * bf16-rounded post-RoPE k / v), and the query of every (request, head) is
+   * quantised with scale max(amax,1e-10)/448 before the exact attention. */
+  float kv_k_scale, kv_v_scale;
 } orc_mfa_dims;
 
 /* x          [B, hidden]              layer input (residual stream)

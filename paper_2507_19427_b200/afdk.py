@@ -125,6 +125,8 @@ SIGNATURES = {
                                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_permute": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_ffn": (c_int, [c_void_p, POINTER(MoeWeights), POINTER(MoeArgs), c_void_p]),
+    "afdk_mfa_layer_fp8": (c_int, [c_void_p, POINTER(MfaWeights), POINTER(MfaLayerArgs), c_float, c_float,
+                                   c_void_p]),
     "afdk_mfa_decode_attention_fp8": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_float, c_float, c_void_p]),
     "afdk_moe_ffn_mx": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), c_void_p]),
     "afdk_quant_mx": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
@@ -232,7 +234,7 @@ class Context:
                                    int(out.dtype == torch.float32), c_void_p(stream)))
 
     def mfa_layer(self, w: dict, x, k_cache, v_cache, block_table, seq_lens, h_res, h_norm,
-                  rms_eps=1e-5, rope_theta=5e5, softmax_scale=None, stream: int = 0) -> None:
+                  rms_eps=1e-5, rope_theta=5e5, softmax_scale=None, stream: int = 0, kv_scales=None) -> None:
         """Attention-side decode layer; `w` holds bf16 device tensors
         in_norm, qkv, q_norm, q_up, o, post_norm (shapes as in include/afdk.h)."""
         hidden = x.shape[1]
@@ -244,7 +246,11 @@ class Context:
                         ptr(w["q_up"]), ptr(w["o"]), ptr(w["post_norm"]), rms_eps, rope_theta, scale)
         a = MfaLayerArgs(x.shape[0], ptr(x), ptr(k_cache), ptr(v_cache), k_cache.shape[0], k_cache.shape[1],
                          ptr(block_table), block_table.shape[1], ptr(seq_lens), ptr(h_res), ptr(h_norm))
-        check(self.lib.afdk_mfa_layer(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+        if kv_scales is None:
+            check(self.lib.afdk_mfa_layer(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+        else:  # e4m3 caches (uint8 codes) with per-tensor (k_scale, v_scale)
+            check(self.lib.afdk_mfa_layer_fp8(self.handle, ctypes.byref(mw), ctypes.byref(a),
+                                              c_float(kv_scales[0]), c_float(kv_scales[1]), c_void_p(stream)))
 
     # -------------------------------------------------------- K5/K6/K7-K9
     def router_topk(self, h, gate_w, k, ids, weights, logits=None, xq=None, xs=None, renormalize=False,

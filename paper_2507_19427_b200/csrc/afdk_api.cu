@@ -191,8 +191,8 @@ afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, 
   return AFDK_OK;
 }
 
-afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
-                           afdk_stream stream) {
+static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
+                                   float k_scale, float v_scale, afdk_stream stream) {
   if (!ctx || !w || !a) { set_error("afdk_mfa_layer: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }
   if (w->n_heads != 64 || w->head_dim != 256 || a->page_size != 64) {
     set_error("afdk_mfa_layer: n_heads/head_dim/page_size must be 64/256/64");
@@ -213,12 +213,27 @@ afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_
   afdk::MfaLayerArgs m{a->batch, w->hidden, w->q_lora, w->n_heads, w->head_dim, a->page_size,
                        w->in_norm, w->w_qkv, w->q_norm, w->w_q_up, w->w_o, w->post_norm,
                        w->rms_eps, w->rope_theta, w->softmax_scale, a->x, a->k_cache, a->v_cache,
-                       a->num_pages, a->block_table, a->max_pages, a->seq_lens, a->h_res, a->h_norm};
+                       a->num_pages, a->block_table, a->max_pages, a->seq_lens, a->h_res, a->h_norm,
+                       k_scale, v_scale};
   void* ws = afdk::workspace(c, afdk::mfa_layer_workspace_bytes(m, c.num_sms));
   if (!ws) { set_error("afdk_mfa_layer: workspace allocation failed"); return AFDK_ERR_CUDA; }
   const cudaError_t e = afdk::mfa_layer_launch(c, m, ws, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail("afdk_mfa_layer", e);
   return AFDK_OK;
+}
+
+afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
+                           afdk_stream stream) {
+  return mfa_layer_entry(ctx, w, a, 0.0f, 0.0f, stream);
+}
+
+afdk_status afdk_mfa_layer_fp8(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
+                               float k_scale, float v_scale, afdk_stream stream) {
+  if (!(k_scale > 0.0f) || !(v_scale > 0.0f) || !std::isfinite(k_scale) || !std::isfinite(v_scale)) {
+    set_error("afdk_mfa_layer_fp8: k_scale and v_scale must be positive and finite");
+    return AFDK_ERR_INVALID;
+  }
+  return mfa_layer_entry(ctx, w, a, k_scale, v_scale, stream);
 }
 
 afdk_status afdk_router_topk(afdk_ctx* ctx, const void* h, const void* gate_w, int T, int H, int E, int k,

@@ -21,8 +21,10 @@
 //
 // Warp roles (256 threads):  w0 = Q/K TMA producer, w1 = QK^T MMA issuer +
 // TMEM owner, w2..w5 = softmax / O-correction / epilogue (TMEM lanes 0-15 of
-// each 32-lane sub-partition hold the M=64 accumulator rows), w6 = V TMA
-// producer, w7 = P.V MMA issuer.  QK^T and P.V are issued by different
+// each 32-lane sub-partition hold the M=64 accumulator rows; the 16x32bx2
+// load shape hands columns [c,c+32) to lanes 0-15 and [c+32,c+64) to lanes
+// 16-31, so every lane owns one head x 32 tokens), w6 = V TMA producer,
+// w7 = P.V MMA issuer.  QK^T and P.V are issued by different
 // threads so K slots recycle at QK^T completion whatever the softmax does.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -244,7 +246,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   } else if (warp >= 2 && warp <= 5) {
     // ------------------------------- softmax / correction / epilogue (w2-5)
     const int sub = warp & 3;                 // TMEM sub-partition of this warp
-    const bool active = lane < 16;            // M=64: lanes 0-15 hold rows
+    const int half = lane >> 4;               // 16x32bx2 TMEM loads: lanes 16-31 read columns +32
     const int head = sub * 16 + (lane & 15);
     const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
     const uint32_t p_row_off = (uint32_t)head * 128;  // K-major SW128: 128B per head row
@@ -254,28 +256,31 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     while (walk.next(req, lo, hi, whole)) {
       const int n = hi - lo;
       const int seq_len = __ldg(prm.seq_lens + req);
+      // lane (head, half) owns tokens [32*half, +32) of each page; l_sum is
+      // this thread's share of the row sum (combined in the epilogue)
       float m_used = -INFINITY, l_sum = 0.0f;
       for (int j = 0; j < n; ++j, ++g) {
         const int sb = g & 1, pb = g & 1;
         mbar_wait(&sm.s_full[sb], (g >> 1) & 1);
         tc_fence_after();
-        uint32_t sr[64];
-        tmem_ld32(t_row + kColS + sb * 64, sr);
-        tmem_ld32(t_row + kColS + sb * 64 + 32, sr + 32);
+        uint32_t sr[32];
+        tmem_ld16x2_32(t_row + kColS + sb * 64, sr);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.s_empty[sb]);
 
         const int tok0 = (lo + j) * kPage;
-        const int nvalid = min(kPage, seq_len - tok0);
-        float s[64];
+        const int nvalid_page = min(kPage, seq_len - tok0);
+        const int nvalid = nvalid_page - half * 32;
+        float s[32];
         float tmax = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
+        for (int i = 0; i < 32; ++i) {
           s[i] = (i < nvalid) ? __uint_as_float(sr[i]) * prm.scale_log2 : -INFINITY;
           tmax = fmaxf(tmax, s[i]);
         }
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffff, tmax, 16));
         const bool need = tmax > m_used + kRescaleThresh;
         float alpha = 1.0f;
         if (need) {
@@ -283,10 +288,10 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
           m_used = tmax;
         }
         l_sum *= alpha;
-        uint32_t pk[32];
+        uint32_t pk[16];
         float psum = 0.0f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < 16; ++i) {
           const float p0 = fast_exp2(s[2 * i] - m_used);
           const float p1 = fast_exp2(s[2 * i + 1] - m_used);
           psum += p0 + p1;
@@ -296,39 +301,39 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
 
         // P slot (and, for a rescale, the O accumulator) must be quiescent
         if (g >= 2) mbar_wait(&sm.p_empty[pb], ((g >> 1) & 1) ^ 1);
-        const bool warp_rescale = __any_sync(0xffffffff, active && need && j > 0);
+        const bool warp_rescale = __any_sync(0xffffffff, need && j > 0);
         if (warp_rescale) {
           const int gp = g - 1;  // PV(g-1) must have landed in O
           mbar_wait(&sm.p_empty[gp & 1], (gp >> 1) & 1);
           tc_fence_after();
-          const float a = (active && need) ? alpha : 1.0f;
+          const float a = need ? alpha : 1.0f;
 #pragma unroll 1
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < 4; ++c) {
             uint32_t o[32];
-            tmem_ld32(t_row + kColO + c * 32, o);
+            tmem_ld16x2_32(t_row + kColO + c * 64, o);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
-            tmem_st32(t_row + kColO + c * 32, o);
+            tmem_st16x2_32(t_row + kColO + c * 64, o);
           }
           tmem_wait_st();
         }
         // Last page of a request: zero V rows past seq_len so P=0 x garbage stays 0.
-        if (nvalid < kPage) {
+        if (nvalid_page < kPage) {
           const int vs = g % kNV;
           mbar_wait(&sm.v_full[vs], (g / kNV) & 1);
           const int tid = (warp - 2) * 32 + lane;  // 0..127
           uint8_t* vt = sm.v[vs];
-          for (int idx = tid; idx < (kPage - nvalid) * 4 * 8; idx += 128) {
-            const int row = nvalid + idx / 32, chunk = (idx / 8) & 3, q16 = idx & 7;
+          for (int idx = tid; idx < (kPage - nvalid_page) * 4 * 8; idx += 128) {
+            const int row = nvalid_page + idx / 32, chunk = (idx / 8) & 3, q16 = idx & 7;
             *reinterpret_cast<uint4*>(vt + chunk * kChunkBytes + row * 128 + q16 * 16) = make_uint4(0, 0, 0, 0);
           }
         }
-        if (active) {
+        {
           const uint32_t pbase = smem_u32(sm.p[pb]) + p_row_off;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint32_t addr = pbase + ((uint32_t)(c ^ (head & 7)) << 4);
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t addr = pbase + ((uint32_t)((half * 4 + c) ^ (head & 7)) << 4);
             st_shared_v4(addr, pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
           }
         }
@@ -341,50 +346,38 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
       const int gl = g - 1;
       mbar_wait(&sm.p_empty[gl & 1], (gl >> 1) & 1);
       tc_fence_after();
-      const float inv_l = 1.0f / l_sum;
+      const float l_tot = l_sum + __shfl_xor_sync(0xffffffff, l_sum, 16);
+      const float inv_l = 1.0f / l_tot;
       const int slot = req + cta;
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t o[32];
-        tmem_ld32(t_row + kColO + c * 32, o);
+        tmem_ld16x2_32(t_row + kColO + c * 64, o);
         tmem_wait_ld();
-        if (active) {
-          if (whole) {
-            uint4* dst = reinterpret_cast<uint4*>(prm.out + ((size_t)req * kHeads + head) * kDim + c * 32);
+        const int d0 = c * 64 + half * 32;
+        if (whole || AFDK_MFA_BF16_PART) {
+          __nv_bfloat16* base = whole ? prm.out : reinterpret_cast<__nv_bfloat16*>(prm.part_o);
+          const size_t row = whole ? (size_t)req * kHeads + head : (size_t)slot * kHeads + head;
+          uint4* dst = reinterpret_cast<uint4*>(base + row * kDim + d0);
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              uint4 v;
-              v.x = pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv_l, __uint_as_float(o[8 * q4 + 1]) * inv_l);
-              v.y = pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv_l, __uint_as_float(o[8 * q4 + 3]) * inv_l);
-              v.z = pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv_l, __uint_as_float(o[8 * q4 + 5]) * inv_l);
-              v.w = pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv_l, __uint_as_float(o[8 * q4 + 7]) * inv_l);
-              dst[q4] = v;
-            }
-          } else {
-#if AFDK_MFA_BF16_PART
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.part_o) +
-                                                  ((size_t)slot * kHeads + head) * kDim + c * 32);
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              uint4 v;
-              v.x = pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv_l, __uint_as_float(o[8 * q4 + 1]) * inv_l);
-              v.y = pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv_l, __uint_as_float(o[8 * q4 + 3]) * inv_l);
-              v.z = pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv_l, __uint_as_float(o[8 * q4 + 5]) * inv_l);
-              v.w = pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv_l, __uint_as_float(o[8 * q4 + 7]) * inv_l);
-              dst[q4] = v;
-            }
-#else
-            float4* dst = reinterpret_cast<float4*>(prm.part_o + ((size_t)slot * kHeads + head) * kDim + c * 32);
-#pragma unroll
-            for (int q4 = 0; q4 < 8; ++q4)
-              dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv_l, __uint_as_float(o[4 * q4 + 1]) * inv_l,
-                                    __uint_as_float(o[4 * q4 + 2]) * inv_l, __uint_as_float(o[4 * q4 + 3]) * inv_l);
-#endif
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint4 v;
+            v.x = pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv_l, __uint_as_float(o[8 * q4 + 1]) * inv_l);
+            v.y = pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv_l, __uint_as_float(o[8 * q4 + 3]) * inv_l);
+            v.z = pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv_l, __uint_as_float(o[8 * q4 + 5]) * inv_l);
+            v.w = pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv_l, __uint_as_float(o[8 * q4 + 7]) * inv_l);
+            dst[q4] = v;
           }
+        } else {
+          float4* dst = reinterpret_cast<float4*>(prm.part_o + ((size_t)slot * kHeads + head) * kDim + d0);
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv_l, __uint_as_float(o[4 * q4 + 1]) * inv_l,
+                                  __uint_as_float(o[4 * q4 + 2]) * inv_l, __uint_as_float(o[4 * q4 + 3]) * inv_l);
         }
       }
-      if (active) {
-        const float lse2 = m_used + __log2f(l_sum);
+      if (half == 0) {
+        const float lse2 = m_used + __log2f(l_tot);
         if (whole) {
           if (prm.lse) prm.lse[(size_t)req * kHeads + head] = lse2 * 0.69314718055994531f;
         } else {

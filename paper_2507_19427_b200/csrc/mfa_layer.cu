@@ -11,6 +11,7 @@
 // the row epilogue that sums that GEMM's partials (lin::SlotTable).  Intermediates are
 // stored in bf16 exactly where the oracle (orc_mfa_layer) rounds.
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -79,7 +80,12 @@ struct QkvEpi {
   const int32_t* block_table;
   const int32_t* seq_lens;
   const double* inv_freq;       // [head_dim/2]
+  float k_scale, v_scale;       // > 0: caches are e4m3, store e4m3(bf16(x) / scale)
 };
+
+__device__ __forceinline__ uint8_t kv_e4m3(float x, float scale) {
+  return (uint8_t)__nv_cvt_float_to_fp8(__fdiv_rn(x, scale), __NV_SATFINITE, __NV_E4M3);
+}
 
 // y = [q_down|k|v] projection of one token row (fp32): q -> RMSNorm -> qa;
 // k -> RoPE -> K cache slot of position seq_len-1; v -> V cache slot.
@@ -109,15 +115,28 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
   const int half = e.head_dim / 2;
   const float* k = row_s + e.q_lora;
   const float* v = k + e.head_dim;
+  const bool fp8 = e.k_scale > 0.0f;
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
     double sn, cs;
     sincos((double)pos * e.inv_freq[i], &sn, &cs);
     const float c = (float)cs, s = (float)sn;
     const float x1 = k[i], x2 = k[i + half];
-    e.k_cache[slot + i] = __float2bfloat16_rn(x1 * c - x2 * s);
-    e.k_cache[slot + i + half] = __float2bfloat16_rn(x2 * c + x1 * s);
+    const __nv_bfloat16 k1 = __float2bfloat16_rn(x1 * c - x2 * s), k2 = __float2bfloat16_rn(x2 * c + x1 * s);
+    if (fp8) {
+      uint8_t* k8 = reinterpret_cast<uint8_t*>(e.k_cache);
+      k8[slot + i] = kv_e4m3(__bfloat162float(k1), e.k_scale);
+      k8[slot + i + half] = kv_e4m3(__bfloat162float(k2), e.k_scale);
+    } else {
+      e.k_cache[slot + i] = k1;
+      e.k_cache[slot + i + half] = k2;
+    }
   }
-  for (int i = threadIdx.x; i < e.head_dim; i += blockDim.x) e.v_cache[slot + i] = __float2bfloat16_rn(v[i]);
+  for (int i = threadIdx.x; i < e.head_dim; i += blockDim.x) {
+    if (fp8)
+      reinterpret_cast<uint8_t*>(e.v_cache)[slot + i] = kv_e4m3(v[i], e.v_scale);
+    else
+      e.v_cache[slot + i] = __float2bfloat16_rn(v[i]);
+  }
 }
 
 // y = q_up projection (fp32 [B, n_heads*head_dim]); per-head NeoX RoPE -> q bf16.
@@ -247,7 +266,7 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   if ((e = linear_bf16_launch(ctx, p1, xn, a.w_qkv, part, stream)) != cudaSuccess) return e;
   QkvEpi qe{QL, D, a.page_size, a.max_pages, p1.n_out, a.rms_eps,
             static_cast<const __nv_bfloat16*>(a.w_q_norm), qa, static_cast<__nv_bfloat16*>(a.k_cache),
-            static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq};
+            static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq, a.k_scale, a.v_scale};
   if ((e = launch_k(ctx.pdl, qkv_epilogue_kernel, dim3(B), dim3(512), p1.n_out * sizeof(float), stream, p1,
                     (const float*)part, linear_grid(ctx, p1), qe)) != cudaSuccess)
     return e;
@@ -259,8 +278,10 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
     return e;
   // K2/K3: MFA decode core over the paged cache (now including this token)
   MfaDecodeArgs md{B, q, a.k_cache, a.v_cache, a.num_pages, a.block_table, a.max_pages, a.seq_lens,
-                   a.softmax_scale, attn, nullptr, part};
-  if ((e = mfa_decode_launch(ctx, md, stream)) != cudaSuccess) return e;
+                   a.softmax_scale, attn, nullptr, part, a.k_scale, a.v_scale};
+  if ((e = (a.k_scale > 0.0f ? mfa_decode_fp8_launch(ctx, md, stream) : mfa_decode_launch(ctx, md, stream))) !=
+      cudaSuccess)
+    return e;
   // K4: o_proj, then residual + post-attention RMSNorm
   const LinearPlan p3 = make_linear_plan(B, Hd, NQ);
   if ((e = linear_bf16_launch(ctx, p3, attn, a.w_o, part, stream)) != cudaSuccess) return e;

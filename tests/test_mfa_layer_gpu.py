@@ -56,3 +56,50 @@ def test_mfa_layer_small_dims(ctx):
 @pytest.mark.gpu
 def test_mfa_layer_step3_dims(ctx):
     check(run_layer(ctx, STEP3, [300, 4096, 65], 5), 64)
+
+
+def run_layer_fp8(ctx, dims, seq_lens, seed):
+    """Same layer over e4m3 KV caches with per-tensor scales."""
+    import torch
+
+    x, w, kc, vc, bt, sl = mg.layer_inputs(dims, seq_lens, seed)
+    ks, vs = float(np.abs(kc).max()) / 448.0, float(np.abs(vc).max()) / 448.0
+    kq = (torch.from_numpy(kc) / ks).to(torch.float8_e4m3fn).view(torch.uint8)
+    vq = (torch.from_numpy(vc) / vs).to(torch.float8_e4m3fn).view(torch.uint8)
+    dev = torch.device("cuda:0")
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(dev)
+    wd = {k: bf(v) for k, v in w.items()}
+    xd = bf(x)
+    kd, vd = kq.to(dev), vq.to(dev)
+    h_res, h_norm = torch.empty_like(xd), torch.empty_like(xd)
+    ctx.mfa_layer(wd, xd, kd, vd, torch.from_numpy(bt).to(dev), torch.from_numpy(sl).to(dev), h_res, h_norm,
+                  kv_scales=(ks, vs))
+    torch.cuda.synchronize()
+    k1 = orc.e4m3_to_f32(kq.numpy()) * np.float32(ks)
+    v1 = orc.e4m3_to_f32(vq.numpy()) * np.float32(vs)
+    r_res, r_norm = orc.mfa_layer(dict(dims, kv_k_scale=ks, kv_v_scale=vs), x, w, k1, v1, bt, sl)
+    gk = orc.e4m3_to_f32(kd.cpu().numpy()) * np.float32(ks)
+    gv = orc.e4m3_to_f32(vd.cpu().numpy()) * np.float32(vs)
+    return h_res.float().cpu().numpy(), h_norm.float().cpu().numpy(), gk, gv, r_res, r_norm, k1, v1, bt, sl, (ks, vs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,seq_lens,seed", [(mg.SMALL, [70, 130, 1, 64], 12), (STEP3, [300, 4096, 65], 5)])
+def test_mfa_layer_fp8_kv(ctx, dims, seq_lens, seed):
+    """FP8 KV: appended token = e4m3(bf16(x)/scale) (one e4m3 ulp allowed where the
+    bf16 projection itself differs by an ulp); h_res/h_norm within 3e-2 of the
+    oracle (exact attention on the dequantised cache; the kernel rounds P to e4m3)."""
+    g_res, g_norm, gk, gv, r_res, r_norm, rk, rv, bt, sl, (ks, vs) = run_layer_fp8(ctx, dims, seq_lens, seed)
+    assert rel_err(g_res, r_res) <= 3e-2, rel_err(g_res, r_res)
+    assert rel_err(g_norm, r_norm) <= 3e-2, rel_err(g_norm, r_norm)
+    page = dims["page"]
+    for b, L in enumerate(sl):
+        pg, s = bt[b, (L - 1) // page], (L - 1) % page
+        for g, r, sc in ((gk[pg, s], rk[pg, s], ks), (gv[pg, s], rv[pg, s], vs)):
+            # one e4m3 step: 2^-3 of the binade (relative), 2^-9 * scale for subnormals
+            close = np.abs(g - r) <= np.maximum(0.125 * np.abs(r), 2.0 ** -9 * sc) * 1.0001
+            assert close.all() and np.mean(g != r) <= 0.05
+    mask = np.ones(gk.shape[:2], bool)
+    for b, L in enumerate(sl):
+        mask[bt[b, (L - 1) // page], (L - 1) % page] = False
+    np.testing.assert_array_equal(gk[mask], rk[mask])

@@ -263,6 +263,46 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8"):
             "gpu_launches_per_layer": 5}
 
 
+DENSE_INTER = 18432
+
+
+def run_dense_bench(ctx, torch, dev, T, n_split, steps, warmup):
+    """One dense Step-3 FFN layer (inter 18432, builtin_catalog.cpp:248-250) in
+    MXFP8 over T tokens, as n_split intermediate slices on this GPU."""
+    Is = DENSE_INTER // n_split
+
+    def e4m3(shape):
+        mag = torch.randint(0x18, 0x40, shape, dtype=torch.int32, device=dev)
+        sgn = torch.randint(0, 2, shape, dtype=torch.int32, device=dev) * 0x80
+        return (mag | sgn).to(torch.uint8)
+
+    w = {"w13": e4m3((n_split, 2 * Is, HIDDEN)), "w2": e4m3((n_split, HIDDEN, Is)),
+         "sf13": torch.full((n_split, 2 * Is, HIDDEN // 32), 120, dtype=torch.uint8, device=dev),
+         "sf2": torch.full((n_split, HIDDEN, Is // 32), 120, dtype=torch.uint8, device=dev)}
+    xq = e4m3((T, HIDDEN))
+    xsf = torch.full((T, HIDDEN // 32), 121, dtype=torch.uint8, device=dev)
+    out = torch.empty(T, HIDDEN, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        ctx.dense_ffn_mx(w, xq, xsf, out, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        ctx.dense_ffn_mx(w, xq, xsf, out, stream=stream.cuda_stream)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    wbytes = 3 * HIDDEN * DENSE_INTER * (1 + 1 / 32)
+    flops = 2.0 * 3 * HIDDEN * DENSE_INTER * T
+    hbm_peak, tf_peak, kind = peaks()
+    return {"T": T, "n_split": n_split, "format": "mxfp8", "ms_per_layer": ms, "tokens_per_s": T / (ms * 1e-3),
+            "hbm": {"achieved": wbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": wbytes / (ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": wbytes},
+            "tensor": {"achieved": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "peak": 2 * tf_peak,
+                       "frac": flops / (ms * 1e-3) / 1e12 / (2 * tf_peak)}}
+
+
 # ------------------------------------------- config 4: 32K split-KV attention
 def run_long_context(ctx, torch, dev, steps, batch=32, ctx_len=32768):
     """MFA decode core at B=32, 32K context (1.07 GB of bf16 KV per layer)."""
@@ -611,12 +651,14 @@ def main():
     fp8kv = None
     if not args.no_fp8kv:
         fp8kv = run_fp8_kv(ctx, torch, dev, s, args.batch, args.ctx, max(5, args.steps // 2))
-    moe = None
+    moe = dense = None
     if not args.no_moe:
         # config 3 FFN layer: 1x128/128x128 fp8 (software-scaled) and MXFP8
         # (hardware block-scaled; CTA-pair kernels at >= 64 rows/expert)
         moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=rank, fmt=f)
                for f, T in (("fp8", 256), ("fp8", 4096), ("mx", 256), ("mx", 4096), ("mx", 8192))]
+        # dense Step-3 layers (inter 18432) as 4 intermediate slices, MXFP8
+        dense = [run_dense_bench(ctx, torch, dev, T, 4, max(5, args.steps // 4), 2) for T in (256, 4096)]
     afd = None
     if not args.no_afd:
         try:
@@ -661,6 +703,7 @@ def main():
             "config2_fp8_kv": fp8kv,
             "config1_cpu": config1_cpu() if (world == 1 and not args.no_cpu_baseline) else None,
             "moe_ffn": moe,
+            "dense_ffn": dense,
             "afd": afd,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),

@@ -229,6 +229,32 @@ typedef struct afdk_moe_mx_args {
 afdk_status afdk_moe_ffn_mx(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
                             afdk_stream stream);
 
+/* ------------------------------------------------ dense FFN (MXFP8)
+ * The dense Step-3 layers (first four and last, inter 18432,
+ * builtin_catalog.cpp:248-250): out = SiLU(x.Wg^T) * (x.Wu^T) . W2^T as a sum
+ * over n_split slices of the intermediate dimension, each a grouped MXFP8
+ * GEMM pair over all T tokens (the MoE kernels with every slice a "virtual
+ * expert" of weight 1).  A GPU holding only some slices returns their
+ * partial; the attention side reduces partials like EP ones
+ * (afdk_add_partials) — the FFN-tier tensor parallelism of PAPER.md:651.
+ *   w13  e4m3 [n_split, 2*inter_split, hidden]: slice j = gate rows
+ *        [j*inter_split, +inter_split) then the matching up rows
+ *   sf13 UE8M0 [n_split, 2*inter_split, hidden/32]
+ *   w2   e4m3 [n_split, hidden, inter_split] (columns of slice j)
+ *   sf2  UE8M0 [n_split, hidden, inter_split/32]
+ * xq/xsf: MXFP8 input [T, hidden] (afdk_quant_mx); out bf16 [T, hidden].
+ * Limits: hidden % 512 == 0, inter_split % 512 == 0, 1 <= T <= 65536.     */
+typedef struct afdk_dense_mx_weights {
+  int hidden, inter_split, n_split;
+  const void* w13;
+  const uint8_t* sf13;
+  const void* w2;
+  const uint8_t* sf2;
+} afdk_dense_mx_weights;
+
+afdk_status afdk_dense_ffn_mx(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,
+                              const uint8_t* xsf, void* out, afdk_stream stream);
+
 /* MXFP8 quantisation of the dispatch payload: x bf16 [T, H] -> q e4m3 [T, H]
  * + sf UE8M0 [T, H/32].  Per 32 elements: e = smallest integer with
  * amax <= 448 * 2^e (e = -127 for an all-zero block), sf = e + 127,

@@ -88,6 +88,11 @@ class MoeMxArgs(Structure):
     ]
 
 
+class DenseMxWeights(Structure):
+    _fields_ = [("hidden", c_int), ("inter_split", c_int), ("n_split", c_int),
+                ("w13", c_void_p), ("sf13", c_void_p), ("w2", c_void_p), ("sf2", c_void_p)]
+
+
 class StagePlan(Structure):
     _fields_ = [("attn_gpus", c_int), ("ffn_gpus", c_int), ("micro_batch", ctypes.c_longlong),
                 ("avg_ctx", ctypes.c_longlong), ("n_layers", c_int), ("hidden", c_int), ("link_gbs", ctypes.c_double)]
@@ -129,6 +134,7 @@ SIGNATURES = {
                                    c_void_p]),
     "afdk_mfa_decode_attention_fp8": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_float, c_float, c_void_p]),
     "afdk_moe_ffn_mx": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), c_void_p]),
+    "afdk_dense_ffn_mx": (c_int, [c_void_p, POINTER(DenseMxWeights), c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_quant_mx": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "afdk_ipc_handle": (c_int, [c_void_p, c_void_p, c_void_p]),
     "afdk_ipc_open": (c_int, [c_void_p, c_void_p, POINTER(c_void_p)]),
@@ -290,6 +296,38 @@ class Context:
         mw = MoeMxWeights(Hd, inter, E, k, expert_lo, hi, ptr(w["w13"]), ptr(w["sf13"]), ptr(w["w2"]), ptr(w["sf2"]))
         a = MoeMxArgs(T, ptr(xq), ptr(xsf), ptr(ids), ptr(weights), sh_lo, sh_hi, ptr(out))
         check(self.lib.afdk_moe_ffn_mx(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+
+    def dense_ffn_mx(self, w: dict, xq, xsf, out, stream: int = 0) -> None:
+        """Dense FFN in slice layout: w13 [n_split, 2*Is, H], sf13, w2 [n_split, H, Is], sf2."""
+        T, Hd = xq.shape
+        n_split, _, Is = w["w2"].shape
+        dw = DenseMxWeights(Hd, Is, n_split, ptr(w["w13"]), ptr(w["sf13"]), ptr(w["w2"]), ptr(w["sf2"]))
+        check(self.lib.afdk_dense_ffn_mx(self.handle, ctypes.byref(dw), T, ptr(xq), ptr(xsf), ptr(out),
+                                         c_void_p(stream)))
+
+    @staticmethod
+    def dense_split_layout(w13, sf13, w2, sf2, n_split):
+        """Re-lay standard dense weights (w13 [2I, H] gate rows then up rows,
+        w2 [H, I]) into the slice layout of afdk_dense_ffn_mx (torch or numpy)."""
+        I = w2.shape[1]
+        Is = I // n_split
+
+        def cat(a, b):
+            import numpy as np
+            return np.concatenate([a, b]) if isinstance(a, np.ndarray) else __import__("torch").cat([a, b])
+
+        def stack(parts):
+            import numpy as np
+            return np.stack(parts) if isinstance(parts[0], np.ndarray) else __import__("torch").stack(parts)
+
+        out = {}
+        for name, t, blk in (("w13", w13, 1), ("sf13", sf13, 1)):
+            out[name] = stack([cat(t[j * Is:(j + 1) * Is], t[I + j * Is:I + (j + 1) * Is]) for j in range(n_split)])
+        out["w2"] = stack([w2[:, j * Is:(j + 1) * Is] for j in range(n_split)])
+        out["sf2"] = stack([sf2[:, j * Is // 32:(j + 1) * Is // 32] for j in range(n_split)])
+        for k in out:
+            out[k] = out[k].contiguous() if hasattr(out[k], "contiguous") else out[k]
+        return out
 
     def quant_mx(self, x, q, sf, stream: int = 0) -> None:
         T, Hd = x.shape

@@ -208,6 +208,21 @@ struct MoeFfnMxArgs {
 size_t moe_ffn_mx_workspace_bytes(int T, int k, int E, int H, int I);
 cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws, cudaStream_t stream);
 
+// Dense FFN as n_split slices of the intermediate dimension ("virtual
+// experts" every token visits with weight 1), MXFP8 (moe_ffn.cu)
+struct DenseFfnMxArgs {
+  int T, H, Is, n_split;  // Is = inter / n_split
+  const void* w13;        // [n_split, 2*Is, H]
+  const uint8_t* sf13;
+  const void* w2;         // [n_split, H, Is]
+  const uint8_t* sf2;
+  const uint8_t* xq;      // [T, H]
+  const uint8_t* xsf;     // [T, H/32]
+  void* out;              // bf16 [T, H]
+};
+size_t dense_ffn_mx_workspace_bytes(int T, int n_split, int H, int Is);
+cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws, cudaStream_t stream);
+
 // ---------------------------------------------------------- AFD exchange
 bool exchange_available();
 cudaError_t exchange_signal(uint32_t* flag, uint32_t value, cudaStream_t s);

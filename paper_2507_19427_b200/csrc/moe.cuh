@@ -26,8 +26,10 @@ struct RouterArgs {
 
 struct Work {
   int group;  // expert id, or E for the shared expert
-  int row0;   // first row in the dispatch buffer
-  int rows;   // <= kChunk
+  int row0;   // first row of this item in the intermediate / output buffers
+  int rows;   // <= chunk
+  int xrow0;  // first row of its W13 input (MoE: = row0 in the dispatch buffer;
+              // dense FFN splits: the token row, shared by every split)
 };
 
 struct PermuteArgs {

@@ -2,6 +2,7 @@
 // K6 permute -> dispatch gather -> K7 W13 (+SwiGLU +FP8 requant) -> K8 W2 ->
 // K9 combine into this rank's bf16 partial (the attention side
 // reduces EP partials of several FFN ranks).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -9,6 +10,7 @@
 
 #include "afdk_internal.h"
 #include "moe.cuh"
+#include "sm100.cuh"
 
 namespace afdk {
 
@@ -129,6 +131,99 @@ cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cu
   moe::CombineArgs ca{y, a.ids, a.weights, inv, T, k, H, a.expert_lo, a.expert_hi, shared_local ? 1 : 0,
                       a.shared_lo, a.shared_hi, static_cast<__nv_bfloat16*>(a.out)};
   return chk(combine_launch(ca, stream, ctx.pdl), "combine");
+}
+
+// ------------------------------------------------------------- dense FFN
+// The 5 dense Step-3 layers (inter 18432, builtin_catalog.cpp:248-250) run
+// through the grouped MXFP8 GEMMs: slice j of the intermediate dimension is a
+// "virtual expert" over ALL tokens (item rows come straight from the input,
+// xrow0 = token row; intermediate / output rows at j*T + token), and the
+// combine sums the slices in fixed order.  Slices held by different FFN GPUs
+// give tensor-parallel partials reduced on the attention side like EP ones.
+namespace moe {
+
+__global__ void dense_work_kernel(int T, int n_split, int chunk, Work* work, int* n_work) {
+  sm100::griddep_wait();
+  sm100::griddep_launch();
+  if (threadIdx.x != 0) return;
+  const int n_items = (T + chunk - 1) / chunk;
+  const int per = ((T + n_items - 1) / n_items + 31) & ~31;
+  int g = 0;
+  for (int j = 0; j < n_split; ++j)
+    for (int r = 0; r < T; r += per) {
+      work[g].group = j;
+      work[g].row0 = j * T + r;
+      work[g].rows = min(per, T - r);
+      work[g].xrow0 = r;
+      ++g;
+    }
+  *n_work = g;
+}
+
+__global__ void __launch_bounds__(256) dense_combine_kernel(const float* y, int T, int n_split, int H,
+                                                            __nv_bfloat16* out) {
+  sm100::griddep_wait();
+  sm100::griddep_launch();
+  const int t = blockIdx.x;
+  for (int f = threadIdx.x * 4; f < H; f += blockDim.x * 4) {
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(y + (size_t)t * H + f));
+    for (int j = 1; j < n_split; ++j) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(y + ((size_t)j * T + t) * H + f));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    __nv_bfloat162 o0 = __floats2bfloat162_rn(acc.x, acc.y), o1 = __floats2bfloat162_rn(acc.z, acc.w);
+    uint2 o;
+    o.x = *reinterpret_cast<uint32_t*>(&o0);
+    o.y = *reinterpret_cast<uint32_t*>(&o1);
+    *reinterpret_cast<uint2*>(out + (size_t)t * H + f) = o;
+  }
+}
+
+}  // namespace moe
+
+static inline int dense_rows_pad(int T, int n_split) { return ((n_split * T + 127) / 128) * 128 + moe::kChunkMX2; }
+static inline int dense_max_work(int T, int n_split) { return n_split * (T / 32 + 2); }
+
+size_t dense_ffn_mx_workspace_bytes(int T, int n_split, int H, int Is) {
+  const int rp = dense_rows_pad(T, n_split);
+  size_t b = align_up((size_t)dense_max_work(T, n_split) * sizeof(moe::Work), 256) + 256;
+  b += align_up((size_t)rp * Is, 256);         // hq
+  b += align_up((size_t)rp * (Is / 32), 256);  // hsf
+  b += align_up((size_t)rp * H * 4, 256);      // y
+  return b;
+}
+
+cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws_base, cudaStream_t stream) {
+  const int rp = dense_rows_pad(a.T, a.n_split);
+  uint8_t* ws = static_cast<uint8_t*>(ws_base);
+  auto take = [&](size_t bytes) { void* p = ws; ws += align_up(bytes, 256); return p; };
+  auto* work = static_cast<moe::Work*>(take((size_t)dense_max_work(a.T, a.n_split) * sizeof(moe::Work)));
+  auto* n_work = static_cast<int*>(take(256));
+  auto* hq = static_cast<uint8_t*>(take((size_t)rp * a.Is));
+  auto* hsf = static_cast<uint8_t*>(take((size_t)rp * (a.Is / 32)));
+  auto* y = static_cast<float*>(take((size_t)rp * a.H * 4));
+  const bool pair = moe_mx_use_pair(a.T, 1, 1);
+  auto gemm = pair ? moe_gemm_mx2_launch : moe_gemm_mx_launch;
+  static const bool dbg = std::getenv("AFDK_DEBUG_SYNC") != nullptr;
+  auto chk = [&](cudaError_t err, const char* what) {
+    if (err == cudaSuccess && dbg) err = cudaStreamSynchronize(stream);
+    if (err != cudaSuccess) set_error(std::string("dense_ffn_mx/") + what + ": " + cudaGetErrorString(err));
+    return err;
+  };
+  cudaError_t e;
+  if ((e = chk(launch_k(ctx.pdl, moe::dense_work_kernel, dim3(1), dim3(32), 0, stream, a.T, a.n_split,
+                        pair ? moe::kChunkMX2 : moe::kChunkMX, work, n_work),
+               "work")) != cudaSuccess)
+    return e;
+  // group j < E = n_split always: weight index j, never the shared slot
+  MoeGemmMxArgs g13{a.w13, a.sf13, a.xq, a.xsf, work, n_work, a.H, a.Is, a.n_split, 0, a.n_split, a.T, hq, hsf,
+                    nullptr};
+  if ((e = chk(gemm(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
+  MoeGemmMxArgs g2{a.w2, a.sf2, hq, hsf, work, n_work, a.H, a.Is, a.n_split, 0, a.n_split, rp, nullptr, nullptr, y};
+  if ((e = chk(gemm(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
+  return chk(launch_k(ctx.pdl, moe::dense_combine_kernel, dim3(a.T), dim3(256), 0, stream, (const float*)y, a.T,
+                      a.n_split, a.H, static_cast<__nv_bfloat16*>(a.out)),
+             "combine");
 }
 
 }  // namespace afdk

@@ -125,7 +125,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
           mbar_expect_tx(&full[s], kAOps * kA + kB);
           tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol_w);
           if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol_w);
-          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, wk.row0, pol_x);
+          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, kGLU ? wk.xrow0 : wk.row0, pol_x);
         }
       }
     }
@@ -141,7 +141,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
       for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
         const int s = i % S, n = i / S;
         if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
-        const float* src = p.xs_t + (size_t)kb * p.rows_pad + wk.row0;
+        const float* src = p.xs_t + (size_t)kb * p.rows_pad + (kGLU ? wk.xrow0 : wk.row0);
         float* dst = xs_ring + s * kRing;
         dst[lane] = (lane < wk.rows) ? __ldg(src + lane) : 0.0f;
         dst[lane + 32] = (lane + 32 < wk.rows) ? __ldg(src + lane + 32) : 0.0f;

@@ -154,7 +154,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
             mbar_expect_tx(&sfg_full[g], kSfGrp);
             tma_load_2d(dst, &tm_wsf, &sfg_full[g], kb * 4, wrow, pol);
             if (kGLU) tma_load_2d(dst + kSfOp, &tm_wsf, &sfg_full[g], kb * 4, wrow + p.up_offset, pol);
-            tma_load_2d(dst + kAOps * kSfOp, &tm_xsf, &sfg_full[g], kb * 4, wk.row0, pol);
+            tma_load_2d(dst + kAOps * kSfOp, &tm_xsf, &sfg_full[g], kb * 4, kGLU ? wk.xrow0 : wk.row0, pol);
           }
           const int s = i % S, n = i / S;
           if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
@@ -162,7 +162,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
           mbar_expect_tx(&full[s], kAOps * kA + kB);
           tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol);
           if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol);
-          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, wk.row0, pol);
+          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, kGLU ? wk.xrow0 : wk.row0, pol);
         }
       }
     }

@@ -133,7 +133,8 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
         const int half = ((wk.rows + 31) & ~31) >> 1;
         const int widx = (wk.group == p.E ? p.n_local : wk.group - p.expert_lo) * p.w_rows;
         const int arow = kGLU ? widx + mt * 128 + 64 * (int)rank : widx + mt * 256 + 128 * (int)rank;
-        const int brow = wk.row0 + (int)rank * half;
+        const int in_row0 = kGLU ? wk.xrow0 : wk.row0;  // W13 reads the token rows, W2 the intermediate
+        const int brow = in_row0 + (int)rank * half;
         for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
           if ((kb & 3) == 0) {
             const int g = gi & 1, ng = gi >> 1;
@@ -143,7 +144,7 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
             mbar_expect_tx(&sfg_full[g], kPSfGrp);
             tma_load_2d(dst, &tm_wsf, &sfg_full[g], kb * 4, arow, pol);
             if (kGLU) tma_load_2d(dst + 1024, &tm_wsf, &sfg_full[g], kb * 4, arow + p.up_offset, pol);
-            tma_load_2d(dst + 2048, &tm_xsf, &sfg_full[g], kb * 4, wk.row0, pol);
+            tma_load_2d(dst + 2048, &tm_xsf, &sfg_full[g], kb * 4, in_row0, pol);
           }
           const int s = i % S, n = i / S;
           if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);

@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
         a.work[g].group = e;
         a.work[g].row0 = row0 + r;
         a.work[g].rows = min(per, rows - r);
+        a.work[g].xrow0 = row0 + r;
         ++g;
       }
     }

@@ -121,3 +121,38 @@ def test_moe_ffn_mx_expert_parallel_partials(ctx, mx_kernel):
     T = 50
     got, ref = run_moe_mx(ctx, T, 512, 512, 8, 3, 4, ranges=[((0, 4), (0, 20)), ((4, 8), (20, T))])
     assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+
+
+def run_dense(ctx, T, H, I, n_split, seed):
+    import torch
+
+    from paper_2507_19427_b200.afdk import Context
+
+    g = torch.Generator().manual_seed(seed)
+    dev = torch.device("cuda:0")
+    full = make_mx_experts(torch, 0, H, I, g, torch.device("cpu"))  # one [2I, H] / [H, I] FFN
+    w13, sf13, w2, sf2 = (full[n][0] for n in ("w13", "sf13", "w2", "sf2"))
+    split = Context.dense_split_layout(w13, sf13, w2, sf2, n_split)
+    wd = {k: v.to(dev) for k, v in split.items()}
+    x = torch.randn(T, H, generator=g)
+    xq, xsf = orc.quant_mx(x.numpy())
+    out = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+    ctx.dense_ffn_mx(wd, torch.from_numpy(xq).to(dev), torch.from_numpy(xsf).to(dev), out)
+    torch.cuda.synchronize()
+    ref = orc.expert_ffn_mx(xq, xsf, w13.numpy(), sf13.numpy(), w2.numpy(), sf2.numpy())
+    return out.float().cpu().numpy(), ref
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T", [1, 37, 300])
+def test_dense_ffn_mx(ctx, mx_kernel, T):
+    """Dense FFN as 4 intermediate slices == the unsplit FFN (fp32 slice sums)."""
+    got, ref = run_dense(ctx, T, 512, 2048, 4, 10 + T)
+    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+
+
+@pytest.mark.gpu
+def test_dense_ffn_mx_step3_dims(ctx):
+    """Step-3 dense layer: hidden 7168, inter 18432 as 4 slices of 4608."""
+    got, ref = run_dense(ctx, 16, 7168, 18432, 4, 3)
+    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)

@@ -379,14 +379,27 @@ def afd_roles(world):
     return {2: (1, 1), 3: (1, 2), 4: (1, 3), 8: (2, 6)}.get(world, (max(1, world // 4), world - max(1, world // 4)))
 
 
-def run_afd_measured(torch, dist, dev, world, rank, local, steps):
+def afd_runs(world):
+    """(plan, ffn format, T_mb) points measured at this world size: the survey's
+    plan (1A1F / 1A3F / 2A6F, config 5 at 8) at the 192-token baseline, then
+    MXFP8 at the largest micro-batch the attention layer takes, and the
+    balanced attention/FFN split."""
+    base = {2: (1, 1), 4: (1, 3), 8: (2, 6)}.get(world, (1, world - 1))
+    runs = [(base, "fp8", 192), (base, "mx", 256)]
+    bal = (world // 2, world - world // 2)
+    if bal != base:
+        runs.append((bal, "mx", 256))
+    return runs
+
+
+def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt="fp8", plan=None):
     """Real pipeline on all ranks: nA attention GPUs + nF FFN GPUs, 2 ping-pong
     micro-batches, 2 layers per step (distinct KV caches), copy-engine NVLink."""
     from paper_2507_19427_b200 import Context
     from paper_2507_19427_b200.afd import AfdConfig, AfdRank, wire_bytes
 
-    na, nf = afd_roles(world)
-    cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=192, n_micro=2, layers=2, ctx_len=CTX)
+    na, nf = plan if plan else afd_roles(world)
+    cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=T_mb, n_micro=2, layers=2, ctx_len=CTX, ffn_format=fmt)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -420,7 +433,9 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps):
     r.close()
     for c in ctxs:
         c.close()
-    return {"plan": f"{na}A{nf}F", "T_mb": cfg.T_mb, "n_micro": cfg.n_micro, "ctx": cfg.ctx_len,
+    del r
+    torch.cuda.empty_cache()
+    return {"plan": f"{na}A{nf}F", "ffn_format": fmt, "T_mb": cfg.T_mb, "n_micro": cfg.n_micro, "ctx": cfg.ctx_len,
             "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
             "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
             "nvlink_bytes_per_layer": {k: v * cfg.n_micro for k, v in wb.items()},
@@ -665,7 +680,11 @@ def main():
             if world == 1:
                 afd = run_afd_modeled(ctx)
             else:
-                afd = run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4))
+                # micro-batch sweep: per-layer throughput depends on balancing the
+                # attention tier (grows with T_mb) against expert weight streaming
+                runs = [run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4), T, f, plan)
+                        for plan, f, T in afd_runs(world)]
+                afd = {"runs": runs, "best": max(runs, key=lambda x: x["tokens_per_s_per_gpu_per_layer"])}
         except Exception as e:  # reported, never silently replaced
             afd = {"error": f"{type(e).__name__}: {e}"}
 

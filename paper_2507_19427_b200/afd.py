@@ -6,7 +6,7 @@ experts (expert parallel) and a share of the shared expert's tokens.  Per
 layer and micro-batch (pipesim.cpp:155-237 models it):
 
   A: mfa_layer -> router/quant into its send buffer -> signal every F
-  F: wait all A -> DMA-pull payloads (fp8 tokens, scales, top-k) -> moe_ffn
+  F: wait all A -> DMA-pull payloads (fp8 tokens, scales, top-k) -> moe_ffn(_mx)
      -> bf16 partial -> signal every A
   A: wait all F -> DMA-pull its rows of every partial -> x = h_res + sum partials
 
@@ -42,6 +42,19 @@ class AfdConfig:
     top_k: int = 3
     inter: int = 5120
     seed: int = 0
+    ffn_format: str = "fp8"   # "fp8": 1x128/128x128 fp32 scales; "mx": MXFP8 (UE8M0 per 32)
+
+    def __post_init__(self):
+        # validated identically on every rank before any buffer exchange: a rank
+        # that failed mid-pipeline would leave its peers waiting on a flag
+        if not 1 <= self.T_mb <= 256:
+            raise ValueError(f"T_mb={self.T_mb}: the attention-side layer takes 1..256 requests per micro-batch")
+        if self.ffn_format not in ("fp8", "mx"):
+            raise ValueError(f"ffn_format={self.ffn_format!r}: expected 'fp8' or 'mx'")
+        if self.ffn_format == "mx" and (self.hidden % 512 or self.inter % 512):
+            raise ValueError("ffn_format='mx' needs hidden and inter to be multiples of 512")
+        if self.n_attn < 1 or self.n_ffn < 1 or self.n_ffn > self.n_experts:
+            raise ValueError("need at least one attention and one FFN GPU, n_ffn <= n_experts")
 
     @property
     def world(self) -> int:
@@ -72,7 +85,9 @@ def shared_token_shard(f: int, cfg: AfdConfig) -> tuple[int, int]:
 @dataclass
 class PayloadLayout:
     """A->F message of one micro-batch, one contiguous buffer per attention GPU:
-    e4m3 tokens | fp32 1x128 scales | int32 top-k ids | fp32 top-k weights."""
+    e4m3 tokens | scales | int32 top-k ids | fp32 top-k weights.  The scale
+    section is T*H/32 bytes in both formats (fp32 per 1x128 block, or one
+    UE8M0 byte per 32 elements for MXFP8)."""
 
     T: int
     H: int
@@ -144,6 +159,7 @@ class AfdRank:
         (seed, e), so every GPU materialises identical shards."""
         t, c = self.torch, self.cfg
         ids = list(range(lo, hi)) + ([c.n_experts] if with_shared else [])
+        mx = c.ffn_format == "mx"
         w13, w2, s13, s2 = [], [], [], []
         for e in ids:
             g = t.Generator(device=self.dev).manual_seed(c.seed * 1000 + e + 1)
@@ -155,8 +171,15 @@ class AfdRank:
 
             w13.append(e4m3((2 * c.inter, c.hidden)))
             w2.append(e4m3((c.hidden, c.inter)))
-            s13.append(t.full((2 * c.inter // 128, c.hidden // 128), 0.5 / c.hidden ** 0.5, device=self.dev))
-            s2.append(t.full((c.hidden // 128, c.inter // 128), 0.5 / c.inter ** 0.5, device=self.dev))
+            if mx:  # UE8M0 2^-7: |w| ~ 2^-6..2^-3 like the 1x128 recipe below
+                s13.append(t.full((2 * c.inter, c.hidden // 32), 120, dtype=t.uint8, device=self.dev))
+                s2.append(t.full((c.hidden, c.inter // 32), 120, dtype=t.uint8, device=self.dev))
+            else:
+                s13.append(t.full((2 * c.inter // 128, c.hidden // 128), 0.5 / c.hidden ** 0.5, device=self.dev))
+                s2.append(t.full((c.hidden // 128, c.inter // 128), 0.5 / c.inter ** 0.5, device=self.dev))
+        if mx:
+            return {"n_experts": c.n_experts, "w13": t.stack(w13), "w2": t.stack(w2), "sf13": t.stack(s13),
+                    "sf2": t.stack(s2)}
         return {"n_experts": c.n_experts, "w13": t.stack(w13), "w2": t.stack(w2), "s13": t.stack(s13),
                 "s2": t.stack(s2)}
 
@@ -195,8 +218,10 @@ class AfdRank:
             self.expert_lo, self.expert_hi = lo, hi
             self.shared = shared_token_shard(self.idx, c)
             Tf = c.T_ffn
+            xs_shape, xs_dtype = ((Tf, c.hidden // 32), t.uint8) if c.ffn_format == "mx" else \
+                ((Tf, c.hidden // 128), t.float32)
             self.rx = [{"xq": t.empty(Tf, c.hidden, dtype=t.uint8, device=dev),
-                        "xs": t.empty(Tf, c.hidden // 128, dtype=t.float32, device=dev),
+                        "xs": t.empty(*xs_shape, dtype=xs_dtype, device=dev),
                         "ids": t.empty(Tf, c.top_k, dtype=t.int32, device=dev),
                         "wts": t.empty(Tf, c.top_k, dtype=t.float32, device=dev)} for _ in range(c.n_micro)]
             self.out = [t.empty(Tf, c.hidden, dtype=t.bfloat16, device=dev) for _ in range(c.n_micro)]
@@ -225,9 +250,15 @@ class AfdRank:
         ctx.mfa_layer(self.w, self.x[mb], k, v, bt, self.seq_lens, self.h_res[mb], self.h_norm[mb], stream=sp)
         buf, L = self.send[mb], self.lay
         view = lambda name, shape, dtype: buf[L.off[name]:L.off[name] + L.size(name)].view(dtype).view(*shape)
-        ctx.router_topk(self.h_norm[mb], self.w["gate"], c.top_k, view("ids", (c.T_mb, c.top_k), t.int32),
-                        view("wts", (c.T_mb, c.top_k), t.float32), xq=view("xq", (c.T_mb, c.hidden), t.uint8),
-                        xs=view("xs", (c.T_mb, c.hidden // 128), t.float32), stream=sp)
+        if c.ffn_format == "mx":
+            ctx.router_topk(self.h_norm[mb], self.w["gate"], c.top_k, view("ids", (c.T_mb, c.top_k), t.int32),
+                            view("wts", (c.T_mb, c.top_k), t.float32), stream=sp)
+            ctx.quant_mx(self.h_norm[mb], view("xq", (c.T_mb, c.hidden), t.uint8),
+                         view("xs", (c.T_mb, c.hidden // 32), t.uint8), stream=sp)
+        else:
+            ctx.router_topk(self.h_norm[mb], self.w["gate"], c.top_k, view("ids", (c.T_mb, c.top_k), t.int32),
+                            view("wts", (c.T_mb, c.top_k), t.float32), xq=view("xq", (c.T_mb, c.hidden), t.uint8),
+                            xs=view("xs", (c.T_mb, c.hidden // 128), t.float32), stream=sp)
         for f in range(c.n_ffn):
             r = c.n_attn + f
             ctx.signal(self.peer_flags[r] + 4 * flag_index(self.idx, mb, c), seq, stream=sp)
@@ -253,8 +284,9 @@ class AfdRank:
         self.copied[mb].record(self.copy_stream)
         st = self.streams[0]
         st.wait_event(self.copied[mb])
-        ctx.moe_ffn(self.moe_w, rx["xq"], rx["xs"], rx["ids"], rx["wts"], self.out[mb], expert_lo=self.expert_lo,
-                    expert_hi=self.expert_hi, shared=self.shared, stream=st.cuda_stream)
+        ffn = ctx.moe_ffn_mx if c.ffn_format == "mx" else ctx.moe_ffn
+        ffn(self.moe_w, rx["xq"], rx["xs"], rx["ids"], rx["wts"], self.out[mb], expert_lo=self.expert_lo,
+            expert_hi=self.expert_hi, shared=self.shared, stream=st.cuda_stream)
         for a in range(c.n_attn):
             ctx.signal(self.peer_flags[a] + 4 * flag_index(self.idx, mb, c), seq, stream=st.cuda_stream)
 

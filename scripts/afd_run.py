@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--fmt", default="fp8", choices=["fp8", "mx"])
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -36,10 +37,10 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     if a.check:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=24, n_micro=2, layers=1, hidden=1024,
-                        q_lora=256, ctx_len=300, n_experts=8, top_k=2, inter=256, seed=3)
+                        q_lora=256, ctx_len=300, n_experts=8, top_k=2, inter=512, seed=3, ffn_format=a.fmt)
     else:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=a.T_mb, n_micro=a.n_micro, layers=a.layers,
-                        ctx_len=a.ctx_len)
+                        ctx_len=a.ctx_len, ffn_format=a.fmt)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -82,10 +83,16 @@ def main():
                 ids = torch.empty(c.T_mb, c.top_k, dtype=torch.int32, device=dev)
                 wts = torch.empty(c.T_mb, c.top_k, device=dev)
                 xq = torch.empty(c.T_mb, c.hidden, dtype=torch.uint8, device=dev)
-                xs = torch.empty(c.T_mb, c.hidden // 128, device=dev)
-                ctxs[0].router_topk(h_norm, r.w["gate"], c.top_k, ids, wts, xq=xq, xs=xs)
                 part = torch.empty_like(h_res)
-                ctxs[0].moe_ffn(wall, xq, xs, ids, wts, part)
+                if c.ffn_format == "mx":
+                    xs = torch.empty(c.T_mb, c.hidden // 32, dtype=torch.uint8, device=dev)
+                    ctxs[0].router_topk(h_norm, r.w["gate"], c.top_k, ids, wts)
+                    ctxs[0].quant_mx(h_norm, xq, xs)
+                    ctxs[0].moe_ffn_mx(wall, xq, xs, ids, wts, part)
+                else:
+                    xs = torch.empty(c.T_mb, c.hidden // 128, device=dev)
+                    ctxs[0].router_topk(h_norm, r.w["gate"], c.top_k, ids, wts, xq=xq, xs=xs)
+                    ctxs[0].moe_ffn(wall, xq, xs, ids, wts, part)
                 torch.cuda.synchronize()
                 ref = (h_res.float() + part.float())
                 errs.append(rel_err(r.x[mb].float().cpu().numpy(), ref.cpu().numpy()))
@@ -97,7 +104,7 @@ def main():
                       "part err", rel_err(r.recv_part[mb][0].float().cpu().numpy(), part.float().cpu().numpy()),
                       "xq eq", bool(torch.equal(sent_xq, xq)), "ids eq", bool(torch.equal(sent_ids, ids)), flush=True)
             ok = max(errs) <= 2e-2
-            print(json.dumps({"afd_check": "ok" if ok else "FAIL", "rel_err": errs, "world": world,
+            print(json.dumps({"afd_check": "ok" if ok else "FAIL", "fmt": c.ffn_format, "rel_err": errs, "world": world,
                               "n_attn": cfg.n_attn}), flush=True)
         dist.barrier()
         r.close()

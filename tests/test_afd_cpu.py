@@ -132,3 +132,17 @@ def test_afd_protocol_gloo(world):
         p.join(120)
         assert p.exitcode == 0
     assert q.get(timeout=5) <= 1e-5
+
+
+def test_afd_config_validation():
+    import pytest
+
+    from paper_2507_19427_b200.afd import AfdConfig
+
+    with pytest.raises(ValueError):
+        AfdConfig(n_attn=1, n_ffn=1, T_mb=384)
+    with pytest.raises(ValueError):
+        AfdConfig(n_attn=1, n_ffn=1, T_mb=64, ffn_format="bf16")
+    with pytest.raises(ValueError):
+        AfdConfig(n_attn=1, n_ffn=1, T_mb=64, ffn_format="mx", inter=256)
+    AfdConfig(n_attn=2, n_ffn=6, T_mb=256, ffn_format="mx")

@@ -199,13 +199,22 @@ def moe_weight_bytes(n_experts):
     return n_experts * (3 * HIDDEN * INTER + 4 * (2 * INTER // 128 * HIDDEN // 128 + HIDDEN // 128 * INTER // 128))
 
 
-def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8"):
+def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=None):
     """One FFN-side MoE layer (permute, gather, W13+SwiGLU+requant, W2, combine)
     over T dispatched tokens, all 48 routed experts + the shared one on this GPU.
     fmt "fp8": e4m3 with 1x128 / 128x128 fp32 block scales (software-scaled
-    MMA); "mx": MXFP8 (UE8M0 per 32, hardware block-scaled MMA)."""
+    MMA); "mx": MXFP8 (UE8M0 per 32, hardware block-scaled MMA).
+    shard=(rank, world, dist): config 3 expert-sharded — this GPU holds experts
+    [r*48/N, (r+1)*48/N) and the shared expert for tokens [r*T/N, (r+1)*T/N)
+    and produces its bf16 partial (reduced on the attention side in AFD);
+    the time is the max over ranks."""
     g = torch.Generator(device="cpu").manual_seed(seed)
-    n = E_ROUTED + 1
+    lo, hi, sh = 0, E_ROUTED, (0, T)
+    if shard:
+        r_, n_, _ = shard
+        lo, hi = r_ * E_ROUTED // n_, (r_ + 1) * E_ROUTED // n_
+        sh = (r_ * T // n_, (r_ + 1) * T // n_)
+    n = hi - lo + 1
 
     def e4m3(shape):
         mag = torch.randint(0x18, 0x40, shape, dtype=torch.int32, device=dev)
@@ -232,10 +241,8 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8"):
     sp = stream.cuda_stream
 
     def step(i):
-        if fmt == "mx":
-            ctx.moe_ffn_mx(w, xq, xs, ids, wts, out, stream=sp)
-        else:
-            ctx.moe_ffn(w, xq, xs, ids, wts, out, stream=sp)
+        f = ctx.moe_ffn_mx if fmt == "mx" else ctx.moe_ffn
+        f(w, xq, xs, ids, wts, out, expert_lo=lo, expert_hi=hi, shared=sh, stream=sp)
 
     for i in range(warmup):
         step(i)
@@ -247,12 +254,18 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8"):
     b.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
-    touched = len(set(ids.flatten().tolist())) + 1
+    if shard:
+        t_ = torch.tensor([ms], device=dev)
+        shard[2].all_reduce(t_, op=shard[2].ReduceOp.MAX)
+        ms = float(t_.item())
+    idl = ids.flatten().tolist()
+    touched = len({e for e in idl if lo <= e < hi}) + 1
     wbytes = moe_weight_bytes(touched)
-    flops = 2.0 * 3 * HIDDEN * INTER * (TOPK + 1) * T
+    flops = 2.0 * 3 * HIDDEN * INTER * (sum(lo <= e < hi for e in idl) + sh[1] - sh[0])
     hbm_peak, tf_peak, kind = peaks()
     del w
     return {"T": T, "format": "mxfp8" if fmt == "mx" else "fp8_block128", "ms_per_layer": ms,
+            "experts_per_gpu": hi - lo, "gpus": shard[1] if shard else 1,
             "tokens_per_s": T / (ms * 1e-3),
             "hbm": {"achieved": wbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": wbytes / (ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": wbytes,
@@ -669,11 +682,16 @@ def main():
     moe = dense = None
     if not args.no_moe:
         # config 3 FFN layer: 1x128/128x128 fp8 (software-scaled) and MXFP8
-        # (hardware block-scaled; CTA-pair kernels at >= 64 rows/expert)
-        moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=rank, fmt=f)
-               for f, T in (("fp8", 256), ("fp8", 4096), ("mx", 256), ("mx", 4096), ("mx", 8192))]
+        # (hardware block-scaled; CTA-pair kernels at >= 64 rows/expert);
+        # at N > 1 the experts are sharded over the GPUs (config 3 at 2/4)
+        shard = (rank, world, dist) if world > 1 else None
+        pts = (("fp8", 256), ("mx", 256)) if shard else \
+            (("fp8", 256), ("fp8", 4096), ("mx", 256), ("mx", 4096), ("mx", 8192))
+        moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=0, fmt=f, shard=shard)
+               for f, T in pts]
         # dense Step-3 layers (inter 18432) as 4 intermediate slices, MXFP8
-        dense = [run_dense_bench(ctx, torch, dev, T, 4, max(5, args.steps // 4), 2) for T in (256, 4096)]
+        dense = None if shard else [run_dense_bench(ctx, torch, dev, T, 4, max(5, args.steps // 4), 2)
+                                    for T in (256, 4096)]
     afd = None
     if not args.no_afd:
         try:

@@ -202,6 +202,10 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
     set_error("afdk_mfa_layer: hidden and q_lora must be multiples of 64");
     return AFDK_ERR_INVALID;
   }
+  if (w->hidden > 16384 || w->q_lora > 4096) {
+    set_error("afdk_mfa_layer: hidden <= 16384 and q_lora <= 4096 (row epilogues span one 4-CTA cluster)");
+    return AFDK_ERR_INVALID;
+  }
   if (a->batch < 1 || a->batch > 256) { set_error("afdk_mfa_layer: batch must be in [1, 256]"); return AFDK_ERR_INVALID; }
   if (!a->x || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->h_res || !a->h_norm ||
       !w->in_norm || !w->w_qkv || !w->q_norm || !w->w_q_up || !w->w_o || !w->post_norm) {

@@ -36,6 +36,20 @@ struct SlotTable {
     for (int k = 0; k < nn; ++k) acc += __ldcg(base + (size_t)k * stride);
     return acc;
   }
+  // features f..f+3 (f % 4 == 0, one tile): one 16-byte load per segment
+  __device__ __forceinline__ float4 sum4(const LinearPlan& P, const float* __restrict__ part, int row,
+                                         int f) const {
+    const int t = f / kBM, c0 = c_lo[t], nn = n[t];
+    const float4* base = reinterpret_cast<const float4*>(part + ((size_t)(t + c0) * P.m_tok + row) * kBM + (f % kBM));
+    const size_t stride = (size_t)P.m_tok * kBM / 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int k = 0; k < nn; ++k) {
+      const float4 v = __ldcg(base + (size_t)k * stride);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    return acc;
+  }
 };
 
 __device__ __forceinline__ void build_slot_table(const LinearPlan& P, int G, SlotTable& tab) {

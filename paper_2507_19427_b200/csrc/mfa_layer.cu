@@ -38,35 +38,61 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-// xn = RMSNorm(x) * w, bf16 out (input_layernorm); dim % 4 == 0
-__global__ void __launch_bounds__(1024) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
-                                                       const __nv_bfloat16* __restrict__ w,
-                                                       __nv_bfloat16* __restrict__ out, int dim, float eps) {
+// Row statistics over a 4-CTA cluster (one row per cluster, a quarter of the
+// features per CTA): block sums exchanged through distributed shared memory,
+// added in rank order so all four CTAs hold the identical total.
+constexpr int kRowCluster = 4;
+__device__ __forceinline__ float cluster_row_sum(float v, float* red, float* slot) {
+  v = block_sum(v, red);
+  if (threadIdx.x == 0) *slot = v;
+  sm100::cluster_sync();
+  float t = 0.0f;
+#pragma unroll
+  for (int r = 0; r < kRowCluster; ++r) t += sm100::ld_shared_cluster_f32(sm100::mapa_shared(slot, r));
+  sm100::cluster_sync();  // peers finished reading `slot` before anyone moves on / exits
+  return t;
+}
+
+// xn = RMSNorm(x) * w, bf16 out (input_layernorm); grid B*4 in 4-CTA clusters,
+// CTA r of a row's cluster owns features [r*dim/4, (r+1)*dim/4); dim % 16 == 0
+__global__ void __launch_bounds__(512) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      const __nv_bfloat16* __restrict__ w,
+                                                      __nv_bfloat16* __restrict__ out, int dim, float eps) {
   __shared__ float red[32];
+  __shared__ float slot;
   sm100::griddep_wait();
   sm100::griddep_launch();
-  const size_t row = blockIdx.x;
+  const size_t row = blockIdx.x / kRowCluster;
+  const int q = dim / kRowCluster, f0 = (int)sm100::cluster_ctarank() * q;
   const __nv_bfloat16* xr = x + row * dim;
+  constexpr int kMax = 4;  // float4 groups per thread (dim/4 <= 4*4*512)
+  float2 a[kMax], b[kMax];
   float ss = 0.0f;
-  for (int i = threadIdx.x * 4; i < dim; i += blockDim.x * 4) {
-    const uint2 xb = *reinterpret_cast<const uint2*>(xr + i);
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.x));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.y));
-    ss += a.x * a.x + a.y * a.y + b.x * b.x + b.y * b.y;
+#pragma unroll
+  for (int j = 0; j < kMax; ++j) {
+    const int i = f0 + (threadIdx.x + j * blockDim.x) * 4;
+    a[j] = b[j] = make_float2(0.f, 0.f);
+    if (i < f0 + q) {
+      const uint2 xb = *reinterpret_cast<const uint2*>(xr + i);
+      a[j] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.x));
+      b[j] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.y));
+      ss += a[j].x * a[j].x + a[j].y * a[j].y + b[j].x * b[j].x + b[j].y * b[j].y;
+    }
   }
-  ss = block_sum(ss, red);
+  ss = cluster_row_sum(ss, red, &slot);
   const float inv = rsqrtf(ss / dim + eps);
-  for (int i = threadIdx.x * 4; i < dim; i += blockDim.x * 4) {
-    const uint2 xb = *reinterpret_cast<const uint2*>(xr + i);
-    const uint2 wb = *reinterpret_cast<const uint2*>(w + i);
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.x));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xb.y));
-    const float2 wa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb.x));
-    const float2 wc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb.y));
-    uint2 o;
-    o.x = sm100::pack_bf16x2((a.x * inv) * wa.x, (a.y * inv) * wa.y);
-    o.y = sm100::pack_bf16x2((b.x * inv) * wc.x, (b.y * inv) * wc.y);
-    *reinterpret_cast<uint2*>(out + row * dim + i) = o;
+#pragma unroll
+  for (int j = 0; j < kMax; ++j) {
+    const int i = f0 + (threadIdx.x + j * blockDim.x) * 4;
+    if (i < f0 + q) {
+      const uint2 wb = *reinterpret_cast<const uint2*>(w + i);
+      const float2 wa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb.x));
+      const float2 wc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb.y));
+      uint2 o;
+      o.x = sm100::pack_bf16x2((a[j].x * inv) * wa.x, (a[j].y * inv) * wa.y);
+      o.y = sm100::pack_bf16x2((b[j].x * inv) * wc.x, (b[j].y * inv) * wc.y);
+      *reinterpret_cast<uint2*>(out + row * dim + i) = o;
+    }
   }
 }
 
@@ -89,32 +115,54 @@ __device__ __forceinline__ uint8_t kv_e4m3(float x, float scale) {
 
 // y = [q_down|k|v] projection of one token row (fp32): q -> RMSNorm -> qa;
 // k -> RoPE -> K cache slot of position seq_len-1; v -> V cache slot.
+// grid B*4 in 4-CTA clusters: CTA r < 3 owns q features [r*QL/4, (r+1)*QL/4),
+// CTA 3 the last quarter of q plus all of k and v (q RMSNorm statistics over
+// the cluster; CTA 3 does the RoPE + KV append).  QL/4 + 2*head_dim <= 2048.
 __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
                                                            int G, const QkvEpi e) {
-  extern __shared__ float row_s[];  // n_out floats
   __shared__ float red[32];
+  __shared__ float slot;
+  __shared__ float kv_s[2 * 256];  // k then v of this row (head_dim <= 256)
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
   sm100::griddep_wait();
   sm100::griddep_launch();
-  const int row = blockIdx.x;
+  const int row = blockIdx.x / kRowCluster;
+  const int rank = (int)sm100::cluster_ctarank();
+  const int qs = e.q_lora / kRowCluster, f0 = rank * qs;
+  const int f1 = rank == kRowCluster - 1 ? e.n_out : f0 + qs;
+  const int f = f0 + threadIdx.x * 4;  // 4 features per thread ((f1 - f0)/4 <= blockDim)
+  const bool act = f < f1;
+  float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
   float ss = 0.0f;
-  for (int f = threadIdx.x; f < e.n_out; f += blockDim.x) {
-    const float v = bf16r(tab.sum(P, part, row, f));
-    row_s[f] = v;
-    if (f < e.q_lora) ss += v * v;
+  if (act) {
+    v4 = tab.sum4(P, part, row, f);
+    v4 = make_float4(bf16r(v4.x), bf16r(v4.y), bf16r(v4.z), bf16r(v4.w));
+    if (f < e.q_lora) ss = v4.x * v4.x + v4.y * v4.y + v4.z * v4.z + v4.w * v4.w;
+    else {
+      const int o = f - e.q_lora;  // k (and v) features of this row
+      kv_s[o] = v4.x; kv_s[o + 1] = v4.y; kv_s[o + 2] = v4.z; kv_s[o + 3] = v4.w;
+    }
   }
-  ss = block_sum(ss, red);  // includes __syncthreads: row_s complete
+  ss = cluster_row_sum(ss, red, &slot);  // includes __syncthreads: kv_s complete
   const float inv = rsqrtf(ss / e.q_lora + e.eps);
-  for (int f = threadIdx.x; f < e.q_lora; f += blockDim.x)
-    e.qa[(size_t)row * e.q_lora + f] = __float2bfloat16_rn((row_s[f] * inv) * __bfloat162float(e.q_norm_w[f]));
+  if (act && f < e.q_lora) {
+    const uint2 wb = *reinterpret_cast<const uint2*>(e.q_norm_w + f);
+    const float2 wa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb.x));
+    const float2 wc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wb.y));
+    uint2 o;
+    o.x = sm100::pack_bf16x2((v4.x * inv) * wa.x, (v4.y * inv) * wa.y);
+    o.y = sm100::pack_bf16x2((v4.z * inv) * wc.x, (v4.w * inv) * wc.y);
+    *reinterpret_cast<uint2*>(e.qa + (size_t)row * e.q_lora + f) = o;
+  }
+  if (f1 <= e.q_lora) return;  // this CTA holds no k/v features
   const int pos = __ldg(e.seq_lens + row) - 1;
   if (pos < 0) return;
   const int pg = __ldg(e.block_table + (size_t)row * e.max_pages + pos / e.page);
-  const size_t slot = ((size_t)pg * e.page + pos % e.page) * e.head_dim;
+  const size_t kslot = ((size_t)pg * e.page + pos % e.page) * e.head_dim;
   const int half = e.head_dim / 2;
-  const float* k = row_s + e.q_lora;
-  const float* v = k + e.head_dim;
+  const float* k = kv_s;
+  const float* v = kv_s + e.head_dim;
   const bool fp8 = e.k_scale > 0.0f;
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
     double sn, cs;
@@ -124,18 +172,18 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
     const __nv_bfloat16 k1 = __float2bfloat16_rn(x1 * c - x2 * s), k2 = __float2bfloat16_rn(x2 * c + x1 * s);
     if (fp8) {
       uint8_t* k8 = reinterpret_cast<uint8_t*>(e.k_cache);
-      k8[slot + i] = kv_e4m3(__bfloat162float(k1), e.k_scale);
-      k8[slot + i + half] = kv_e4m3(__bfloat162float(k2), e.k_scale);
+      k8[kslot + i] = kv_e4m3(__bfloat162float(k1), e.k_scale);
+      k8[kslot + i + half] = kv_e4m3(__bfloat162float(k2), e.k_scale);
     } else {
-      e.k_cache[slot + i] = k1;
-      e.k_cache[slot + i + half] = k2;
+      e.k_cache[kslot + i] = k1;
+      e.k_cache[kslot + i + half] = k2;
     }
   }
   for (int i = threadIdx.x; i < e.head_dim; i += blockDim.x) {
     if (fp8)
-      reinterpret_cast<uint8_t*>(e.v_cache)[slot + i] = kv_e4m3(v[i], e.v_scale);
+      reinterpret_cast<uint8_t*>(e.v_cache)[kslot + i] = kv_e4m3(v[i], e.v_scale);
     else
-      e.v_cache[slot + i] = __float2bfloat16_rn(v[i]);
+      e.v_cache[kslot + i] = __float2bfloat16_rn(v[i]);
   }
 }
 
@@ -147,67 +195,84 @@ __global__ void __launch_bounds__(1024) qup_epilogue_kernel(const LinearPlan P, 
                                                             const double* __restrict__ inv_freq,
                                                             __nv_bfloat16* __restrict__ q) {
   __shared__ lin::SlotTable tab;
+  __shared__ float2 cs_s[256];  // (cos, sin) of the row's position per frequency (head_dim <= 512)
   lin::build_slot_table(P, G, tab);
-  sm100::griddep_wait();
-  sm100::griddep_launch();
   const int row = blockIdx.x;
   const int half = head_dim / 2;
   const int pos = max(__ldg(seq_lens + row) - 1, 0);
+  // every head shares the row's rotation: one double-precision sincos per
+  // frequency per CTA (seq_lens / inv_freq are inputs: before griddep_wait)
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    double sn, cs;
+    sincos((double)pos * inv_freq[i], &sn, &cs);
+    cs_s[i] = make_float2((float)cs, (float)sn);
+  }
+  __syncthreads();
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const int idx = blockIdx.y * blockDim.x + threadIdx.x;  // pair index in the row
   if (idx >= n_out / 2) return;
   const int h = idx / half, i = idx % half;
   const int c1 = h * head_dim + i;
   const size_t f1 = (size_t)row * n_out + c1, f2 = f1 + half;
   const float x1 = bf16r(tab.sum(P, part, row, c1)), x2 = bf16r(tab.sum(P, part, row, c1 + half));
-  double sn, cs;
-  sincos((double)pos * inv_freq[i], &sn, &cs);
-  const float c = (float)cs, s = (float)sn;
+  const float c = cs_s[i].x, s = cs_s[i].y;
   q[f1] = __float2bfloat16_rn(x1 * c - x2 * s);
   q[f2] = __float2bfloat16_rn(x2 * c + x1 * s);
 }
 
 // y = o_proj (fp32); h_res = bf16(x + y); h_norm = RMSNorm(h_res) (post_attention_layernorm)
-__global__ void __launch_bounds__(1024) o_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
-                                                          int G, int n, const __nv_bfloat16* __restrict__ x,
-                                                          const __nv_bfloat16* __restrict__ w_post, float eps,
-                                                          __nv_bfloat16* __restrict__ h_res,
-                                                          __nv_bfloat16* __restrict__ h_norm) {
-  extern __shared__ float row_s[];
+// grid B*4 in 4-CTA clusters, CTA r owns features [r*n/4, (r+1)*n/4); n % 16 == 0
+__global__ void __launch_bounds__(512) o_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
+                                                         int G, int n, const __nv_bfloat16* __restrict__ x,
+                                                         const __nv_bfloat16* __restrict__ w_post, float eps,
+                                                         __nv_bfloat16* __restrict__ h_res,
+                                                         __nv_bfloat16* __restrict__ h_norm) {
   __shared__ float red[32];
+  __shared__ float slot;
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
   sm100::griddep_wait();
   sm100::griddep_launch();
-  const size_t row = blockIdx.x;
+  const size_t row = blockIdx.x / kRowCluster;
+  const int q = n / kRowCluster, f0 = (int)sm100::cluster_ctarank() * q;
+  constexpr int kMax = 2;  // float4 groups per thread (n/4 <= 2*4*512)
+  float r[kMax][4];
   float ss = 0.0f;
-  for (int f = threadIdx.x * 4; f < n; f += blockDim.x * 4) {
-    const float4 o = make_float4(tab.sum(P, part, (int)row, f), tab.sum(P, part, (int)row, f + 1),
-                                 tab.sum(P, part, (int)row, f + 2), tab.sum(P, part, (int)row, f + 3));
-    const uint2 xb = *reinterpret_cast<const uint2*>(x + row * n + f);
-    const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&xb.x);
-    const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&xb.y);
-    const float r[4] = {bf16r(__low2float(x01) + o.x), bf16r(__high2float(x01) + o.y),
-                        bf16r(__low2float(x23) + o.z), bf16r(__high2float(x23) + o.w)};
-    uint2 ob;
-    ob.x = sm100::pack_bf16x2(r[0], r[1]);
-    ob.y = sm100::pack_bf16x2(r[2], r[3]);
-    *reinterpret_cast<uint2*>(h_res + row * n + f) = ob;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      row_s[f + q] = r[q];
-      ss += r[q] * r[q];
+  for (int j = 0; j < kMax; ++j) {
+    const int f = f0 + (threadIdx.x + j * blockDim.x) * 4;
+    if (f < f0 + q) {
+      const float4 o = tab.sum4(P, part, (int)row, f);
+      const uint2 xb = *reinterpret_cast<const uint2*>(x + row * n + f);
+      const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&xb.x);
+      const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&xb.y);
+      r[j][0] = bf16r(__low2float(x01) + o.x);
+      r[j][1] = bf16r(__high2float(x01) + o.y);
+      r[j][2] = bf16r(__low2float(x23) + o.z);
+      r[j][3] = bf16r(__high2float(x23) + o.w);
+      uint2 ob;
+      ob.x = sm100::pack_bf16x2(r[j][0], r[j][1]);
+      ob.y = sm100::pack_bf16x2(r[j][2], r[j][3]);
+      *reinterpret_cast<uint2*>(h_res + row * n + f) = ob;
+#pragma unroll
+      for (int z = 0; z < 4; ++z) ss += r[j][z] * r[j][z];
     }
   }
-  ss = block_sum(ss, red);
+  ss = cluster_row_sum(ss, red, &slot);
   const float inv = rsqrtf(ss / n + eps);
-  for (int f = threadIdx.x * 4; f < n; f += blockDim.x * 4) {
-    const uint2 wb = *reinterpret_cast<const uint2*>(w_post + f);
-    const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&wb.x);
-    const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&wb.y);
-    uint2 ob;
-    ob.x = sm100::pack_bf16x2((row_s[f] * inv) * __low2float(w01), (row_s[f + 1] * inv) * __high2float(w01));
-    ob.y = sm100::pack_bf16x2((row_s[f + 2] * inv) * __low2float(w23), (row_s[f + 3] * inv) * __high2float(w23));
-    *reinterpret_cast<uint2*>(h_norm + row * n + f) = ob;
+#pragma unroll
+  for (int j = 0; j < kMax; ++j) {
+    const int f = f0 + (threadIdx.x + j * blockDim.x) * 4;
+    if (f < f0 + q) {
+      const uint2 wb = *reinterpret_cast<const uint2*>(w_post + f);
+      const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&wb.x);
+      const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&wb.y);
+      uint2 ob;
+      ob.x = sm100::pack_bf16x2((r[j][0] * inv) * __low2float(w01), (r[j][1] * inv) * __high2float(w01));
+      ob.y = sm100::pack_bf16x2((r[j][2] * inv) * __low2float(w23), (r[j][3] * inv) * __high2float(w23));
+      *reinterpret_cast<uint2*>(h_norm + row * n + f) = ob;
+    }
   }
 }
 
@@ -258,8 +323,9 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   cudaError_t e;
 
   // K1a: input RMSNorm
-  if ((e = launch_k(ctx.pdl, rmsnorm_kernel, dim3(B), dim3(1024), 0, stream, static_cast<const __nv_bfloat16*>(a.x),
-                    static_cast<const __nv_bfloat16*>(a.w_in_norm), xn, Hd, a.rms_eps)) != cudaSuccess)
+  if ((e = launch_cluster_k(ctx.pdl, kRowCluster, rmsnorm_kernel, dim3(B * kRowCluster), dim3(512), 0, stream,
+                            static_cast<const __nv_bfloat16*>(a.x), static_cast<const __nv_bfloat16*>(a.w_in_norm),
+                            xn, Hd, a.rms_eps)) != cudaSuccess)
     return e;
   // K1b: [q_down | k | v] projection, then q RMSNorm + RoPE(k) + paged KV append
   const LinearPlan p1 = make_linear_plan(B, QL + 2 * D, Hd);
@@ -267,8 +333,8 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   QkvEpi qe{QL, D, a.page_size, a.max_pages, p1.n_out, a.rms_eps,
             static_cast<const __nv_bfloat16*>(a.w_q_norm), qa, static_cast<__nv_bfloat16*>(a.k_cache),
             static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq, a.k_scale, a.v_scale};
-  if ((e = launch_k(ctx.pdl, qkv_epilogue_kernel, dim3(B), dim3(512), p1.n_out * sizeof(float), stream, p1,
-                    (const float*)part, linear_grid(ctx, p1), qe)) != cudaSuccess)
+  if ((e = launch_cluster_k(ctx.pdl, kRowCluster, qkv_epilogue_kernel, dim3(B * kRowCluster), dim3(512), 0, stream,
+                            p1, (const float*)part, linear_grid(ctx, p1), qe)) != cudaSuccess)
     return e;
   // K1c: q_up projection + RoPE(q)
   const LinearPlan p2 = make_linear_plan(B, NQ, QL);
@@ -285,10 +351,11 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   // K4: o_proj, then residual + post-attention RMSNorm
   const LinearPlan p3 = make_linear_plan(B, Hd, NQ);
   if ((e = linear_bf16_launch(ctx, p3, attn, a.w_o, part, stream)) != cudaSuccess) return e;
-  if ((e = launch_k(ctx.pdl, o_epilogue_kernel, dim3(B), dim3(1024), Hd * sizeof(float), stream, p3,
-                    (const float*)part, linear_grid(ctx, p3), Hd, static_cast<const __nv_bfloat16*>(a.x),
-                    static_cast<const __nv_bfloat16*>(a.w_post_norm), a.rms_eps,
-                    static_cast<__nv_bfloat16*>(a.h_res), static_cast<__nv_bfloat16*>(a.h_norm))) != cudaSuccess)
+  if ((e = launch_cluster_k(ctx.pdl, kRowCluster, o_epilogue_kernel, dim3(B * kRowCluster), dim3(512), 0, stream, p3,
+                            (const float*)part, linear_grid(ctx, p3), Hd, static_cast<const __nv_bfloat16*>(a.x),
+                            static_cast<const __nv_bfloat16*>(a.w_post_norm), a.rms_eps,
+                            static_cast<__nv_bfloat16*>(a.h_res), static_cast<__nv_bfloat16*>(a.h_norm))) !=
+      cudaSuccess)
     return e;
   return cudaGetLastError();
 }

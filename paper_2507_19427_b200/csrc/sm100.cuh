@@ -86,6 +86,12 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
+__device__ __forceinline__ float ld_shared_cluster_f32(uint32_t cluster_addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
+
 // ------------------------------------------- programmatic dependent launch
 // Every kernel waits for its stream predecessor (griddepcontrol.wait, a no-op
 // when launched without the PDL attribute) before touching data it may have

@@ -188,8 +188,8 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
 }
 
 // y = q_up projection (fp32 [B, n_heads*head_dim]); per-head NeoX RoPE -> q bf16.
-// grid (B, n_heads/8), 8 heads x head_dim/2 pairs per CTA.
-__global__ void __launch_bounds__(1024) qup_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
+// grid (B, ceil(n_out/8/blockDim)): each thread rotates 4 consecutive pairs.
+__global__ void __launch_bounds__(256) qup_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
                                                             int G, int n_out, int head_dim,
                                                             const int32_t* __restrict__ seq_lens,
                                                             const double* __restrict__ inv_freq,
@@ -210,15 +210,24 @@ __global__ void __launch_bounds__(1024) qup_epilogue_kernel(const LinearPlan P, 
   __syncthreads();
   sm100::griddep_wait();
   sm100::griddep_launch();
-  const int idx = blockIdx.y * blockDim.x + threadIdx.x;  // pair index in the row
+  const int idx = (blockIdx.y * blockDim.x + threadIdx.x) * 4;  // first of 4 consecutive pairs in the row
   if (idx >= n_out / 2) return;
-  const int h = idx / half, i = idx % half;
+  const int h = idx / half, i = idx % half;  // half % 4 == 0: the 4 pairs share the head
   const int c1 = h * head_dim + i;
-  const size_t f1 = (size_t)row * n_out + c1, f2 = f1 + half;
-  const float x1 = bf16r(tab.sum(P, part, row, c1)), x2 = bf16r(tab.sum(P, part, row, c1 + half));
-  const float c = cs_s[i].x, s = cs_s[i].y;
-  q[f1] = __float2bfloat16_rn(x1 * c - x2 * s);
-  q[f2] = __float2bfloat16_rn(x2 * c + x1 * s);
+  const float4 a = tab.sum4(P, part, row, c1), b = tab.sum4(P, part, row, c1 + half);
+  const float x1[4] = {bf16r(a.x), bf16r(a.y), bf16r(a.z), bf16r(a.w)};
+  const float x2[4] = {bf16r(b.x), bf16r(b.y), bf16r(b.z), bf16r(b.w)};
+  float o1[4], o2[4];
+#pragma unroll
+  for (int z = 0; z < 4; ++z) {
+    const float c = cs_s[i + z].x, s = cs_s[i + z].y;
+    o1[z] = x1[z] * c - x2[z] * s;
+    o2[z] = x2[z] * c + x1[z] * s;
+  }
+  const size_t f1 = (size_t)row * n_out + c1;
+  *reinterpret_cast<uint2*>(q + f1) = make_uint2(sm100::pack_bf16x2(o1[0], o1[1]), sm100::pack_bf16x2(o1[2], o1[3]));
+  *reinterpret_cast<uint2*>(q + f1 + half) =
+      make_uint2(sm100::pack_bf16x2(o2[0], o2[1]), sm100::pack_bf16x2(o2[2], o2[3]));
 }
 
 // y = o_proj (fp32); h_res = bf16(x + y); h_norm = RMSNorm(h_res) (post_attention_layernorm)
@@ -339,7 +348,7 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   // K1c: q_up projection + RoPE(q)
   const LinearPlan p2 = make_linear_plan(B, NQ, QL);
   if ((e = linear_bf16_launch(ctx, p2, qa, a.w_q_up, part, stream)) != cudaSuccess) return e;
-  if ((e = launch_k(ctx.pdl, qup_epilogue_kernel, dim3(B, (NQ / 2 + 1023) / 1024), dim3(1024), 0, stream, p2,
+  if ((e = launch_k(ctx.pdl, qup_epilogue_kernel, dim3(B, (NQ / 8 + 255) / 256), dim3(256), 0, stream, p2,
                     (const float*)part, linear_grid(ctx, p2), NQ, D, a.seq_lens, inv_freq, q)) != cudaSuccess)
     return e;
   // K2/K3: MFA decode core over the paged cache (now including this token)

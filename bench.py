@@ -191,6 +191,36 @@ def run_fp8_kv(ctx, torch, dev, s, batch, ctx_len, steps):
                          "frac": core_bytes / (core_ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": core_bytes}}
 
 
+def run_mtp(ctx, torch, dev, s, batch, ctx_len, steps):
+    """MTP what-if (costmodel.cpp:46-58): the MFA core with 2 query tokens per
+    request over the same config-2 bf16 KV (one M=128 contraction per page)."""
+    q2 = torch.randn(batch, 2, H, D, device=dev).to(torch.bfloat16)
+    o2 = torch.empty(batch, 2, H, D, device=dev, dtype=torch.bfloat16)
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        k, v = s["kv"][i % N_ROT]
+        ctx.mfa_decode_attention_mtp(q2, k, v, s["block_table"], s["seq_lens"], o2, D ** -0.5,
+                                     stream=stream.cuda_stream)
+
+    for i in range(3):
+        step(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(steps):
+        step(i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    nbytes = kv_bytes(batch, ctx_len) + 2 * batch * 2 * H * D * 2
+    hbm_peak = peaks()[0]
+    return {"workload": "config2 MFA core, mtp=2 (2 query tokens per request, causal)", "batch": batch,
+            "ctx": ctx_len, "core_ms": ms, "query_tokens_per_s": 2 * batch / (ms * 1e-3),
+            "hbm": {"achieved": nbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": nbytes / (ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": nbytes}}
+
+
 # ------------------------------------------------- config 3: MoE FFN layer
 E_ROUTED, TOPK, INTER = 48, 3, 5120
 
@@ -676,9 +706,10 @@ def main():
     long_ctx = None
     if not args.no_long:
         long_ctx = run_long_context(ctx, torch, dev, max(3, args.steps // 4))
-    fp8kv = None
+    fp8kv = mtp = None
     if not args.no_fp8kv:
         fp8kv = run_fp8_kv(ctx, torch, dev, s, args.batch, args.ctx, max(5, args.steps // 2))
+        mtp = run_mtp(ctx, torch, dev, s, args.batch, args.ctx, max(5, args.steps // 2))
     moe = dense = None
     if not args.no_moe:
         # config 3 FFN layer: 1x128/128x128 fp8 (software-scaled) and MXFP8
@@ -738,6 +769,7 @@ def main():
                     "d2h_bytes_per_step": out_host.numel() * out_host.element_size()},
             "config4_long_context": long_ctx,
             "config2_fp8_kv": fp8kv,
+            "config2_mtp2": mtp,
             "config1_cpu": config1_cpu() if (world == 1 and not args.no_cpu_baseline) else None,
             "moe_ffn": moe,
             "dense_ffn": dense,

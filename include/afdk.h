@@ -101,6 +101,16 @@ afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args*
 afdk_status afdk_mfa_decode_attention_fp8(afdk_ctx* ctx, const afdk_mfa_decode_args* a, float k_scale,
                                           float v_scale, afdk_stream stream);
 
+/* Multi-token decode (MTP, mtp in {1, 2}): the mtp newest tokens of every
+ * request (positions L-mtp .. L-1, already appended) query the bf16 cache
+ * together; token j attends causally to positions <= L-mtp+j.  The
+ * reference's mtp multiplier on attention FLOPs with KV bytes unchanged
+ * (costmodel.cpp:46-58).  q/out [batch, mtp, n_heads, head_dim] bf16,
+ * lse [batch, mtp, n_heads]; a token that sees no key gives zeros / -inf.
+ * mtp = 2 runs one M=128 tensor-core contraction per KV page; batch <= 128. */
+afdk_status afdk_mfa_decode_attention_mtp(afdk_ctx* ctx, const afdk_mfa_decode_args* a, int mtp,
+                                          afdk_stream stream);
+
 /* ------------------------------------------------------------ K1/K4 GEMM
  * y[m, n] = x[m, k] . w[n, k]^T, bf16 inputs, fp32 accumulate, decode-shaped
  * (1 <= m <= 256, k % 64 == 0).  out is bf16 (out_fp32 = 0) or fp32.      */

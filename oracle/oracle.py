@@ -134,6 +134,25 @@ def mfa_decode_attention(q, k_cache, v_cache, block_table, seq_lens, scale, roun
     return out, lse
 
 
+def mfa_decode_attention_mtp(q, k_cache, v_cache, block_table, seq_lens, scale, round_bf16=False):
+    """Multi-token decode (MTP what-if, costmodel.cpp:46-58 mtp factor).
+
+    q [B, mtp, H, D]: the mtp newest tokens of every request (positions
+    L-mtp .. L-1, all already in the KV cache).  Query j attends causally to
+    keys at positions <= L-mtp+j; a query whose position is negative (L < mtp)
+    yields zeros / -inf LSE.  Exact attention per query, as orc_mfa_decode_attention."""
+    q = _f32(q)
+    B, mtp, H, D = q.shape
+    seq_lens = _i32(seq_lens)
+    out = np.empty_like(q)
+    lse = np.empty((B, mtp, H), np.float32)
+    for j in range(mtp):
+        sl = np.maximum(seq_lens - (mtp - 1 - j), 0).astype(np.int32)
+        o, l = mfa_decode_attention(q[:, j], k_cache, v_cache, block_table, sl, scale, round_bf16=round_bf16)
+        out[:, j], lse[:, j] = o, l
+    return out, lse
+
+
 def mfa_decode_attention_fp8(q, kq, vq, k_scale, v_scale, block_table, seq_lens, scale, round_bf16=False):
     """FP8-KV MFA decode (the paper's production setting).
 

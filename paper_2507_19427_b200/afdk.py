@@ -132,6 +132,7 @@ SIGNATURES = {
     "afdk_moe_ffn": (c_int, [c_void_p, POINTER(MoeWeights), POINTER(MoeArgs), c_void_p]),
     "afdk_mfa_layer_fp8": (c_int, [c_void_p, POINTER(MfaWeights), POINTER(MfaLayerArgs), c_float, c_float,
                                    c_void_p]),
+    "afdk_mfa_decode_attention_mtp": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_int, c_void_p]),
     "afdk_mfa_decode_attention_fp8": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_float, c_float, c_void_p]),
     "afdk_moe_ffn_mx": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), c_void_p]),
     "afdk_dense_ffn_mx": (c_int, [c_void_p, POINTER(DenseMxWeights), c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -219,6 +220,15 @@ class Context:
                           k_cache.shape[0], ptr(block_table), block_table.shape[1], ptr(seq_lens),
                           softmax_scale, ptr(out), ptr(lse))
         check(self.lib.afdk_mfa_decode_attention(self.handle, ctypes.byref(a), c_void_p(stream)))
+
+    def mfa_decode_attention_mtp(self, q, k_cache, v_cache, block_table, seq_lens, out, softmax_scale: float,
+                                 lse=None, stream: int = 0) -> None:
+        """q/out [B, mtp, H, D]: the mtp newest tokens of each request (causal among them)."""
+        B, mtp, H, D = q.shape
+        a = MfaDecodeArgs(B, H, D, k_cache.shape[1], ptr(q), ptr(k_cache), ptr(v_cache),
+                          k_cache.shape[0], ptr(block_table), block_table.shape[1], ptr(seq_lens),
+                          softmax_scale, ptr(out), ptr(lse))
+        check(self.lib.afdk_mfa_decode_attention_mtp(self.handle, ctypes.byref(a), mtp, c_void_p(stream)))
 
     def mfa_decode_attention_fp8(self, q, k_cache, v_cache, block_table, seq_lens, out, softmax_scale: float,
                                  k_scale: float, v_scale: float, lse=None, stream: int = 0) -> None:

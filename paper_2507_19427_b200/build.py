@@ -20,6 +20,7 @@ CU_SOURCES = [
     "afdk_api.cu",
     "mfa_decode.cu",
     "mfa_decode_fp8.cu",
+    "mfa_decode_mtp.cu",
     "linear.cu",
     "moe_gemm_mx.cu",
     "moe_gemm_mx2.cu",

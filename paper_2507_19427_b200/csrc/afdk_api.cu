@@ -174,6 +174,32 @@ afdk_status afdk_mfa_decode_attention_fp8(afdk_ctx* ctx, const afdk_mfa_decode_a
   return mfa_decode_entry(ctx, a, true, k_scale, v_scale, stream);
 }
 
+afdk_status afdk_mfa_decode_attention_mtp(afdk_ctx* ctx, const afdk_mfa_decode_args* a, int mtp,
+                                          afdk_stream stream) {
+  if (!ctx || !a) { set_error("afdk_mfa_decode_attention_mtp: NULL ctx/args"); return AFDK_ERR_INVALID; }
+  if (mtp == 1) return mfa_decode_entry(ctx, a, false, 1.0f, 1.0f, stream);
+  if (mtp != 2) { set_error("mfa_decode_mtp: mtp must be 1 or 2"); return AFDK_ERR_INVALID; }
+  if (a->n_heads != 64 || a->head_dim != 256 || a->page_size != 64) {
+    set_error("mfa_decode_mtp: n_heads/head_dim/page_size must be 64/256/64");
+    return AFDK_ERR_INVALID;
+  }
+  if (a->batch <= 0 || a->batch > 128) { set_error("mfa_decode_mtp: batch must be in [1, 128]"); return AFDK_ERR_INVALID; }
+  if (a->num_pages <= 0 || a->max_pages <= 0) { set_error("mfa_decode_mtp: num_pages/max_pages must be > 0"); return AFDK_ERR_INVALID; }
+  if (!a->q || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->out) {
+    set_error("mfa_decode_mtp: NULL tensor pointer");
+    return AFDK_ERR_INVALID;
+  }
+  afdk::Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  void* ws = afdk::workspace(c, afdk::mfa_decode_mtp_workspace_bytes(a->batch, c.num_sms));
+  if (!ws) { set_error("mfa_decode_mtp: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  afdk::MfaDecodeArgs m{a->batch, a->q, a->k_cache, a->v_cache, a->num_pages, a->block_table,
+                        a->max_pages, a->seq_lens, a->softmax_scale, a->out, a->lse, ws};
+  const cudaError_t e = afdk::mfa_decode_mtp_launch(c, m, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("mfa_decode_mtp launch", e);
+  return AFDK_OK;
+}
+
 afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, int m, int n, int k,
                         int out_fp32, afdk_stream stream) {
   if (!ctx || !x || !w || !out) { set_error("afdk_linear: NULL argument"); return AFDK_ERR_INVALID; }

@@ -106,6 +106,9 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
 // e4m3 KV cache variant (mfa_decode_fp8.cu): same args, k_cache/v_cache hold
 // e4m3 codes [num_pages, 64, 256] dequantised by k_scale / v_scale
 cudaError_t mfa_decode_fp8_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream);
+// multi-token decode, mtp = 2 (mfa_decode_mtp.cu): q/out [B, 2, 64, 256], lse [B, 2, 64]
+size_t mfa_decode_mtp_workspace_bytes(int batch, int num_sms);
+cudaError_t mfa_decode_mtp_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream);
 
 LinearPlan make_linear_plan(int m_tok, int n_out, int k);
 size_t linear_workspace_bytes(const LinearPlan& p, int num_sms);

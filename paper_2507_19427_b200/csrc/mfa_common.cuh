@@ -31,6 +31,7 @@ struct Params {
   int batch, max_pages;
   float scale_log2;            // softmax scale * log2(e)
   float k_scale, v_scale;      // e4m3 KV cache dequantisation scales (fp8 kernel)
+  int rows;                    // query rows per request: 64 heads x mtp (0 = 64)
 };
 
 // Contiguous page range of CTA c out of G over T total pages.

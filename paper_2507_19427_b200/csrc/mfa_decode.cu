@@ -409,14 +409,15 @@ __global__ void __launch_bounds__(256) mfa_combine_kernel(const Params prm, int 
   __shared__ int s_n;
   griddep_wait();
   griddep_launch();
+  const int R = prm.rows > 0 ? prm.rows : kHeads;  // query rows per request
   const int req = blockIdx.x;
   const int T = prm.prefix_out[prm.batch];
   const int p0 = prm.prefix_out[req], p1 = prm.prefix_out[req + 1];
   const int hl = threadIdx.x >> 6, head = blockIdx.y * 4 + hl;
   const int d = (threadIdx.x & 63) * 4;
   if (p1 <= p0) {
-    *reinterpret_cast<uint2*>(prm.out + ((size_t)req * kHeads + head) * kDim + d) = make_uint2(0, 0);
-    if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * kHeads + head] = -INFINITY;
+    *reinterpret_cast<uint2*>(prm.out + ((size_t)req * R + head) * kDim + d) = make_uint2(0, 0);
+    if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * R + head] = -INFINITY;
     return;
   }
   if (threadIdx.x == 0) {
@@ -435,10 +436,15 @@ __global__ void __launch_bounds__(256) mfa_combine_kernel(const Params prm, int 
   const int n = s_n;
   if (n == 1) return;  // whole request: written by the main kernel
   for (int i = threadIdx.x; i < 4 * n; i += blockDim.x)
-    s_w[i / n][i % n] = __ldcg(prm.part_lse + (size_t)s_slot[i % n] * kHeads + blockIdx.y * 4 + i / n);
+    s_w[i / n][i % n] = __ldcg(prm.part_lse + (size_t)s_slot[i % n] * R + blockIdx.y * 4 + i / n);
   __syncthreads();
   float m = -INFINITY;
   for (int k = 0; k < n; ++k) m = fmaxf(m, s_w[hl][k]);
+  if (m == -INFINITY) {  // a causal MTP row that sees no token in any part
+    *reinterpret_cast<uint2*>(prm.out + ((size_t)req * R + head) * kDim + d) = make_uint2(0, 0);
+    if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * R + head] = -INFINITY;
+    return;
+  }
   float wsum = 0.0f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 4
@@ -447,12 +453,12 @@ __global__ void __launch_bounds__(256) mfa_combine_kernel(const Params prm, int 
     wsum += w;
 #if AFDK_MFA_BF16_PART
     const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(prm.part_o) +
-                                                            ((size_t)s_slot[k] * kHeads + head) * kDim + d));
+                                                            ((size_t)s_slot[k] * R + head) * kDim + d));
     const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
     const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
     const float4 v = make_float4(v01.x, v01.y, v23.x, v23.y);
 #else
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(prm.part_o + ((size_t)s_slot[k] * kHeads + head) * kDim + d));
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(prm.part_o + ((size_t)s_slot[k] * R + head) * kDim + d));
 #endif
     acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
   }
@@ -460,8 +466,8 @@ __global__ void __launch_bounds__(256) mfa_combine_kernel(const Params prm, int 
   uint2 o;
   o.x = pack_bf16x2(acc.x * inv, acc.y * inv);
   o.y = pack_bf16x2(acc.z * inv, acc.w * inv);
-  *reinterpret_cast<uint2*>(prm.out + ((size_t)req * kHeads + head) * kDim + d) = o;
-  if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * kHeads + head] = (m + __log2f(wsum)) * 0.69314718055994531f;
+  *reinterpret_cast<uint2*>(prm.out + ((size_t)req * R + head) * kDim + d) = o;
+  if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * R + head] = (m + __log2f(wsum)) * 0.69314718055994531f;
 }
 
 }  // namespace mfa
@@ -529,7 +535,8 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
 }
 
 cudaError_t mfa_combine_launch(bool pdl, const mfa::Params& prm, int G, cudaStream_t stream) {
-  return launch_k(pdl, mfa::mfa_combine_kernel, dim3(prm.batch, mfa::kHeads / 4), dim3(256), 0, stream, prm, G);
+  const int R = prm.rows > 0 ? prm.rows : mfa::kHeads;
+  return launch_k(pdl, mfa::mfa_combine_kernel, dim3(prm.batch, R / 4), dim3(256), 0, stream, prm, G);
 }
 
 }  // namespace afdk

@@ -49,3 +49,27 @@ for fp8 in (False, True):
     kv = B * L * 2 * 256 * (1 if fp8 else 2)
     gbs = (kv + 2 * B * 64 * 256 * 2) / (ms * 1e-3) / 1e9
     print(f"{'e4m3' if fp8 else 'bf16'} KV  B={B} ctx={L}: {ms * 1e3:.1f} us  {gbs:.0f} GB/s  {gbs / peak:.3f} of HBM peak")
+
+# MTP (mtp = 2): two query tokens per request over the same bf16 KV
+q2 = torch.randn(B, 2, 64, 256, device=dev).to(torch.bfloat16)
+o2 = torch.empty(B, 2, 64, 256, device=dev, dtype=torch.bfloat16)
+
+
+def step_mtp(i):
+    k, v = w["kv"][i % 2]
+    ctx.mfa_decode_attention_mtp(q2, k, v, w["block_table"], w["seq_lens"], o2, 0.0625, stream=s.cuda_stream)
+
+
+for i in range(3):
+    step_mtp(i)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record(s)
+for i in range(20):
+    step_mtp(i)
+b.record(s)
+torch.cuda.synchronize()
+ms = a.elapsed_time(b) / 20
+kv = B * L * 2 * 256 * 2
+print(f"mtp=2 bf16 KV B={B} ctx={L}: {ms * 1e3:.1f} us  {(kv + 4 * B * 128 * 256) / (ms * 1e-3) / 1e9:.0f} GB/s  "
+      f"{2 * B / (ms * 1e-3):.0f} query tokens/s")

@@ -482,7 +482,8 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
             "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
             "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
             "nvlink_bytes_per_layer": {k: v * cfg.n_micro for k, v in wb.items()},
-            "transport": "copy-engine DMA pulls + cuStreamWaitValue32 flags (zero SM)", "measured": True}
+            "transport": ("A->F copy-engine DMA pulls; F->A partial rows stored over NVLink by the combine kernel "
+                          "(fused); cuStreamWrite/WaitValue32 flags"), "measured": True}
 
 
 def run_afd_modeled(ctx):

@@ -271,6 +271,24 @@ afdk_status afdk_dense_ffn_mx(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int
  * q = e4m3_rn_satfinite(x * 2^-e).  H % 32 == 0. */
 afdk_status afdk_quant_mx(afdk_ctx* ctx, const void* x, int T, int H, void* q, uint8_t* sf, afdk_stream stream);
 
+/* ------------------------------------- fused F->A return over NVLink
+ * The same MoE layers with the combine kernel (K9) writing every token row
+ * straight into the attention GPU that owns it: row t goes to
+ * dst[t / rows_per_dst] + (t % rows_per_dst) * hidden (bf16), where dst is a
+ * DEVICE array of n_dst pointers, typically peer buffers opened with
+ * afdk_ipc_open.  The partial crosses NVLink as the combine produces it (no
+ * separate copy); order a stream-ordered afdk_signal after the call, whose
+ * implied system fence publishes the rows before the flag.               */
+typedef struct afdk_row_scatter {
+  int n_dst, rows_per_dst;
+  const uint64_t* dst;
+} afdk_row_scatter;
+
+afdk_status afdk_moe_ffn_scatter(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a,
+                                 const afdk_row_scatter* sc, afdk_stream stream);
+afdk_status afdk_moe_ffn_mx_scatter(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
+                                    const afdk_row_scatter* sc, afdk_stream stream);
+
 /* ------------------------------------------- C1/C2 AFD exchange (NVLink)
  * Zero-SM point-to-point transport between attention and FFN GPUs of one
  * box (the StepMesh pattern of PAPER.md:701-724 on NVLink 5 / NVSwitch):

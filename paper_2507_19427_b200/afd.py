@@ -7,8 +7,10 @@ layer and micro-batch (pipesim.cpp:155-237 models it):
 
   A: mfa_layer -> router/quant into its send buffer -> signal every F
   F: wait all A -> DMA-pull payloads (fp8 tokens, scales, top-k) -> moe_ffn(_mx)
-     -> bf16 partial -> signal every A
-  A: wait all F -> DMA-pull its rows of every partial -> x = h_res + sum partials
+     whose combine kernel stores each token's bf16 partial row straight into
+     the owning attention GPU's receive buffer over NVLink -> signal every A
+     (f2a="pull": local partial, the attention GPU DMA-pulls its rows)
+  A: wait all F -> x = h_res + sum partials
 
 n_micro micro-batches per attention GPU run on their own streams (ping-pong),
 so the attention of one overlaps the exchange/FFN of the other.  All data
@@ -43,12 +45,16 @@ class AfdConfig:
     inter: int = 5120
     seed: int = 0
     ffn_format: str = "fp8"   # "fp8": 1x128/128x128 fp32 scales; "mx": MXFP8 (UE8M0 per 32)
+    f2a: str = "push"         # "push": the FFN combine writes into the attention GPUs' receive
+                              # buffers over NVLink (fused); "pull": attention DMA-pulls
 
     def __post_init__(self):
         # validated identically on every rank before any buffer exchange: a rank
         # that failed mid-pipeline would leave its peers waiting on a flag
         if not 1 <= self.T_mb <= 256:
             raise ValueError(f"T_mb={self.T_mb}: the attention-side layer takes 1..256 requests per micro-batch")
+        if self.f2a not in ("push", "pull"):
+            raise ValueError(f"f2a={self.f2a!r}: expected 'push' or 'pull'")
         if self.ffn_format not in ("fp8", "mx"):
             raise ValueError(f"ffn_format={self.ffn_format!r}: expected 'fp8' or 'mx'")
         if self.ffn_format == "mx" and (self.hidden % 512 or self.inter % 512):
@@ -141,6 +147,7 @@ class AfdRank:
         self.flags = torch.zeros(256, dtype=torch.int32, device=dev)
         self.peer_flags = {}
         self.peer_bufs = {}
+        self.peer_recv = {}
 
     # ---------------------------------------------------------------- setup
     def _weights_attn(self, g):
@@ -211,7 +218,8 @@ class AfdRank:
                 self.kv.append(per_mb)
             self.seq_lens = t.full((c.T_mb,), c.ctx_len, dtype=t.int32, device=dev)
             mine = {"flags": self.ctx.ipc_handle(self.flags),
-                    "send": [self.ctx.ipc_handle(b) for b in self.send]}
+                    "send": [self.ctx.ipc_handle(b) for b in self.send],
+                    "recv": [self.ctx.ipc_handle(b) for b in self.recv_part]}
         else:
             lo, hi = expert_shard(self.idx, c)
             self.moe_w = self.expert_weights(lo, hi)
@@ -238,6 +246,13 @@ class AfdRank:
             self.peer_flags[r] = self.ctx.ipc_open(h["flags"])
             key = "send" if peer_role == "attn" else "out"
             self.peer_bufs[r] = [self.ctx.ipc_open(x) for x in h[key]]
+            if peer_role == "attn" and c.f2a == "push":
+                self.peer_recv[r] = [self.ctx.ipc_open(x) for x in h["recv"]]
+        if self.role == "ffn" and c.f2a == "push":
+            # my slot f of every attention GPU's [n_ffn, T_mb, H] receive buffer
+            slot = self.idx * c.T_mb * c.hidden * 2
+            self.dst = [t.tensor([self.peer_recv[a][mb] + slot for a in range(c.n_attn)], dtype=t.int64,
+                                 device=dev) for mb in range(c.n_micro)]
         t.cuda.synchronize()
         self.dist.barrier()
 
@@ -267,8 +282,9 @@ class AfdRank:
         for f in range(c.n_ffn):
             r = c.n_attn + f
             ctx.wait(self.flags.data_ptr() + 4 * flag_index(f, mb, c), seq, stream=sp)
-            ctx.copy(self.recv_part[mb][f].data_ptr(), self.peer_bufs[r][mb] + self.idx * row_bytes, row_bytes,
-                     stream=sp)
+            if c.f2a == "pull":
+                ctx.copy(self.recv_part[mb][f].data_ptr(), self.peer_bufs[r][mb] + self.idx * row_bytes, row_bytes,
+                         stream=sp)
         ctx.add_partials(self.h_res[mb], self.part_ptrs[mb], c.n_ffn, self.x[mb], stream=sp)
 
     def _ffn_layer(self, mb, seq):
@@ -286,7 +302,8 @@ class AfdRank:
         st.wait_event(self.copied[mb])
         ffn = ctx.moe_ffn_mx if c.ffn_format == "mx" else ctx.moe_ffn
         ffn(self.moe_w, rx["xq"], rx["xs"], rx["ids"], rx["wts"], self.out[mb], expert_lo=self.expert_lo,
-            expert_hi=self.expert_hi, shared=self.shared, stream=st.cuda_stream)
+            expert_hi=self.expert_hi, shared=self.shared, stream=st.cuda_stream,
+            scatter=(self.dst[mb], c.T_mb) if c.f2a == "push" else None)
         for a in range(c.n_attn):
             ctx.signal(self.peer_flags[a] + 4 * flag_index(self.idx, mb, c), seq, stream=st.cuda_stream)
 
@@ -310,6 +327,10 @@ class AfdRank:
         return self.streams + [self.copy_stream]
 
     def close(self):
+        for r, bufs in self.peer_recv.items():
+            for p in bufs:
+                self.ctx.ipc_close(p)
+        self.peer_recv = {}
         for r, p in self.peer_flags.items():
             self.ctx.ipc_close(p)
         for r, bufs in self.peer_bufs.items():

@@ -93,6 +93,10 @@ class DenseMxWeights(Structure):
                 ("w13", c_void_p), ("sf13", c_void_p), ("w2", c_void_p), ("sf2", c_void_p)]
 
 
+class RowScatter(Structure):
+    _fields_ = [("n_dst", c_int), ("rows_per_dst", c_int), ("dst", c_void_p)]
+
+
 class StagePlan(Structure):
     _fields_ = [("attn_gpus", c_int), ("ffn_gpus", c_int), ("micro_batch", ctypes.c_longlong),
                 ("avg_ctx", ctypes.c_longlong), ("n_layers", c_int), ("hidden", c_int), ("link_gbs", ctypes.c_double)]
@@ -134,6 +138,10 @@ SIGNATURES = {
                                    c_void_p]),
     "afdk_mfa_decode_attention_mtp": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_int, c_void_p]),
     "afdk_mfa_decode_attention_fp8": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_float, c_float, c_void_p]),
+    "afdk_moe_ffn_scatter": (c_int, [c_void_p, POINTER(MoeWeights), POINTER(MoeArgs), POINTER(RowScatter),
+                                     c_void_p]),
+    "afdk_moe_ffn_mx_scatter": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), POINTER(RowScatter),
+                                        c_void_p]),
     "afdk_moe_ffn_mx": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), c_void_p]),
     "afdk_dense_ffn_mx": (c_int, [c_void_p, POINTER(DenseMxWeights), c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_quant_mx": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
@@ -282,7 +290,7 @@ class Context:
                                         ptr(inv), c_void_p(stream)))
 
     def moe_ffn(self, w: dict, xq, xs, ids, weights, out, expert_lo=0, expert_hi=None, shared=(0, None),
-                stream: int = 0) -> None:
+                stream: int = 0, scatter=None) -> None:
         """w: n_experts, w13, s13, w2, s2 (local experts then the shared one)."""
         T, Hd = xq.shape
         k = ids.shape[1]
@@ -292,10 +300,15 @@ class Context:
         sh_lo, sh_hi = shared[0], (T if shared[1] is None else shared[1])
         mw = MoeWeights(Hd, inter, E, k, expert_lo, hi, ptr(w["w13"]), ptr(w["s13"]), ptr(w["w2"]), ptr(w["s2"]))
         a = MoeArgs(T, ptr(xq), ptr(xs), ptr(ids), ptr(weights), sh_lo, sh_hi, ptr(out))
-        check(self.lib.afdk_moe_ffn(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+        if scatter is None:
+            check(self.lib.afdk_moe_ffn(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+        else:  # (dst device int64 tensor of peer row-block pointers, rows_per_dst)
+            sc = RowScatter(scatter[0].numel(), scatter[1], ptr(scatter[0]))
+            check(self.lib.afdk_moe_ffn_scatter(self.handle, ctypes.byref(mw), ctypes.byref(a), ctypes.byref(sc),
+                                                c_void_p(stream)))
 
     def moe_ffn_mx(self, w: dict, xq, xsf, ids, weights, out, expert_lo=0, expert_hi=None, shared=(0, None),
-                   stream: int = 0) -> None:
+                   stream: int = 0, scatter=None) -> None:
         """MXFP8 path. w: n_experts, w13, sf13, w2, sf2 (local experts then the shared one)."""
         T, Hd = xq.shape
         k = ids.shape[1]
@@ -305,7 +318,12 @@ class Context:
         sh_lo, sh_hi = shared[0], (T if shared[1] is None else shared[1])
         mw = MoeMxWeights(Hd, inter, E, k, expert_lo, hi, ptr(w["w13"]), ptr(w["sf13"]), ptr(w["w2"]), ptr(w["sf2"]))
         a = MoeMxArgs(T, ptr(xq), ptr(xsf), ptr(ids), ptr(weights), sh_lo, sh_hi, ptr(out))
-        check(self.lib.afdk_moe_ffn_mx(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+        if scatter is None:
+            check(self.lib.afdk_moe_ffn_mx(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+        else:
+            sc = RowScatter(scatter[0].numel(), scatter[1], ptr(scatter[0]))
+            check(self.lib.afdk_moe_ffn_mx_scatter(self.handle, ctypes.byref(mw), ctypes.byref(a), ctypes.byref(sc),
+                                                   c_void_p(stream)))
 
     def dense_ffn_mx(self, w: dict, xq, xsf, out, stream: int = 0) -> None:
         """Dense FFN in slice layout: w13 [n_split, 2*Is, H], sf13, w2 [n_split, H, Is], sf2."""

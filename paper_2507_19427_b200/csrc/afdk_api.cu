@@ -302,7 +302,17 @@ afdk_status afdk_moe_permute(afdk_ctx* ctx, const int32_t* ids, int T, int k, in
   return AFDK_OK;
 }
 
-afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a, afdk_stream stream) {
+static bool scatter_ok(const afdk_row_scatter* sc, int T, const char* who) {
+  if (!sc) return true;
+  if (!sc->dst || sc->n_dst < 1 || sc->rows_per_dst < 1 || (long)sc->n_dst * sc->rows_per_dst < T) {
+    set_error(std::string(who) + ": scatter needs dst[n_dst] with n_dst * rows_per_dst >= T");
+    return false;
+  }
+  return true;
+}
+
+static afdk_status moe_ffn_entry(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a,
+                                 const afdk_row_scatter* sc, afdk_stream stream) {
   if (!ctx || !w || !a) { set_error("afdk_moe_ffn: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }
   if (w->hidden % 128 || w->inter % 128 || w->hidden < 128 || w->inter < 128) {
     set_error("afdk_moe_ffn: hidden and inter must be positive multiples of 128");
@@ -328,6 +338,8 @@ afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_mo
   afdk::MoeFfnArgs m{a->T, w->top_k, w->n_experts, w->hidden, w->inter, w->expert_lo, w->expert_hi,
                      w->w13, w->s13, w->w2, w->s2, static_cast<const uint8_t*>(a->xq), a->xs, a->ids,
                      a->weights, sh_lo, sh_hi, a->out};
+  if (!scatter_ok(sc, a->T, "afdk_moe_ffn")) return AFDK_ERR_INVALID;
+  if (sc) { m.dst = sc->dst; m.rows_per_dst = sc->rows_per_dst; }
   void* ws = afdk::workspace(c, afdk::moe_ffn_workspace_bytes(a->T, w->top_k, w->n_experts, w->hidden, w->inter));
   if (!ws) { set_error("afdk_moe_ffn: workspace allocation failed"); return AFDK_ERR_CUDA; }
   const cudaError_t e = afdk::moe_ffn_launch(c, m, ws, static_cast<cudaStream_t>(stream));
@@ -335,8 +347,8 @@ afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_mo
   return AFDK_OK;
 }
 
-afdk_status afdk_moe_ffn_mx(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
-                            afdk_stream stream) {
+static afdk_status moe_ffn_mx_entry(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
+                                    const afdk_row_scatter* sc, afdk_stream stream) {
   if (!ctx || !w || !a) { set_error("afdk_moe_ffn_mx: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }
   if (w->hidden % 512 || w->inter % 512 || w->hidden < 512 || w->inter < 512) {
     set_error("afdk_moe_ffn_mx: hidden and inter must be positive multiples of 512");
@@ -362,11 +374,31 @@ afdk_status afdk_moe_ffn_mx(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const a
   afdk::MoeFfnMxArgs m{a->T, w->top_k, w->n_experts, w->hidden, w->inter, w->expert_lo, w->expert_hi,
                        w->w13, w->sf13, w->w2, w->sf2, static_cast<const uint8_t*>(a->xq), a->xsf, a->ids,
                        a->weights, sh_lo, sh_hi, a->out};
+  if (!scatter_ok(sc, a->T, "afdk_moe_ffn_mx")) return AFDK_ERR_INVALID;
+  if (sc) { m.dst = sc->dst; m.rows_per_dst = sc->rows_per_dst; }
   void* ws = afdk::workspace(c, afdk::moe_ffn_mx_workspace_bytes(a->T, w->top_k, w->n_experts, w->hidden, w->inter));
   if (!ws) { set_error("afdk_moe_ffn_mx: workspace allocation failed"); return AFDK_ERR_CUDA; }
   const cudaError_t e = afdk::moe_ffn_mx_launch(c, m, ws, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return AFDK_ERR_CUDA;
   return AFDK_OK;
+}
+
+afdk_status afdk_moe_ffn(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a, afdk_stream stream) {
+  return moe_ffn_entry(ctx, w, a, nullptr, stream);
+}
+afdk_status afdk_moe_ffn_scatter(afdk_ctx* ctx, const afdk_moe_weights* w, const afdk_moe_args* a,
+                                 const afdk_row_scatter* sc, afdk_stream stream) {
+  if (!sc) { set_error("afdk_moe_ffn_scatter: NULL scatter"); return AFDK_ERR_INVALID; }
+  return moe_ffn_entry(ctx, w, a, sc, stream);
+}
+afdk_status afdk_moe_ffn_mx(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
+                            afdk_stream stream) {
+  return moe_ffn_mx_entry(ctx, w, a, nullptr, stream);
+}
+afdk_status afdk_moe_ffn_mx_scatter(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
+                                    const afdk_row_scatter* sc, afdk_stream stream) {
+  if (!sc) { set_error("afdk_moe_ffn_mx_scatter: NULL scatter"); return AFDK_ERR_INVALID; }
+  return moe_ffn_mx_entry(ctx, w, a, sc, stream);
 }
 
 afdk_status afdk_dense_ffn_mx(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,

@@ -172,6 +172,8 @@ struct MoeFfnArgs {
   const float* weights;
   int shared_lo, shared_hi;
   void* out;
+  const uint64_t* dst = nullptr;  // fused F->A return (CombineArgs::dst)
+  int rows_per_dst = 0;
 };
 size_t moe_ffn_workspace_bytes(int T, int k, int E, int H, int I);
 cudaError_t moe_ffn_launch(Ctx& ctx, const MoeFfnArgs& a, void* ws, cudaStream_t stream);
@@ -207,6 +209,8 @@ struct MoeFfnMxArgs {
   const float* weights;
   int shared_lo, shared_hi;
   void* out;
+  const uint64_t* dst = nullptr;
+  int rows_per_dst = 0;
 };
 size_t moe_ffn_mx_workspace_bytes(int T, int k, int E, int H, int I);
 cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws, cudaStream_t stream);

@@ -64,6 +64,10 @@ struct CombineArgs {
   int T, k, H;
   int expert_lo, expert_hi, shared_local, shared_lo, shared_hi;
   __nv_bfloat16* out;  // [T, H]
+  // fused F->A return (optional): token row t goes to
+  // dst[t / rows_per_dst] + (t % rows_per_dst) * H (peer memory over NVLink)
+  const uint64_t* dst;
+  int rows_per_dst;
 };
 
 inline int max_work(int T, int k, int E) { return E + (T * k) / kChunk + 1 + T / kChunk + 1; }

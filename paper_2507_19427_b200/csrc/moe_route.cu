@@ -317,6 +317,9 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   }
   const bool sh = a.shared_local && t >= a.shared_lo && t < a.shared_hi;
   const size_t sh_row = (size_t)n_routed + t;
+  __nv_bfloat16* orow = a.dst ? reinterpret_cast<__nv_bfloat16*>(__ldg(a.dst + t / a.rows_per_dst)) +
+                                    (size_t)(t % a.rows_per_dst) * a.H
+                              : a.out + (size_t)t * a.H;
   for (int f = threadIdx.x * 4; f < a.H; f += blockDim.x * 4) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (sh) acc = __ldcg(reinterpret_cast<const float4*>(a.y + sh_row * a.H + f));
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
     uint2 o;
     o.x = *reinterpret_cast<uint32_t*>(&o0);
     o.y = *reinterpret_cast<uint32_t*>(&o1);
-    *reinterpret_cast<uint2*>(a.out + (size_t)t * a.H + f) = o;
+    *reinterpret_cast<uint2*>(orow + f) = o;
   }
 }
 

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--fmt", default="fp8", choices=["fp8", "mx"])
+    ap.add_argument("--f2a", default="push", choices=["push", "pull"])
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -37,10 +38,10 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     if a.check:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=24, n_micro=2, layers=1, hidden=1024,
-                        q_lora=256, ctx_len=300, n_experts=8, top_k=2, inter=512, seed=3, ffn_format=a.fmt)
+                        q_lora=256, ctx_len=300, n_experts=8, top_k=2, inter=512, seed=3, ffn_format=a.fmt, f2a=a.f2a)
     else:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=a.T_mb, n_micro=a.n_micro, layers=a.layers,
-                        ctx_len=a.ctx_len, ffn_format=a.fmt)
+                        ctx_len=a.ctx_len, ffn_format=a.fmt, f2a=a.f2a)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -104,7 +105,7 @@ def main():
                       "part err", rel_err(r.recv_part[mb][0].float().cpu().numpy(), part.float().cpu().numpy()),
                       "xq eq", bool(torch.equal(sent_xq, xq)), "ids eq", bool(torch.equal(sent_ids, ids)), flush=True)
             ok = max(errs) <= 2e-2
-            print(json.dumps({"afd_check": "ok" if ok else "FAIL", "fmt": c.ffn_format, "rel_err": errs, "world": world,
+            print(json.dumps({"afd_check": "ok" if ok else "FAIL", "fmt": c.ffn_format, "f2a": c.f2a, "rel_err": errs, "world": world,
                               "n_attn": cfg.n_attn}), flush=True)
         dist.barrier()
         r.close()
@@ -119,7 +120,7 @@ def main():
     tokens = cfg.n_attn * cfg.n_micro * cfg.T_mb
     wb = wire_bytes(cfg)
     if rank == 0:
-        print(json.dumps({"afd": f"{cfg.n_attn}A{cfg.n_ffn}F", "world": world, "T_mb": cfg.T_mb,
+        print(json.dumps({"afd": f"{cfg.n_attn}A{cfg.n_ffn}F", "fmt": cfg.ffn_format, "f2a": cfg.f2a, "world": world, "T_mb": cfg.T_mb,
                           "n_micro": cfg.n_micro, "layers": cfg.layers, "ctx": cfg.ctx_len,
                           "layer_period_ms": period_ms, "tokens_per_layer_period": tokens,
                           "tokens_per_s": tokens / (period_ms * 1e-3),

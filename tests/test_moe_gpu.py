@@ -143,3 +143,37 @@ def test_moe_ffn_expert_parallel_partials(ctx):
     T = 50
     got, ref = run_moe(ctx, T, 256, 256, 8, 3, 4, ranges=[((0, 4), (0, 20)), ((4, 8), (20, T))])
     assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", ["fp8", "mx"])
+def test_moe_ffn_row_scatter_matches_local(ctx, fmt):
+    """Fused F->A return: the combine writes token rows into n_dst buffers
+    (row blocks of rows_per_dst) bit-identically to the local output."""
+    import torch
+
+    from tests.test_moe_mx_gpu import make_mx_experts
+
+    T, H, I, E, k, rpd = 50, 512, 512, 8, 3, 20
+    g = torch.Generator().manual_seed(21)
+    dev = torch.device("cuda:0")
+    x = torch.randn(T, H, generator=g)
+    ids_np, w_np = orc.router_topk(torch.randn(T, E, generator=g).numpy(), k)
+    ids, wts = torch.from_numpy(ids_np).to(dev), torch.from_numpy(w_np).to(dev)
+    if fmt == "mx":
+        ex = make_mx_experts(torch, E, H, I, g, dev)
+        xq, xs = (torch.from_numpy(a).to(dev) for a in orc.quant_mx(x.numpy()))
+        run = ctx.moe_ffn_mx
+    else:
+        ex = make_experts(torch, E, H, I, g, dev)
+        xq, xs = (torch.from_numpy(a).to(dev) for a in orc.quant_fp8_rowblock(x.numpy()))
+        run = ctx.moe_ffn
+    local = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+    run(dict(n_experts=E, **ex), xq, xs, ids, wts, local)
+    bufs = [torch.full((rpd, H), float("nan"), dtype=torch.bfloat16, device=dev) for _ in range(3)]
+    dst = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=dev)
+    run(dict(n_experts=E, **ex), xq, xs, ids, wts, local, scatter=(dst, rpd))
+    torch.cuda.synchronize()
+    got = torch.cat(bufs)[:T]
+    assert torch.equal(got, local)
+    assert torch.isnan(torch.cat(bufs)[T:].float()).all()  # rows past T untouched

@@ -137,9 +137,12 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
 
   if (warp == 0) {
     if (lane == 0) {
-      // weight tiles are shared by the expert's concurrently running chunks and
-      // activation panels by the m-tiles of the same chunk: no eviction hints
-      const uint64_t pol = policy_evict_normal();
+      // this kernel runs at decode batches: every weight tile is read by about
+      // one item, so weights stream through L2 (evict_first) and leave it to
+      // the activation panels shared by a chunk's m-tiles and to the y / hq
+      // outputs the next kernel reads
+      const uint64_t pol = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
       int i = 0, gi = 0;
       for (int it = cta; it < n_items; it += G) {
         const int mt = it % p.m_tiles;
@@ -154,7 +157,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
             mbar_expect_tx(&sfg_full[g], kSfGrp);
             tma_load_2d(dst, &tm_wsf, &sfg_full[g], kb * 4, wrow, pol);
             if (kGLU) tma_load_2d(dst + kSfOp, &tm_wsf, &sfg_full[g], kb * 4, wrow + p.up_offset, pol);
-            tma_load_2d(dst + kAOps * kSfOp, &tm_xsf, &sfg_full[g], kb * 4, kGLU ? wk.xrow0 : wk.row0, pol);
+            tma_load_2d(dst + kAOps * kSfOp, &tm_xsf, &sfg_full[g], kb * 4, kGLU ? wk.xrow0 : wk.row0, pol_x);
           }
           const int s = i % S, n = i / S;
           if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
@@ -162,7 +165,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
           mbar_expect_tx(&full[s], kAOps * kA + kB);
           tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol);
           if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol);
-          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, kGLU ? wk.xrow0 : wk.row0, pol);
+          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, kGLU ? wk.xrow0 : wk.row0, pol_x);
         }
       }
     }

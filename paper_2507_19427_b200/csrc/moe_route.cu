@@ -180,31 +180,54 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
     s_tot[e] = run;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int run = 0;
-    for (int e = 0; e < a.E; ++e) { s_off[e] = run; run += s_tot[e]; }
-    s_off[a.E] = run;
-    for (int e = 0; e <= a.E; ++e) a.offsets[e] = s_off[e];
-    int g = 0;
-    for (int e = 0; e <= a.E; ++e) {
-      const bool local = (e == a.E) ? a.shared_local : (e >= a.expert_lo && e < a.expert_hi);
-      if (!local) continue;
-      const int row0 = (e == a.E) ? n + a.shared_lo : s_off[e];
-      const int rows = (e == a.E) ? a.shared_hi - a.shared_lo : s_tot[e];
-      // ceil(rows/chunk) items of near-equal size (multiples of 32 rows), so
-      // an expert never ends in a tiny item that streams its weights for a
-      // handful of tokens
-      const int n_items = (rows + a.chunk - 1) / a.chunk;
-      const int per = n_items > 0 ? ((rows + n_items - 1) / n_items + 31) & ~31 : 0;
-      for (int r = 0; r < rows; r += per) {
-        a.work[g].group = e;
+  if (warp == 0) {
+    // expert offsets and the work list, one lane per expert (E <= 64): warp
+    // scans instead of a serial loop (the CTA waits on this section)
+    const int e0 = lane, e1 = lane + 32;
+    const int c0 = e0 < a.E ? s_tot[e0] : 0, c1 = e1 < a.E ? s_tot[e1] : 0;
+    int x0 = c0, x1 = c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y0 = __shfl_up_sync(0xffffffff, x0, o), y1 = __shfl_up_sync(0xffffffff, x1, o);
+      if (lane >= o) { x0 += y0; x1 += y1; }
+    }
+    const int tot0 = __shfl_sync(0xffffffff, x0, 31), tot1 = __shfl_sync(0xffffffff, x1, 31);
+    if (e0 < a.E) { s_off[e0] = x0 - c0; a.offsets[e0] = x0 - c0; }
+    if (e1 < a.E) { s_off[e1] = tot0 + x1 - c1; a.offsets[e1] = tot0 + x1 - c1; }
+    if (lane == 0) { s_off[a.E] = tot0 + tot1; a.offsets[a.E] = tot0 + tot1; }
+    // items per group: ceil(rows/chunk) near-equal pieces (multiples of 32 rows)
+    auto items = [&](int rows) { return (rows + a.chunk - 1) / a.chunk; };
+    const bool l0 = e0 < a.E && e0 >= a.expert_lo && e0 < a.expert_hi;
+    const bool l1 = e1 < a.E && e1 >= a.expert_lo && e1 < a.expert_hi;
+    const int n0 = l0 ? items(c0) : 0, n1 = l1 ? items(c1) : 0;
+    int y0 = n0, y1 = n1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int z0 = __shfl_up_sync(0xffffffff, y0, o), z1 = __shfl_up_sync(0xffffffff, y1, o);
+      if (lane >= o) { y0 += z0; y1 += z1; }
+    }
+    const int w0 = __shfl_sync(0xffffffff, y0, 31), w1 = __shfl_sync(0xffffffff, y1, 31);
+    auto emit = [&](int g, int group, int row0, int rows) {
+      const int n_it = items(rows);
+      const int per = n_it > 0 ? ((rows + n_it - 1) / n_it + 31) & ~31 : 0;
+      for (int r = 0; r < rows; r += per, ++g) {
+        a.work[g].group = group;
         a.work[g].row0 = row0 + r;
         a.work[g].rows = min(per, rows - r);
         a.work[g].xrow0 = row0 + r;
-        ++g;
       }
+    };
+    if (l0) emit(y0 - n0, e0, x0 - c0, c0);
+    if (l1) emit(w0 + y1 - n1, e1, tot0 + x1 - c1, c1);
+    if (lane == 0) {
+      int g = w0 + w1;
+      if (a.shared_local) {
+        const int rows = a.shared_hi - a.shared_lo;
+        emit(g, a.E, n + a.shared_lo, rows);
+        g += items(rows);
+      }
+      *a.n_work = g;
     }
-    *a.n_work = g;
   }
   __syncthreads();
   if (threadIdx.x < a.E)

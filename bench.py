@@ -428,10 +428,10 @@ def afd_runs(world):
     MXFP8 at the largest micro-batch the attention layer takes, and the
     balanced attention/FFN split."""
     base = {2: (1, 1), 4: (1, 3), 8: (2, 6)}.get(world, (1, world - 1))
-    runs = [(base, "fp8", 192), (base, "mx", 256)]
+    runs = [(base, "fp8", 192), (base, "mx", 256), (base, "mx", 512)]
     bal = (world // 2, world - world // 2)
     if bal != base:
-        runs.append((bal, "mx", 256))
+        runs += [(bal, "mx", 256), (bal, "mx", 512)]
     return runs
 
 

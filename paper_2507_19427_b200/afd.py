@@ -47,12 +47,17 @@ class AfdConfig:
     ffn_format: str = "fp8"   # "fp8": 1x128/128x128 fp32 scales; "mx": MXFP8 (UE8M0 per 32)
     f2a: str = "push"         # "push": the FFN combine writes into the attention GPUs' receive
                               # buffers over NVLink (fused); "pull": attention DMA-pulls
+    attn_chunk: int = 256     # requests per attention-layer call (its GEMM N limit); a larger
+                              # T_mb runs the attention side in chunks and ships ONE payload,
+                              # so the FFN tier streams its expert weights once per micro-batch
 
     def __post_init__(self):
         # validated identically on every rank before any buffer exchange: a rank
         # that failed mid-pipeline would leave its peers waiting on a flag
-        if not 1 <= self.T_mb <= 256:
-            raise ValueError(f"T_mb={self.T_mb}: the attention-side layer takes 1..256 requests per micro-batch")
+        if not 1 <= self.attn_chunk <= 256:
+            raise ValueError(f"attn_chunk={self.attn_chunk}: the attention-side layer takes 1..256 requests per call")
+        if not 1 <= self.T_mb <= 4096:
+            raise ValueError(f"T_mb={self.T_mb}: expected 1..4096 requests per micro-batch")
         if self.f2a not in ("push", "pull"):
             raise ValueError(f"f2a={self.f2a!r}: expected 'push' or 'pull'")
         if self.ffn_format not in ("fp8", "mx"):
@@ -262,7 +267,10 @@ class AfdRank:
         st = self.streams[mb]
         sp = st.cuda_stream
         k, v, bt = self.kv[layer][mb]
-        ctx.mfa_layer(self.w, self.x[mb], k, v, bt, self.seq_lens, self.h_res[mb], self.h_norm[mb], stream=sp)
+        for c0 in range(0, c.T_mb, c.attn_chunk):
+            c1 = min(c.T_mb, c0 + c.attn_chunk)
+            ctx.mfa_layer(self.w, self.x[mb][c0:c1], k, v, bt[c0:c1], self.seq_lens[c0:c1], self.h_res[mb][c0:c1],
+                          self.h_norm[mb][c0:c1], stream=sp)
         buf, L = self.send[mb], self.lay
         view = lambda name, shape, dtype: buf[L.off[name]:L.off[name] + L.size(name)].view(dtype).view(*shape)
         if c.ffn_format == "mx":

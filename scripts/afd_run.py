@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--fmt", default="fp8", choices=["fp8", "mx"])
     ap.add_argument("--f2a", default="push", choices=["push", "pull"])
+    ap.add_argument("--attn-chunk", type=int, default=256)
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -38,10 +39,11 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     if a.check:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=24, n_micro=2, layers=1, hidden=1024,
-                        q_lora=256, ctx_len=300, n_experts=8, top_k=2, inter=512, seed=3, ffn_format=a.fmt, f2a=a.f2a)
+                        q_lora=256, ctx_len=300, n_experts=8, top_k=2, inter=512, seed=3, ffn_format=a.fmt, f2a=a.f2a,
+                        attn_chunk=min(a.attn_chunk, 256))
     else:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=a.T_mb, n_micro=a.n_micro, layers=a.layers,
-                        ctx_len=a.ctx_len, ffn_format=a.fmt, f2a=a.f2a)
+                        ctx_len=a.ctx_len, ffn_format=a.fmt, f2a=a.f2a, attn_chunk=a.attn_chunk)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()

@@ -140,7 +140,10 @@ def test_afd_config_validation():
     from paper_2507_19427_b200.afd import AfdConfig
 
     with pytest.raises(ValueError):
-        AfdConfig(n_attn=1, n_ffn=1, T_mb=384)
+        AfdConfig(n_attn=1, n_ffn=1, T_mb=8192)
+    with pytest.raises(ValueError):
+        AfdConfig(n_attn=1, n_ffn=1, T_mb=64, attn_chunk=512)
+    AfdConfig(n_attn=1, n_ffn=1, T_mb=768)
     with pytest.raises(ValueError):
         AfdConfig(n_attn=1, n_ffn=1, T_mb=64, ffn_format="bf16")
     with pytest.raises(ValueError):

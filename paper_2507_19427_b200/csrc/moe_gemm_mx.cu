@@ -93,7 +93,6 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
   constexpr int kA = 128 * 128;
   constexpr int kAOps = kGLU ? 2 : 1;
   constexpr int kB = kChunkMX * 128;
-  constexpr int kAcc = kGLU ? 1 : 2;           // accumulator buffers
   constexpr int kSfCols = 4 * kAOps + 4;       // scale columns per ring slot
   constexpr int kSfOp = 128 * 16;              // one operand's scales for 4 k-blocks
   constexpr int kSfGrp = (kAOps + 1) * kSfOp;  // smem scale group (4 k-blocks)

@@ -595,7 +595,7 @@ def main():
         ctx.mfa_layer(s["w"], s["x"], k, v, s["block_table"], s["seq_lens"], s["h_res"], s["h_norm"], stream=sp)
 
     step = layer_step if args.workload == "layer" else attn_step
-    launches_per_step = 10 if args.workload == "layer" else 3
+    launches_per_step = 9 if args.workload == "layer" else 2  # rmsnorm, 3 x (GEMM + row epilogue), K2, K3
 
     for i in range(max(args.warmup, 3)):
         step(i)

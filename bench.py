@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--no-long", action="store_true", help="skip the config-4 32K measurement")
     p.add_argument("--no-fp8kv", action="store_true", help="skip the config-2 e4m3 KV-cache measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="time direct launches instead of CUDA-graph replay")
     return p.parse_args()
 
 
@@ -582,7 +583,10 @@ def main():
 
     ctx = Context(local)
     s = make_workload(torch, dev, args.batch, args.ctx, seed=rank)
-    stream = torch.cuda.current_stream()
+    # one side stream for everything (CUDA-graph capture needs a non-default stream)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()  # inputs were initialised on the default stream
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
     scale = D ** -0.5
 
@@ -601,6 +605,25 @@ def main():
         step(i)
         attn_step(i)
     torch.cuda.synchronize()
+    # the layer as CUDA graphs (one per rotating KV cache; the 9 PDL launches keep
+    # their programmatic edges); replay is what a serving loop would run
+    graphs, graph_note = None, "off"
+    if args.workload == "layer" and not args.no_graph:
+        try:
+            graphs = []
+            for r in range(N_ROT):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    layer_step(r)
+                graphs.append(g)
+            for r in range(N_ROT):
+                graphs[r].replay()
+            torch.cuda.synchronize()
+            step = lambda i: graphs[i % N_ROT].replay()  # noqa: E731
+            graph_note = "cuda graph replay"
+        except Exception as e:  # direct launches instead, reported
+            graphs, graph_note = None, f"direct launches (capture failed: {type(e).__name__})"
+            torch.cuda.synchronize()
 
     def timed(fn, n):
         if world > 1:
@@ -755,7 +778,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"config2-mfa-decode-{args.workload} (Step-3 full dims, paged bf16 KV)",
                        "batch": args.batch, "ctx": args.ctx, "hidden": HIDDEN, "q_lora": QL, "n_heads": H,
-                       "head_dim": D, "page": PAGE, "parallelism": f"dp{world} (replicas)",
+                       "head_dim": D, "page": PAGE, "parallelism": f"dp{world} (replicas)", "launch": graph_note,
                        "l2": f"inputs > L2: {N_ROT} rotating KV layers of {kv_bytes(args.batch, args.ctx) / 1e6:.0f} MB"
                              f" + {weight_bytes() / 1e6:.0f} MB weights"},
             "roofline": {"bound": "hbm", "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",

@@ -230,7 +230,7 @@ def moe_weight_bytes(n_experts):
     return n_experts * (3 * HIDDEN * INTER + 4 * (2 * INTER // 128 * HIDDEN // 128 + HIDDEN // 128 * INTER // 128))
 
 
-def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=None):
+def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=None, time_only=False):
     """One FFN-side MoE layer (permute, gather, W13+SwiGLU+requant, W2, combine)
     over T dispatched tokens, all 48 routed experts + the shared one on this GPU.
     fmt "fp8": e4m3 with 1x128 / 128x128 fp32 block scales (software-scaled
@@ -285,10 +285,13 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=No
     b.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
-    if shard:
+    if shard and shard[2] is not None:
         t_ = torch.tensor([ms], device=dev)
         shard[2].all_reduce(t_, op=shard[2].ReduceOp.MAX)
         ms = float(t_.item())
+    if time_only:
+        del w
+        return ms * 1e-3
     idl = ids.flatten().tolist()
     touched = len({e for e in idl if lo <= e < hi}) + 1
     wbytes = moe_weight_bytes(touched)
@@ -505,6 +508,68 @@ def run_afd_modeled(ctx):
             "link": {"gbs": d["link_gbs"], "measured": bool(d["link_measured"])},
             "tpot_ms": 1e3 * sim["tpot"], "tgs_tok_per_gpu_s": sim["tgs"],
             "tokens_per_s_per_gpu_per_layer": sim["tgs"] * 61, "utilization": sim["utilization"]}
+
+
+def run_afd_modeled_mx(ctx, torch, dev, plans=((2, 6), (4, 4)), T_mb=512, n_micro=2, link_gbs=770.0):
+    """8-GPU AFD with the MXFP8 FFN tier and chunked attention, modeled from
+    ingredients measured HERE on one GPU: the attention-side layer for T_mb
+    requests (256-request chunks), router + MXFP8 dispatch quant, one FFN
+    GPU's expert shard (48/nF experts + 1/nF of the shared expert's tokens)
+    over the nA*T_mb dispatched tokens, and NVLink bytes at the pool's peer
+    copy rate; fed to the pipeline model (pipesim.cpp:155 semantics) as one
+    MoE layer in steady state."""
+    from paper_2507_19427_b200 import afdk
+
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, n=5):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n * 1e-3
+
+    chunk = 256
+    s = make_workload(torch, dev, chunk, CTX, seed=11)
+    k, v = s["kv"][0]
+    attn_s = timed(lambda: ctx.mfa_layer(s["w"], s["x"], k, v, s["block_table"], s["seq_lens"], s["h_res"],
+                                         s["h_norm"], stream=stream.cuda_stream)) * ((T_mb + chunk - 1) // chunk)
+    gate = (torch.randn(E_ROUTED, HIDDEN, device=dev) / HIDDEN ** 0.5).to(torch.bfloat16)
+    ids = torch.empty(chunk, TOPK, dtype=torch.int32, device=dev)
+    wts = torch.empty(chunk, TOPK, device=dev)
+    xq = torch.empty(chunk, HIDDEN, dtype=torch.uint8, device=dev)
+    xsf = torch.empty(chunk, HIDDEN // 32, dtype=torch.uint8, device=dev)
+
+    def route():
+        ctx.router_topk(s["h_norm"], gate, TOPK, ids, wts, stream=stream.cuda_stream)
+        ctx.quant_mx(s["h_norm"], xq, xsf, stream=stream.cuda_stream)
+    attn_s += timed(route) * ((T_mb + chunk - 1) // chunk)
+    del s
+    torch.cuda.empty_cache()
+    out = []
+    for na, nf in plans:
+        T = na * T_mb
+        # FFN GPU 0's shard (routing is uniform, every shard is alike)
+        ffn = run_moe_bench(ctx, torch, dev, T, 5, 2, fmt="mx", shard=(0, nf, None), time_only=True)
+        tok_fwd = HIDDEN + HIDDEN // 32 + TOPK * 8  # e4m3 row + UE8M0 scales + ids/weights
+        fwd_s = T * tok_fwd / (link_gbs * 1e9)      # each FFN GPU pulls the whole micro-batch
+        bwd_s = T * 2 * HIDDEN / nf / (link_gbs * 1e9) * na  # its bf16 partial rows, spread over nA
+        sim = afdk.simulate([attn_s], [fwd_s], [ffn], [bwd_s], n_micro=n_micro, total_batch=na * T_mb * n_micro,
+                            total_gpus=na + nf)
+        period = sim["tpot"]
+        tok = na * T_mb * n_micro
+        out.append({"plan": f"{na}A{nf}F", "ffn_format": "mxfp8", "T_mb": T_mb, "n_micro": n_micro, "modeled": True,
+                    "stage_us": {"attn": attn_s * 1e6, "moe_ffn": ffn * 1e6, "comm_fwd": fwd_s * 1e6,
+                                 "comm_bwd": bwd_s * 1e6},
+                    "layer_period_ms": period * 1e3,
+                    "tokens_per_s_per_gpu_per_layer": tok / period / (na + nf),
+                    "utilization": sim["utilization"]})
+    return out
 
 
 # ------------------------------------------------- CPU port (oracle) legs
@@ -752,6 +817,7 @@ def main():
         try:
             if world == 1:
                 afd = run_afd_modeled(ctx)
+                afd["modeled_mx"] = run_afd_modeled_mx(ctx, torch, dev)
             else:
                 # micro-batch sweep: per-layer throughput depends on balancing the
                 # attention tier (grows with T_mb) against expert weight streaming

@@ -548,7 +548,9 @@ def run_afd_modeled_mx(ctx, torch, dev, plans=((2, 6), (4, 4)), T_mb=512, n_micr
     def route():
         ctx.router_topk(s["h_norm"], gate, TOPK, ids, wts, stream=stream.cuda_stream)
         ctx.quant_mx(s["h_norm"], xq, xsf, stream=stream.cuda_stream)
-    attn_s += timed(route) * ((T_mb + chunk - 1) // chunk)
+    layer_s = attn_s
+    route_s = timed(route) * ((T_mb + chunk - 1) // chunk)
+    attn_s += route_s
     del s
     torch.cuda.empty_cache()
     out = []
@@ -564,7 +566,8 @@ def run_afd_modeled_mx(ctx, torch, dev, plans=((2, 6), (4, 4)), T_mb=512, n_micr
         period = sim["tpot"]
         tok = na * T_mb * n_micro
         out.append({"plan": f"{na}A{nf}F", "ffn_format": "mxfp8", "T_mb": T_mb, "n_micro": n_micro, "modeled": True,
-                    "stage_us": {"attn": attn_s * 1e6, "moe_ffn": ffn * 1e6, "comm_fwd": fwd_s * 1e6,
+                    "stage_us": {"attn": attn_s * 1e6, "attn_layer": layer_s * 1e6, "router_quant": route_s * 1e6,
+                                 "moe_ffn": ffn * 1e6, "comm_fwd": fwd_s * 1e6,
                                  "comm_bwd": bwd_s * 1e6},
                     "layer_period_ms": period * 1e3,
                     "tokens_per_s_per_gpu_per_layer": tok / period / (na + nf),

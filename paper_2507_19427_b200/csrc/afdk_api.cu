@@ -273,11 +273,14 @@ afdk_status afdk_router_topk(afdk_ctx* ctx, const void* h, const void* gate_w, i
   if (E < 1 || E > afdk::moe::kMaxExperts) { set_error("afdk_router_topk: E must be in [1, 64]"); return AFDK_ERR_INVALID; }
   if (k < 1 || k > afdk::moe::kMaxTopK || k > E) { set_error("afdk_router_topk: k must be in [1, min(8, E)]"); return AFDK_ERR_INVALID; }
   if (T < 1 || H < 256 || H % 256) { set_error("afdk_router_topk: H must be a positive multiple of 256"); return AFDK_ERR_INVALID; }
+  if (H > 65536) { set_error("afdk_router_topk: H must be <= 65536"); return AFDK_ERR_INVALID; }
   if (xq && !xs) { set_error("afdk_router_topk: xq requires xs"); return AFDK_ERR_INVALID; }
   cudaSetDevice(ctx->c.device);
   afdk::moe::RouterArgs a{static_cast<const __nv_bfloat16*>(h), static_cast<const __nv_bfloat16*>(gate_w), T, H, E, k,
                           renormalize, logits, ids, weights, static_cast<uint8_t*>(xq), xs};
-  const cudaError_t e = afdk::router_launch(a, static_cast<cudaStream_t>(stream), ctx->c.pdl);
+  void* ws = afdk::workspace(ctx->c, afdk::router_workspace_bytes(H, E, ctx->c.num_sms));
+  if (!ws) { set_error("afdk_router_topk: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  const cudaError_t e = afdk::router_launch(ctx->c, a, ws, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail("afdk_router_topk", e);
   return AFDK_OK;
 }

@@ -140,7 +140,8 @@ size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms);
 cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws, cudaStream_t stream);
 
 // ---------------------------------------------------------------- MoE FFN
-cudaError_t router_launch(const moe::RouterArgs& a, cudaStream_t stream, bool pdl);
+size_t router_workspace_bytes(int H, int E, int num_sms);
+cudaError_t router_launch(Ctx& ctx, const moe::RouterArgs& a, void* ws, cudaStream_t stream);
 cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream, bool pdl);
 cudaError_t gather_launch(const moe::GatherArgs& a, cudaStream_t stream, bool pdl);
 cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream, bool pdl);

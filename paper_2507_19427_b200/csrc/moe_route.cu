@@ -21,123 +21,97 @@
 #include <cstdint>
 
 #include "afdk_internal.h"
+#include "linear.cuh"
 #include "moe.cuh"
 #include "sm100.cuh"
 
 namespace afdk {
 namespace moe {
 
-constexpr int kRouterTok = 8;  // tokens per router CTA
 
 __device__ __forceinline__ uint8_t to_e4m3(float v) {
   return (uint8_t)__nv_cvt_float_to_fp8(v, __NV_SATFINITE, __NV_E4M3);
 }
 
 // ---------------------------------------------------------------- K5 router
-// grid ceil(T/8), 256 threads.  Warp w computes experts e = w, w+8, ... for the
-// CTA's 8 tokens; lane l owns k = 8l + 256i; reduction is a fixed xor-tree so
-// the logits are bitwise reproducible run to run.
-__global__ void __launch_bounds__(256) router_kernel(RouterArgs a) {
-  __shared__ float s_logit[kRouterTok][kMaxExperts];
+// logits = h . gate^T runs on the tcgen05 stream-K linear kernel (linear.cu:
+// gate rows on MMA M, up to 256 tokens on N, fp32 partials); this epilogue
+// sums the partials in fixed segment order (deterministic; identical gate rows
+// give identical logits), then per token (one warp, lanes own experts l and
+// l+32): max-subtracted softmax, top-k by repeated warp argmax with ties to
+// the lower expert id, weights = softmax[id] (optionally renormalised).
+__global__ void __launch_bounds__(256) router_topk_kernel(const LinearPlan P, const float* __restrict__ part, int G,
+                                                          RouterArgs a, int t_base) {
+  __shared__ lin::SlotTable tab;
+  lin::build_slot_table(P, G, tab);
   sm100::griddep_wait();
   sm100::griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * kRouterTok;
-  const int nt = min(kRouterTok, a.T - t0);
-  const int H = a.H;
-  for (int e0 = warp; e0 < a.E; e0 += 8 * 2) {
-    // two experts per pass to reuse the token loads
-    const int e1 = e0 + 8;
-    float acc0[kRouterTok], acc1[kRouterTok];
-#pragma unroll
-    for (int t = 0; t < kRouterTok; ++t) acc0[t] = acc1[t] = 0.0f;
-    const __nv_bfloat16* w0 = a.gate_w + (size_t)e0 * H;
-    const __nv_bfloat16* w1 = a.gate_w + (size_t)(e1 < a.E ? e1 : e0) * H;
-    for (int k = lane * 8; k < H; k += 256) {
-      const uint4 wa = __ldg(reinterpret_cast<const uint4*>(w0 + k));
-      const uint4 wb = __ldg(reinterpret_cast<const uint4*>(w1 + k));
-      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&wa);
-      const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&wb);
-#pragma unroll
-      for (int t = 0; t < kRouterTok; ++t) {
-        if (t < nt) {
-          const uint4 xa = __ldg(reinterpret_cast<const uint4*>(a.h + (size_t)(t0 + t) * H + k));
-          const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&xa);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 xf = __bfloat1622float2(px[q]);
-            const float2 fa = __bfloat1622float2(pa[q]);
-            const float2 fb = __bfloat1622float2(pb[q]);
-            acc0[t] = fmaf(xf.x, fa.x, acc0[t]);
-            acc0[t] = fmaf(xf.y, fa.y, acc0[t]);
-            acc1[t] = fmaf(xf.x, fb.x, acc1[t]);
-            acc1[t] = fmaf(xf.y, fb.y, acc1[t]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < kRouterTok; ++t) {
-      float v0 = acc0[t], v1 = acc1[t];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        v0 += __shfl_xor_sync(0xffffffff, v0, o);
-        v1 += __shfl_xor_sync(0xffffffff, v1, o);
-      }
-      if (lane == 0) {
-        s_logit[t][e0] = v0;
-        if (e1 < a.E) s_logit[t][e1] = v1;
-      }
-    }
+  const int row = blockIdx.x * 8 + warp;  // token within this chunk
+  if (row >= P.m_tok) return;
+  const int tok = t_base + row;
+  const int e0 = lane, e1 = lane + 32;
+  const float l0 = e0 < a.E ? tab.sum(P, part, row, e0) : -INFINITY;
+  const float l1 = e1 < a.E ? tab.sum(P, part, row, e1) : -INFINITY;
+  if (a.logits) {
+    if (e0 < a.E) a.logits[(size_t)tok * a.E + e0] = l0;
+    if (e1 < a.E) a.logits[(size_t)tok * a.E + e1] = l1;
   }
-  __syncthreads();
-  // softmax + top-k: one thread per token, sequential in expert order (matches
-  // orc_router_topk's summation order exactly)
-  if (threadIdx.x < nt) {
-    const int t = threadIdx.x, tok = t0 + t;
-    const float* lg = s_logit[t];
-    float mx = lg[0];
-    for (int e = 1; e < a.E; ++e) mx = lg[e] > mx ? lg[e] : mx;
-    float sum = 0.0f;
-    for (int e = 0; e < a.E; ++e) sum += expf(lg[e] - mx);
-    uint64_t taken = 0;
-    float wsum = 0.0f;
-    float wk[kMaxTopK];
+  float mx = fmaxf(l0, l1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffff, mx, o));
+  float sum = (e0 < a.E ? expf(l0 - mx) : 0.0f) + (e1 < a.E ? expf(l1 - mx) : 0.0f);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
+  bool t0 = e0 >= a.E, t1 = e1 >= a.E;  // taken (or absent)
+  float wk[kMaxTopK];
+  int idk[kMaxTopK];
+  float wsum = 0.0f;
+  for (int j = 0; j < a.k; ++j) {
+    // lane candidate: its larger untaken logit (lower id on ties)
+    float bv = -INFINITY;
+    int bi = 1 << 30;
+    if (!t0) { bv = l0; bi = e0; }
+    if (!t1 && (l1 > bv || bi == (1 << 30))) { bv = l1; bi = e1; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffff, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffff, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (bi == e0) t0 = true;
+    if (bi == e1) t1 = true;
+    idk[j] = bi;
+    wk[j] = expf(bv - mx) / sum;
+    wsum += wk[j];
+  }
+  if (lane == 0)
     for (int j = 0; j < a.k; ++j) {
-      int best = -1;
-      for (int e = 0; e < a.E; ++e) {
-        if ((taken >> e) & 1) continue;
-        if (best < 0 || lg[e] > lg[best]) best = e;
-      }
-      taken |= 1ull << best;
-      a.ids[(size_t)tok * a.k + j] = best;
-      wk[j] = expf(lg[best] - mx) / sum;
-      wsum += wk[j];
+      a.ids[(size_t)tok * a.k + j] = idk[j];
+      a.weights[(size_t)tok * a.k + j] = a.renormalize ? wk[j] / wsum : wk[j];
     }
-    for (int j = 0; j < a.k; ++j) a.weights[(size_t)tok * a.k + j] = a.renormalize ? wk[j] / wsum : wk[j];
-    if (a.logits)
-      for (int e = 0; e < a.E; ++e) a.logits[(size_t)tok * a.E + e] = lg[e];
-  }
-  // FP8 dispatch payload: one warp per 128-feature block, 4 features per lane
-  if (a.xq) {
-    const int nb = H / 128;
-    for (int blk = warp; blk < nt * nb; blk += 8) {
-      const int t = blk / nb, b = blk % nb;
-      const __nv_bfloat16* src = a.h + (size_t)(t0 + t) * H + b * 128 + lane * 4;
-      const uint2 raw = *reinterpret_cast<const uint2*>(src);
-      const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-      const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-      float amax = fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y)));
+}
+
+// FP8 dispatch payload (1x128 blocks): one warp per (token, block), 4 features per lane
+__global__ void __launch_bounds__(256) router_quant_kernel(RouterArgs a) {
+  sm100::griddep_wait();
+  sm100::griddep_launch();
+  const int nb = a.H / 128;
+  const int blk = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (blk >= a.T * nb) return;
+  const int t = blk / nb, b = blk % nb;
+  const __nv_bfloat16* src = a.h + (size_t)t * a.H + b * 128 + lane * 4;
+  const uint2 raw = *reinterpret_cast<const uint2*>(src);
+  const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+  const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+  float amax = fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y)));
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, o));
-      const float sc = __fdiv_rn(fmaxf(amax, 1e-10f), 448.0f);
-      const uint32_t q = (uint32_t)to_e4m3(__fdiv_rn(f01.x, sc)) | ((uint32_t)to_e4m3(__fdiv_rn(f01.y, sc)) << 8) |
-                         ((uint32_t)to_e4m3(__fdiv_rn(f23.x, sc)) << 16) |
-                         ((uint32_t)to_e4m3(__fdiv_rn(f23.y, sc)) << 24);
-      *reinterpret_cast<uint32_t*>(a.xq + (size_t)(t0 + t) * H + b * 128 + lane * 4) = q;
-      if (lane == 0) a.xs[(size_t)(t0 + t) * nb + b] = sc;
-    }
-  }
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffff, amax, o));
+  const float sc = __fdiv_rn(fmaxf(amax, 1e-10f), 448.0f);
+  const uint32_t q = (uint32_t)to_e4m3(__fdiv_rn(f01.x, sc)) | ((uint32_t)to_e4m3(__fdiv_rn(f01.y, sc)) << 8) |
+                     ((uint32_t)to_e4m3(__fdiv_rn(f23.x, sc)) << 16) | ((uint32_t)to_e4m3(__fdiv_rn(f23.y, sc)) << 24);
+  *reinterpret_cast<uint32_t*>(a.xq + (size_t)t * a.H + b * 128 + lane * 4) = q;
+  if (lane == 0) a.xs[(size_t)t * nb + b] = sc;
 }
 
 // ------------------------------------------------------------- K6 permute
@@ -364,8 +338,24 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
 
 }  // namespace moe
 
-cudaError_t router_launch(const moe::RouterArgs& a, cudaStream_t stream, bool pdl) {
-  return launch_k(pdl, moe::router_kernel, dim3((a.T + moe::kRouterTok - 1) / moe::kRouterTok), dim3(256), 0, stream, a);
+size_t router_workspace_bytes(int H, int E, int num_sms) {
+  return linear_workspace_bytes(make_linear_plan(256, E, H), num_sms);
+}
+
+cudaError_t router_launch(Ctx& ctx, const moe::RouterArgs& a, void* ws, cudaStream_t stream) {
+  float* part = static_cast<float*>(ws);
+  for (int c0 = 0; c0 < a.T; c0 += 256) {
+    const int m = min(256, a.T - c0);
+    const LinearPlan p = make_linear_plan(m, a.E, a.H);
+    cudaError_t e = linear_bf16_launch(ctx, p, a.h + (size_t)c0 * a.H, a.gate_w, part, stream);
+    if (e == cudaSuccess)
+      e = launch_k(ctx.pdl, moe::router_topk_kernel, dim3((m + 7) / 8), dim3(256), 0, stream, p, (const float*)part,
+                   linear_grid(ctx, p), a, c0);
+    if (e != cudaSuccess) return e;
+  }
+  if (!a.xq) return cudaSuccess;
+  const int blocks = a.T * (a.H / 128);
+  return launch_k(ctx.pdl, moe::router_quant_kernel, dim3((blocks + 7) / 8), dim3(256), 0, stream, a);
 }
 
 cudaError_t permute_launch(const moe::PermuteArgs& a, cudaStream_t stream, bool pdl) {

@@ -196,6 +196,22 @@ class AfdRank:
                 "s2": t.stack(s2)}
 
     def setup(self):
+        """alloc() on every rank, agree that all succeeded, then connect().
+        A rank that failed to allocate makes EVERY rank raise here, before any
+        buffer exchange, instead of leaving its peers waiting on a flag."""
+        err = None
+        try:
+            mine = self.alloc()
+        except Exception as e:  # noqa: BLE001 - reported on all ranks below
+            err, mine = e, None
+        ok = self.torch.tensor([0 if err else 1], dtype=self.torch.int32, device=self.dev)
+        self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            raise RuntimeError(f"AFD setup failed on some rank (this rank: {err!r})")
+        self.connect(mine)
+
+    def alloc(self) -> dict:
+        """Local allocations and IPC handle export (no collectives)."""
         t, c, dev = self.torch, self.cfg, self.dev
         g = t.Generator().manual_seed(c.seed)
         if self.role == "attn":
@@ -240,6 +256,11 @@ class AfdRank:
             self.out = [t.empty(Tf, c.hidden, dtype=t.bfloat16, device=dev) for _ in range(c.n_micro)]
             self.copied = [t.cuda.Event() for _ in range(c.n_micro)]
             mine = {"flags": self.ctx.ipc_handle(self.flags), "out": [self.ctx.ipc_handle(b) for b in self.out]}
+        return mine
+
+    def connect(self, mine: dict) -> None:
+        """Collective: exchange IPC handles and open the peers' buffers."""
+        t, c, dev = self.torch, self.cfg, self.dev
         allh = [None] * c.world
         self.dist.all_gather_object(allh, (self.rank, mine))
         for r, h in allh:

@@ -7,7 +7,9 @@ Stated bars:
   * router weights: |gpu - oracle| <= 1e-6; logits vs torch fp32: rel <= 1e-5
   * FP8 dispatch payload (e4m3 codes and fp32 scales): bit-exact
   * MoE FFN output vs the oracle on the same e4m3 inputs/weights:
-    max|gpu-ref|/max|ref| <= 2e-2 (bf16 output, fp8 re-quantised intermediate)
+    max|gpu-ref|/max|ref| <= 5e-3 (both sides round the output to bf16: one
+    bf16 ulp at the largest element is 3.9e-3 of this norm; measured 1.3-1.7e-3);
+    1e-2 for expert-parallel partials (two bf16-rounded partials summed)
 """
 import numpy as np
 import pytest
@@ -120,21 +122,21 @@ def run_moe(ctx, T, H, I, E, k, seed, ranges=None):
 def test_moe_ffn_small(ctx):
     got, ref = run_moe(ctx, 33, 256, 256, 8, 2, 1)
     assert np.isfinite(got).all()
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 5e-3, rel_err(got, ref)
 
 
 @pytest.mark.gpu
 def test_moe_ffn_step3_dims_reduced_experts(ctx):
     """hidden 7168 / inter 5120 (Step-3 expert shape), 8 routed + shared, top-3."""
     got, ref = run_moe(ctx, 40, 7168, 5120, 8, 3, 2)
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 5e-3, rel_err(got, ref)
 
 
 @pytest.mark.gpu
 def test_moe_ffn_many_rows_per_expert(ctx):
     """> 64 rows for one expert (several GEMM work chunks) and the shared expert over 300 tokens."""
     got, ref = run_moe(ctx, 300, 256, 384, 4, 2, 3)
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 5e-3, rel_err(got, ref)
 
 
 @pytest.mark.gpu
@@ -142,7 +144,7 @@ def test_moe_ffn_expert_parallel_partials(ctx):
     """Two EP ranks (experts split, shared expert tokens split) sum to the whole layer."""
     T = 50
     got, ref = run_moe(ctx, T, 256, 256, 8, 3, 4, ranges=[((0, 4), (0, 20)), ((4, 8), (20, T))])
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu

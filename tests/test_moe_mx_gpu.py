@@ -3,9 +3,10 @@
 Stated bars:
   * MXFP8 quantisation (e4m3 codes and UE8M0 scales): bit-exact vs
     orc_quant_mx on the same bf16 input
-  * MoE FFN output vs orc_moe_layer_mx on the same MXFP8 inputs/weights:
-    max|gpu-ref|/max|ref| <= 2e-2 (bf16 output, MXFP8 re-quantised
-    intermediate; a SiLU ulp can flip one e4m3 rounding of the intermediate)
+  * MoE / dense FFN output vs orc_moe_layer_mx / orc_expert_ffn_mx on the same
+    MXFP8 inputs/weights: max|gpu-ref|/max|ref| <= 1e-2 (bf16 output: one ulp at
+    the largest element is 3.9e-3 of this norm; a fast-exp SiLU can flip an
+    e4m3 rounding of the re-quantised intermediate; measured <= 4.8e-3)
 """
 import numpy as np
 import pytest
@@ -92,35 +93,35 @@ def mx_kernel(request, monkeypatch):
 def test_moe_ffn_mx_small(ctx, mx_kernel):
     got, ref = run_moe_mx(ctx, 33, 512, 512, 8, 2, 1)
     assert np.isfinite(got).all()
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu
 def test_moe_ffn_mx_many_rows_per_expert(ctx, mx_kernel):
     """> 256 rows for one expert (several work chunks) and a ragged last chunk."""
     got, ref = run_moe_mx(ctx, 300, 512, 1024, 4, 2, 3)
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu
 def test_moe_ffn_mx_step3_dims_reduced_experts(ctx, mx_kernel):
     """hidden 7168 / inter 5120 (Step-3 expert shape), 8 routed + shared, top-3."""
     got, ref = run_moe_mx(ctx, 40, 7168, 5120, 8, 3, 2)
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu
 def test_moe_ffn_mx_step3_dims_large_batch(ctx, mx_kernel):
     """Step-3 expert shape at ~200 rows per expert (the tensor-bound regime)."""
     got, ref = run_moe_mx(ctx, 400, 7168, 5120, 4, 2, 5)
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu
 def test_moe_ffn_mx_expert_parallel_partials(ctx, mx_kernel):
     T = 50
     got, ref = run_moe_mx(ctx, T, 512, 512, 8, 3, 4, ranges=[((0, 4), (0, 20)), ((4, 8), (20, T))])
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
 
 
 def run_dense(ctx, T, H, I, n_split, seed):
@@ -148,11 +149,11 @@ def run_dense(ctx, T, H, I, n_split, seed):
 def test_dense_ffn_mx(ctx, mx_kernel, T):
     """Dense FFN as 4 intermediate slices == the unsplit FFN (fp32 slice sums)."""
     got, ref = run_dense(ctx, T, 512, 2048, 4, 10 + T)
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
 
 
 @pytest.mark.gpu
 def test_dense_ffn_mx_step3_dims(ctx):
     """Step-3 dense layer: hidden 7168, inter 18432 as 4 slices of 4608."""
     got, ref = run_dense(ctx, 16, 7168, 18432, 4, 3)
-    assert rel_err(got, ref) <= 2e-2, rel_err(got, ref)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)

@@ -210,7 +210,7 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     // ------------------------------- softmax / correction / epilogue (w2-5)
     const int sub = warp & 3;
     const int r = sub * 32 + lane;               // query row = TMEM lane (M=128)
-    const int jt = r / kHeads, head = r % kHeads;  // query token, head
+    const int jt = r / kHeads;  // query token of this row (head = r % 64)
     const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
     const uint32_t p_row_off = (uint32_t)r * 128;
     SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);

@@ -96,8 +96,9 @@ afdk_status afdk_mfa_decode_attention(afdk_ctx* ctx, const afdk_mfa_decode_args*
  * the paper's FP8 attention).  k_cache / v_cache hold e4m3
  * codes [num_pages, page_size, head_dim], dequantised by the per-tensor
  * k_scale / v_scale (> 0).  q stays bf16; the kernel quantises it per
- * (request, head) with scale = max(amax,1e-10)/448 and runs Q.K^T and P.V as
- * FP8 tensor-core MMAs (P rounded to e4m3); out/lse as above.            */
+ * (request, head) with a power-of-two scale 2^e (smallest e with
+ * amax <= 448*2^e) and runs Q.K^T and P.V as FP8 tensor-core MMAs (P rounded
+ * to e4m3); out/lse as above.                                              */
 afdk_status afdk_mfa_decode_attention_fp8(afdk_ctx* ctx, const afdk_mfa_decode_args* a, float k_scale,
                                           float v_scale, afdk_stream stream);
 

@@ -213,13 +213,13 @@ void orc_mfa_layer(const orc_mfa_dims* d, int B, const float* x,
       memcpy(vdst, vb, sizeof(float) * D);
     }
   }
-  if (d->kv_k_scale > 0.0f) { /* per-(request, head) e4m3 query, as the fp8 kernel */
+  if (d->kv_k_scale > 0.0f) { /* per-(request, head) e4m3 query, power-of-two scale, as the fp8 kernel */
     for (size_t r = 0; r < (size_t)B * NH; ++r) {
       float* qr = q + r * D;
       float amax = 0.0f;
       for (int i = 0; i < D; ++i) amax = fmaxf(amax, fabsf(qr[i]));
-      const float sc = fmaxf(amax, 1e-10f) / 448.0f;
-      for (int i = 0; i < D; ++i) qr[i] = orc_e4m3_to_f32(orc_f32_to_e4m3(qr[i] / sc)) * sc;
+      const int e = orc_mx_exponent(amax);
+      for (int i = 0; i < D; ++i) qr[i] = ldexpf(orc_e4m3_to_f32(orc_f32_to_e4m3(qr[i] * ldexpf(1.0f, -e))), e);
     }
   }
   orc_mfa_decode_attention(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, NH, D,
@@ -412,6 +412,20 @@ int orc_mx_exponent(float amax) {
 }
 
 float orc_mx_scale(uint8_t sf) { return ldexpf(1.0f, (int)sf - 127); }
+
+void orc_quant_pow2(const float* x, int rows, int cols, int block, uint8_t* q, int32_t* eo) {
+  const int nb = cols / block;
+  for (int r = 0; r < rows; ++r)
+    for (int b = 0; b < nb; ++b) {
+      const float* xb = x + (size_t)r * cols + (size_t)b * block;
+      float amax = 0.0f;
+      for (int i = 0; i < block; ++i) amax = fmaxf(amax, fabsf(xb[i]));
+      const int e = orc_mx_exponent(amax);
+      eo[(size_t)r * nb + b] = e;
+      const float inv = ldexpf(1.0f, -e);
+      for (int i = 0; i < block; ++i) q[(size_t)r * cols + (size_t)b * block + i] = orc_f32_to_e4m3(xb[i] * inv);
+    }
+}
 
 void orc_quant_mx(const float* x, int rows, int cols, uint8_t* q, uint8_t* sf) {
   const int nb = cols / 32;

@@ -77,7 +77,8 @@ typedef struct {
   /* e4m3 KV cache (0 = off): the caches hold DEQUANTISED values
    * e4m3(code)*scale; the appended token is stored as e4m3(x/scale) (x the
    * bf16-rounded post-RoPE k / v), and the query of every (request, head) is
-   * quantised with scale max(amax,1e-10)/448 before the exact attention. */
+   * quantised with a power-of-two scale (orc_quant_pow2, block = head_dim)
+   * before the exact attention. */
   float kv_k_scale, kv_v_scale;
 } orc_mfa_dims;
 
@@ -150,6 +151,10 @@ void orc_moe_layer_fp8(const uint8_t* xq, const float* xs, int T, int H, int I, 
  * q = e4m3_rn_satfinite(x * 2^-e) (exact power-of-two scaling). */
 int orc_mx_exponent(float amax);
 void orc_quant_mx(const float* x, int rows, int cols, uint8_t* q, uint8_t* sf);
+/* The same power-of-two rule over `block` contiguous elements: e per block
+ * (orc_mx_exponent of the block amax), q = e4m3_rn_satfinite(x * 2^-e).
+ * Used for the FP8-KV attention query (block = head_dim). */
+void orc_quant_pow2(const float* x, int rows, int cols, int block, uint8_t* q, int32_t* e);
 float orc_mx_scale(uint8_t sf); /* 2^(sf-127) */
 /* One gated expert, all operands MXFP8: xq [rows,H] + xsf [rows,H/32],
  * w13 [2I,H] + sf13 [2I,H/32], w2 [H,I] + sf2 [H,I/32]; the SiLU(gate)*up

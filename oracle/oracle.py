@@ -158,15 +158,15 @@ def mfa_decode_attention_fp8(q, kq, vq, k_scale, v_scale, block_table, seq_lens,
 
     Semantics: K = e4m3(kq)*k_scale, V = e4m3(vq)*v_scale (per-tensor scales,
     512 B of KV per token, builtin_catalog.cpp:242); the query of every
-    (request, head) is quantised like the dispatch payload with one block of
-    256 (scale = max(amax,1e-10)/448, orc_quant_fp8_rowblock); attention is then
-    exact (double) on the dequantised Q/K/V.  The B200 kernel additionally
+    (request, head) is quantised with a power-of-two scale 2^e over its 256
+    dims (the MXFP8 exponent rule, orc_quant_pow2); attention is then exact
+    (double) on the dequantised Q/K/V.  The B200 kernel additionally
     rounds the softmax probabilities to e4m3 for the P.V tensor-core MMA
     (stated tolerance in tests/test_mfa_fp8_gpu.py)."""
     q = _f32(q)
     B, H, D = q.shape
-    qq, qs = quant_fp8_rowblock(q.reshape(B * H, D), block=D)
-    qd = (e4m3_to_f32(qq) * qs).reshape(B, H, D)
+    qq, qe = quant_pow2(q.reshape(B * H, D), block=D)
+    qd = np.ldexp(e4m3_to_f32(qq), np.repeat(qe, D, axis=1)).astype(np.float32).reshape(B, H, D)
     kd = e4m3_to_f32(kq) * np.float32(k_scale)
     vd = e4m3_to_f32(vq) * np.float32(v_scale)
     return mfa_decode_attention(qd, kd, vd, block_table, seq_lens, scale, round_bf16=round_bf16)
@@ -280,6 +280,16 @@ def quant_mx(x):
     sf = np.empty((rows, cols // 32), np.uint8)
     orc().orc_quant_mx(_p(x, c_float), c_int(rows), c_int(cols), _p(q, c_uint8), _p(sf, c_uint8))
     return q, sf
+
+
+def quant_pow2(x, block):
+    """e4m3 codes + per-block power-of-two exponents (orc_quant_pow2)."""
+    x = _f32(x)
+    rows, cols = x.shape
+    q = np.empty((rows, cols), np.uint8)
+    e = np.empty((rows, cols // block), np.int32)
+    orc().orc_quant_pow2(_p(x, c_float), c_int(rows), c_int(cols), c_int(block), _p(q, c_uint8), _p(e, c_int32))
+    return q, e
 
 
 def mx_dequant(q, sf):

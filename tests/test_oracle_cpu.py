@@ -261,3 +261,21 @@ def test_b200_batching_thresholds():
     """b_dense / b_moe (moeplan.cpp:7-15) with datasheet B200 peaks."""
     bd8, bd16, bm = orc.ref_b_dense_moe(2.25e15, 4.5e15, 8e12)
     assert (bd8, bd16, bm) == (282, 141, 3455)
+
+
+def test_quant_pow2_matches_mx_rule():
+    """orc_quant_pow2 (the FP8-KV attention query quantiser) is the MXFP8 rule
+    over an arbitrary block: at block 32 it equals orc_quant_mx exactly."""
+    rng = np.random.default_rng(14)
+    x = (rng.standard_normal((16, 256)) * np.exp2(rng.integers(-20, 20, (16, 1)))).astype(np.float32)
+    x[0] = 0.0
+    q32, e32 = orc.quant_pow2(x, 32)
+    qm, sf = orc.quant_mx(x)
+    np.testing.assert_array_equal(q32, qm)
+    np.testing.assert_array_equal(e32 + 127, sf.astype(np.int32))
+    q, e = orc.quant_pow2(x, 256)
+    amax = np.abs(x).max(axis=1)
+    nz = amax > 0
+    assert np.all(amax[nz] <= 448.0 * np.exp2(e[nz, 0].astype(np.float64)))
+    assert np.all(amax[nz] > 448.0 * np.exp2(e[nz, 0].astype(np.float64) - 1))
+    assert e[0, 0] == -127

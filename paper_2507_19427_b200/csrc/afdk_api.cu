@@ -10,12 +10,29 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/afdk.h"
 #include "afdk_internal.h"
 
 namespace afdk {
+
+cudaError_t ensure_smem_attr(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{func, dev}];
+  if (bytes <= have) return cudaSuccess;
+  if ((e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)) != cudaSuccess)
+    return e;
+  have = bytes;
+  return cudaSuccess;
+}
 
 namespace {
 thread_local std::string g_last_error;

@@ -47,6 +47,15 @@ bool encode_tma(Ctx& ctx, CUtensorMap* map, CUtensorMapDataType dt, int rank, vo
 
 void set_error(const std::string& msg);
 
+// Raise a kernel's dynamic shared-memory limit on the CURRENT device (function
+// attributes are per device and a process may drive several GPUs); cached per
+// (kernel, device) under a mutex.
+cudaError_t ensure_smem_attr(const void* func, size_t bytes);
+template <typename... KArgs>
+cudaError_t ensure_smem(void (*kernel)(KArgs...), size_t bytes) {
+  return ensure_smem_attr(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 // cudaLaunchKernelEx with optional programmatic stream serialization (PDL).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -248,12 +248,7 @@ cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, con
   kp.stages = budget / kp.stage_bytes;
   if (kp.stages > 8) kp.stages = 8;
   const size_t smem = (size_t)kp.stages * kp.stage_bytes + 1024 + 256;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(linear_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  if (const cudaError_t e = ensure_smem(linear_bf16_kernel, smem); e != cudaSuccess) return e;
   return launch_k(ctx.pdl, linear_bf16_kernel, dim3(linear_grid(ctx, p)), dim3(kThreads), smem, stream, tw, tx, kp);
 }
 

@@ -461,13 +461,9 @@ cudaError_t mfa_decode_fp8_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t
       return cudaErrorInvalidValue;
   }
   const size_t smem = sizeof(Smem8) + 1024 + (size_t)(a.batch + 1) * sizeof(int32_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(mfa_decode_fp8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(Smem8) + 1024 + (kMaxBatch + 1) * sizeof(int32_t)));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (const cudaError_t ea = ensure_smem(mfa_decode_fp8_kernel, sizeof(Smem8) + 1024 + (kMaxBatch + 1) * sizeof(int32_t));
+      ea != cudaSuccess)
+    return ea;
   cudaError_t e = launch_k(ctx.pdl, mfa_decode_fp8_kernel, dim3(G), dim3(kThreads8), smem, stream, tq, tk, tv, prm);
   if (e != cudaSuccess) return e;
   return mfa_combine_launch(ctx.pdl, prm, G, stream);

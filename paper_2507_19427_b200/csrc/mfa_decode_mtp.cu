@@ -401,13 +401,9 @@ cudaError_t mfa_decode_mtp_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t
       return cudaErrorInvalidValue;
   }
   const size_t smem = sizeof(SmemM) + 1024 + (size_t)(a.batch + 1) * sizeof(int32_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(mfa_decode_mtp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(SmemM) + 1024 + (kMaxBatchMtp + 1) * sizeof(int32_t)));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (const cudaError_t ea = ensure_smem(mfa_decode_mtp_kernel, sizeof(SmemM) + 1024 + (kMaxBatchMtp + 1) * sizeof(int32_t));
+      ea != cudaSuccess)
+    return ea;
   cudaError_t e = launch_k(ctx.pdl, mfa_decode_mtp_kernel, dim3(G), dim3(kThreadsM), smem, stream, tq, tk, tv, prm);
   if (e != cudaSuccess) return e;
   return mfa_combine_launch(ctx.pdl, prm, G, stream);

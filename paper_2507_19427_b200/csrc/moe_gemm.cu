@@ -329,20 +329,10 @@ cudaError_t moe_gemm_launch(Ctx& ctx, bool glu, const MoeGemmArgs& a, cudaStream
   const size_t smem = (size_t)p.stages * (p.stage_bytes + (kChunk + 4) * 4) + 1024 + 512;
   cudaError_t e;
   if (glu) {
-    static size_t attr = 0;
-    if (smem > attr) {
-      if ((e = cudaFuncSetAttribute(moe_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
-        return e;
-      attr = smem;
-    }
+    if ((e = ensure_smem(moe_gemm_kernel<true>, smem)) != cudaSuccess) return e;
     return launch_k(ctx.pdl, moe_gemm_kernel<true>, dim3(ctx.num_sms), dim3(kThreads), smem, stream, tw, tx, p);
   } else {
-    static size_t attr = 0;
-    if (smem > attr) {
-      if ((e = cudaFuncSetAttribute(moe_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
-        return e;
-      attr = smem;
-    }
+    if ((e = ensure_smem(moe_gemm_kernel<false>, smem)) != cudaSuccess) return e;
     return launch_k(ctx.pdl, moe_gemm_kernel<false>, dim3(ctx.num_sms), dim3(kThreads), smem, stream, tw, tx, p);
   }
   return cudaGetLastError();

@@ -355,22 +355,10 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
   const size_t smem = (size_t)p.stages * p.stage_bytes + 2 * (glu ? 3 : 2) * 2048 + 1024 + 512;
   cudaError_t e;
   if (glu) {
-    static size_t attr = 0;
-    if (smem > attr) {
-      if ((e = cudaFuncSetAttribute(moe_gemm_mx_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem)) != cudaSuccess)
-        return e;
-      attr = smem;
-    }
+    if ((e = ensure_smem(moe_gemm_mx_kernel<true>, smem)) != cudaSuccess) return e;
     return launch_k(ctx.pdl, moe_gemm_mx_kernel<true>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, twsf, txsf, p);
   }
-  static size_t attr = 0;
-  if (smem > attr) {
-    if ((e = cudaFuncSetAttribute(moe_gemm_mx_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem)) != cudaSuccess)
-      return e;
-    attr = smem;
-  }
+  if ((e = ensure_smem(moe_gemm_mx_kernel<false>, smem)) != cudaSuccess) return e;
   return launch_k(ctx.pdl, moe_gemm_mx_kernel<false>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, twsf, txsf, p);
 }
 

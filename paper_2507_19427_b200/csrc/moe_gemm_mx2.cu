@@ -369,23 +369,11 @@ cudaError_t moe_gemm_mx2_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cuda
   const int grid = (ctx.num_sms / 2) * 2;
   cudaError_t e;
   if (glu) {
-    static size_t attr = 0;
-    if (smem > attr) {
-      if ((e = cudaFuncSetAttribute(moe_gemm_mx2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem)) != cudaSuccess)
-        return e;
-      attr = smem;
-    }
+    if ((e = ensure_smem(moe_gemm_mx2_kernel<true>, smem)) != cudaSuccess) return e;
     return launch_cluster_k(ctx.pdl, 2, moe_gemm_mx2_kernel<true>, dim3(grid), dim3(kPairThreads), smem, stream, tw,
                             tx, twsf, txsf, p);
   }
-  static size_t attr = 0;
-  if (smem > attr) {
-    if ((e = cudaFuncSetAttribute(moe_gemm_mx2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem)) != cudaSuccess)
-      return e;
-    attr = smem;
-  }
+  if ((e = ensure_smem(moe_gemm_mx2_kernel<false>, smem)) != cudaSuccess) return e;
   return launch_cluster_k(ctx.pdl, 2, moe_gemm_mx2_kernel<false>, dim3(grid), dim3(kPairThreads), smem, stream, tw,
                           tx, twsf, txsf, p);
 }

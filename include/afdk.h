@@ -23,7 +23,11 @@
  * message of the last failure on the calling thread is afdk_last_error().
  * A context is used from one host thread at a time; work is enqueued on the
  * caller's CUDA stream (afdk_stream == cudaStream_t, NULL = legacy stream)
- * and calls do not synchronise the device unless stated.
+ * and calls do not synchronise the device unless stated.  Calls are CUDA-graph
+ * capturable (kernels are chained with programmatic dependent launch); the
+ * context's workspace grows on demand (cudaFree + cudaMalloc, synchronising),
+ * so capture after a warm-up call of the largest shape, and recapture if a
+ * later call needs a larger workspace.  One context per stream in flight.
  *
  * Tensor formats: bf16 = IEEE bfloat16 (uint16 storage), e4m3 = OCP FP8
  * E4M3FN (max 448), all tensors dense row-major unless stated.

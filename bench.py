@@ -432,21 +432,22 @@ def afd_runs(world):
     MXFP8 at the largest micro-batch the attention layer takes, and the
     balanced attention/FFN split."""
     base = {2: (1, 1), 4: (1, 3), 8: (2, 6)}.get(world, (1, world - 1))
-    runs = [(base, "fp8", 192), (base, "mx", 256), (base, "mx", 512)]
+    runs = [(base, "fp8", 192, "moe"), (base, "mx", 256, "moe"), (base, "mx", 512, "moe")]
     bal = (world // 2, world - world // 2)
     if bal != base:
-        runs += [(bal, "mx", 256), (bal, "mx", 512)]
+        runs += [(bal, "mx", 256, "moe"), (bal, "mx", 512, "moe")]
+    runs.append((bal, "mx", 512, "dense"))  # a dense layer: FFN tier tensor-parallel over intermediate slices
     return runs
 
 
-def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt="fp8", plan=None):
+def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt="fp8", plan=None, kind="moe"):
     """Real pipeline on all ranks: nA attention GPUs + nF FFN GPUs, 2 ping-pong
     micro-batches, 2 layers per step (distinct KV caches), copy-engine NVLink."""
     from paper_2507_19427_b200 import Context
     from paper_2507_19427_b200.afd import AfdConfig, AfdRank, wire_bytes
 
     na, nf = plan if plan else afd_roles(world)
-    cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=T_mb, n_micro=2, layers=2, ctx_len=CTX, ffn_format=fmt)
+    cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=T_mb, n_micro=2, layers=2, ctx_len=CTX, ffn_format=fmt, layer_kind=kind)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -482,7 +483,8 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
         c.close()
     del r
     torch.cuda.empty_cache()
-    return {"plan": f"{na}A{nf}F", "ffn_format": fmt, "T_mb": cfg.T_mb, "n_micro": cfg.n_micro, "ctx": cfg.ctx_len,
+    return {"plan": f"{na}A{nf}F", "layer": kind, "ffn_format": fmt, "T_mb": cfg.T_mb, "n_micro": cfg.n_micro,
+            "ctx": cfg.ctx_len,
             "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
             "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
             "nvlink_bytes_per_layer": {k: v * cfg.n_micro for k, v in wb.items()},
@@ -824,9 +826,10 @@ def main():
             else:
                 # micro-batch sweep: per-layer throughput depends on balancing the
                 # attention tier (grows with T_mb) against expert weight streaming
-                runs = [run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4), T, f, plan)
-                        for plan, f, T in afd_runs(world)]
-                afd = {"runs": runs, "best": max(runs, key=lambda x: x["tokens_per_s_per_gpu_per_layer"])}
+                runs = [run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4), T, f, plan, kind)
+                        for plan, f, T, kind in afd_runs(world)]
+                moe_runs = [x for x in runs if x["layer"] == "moe"]
+                afd = {"runs": runs, "best": max(moe_runs, key=lambda x: x["tokens_per_s_per_gpu_per_layer"])}
         except Exception as e:  # reported, never silently replaced
             afd = {"error": f"{type(e).__name__}: {e}"}
 

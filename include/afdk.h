@@ -293,6 +293,9 @@ afdk_status afdk_moe_ffn_scatter(afdk_ctx* ctx, const afdk_moe_weights* w, const
                                  const afdk_row_scatter* sc, afdk_stream stream);
 afdk_status afdk_moe_ffn_mx_scatter(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
                                     const afdk_row_scatter* sc, afdk_stream stream);
+/* dense layer, this GPU's intermediate slices (tensor-parallel partial) */
+afdk_status afdk_dense_ffn_mx_scatter(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,
+                                      const uint8_t* xsf, const afdk_row_scatter* sc, afdk_stream stream);
 
 /* ------------------------------------------- C1/C2 AFD exchange (NVLink)
  * Zero-SM point-to-point transport between attention and FFN GPUs of one

@@ -47,6 +47,9 @@ class AfdConfig:
     ffn_format: str = "fp8"   # "fp8": 1x128/128x128 fp32 scales; "mx": MXFP8 (UE8M0 per 32)
     f2a: str = "push"         # "push": the FFN combine writes into the attention GPUs' receive
                               # buffers over NVLink (fused); "pull": attention DMA-pulls
+    layer_kind: str = "moe"   # "moe": routed experts (EP over FFN GPUs); "dense": the dense Step-3
+                              # FFN (inter dense_inter) as intermediate slices, tensor-parallel over FFN GPUs
+    dense_inter: int = 18432
     attn_chunk: int = 256     # requests per attention-layer call (its GEMM N limit); a larger
                               # T_mb runs the attention side in chunks and ships ONE payload,
                               # so the FFN tier streams its expert weights once per micro-batch
@@ -64,8 +67,24 @@ class AfdConfig:
             raise ValueError(f"ffn_format={self.ffn_format!r}: expected 'fp8' or 'mx'")
         if self.ffn_format == "mx" and (self.hidden % 512 or self.inter % 512):
             raise ValueError("ffn_format='mx' needs hidden and inter to be multiples of 512")
+        if self.layer_kind not in ("moe", "dense"):
+            raise ValueError(f"layer_kind={self.layer_kind!r}: expected 'moe' or 'dense'")
+        if self.layer_kind == "dense":
+            if self.ffn_format != "mx":
+                raise ValueError("layer_kind='dense' runs the MXFP8 dense FFN (ffn_format='mx')")
+            if self.dense_inter % (self.dense_slices_total * 512):
+                raise ValueError(f"dense_inter={self.dense_inter} is not a multiple of "
+                                 f"{self.dense_slices_total} slices x 512")
         if self.n_attn < 1 or self.n_ffn < 1 or self.n_ffn > self.n_experts:
             raise ValueError("need at least one attention and one FFN GPU, n_ffn <= n_experts")
+
+    @property
+    def dense_slices_per_gpu(self) -> int:
+        return max(1, 4 // self.n_ffn)
+
+    @property
+    def dense_slices_total(self) -> int:
+        return self.n_ffn * self.dense_slices_per_gpu
 
     @property
     def world(self) -> int:
@@ -195,6 +214,27 @@ class AfdRank:
         return {"n_experts": c.n_experts, "w13": t.stack(w13), "w2": t.stack(w2), "s13": t.stack(s13),
                 "s2": t.stack(s2)}
 
+    def dense_weights(self, lo, hi):
+        """MXFP8 slices [lo, hi) of the dense FFN (slice layout of afdk_dense_ffn_mx);
+        slice j's tensors depend only on (seed, j)."""
+        t, c = self.torch, self.cfg
+        Is = c.dense_inter // c.dense_slices_total
+        w13, w2 = [], []
+        for j in range(lo, hi):
+            g = t.Generator(device=self.dev).manual_seed(c.seed * 1000 + 500 + j)
+
+            def e4m3(shape):
+                mag = t.randint(0x18, 0x40, shape, generator=g, dtype=t.int32, device=self.dev)
+                sgn = t.randint(0, 2, shape, generator=g, dtype=t.int32, device=self.dev) * 0x80
+                return (mag | sgn).to(t.uint8)
+
+            w13.append(e4m3((2 * Is, c.hidden)))
+            w2.append(e4m3((c.hidden, Is)))
+        n = hi - lo
+        return {"w13": t.stack(w13), "w2": t.stack(w2),
+                "sf13": t.full((n, 2 * Is, c.hidden // 32), 120, dtype=t.uint8, device=self.dev),
+                "sf2": t.full((n, c.hidden, Is // 32), 120, dtype=t.uint8, device=self.dev)}
+
     def setup(self):
         """alloc() on every rank, agree that all succeeded, then connect().
         A rank that failed to allocate makes EVERY rank raise here, before any
@@ -243,7 +283,11 @@ class AfdRank:
                     "recv": [self.ctx.ipc_handle(b) for b in self.recv_part]}
         else:
             lo, hi = expert_shard(self.idx, c)
-            self.moe_w = self.expert_weights(lo, hi)
+            if c.layer_kind == "dense":
+                S = c.dense_slices_per_gpu
+                self.moe_w = self.dense_weights(self.idx * S, (self.idx + 1) * S)
+            else:
+                self.moe_w = self.expert_weights(lo, hi)
             self.expert_lo, self.expert_hi = lo, hi
             self.shared = shared_token_shard(self.idx, c)
             Tf = c.T_ffn
@@ -295,8 +339,9 @@ class AfdRank:
         buf, L = self.send[mb], self.lay
         view = lambda name, shape, dtype: buf[L.off[name]:L.off[name] + L.size(name)].view(dtype).view(*shape)
         if c.ffn_format == "mx":
-            ctx.router_topk(self.h_norm[mb], self.w["gate"], c.top_k, view("ids", (c.T_mb, c.top_k), t.int32),
-                            view("wts", (c.T_mb, c.top_k), t.float32), stream=sp)
+            if c.layer_kind == "moe":
+                ctx.router_topk(self.h_norm[mb], self.w["gate"], c.top_k, view("ids", (c.T_mb, c.top_k), t.int32),
+                                view("wts", (c.T_mb, c.top_k), t.float32), stream=sp)
             ctx.quant_mx(self.h_norm[mb], view("xq", (c.T_mb, c.hidden), t.uint8),
                          view("xs", (c.T_mb, c.hidden // 32), t.uint8), stream=sp)
         else:
@@ -329,10 +374,13 @@ class AfdRank:
         self.copied[mb].record(self.copy_stream)
         st = self.streams[0]
         st.wait_event(self.copied[mb])
-        ffn = ctx.moe_ffn_mx if c.ffn_format == "mx" else ctx.moe_ffn
-        ffn(self.moe_w, rx["xq"], rx["xs"], rx["ids"], rx["wts"], self.out[mb], expert_lo=self.expert_lo,
-            expert_hi=self.expert_hi, shared=self.shared, stream=st.cuda_stream,
-            scatter=(self.dst[mb], c.T_mb) if c.f2a == "push" else None)
+        scatter = (self.dst[mb], c.T_mb) if c.f2a == "push" else None
+        if c.layer_kind == "dense":  # this GPU's slices of the dense FFN: a tensor-parallel partial
+            ctx.dense_ffn_mx(self.moe_w, rx["xq"], rx["xs"], self.out[mb], stream=st.cuda_stream, scatter=scatter)
+        else:
+            ffn = ctx.moe_ffn_mx if c.ffn_format == "mx" else ctx.moe_ffn
+            ffn(self.moe_w, rx["xq"], rx["xs"], rx["ids"], rx["wts"], self.out[mb], expert_lo=self.expert_lo,
+                expert_hi=self.expert_hi, shared=self.shared, stream=st.cuda_stream, scatter=scatter)
         for a in range(c.n_attn):
             ctx.signal(self.peer_flags[a] + 4 * flag_index(self.idx, mb, c), seq, stream=st.cuda_stream)
 

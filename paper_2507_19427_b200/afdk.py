@@ -144,6 +144,8 @@ SIGNATURES = {
                                         c_void_p]),
     "afdk_moe_ffn_mx": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), c_void_p]),
     "afdk_dense_ffn_mx": (c_int, [c_void_p, POINTER(DenseMxWeights), c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "afdk_dense_ffn_mx_scatter": (c_int, [c_void_p, POINTER(DenseMxWeights), c_int, c_void_p, c_void_p,
+                                          POINTER(RowScatter), c_void_p]),
     "afdk_quant_mx": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "afdk_ipc_handle": (c_int, [c_void_p, c_void_p, c_void_p]),
     "afdk_ipc_open": (c_int, [c_void_p, c_void_p, POINTER(c_void_p)]),
@@ -325,13 +327,18 @@ class Context:
             check(self.lib.afdk_moe_ffn_mx_scatter(self.handle, ctypes.byref(mw), ctypes.byref(a), ctypes.byref(sc),
                                                    c_void_p(stream)))
 
-    def dense_ffn_mx(self, w: dict, xq, xsf, out, stream: int = 0) -> None:
+    def dense_ffn_mx(self, w: dict, xq, xsf, out, stream: int = 0, scatter=None) -> None:
         """Dense FFN in slice layout: w13 [n_split, 2*Is, H], sf13, w2 [n_split, H, Is], sf2."""
         T, Hd = xq.shape
         n_split, _, Is = w["w2"].shape
         dw = DenseMxWeights(Hd, Is, n_split, ptr(w["w13"]), ptr(w["sf13"]), ptr(w["w2"]), ptr(w["sf2"]))
-        check(self.lib.afdk_dense_ffn_mx(self.handle, ctypes.byref(dw), T, ptr(xq), ptr(xsf), ptr(out),
-                                         c_void_p(stream)))
+        if scatter is None:
+            check(self.lib.afdk_dense_ffn_mx(self.handle, ctypes.byref(dw), T, ptr(xq), ptr(xsf), ptr(out),
+                                             c_void_p(stream)))
+        else:
+            sc = RowScatter(scatter[0].numel(), scatter[1], ptr(scatter[0]))
+            check(self.lib.afdk_dense_ffn_mx_scatter(self.handle, ctypes.byref(dw), T, ptr(xq), ptr(xsf),
+                                                     ctypes.byref(sc), c_void_p(stream)))
 
     @staticmethod
     def dense_split_layout(w13, sf13, w2, sf2, n_split):

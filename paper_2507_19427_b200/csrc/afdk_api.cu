@@ -421,8 +421,8 @@ afdk_status afdk_moe_ffn_mx_scatter(afdk_ctx* ctx, const afdk_moe_mx_weights* w,
   return moe_ffn_mx_entry(ctx, w, a, sc, stream);
 }
 
-afdk_status afdk_dense_ffn_mx(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,
-                              const uint8_t* xsf, void* out, afdk_stream stream) {
+static afdk_status dense_ffn_mx_entry(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,
+                                      const uint8_t* xsf, void* out, const afdk_row_scatter* sc, afdk_stream stream) {
   if (!ctx || !w) { set_error("afdk_dense_ffn_mx: NULL ctx/weights"); return AFDK_ERR_INVALID; }
   if (w->hidden % 512 || w->hidden < 512 || w->inter_split % 512 || w->inter_split < 512) {
     set_error("afdk_dense_ffn_mx: hidden and inter_split must be positive multiples of 512");
@@ -430,7 +430,7 @@ afdk_status afdk_dense_ffn_mx(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int
   }
   if (w->n_split < 1 || w->n_split > 64) { set_error("afdk_dense_ffn_mx: n_split must be in [1, 64]"); return AFDK_ERR_INVALID; }
   if (T < 1 || T > 65536) { set_error("afdk_dense_ffn_mx: T out of range"); return AFDK_ERR_INVALID; }
-  if (!xq || !xsf || !out || !w->w13 || !w->sf13 || !w->w2 || !w->sf2) {
+  if (!xq || !xsf || (!out && !sc) || !w->w13 || !w->sf13 || !w->w2 || !w->sf2) {
     set_error("afdk_dense_ffn_mx: NULL tensor pointer");
     return AFDK_ERR_INVALID;
   }
@@ -438,10 +438,22 @@ afdk_status afdk_dense_ffn_mx(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int
   cudaSetDevice(c.device);
   afdk::DenseFfnMxArgs d{T, w->hidden, w->inter_split, w->n_split, w->w13, w->sf13, w->w2, w->sf2,
                          static_cast<const uint8_t*>(xq), xsf, out};
+  if (!scatter_ok(sc, T, "afdk_dense_ffn_mx")) return AFDK_ERR_INVALID;
+  if (sc) { d.dst = sc->dst; d.rows_per_dst = sc->rows_per_dst; }
   void* ws = afdk::workspace(c, afdk::dense_ffn_mx_workspace_bytes(T, w->n_split, w->hidden, w->inter_split));
   if (!ws) { set_error("afdk_dense_ffn_mx: workspace allocation failed"); return AFDK_ERR_CUDA; }
   if (afdk::dense_ffn_mx_launch(c, d, ws, static_cast<cudaStream_t>(stream)) != cudaSuccess) return AFDK_ERR_CUDA;
   return AFDK_OK;
+}
+
+afdk_status afdk_dense_ffn_mx(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,
+                              const uint8_t* xsf, void* out, afdk_stream stream) {
+  return dense_ffn_mx_entry(ctx, w, T, xq, xsf, out, nullptr, stream);
+}
+afdk_status afdk_dense_ffn_mx_scatter(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,
+                                      const uint8_t* xsf, const afdk_row_scatter* sc, afdk_stream stream) {
+  if (!sc) { set_error("afdk_dense_ffn_mx_scatter: NULL scatter"); return AFDK_ERR_INVALID; }
+  return dense_ffn_mx_entry(ctx, w, T, xq, xsf, nullptr, sc, stream);
 }
 
 afdk_status afdk_quant_mx(afdk_ctx* ctx, const void* x, int T, int H, void* q, uint8_t* sf, afdk_stream stream) {

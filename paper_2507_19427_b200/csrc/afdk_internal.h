@@ -236,6 +236,8 @@ struct DenseFfnMxArgs {
   const uint8_t* xq;      // [T, H]
   const uint8_t* xsf;     // [T, H/32]
   void* out;              // bf16 [T, H]
+  const uint64_t* dst = nullptr;  // fused return (see moe::CombineArgs::dst)
+  int rows_per_dst = 0;
 };
 size_t dense_ffn_mx_workspace_bytes(int T, int n_split, int H, int Is);
 cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws, cudaStream_t stream);

@@ -161,10 +161,14 @@ __global__ void dense_work_kernel(int T, int n_split, int chunk, Work* work, int
 }
 
 __global__ void __launch_bounds__(256) dense_combine_kernel(const float* y, int T, int n_split, int H,
-                                                            __nv_bfloat16* out) {
+                                                            __nv_bfloat16* out, const uint64_t* dst, int rows_per_dst) {
   sm100::griddep_wait();
   sm100::griddep_launch();
   const int t = blockIdx.x;
+  // fused TP return: row t straight into the attention GPU that owns it
+  __nv_bfloat16* orow = dst ? reinterpret_cast<__nv_bfloat16*>(__ldg(dst + t / rows_per_dst)) +
+                                  (size_t)(t % rows_per_dst) * H
+                            : out + (size_t)t * H;
   for (int f = threadIdx.x * 4; f < H; f += blockDim.x * 4) {
     float4 acc = __ldcg(reinterpret_cast<const float4*>(y + (size_t)t * H + f));
     for (int j = 1; j < n_split; ++j) {
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(256) dense_combine_kernel(const float* y, int 
     uint2 o;
     o.x = *reinterpret_cast<uint32_t*>(&o0);
     o.y = *reinterpret_cast<uint32_t*>(&o1);
-    *reinterpret_cast<uint2*>(out + (size_t)t * H + f) = o;
+    *reinterpret_cast<uint2*>(orow + f) = o;
   }
 }
 
@@ -222,7 +226,7 @@ cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws_base
   MoeGemmMxArgs g2{a.w2, a.sf2, hq, hsf, work, n_work, a.H, a.Is, a.n_split, 0, a.n_split, rp, nullptr, nullptr, y};
   if ((e = chk(gemm(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
   return chk(launch_k(ctx.pdl, moe::dense_combine_kernel, dim3(a.T), dim3(256), 0, stream, (const float*)y, a.T,
-                      a.n_split, a.H, static_cast<__nv_bfloat16*>(a.out)),
+                      a.n_split, a.H, static_cast<__nv_bfloat16*>(a.out), a.dst, a.rows_per_dst),
              "combine");
 }
 

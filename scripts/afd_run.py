@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--fmt", default="fp8", choices=["fp8", "mx"])
     ap.add_argument("--f2a", default="push", choices=["push", "pull"])
     ap.add_argument("--attn-chunk", type=int, default=256)
+    ap.add_argument("--layer", default="moe", choices=["moe", "dense"])
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -40,10 +41,11 @@ def main():
     if a.check:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=24, n_micro=2, layers=1, hidden=1024,
                         q_lora=256, ctx_len=300, n_experts=8, top_k=2, inter=512, seed=3, ffn_format=a.fmt, f2a=a.f2a,
-                        attn_chunk=min(a.attn_chunk, 256))
+                        attn_chunk=min(a.attn_chunk, 256), layer_kind=a.layer, dense_inter=2048 * 6)
     else:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=a.T_mb, n_micro=a.n_micro, layers=a.layers,
-                        ctx_len=a.ctx_len, ffn_format=a.fmt, f2a=a.f2a, attn_chunk=a.attn_chunk)
+                        ctx_len=a.ctx_len, ffn_format=a.fmt, f2a=a.f2a, attn_chunk=a.attn_chunk,
+                        layer_kind=a.layer)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -87,7 +89,11 @@ def main():
                 wts = torch.empty(c.T_mb, c.top_k, device=dev)
                 xq = torch.empty(c.T_mb, c.hidden, dtype=torch.uint8, device=dev)
                 part = torch.empty_like(h_res)
-                if c.ffn_format == "mx":
+                if c.layer_kind == "dense":
+                    xs = torch.empty(c.T_mb, c.hidden // 32, dtype=torch.uint8, device=dev)
+                    ctxs[0].quant_mx(h_norm, xq, xs)
+                    ctxs[0].dense_ffn_mx(r.dense_weights(0, c.dense_slices_total), xq, xs, part)
+                elif c.ffn_format == "mx":
                     xs = torch.empty(c.T_mb, c.hidden // 32, dtype=torch.uint8, device=dev)
                     ctxs[0].router_topk(h_norm, r.w["gate"], c.top_k, ids, wts)
                     ctxs[0].quant_mx(h_norm, xq, xs)
@@ -107,7 +113,7 @@ def main():
                       "part err", rel_err(r.recv_part[mb][0].float().cpu().numpy(), part.float().cpu().numpy()),
                       "xq eq", bool(torch.equal(sent_xq, xq)), "ids eq", bool(torch.equal(sent_ids, ids)), flush=True)
             ok = max(errs) <= 2e-2
-            print(json.dumps({"afd_check": "ok" if ok else "FAIL", "fmt": c.ffn_format, "f2a": c.f2a, "rel_err": errs, "world": world,
+            print(json.dumps({"afd_check": "ok" if ok else "FAIL", "layer": c.layer_kind, "fmt": c.ffn_format, "f2a": c.f2a, "rel_err": errs, "world": world,
                               "n_attn": cfg.n_attn}), flush=True)
         dist.barrier()
         r.close()

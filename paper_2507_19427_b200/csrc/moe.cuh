@@ -30,7 +30,22 @@ struct Work {
   int rows;   // <= chunk
   int xrow0;  // first row of its W13 input (MoE: = row0 in the dispatch buffer;
               // dense FFN splits: the token row, shared by every split)
+  int gfirst, gcnt;  // its group's chunks: work[gfirst, gfirst + gcnt)
 };
+
+// GEMM item order over (group, m-tile, chunk): a group's chunks are adjacent,
+// so they share each weight tile while it is in L2, and a chunk's activation
+// panel is re-read by the group's m-tiles within one wave.  Items of a group
+// occupy [gfirst*m_tiles, (gfirst+gcnt)*m_tiles), hence any chunk index
+// it/m_tiles inside that range names the group.
+struct ItemRef {
+  int mt, chunk;
+};
+__device__ __forceinline__ ItemRef item_of(const Work* work, int it, int m_tiles) {
+  const Work w = work[it / m_tiles];
+  const int local = it - w.gfirst * m_tiles;
+  return {local / w.gcnt, w.gfirst + local % w.gcnt};
+}
 
 struct PermuteArgs {
   const int32_t* ids;  // [T, k]

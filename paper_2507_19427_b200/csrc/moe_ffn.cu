@@ -149,14 +149,18 @@ __global__ void dense_work_kernel(int T, int n_split, int chunk, Work* work, int
   const int n_items = (T + chunk - 1) / chunk;
   const int per = ((T + n_items - 1) / n_items + 31) & ~31;
   int g = 0;
-  for (int j = 0; j < n_split; ++j)
+  for (int j = 0; j < n_split; ++j) {
+    const int first = g;
     for (int r = 0; r < T; r += per) {
       work[g].group = j;
       work[g].row0 = j * T + r;
       work[g].rows = min(per, T - r);
       work[g].xrow0 = r;
+      work[g].gfirst = first;
+      work[g].gcnt = (T + per - 1) / per;
       ++g;
     }
+  }
   *n_work = g;
 }
 

@@ -144,8 +144,9 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       const uint64_t pol_x = policy_evict_last();
       int i = 0, gi = 0;
       for (int it = cta; it < n_items; it += G) {
-        const int mt = it % p.m_tiles;
-        const Work wk = p.work[it / p.m_tiles];
+        const ItemRef ir = item_of(p.work, it, p.m_tiles);
+        const int mt = ir.mt;
+        const Work wk = p.work[ir.chunk];
         const int wrow = mx_weight_index(p, wk.group) * p.w_rows + mt * 128;
         for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
           if ((kb & 3) == 0) {  // scale group of k-blocks kb..kb+3
@@ -172,7 +173,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     if (lane == 0) {
       int i = 0, li = 0;
       for (int it = cta; it < n_items; it += G, ++li) {
-        const Work wk = p.work[it / p.m_tiles];
+        const Work wk = p.work[item_of(p.work, it, p.m_tiles).chunk];
         const int b = kGLU ? 0 : (li & 1);
         const int nb = kGLU ? li : (li >> 1);
         if (nb > 0) mbar_wait(&acc_empty[b], (nb & 1) ^ 1);
@@ -237,8 +238,9 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     const uint32_t t_lane = tmem + ((uint32_t)(sub * 32) << 16);
     int li = 0;
     for (int it = cta; it < n_items; it += G, ++li) {
-      const int mt = it % p.m_tiles;
-      const Work wk = p.work[it / p.m_tiles];
+      const ItemRef ir = item_of(p.work, it, p.m_tiles);
+      const int mt = ir.mt;
+      const Work wk = p.work[ir.chunk];
       const int b = kGLU ? 0 : (li & 1);
       const int nb = kGLU ? li : (li >> 1);
       mbar_wait(&acc_full[b], nb & 1);

@@ -128,8 +128,9 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
       const uint32_t full_l = mapa_shared(full, 0);
       int i = 0, gi = 0;
       for (int it = pair; it < n_items; it += n_pairs) {
-        const int mt = it % p.m_tiles;
-        const Work wk = p.work[it / p.m_tiles];
+        const ItemRef ir = item_of(p.work, it, p.m_tiles);
+        const int mt = ir.mt;
+        const Work wk = p.work[ir.chunk];
         const int half = ((wk.rows + 31) & ~31) >> 1;
         const int widx = (wk.group == p.E ? p.n_local : wk.group - p.expert_lo) * p.w_rows;
         const int arow = kGLU ? widx + mt * 128 + 64 * (int)rank : widx + mt * 256 + 128 * (int)rank;
@@ -167,7 +168,7 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
 #define MX2_T(x)
 #endif
       for (int it = pair; it < n_items; it += n_pairs, ++li) {
-        const Work wk = p.work[it / p.m_tiles];
+        const Work wk = p.work[item_of(p.work, it, p.m_tiles).chunk];
         const uint32_t N = (uint32_t)((wk.rows + 31) & ~31);
         const uint32_t idesc = idesc_mxf8(256, N);
 #ifdef AFDK_MX2_PROF
@@ -244,8 +245,9 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
     const uint32_t acc_empty_l = mapa_shared(acc_empty, 0);
     int li = 0;
     for (int it = pair; it < n_items; it += n_pairs, ++li) {
-      const int mt = it % p.m_tiles;
-      const Work wk = p.work[it / p.m_tiles];
+      const ItemRef ir = item_of(p.work, it, p.m_tiles);
+      const int mt = ir.mt;
+      const Work wk = p.work[ir.chunk];
       const int n_chunks = (wk.rows + 31) >> 5;
       mbar_wait(acc_full, li & 1);
       tc_fence_after();

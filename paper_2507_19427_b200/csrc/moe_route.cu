@@ -184,11 +184,14 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
     auto emit = [&](int g, int group, int row0, int rows) {
       const int n_it = items(rows);
       const int per = n_it > 0 ? ((rows + n_it - 1) / n_it + 31) & ~31 : 0;
+      const int first = g;
       for (int r = 0; r < rows; r += per, ++g) {
         a.work[g].group = group;
         a.work[g].row0 = row0 + r;
         a.work[g].rows = min(per, rows - r);
         a.work[g].xrow0 = row0 + r;
+        a.work[g].gfirst = first;
+        a.work[g].gcnt = n_it;
       }
     };
     if (l0) emit(y0 - n0, e0, x0 - c0, c0);

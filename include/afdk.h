@@ -160,6 +160,15 @@ afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_
 afdk_status afdk_mfa_layer_fp8(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
                                float k_scale, float v_scale, afdk_stream stream);
 
+/* MTP decode layer (mtp in {1, 2}): every request carries its mtp newest
+ * tokens (positions L-mtp .. L-1, L = seq_lens[b] counts them).  x, h_res and
+ * h_norm have batch*mtp rows ordered (request, token); the projections run on
+ * all rows, each row appends its K/V at its own position, and the core is
+ * afdk_mfa_decode_attention_mtp (causal among the new tokens).
+ * batch*mtp <= 256, batch <= 128 for mtp = 2.                              */
+afdk_status afdk_mfa_layer_mtp(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a, int mtp,
+                               afdk_stream stream);
+
 /* ------------------------------------------------ K5 router + FP8 dispatch
  * Attention-side router: logits = h . gate_w^T (fp32), softmax,
  * top-k by logit (ties -> lower expert id), weights = softmax probability

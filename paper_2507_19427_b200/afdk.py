@@ -134,6 +134,7 @@ SIGNATURES = {
                                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_permute": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_moe_ffn": (c_int, [c_void_p, POINTER(MoeWeights), POINTER(MoeArgs), c_void_p]),
+    "afdk_mfa_layer_mtp": (c_int, [c_void_p, POINTER(MfaWeights), POINTER(MfaLayerArgs), c_int, c_void_p]),
     "afdk_mfa_layer_fp8": (c_int, [c_void_p, POINTER(MfaWeights), POINTER(MfaLayerArgs), c_float, c_float,
                                    c_void_p]),
     "afdk_mfa_decode_attention_mtp": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_int, c_void_p]),
@@ -260,7 +261,8 @@ class Context:
                                    int(out.dtype == torch.float32), c_void_p(stream)))
 
     def mfa_layer(self, w: dict, x, k_cache, v_cache, block_table, seq_lens, h_res, h_norm,
-                  rms_eps=1e-5, rope_theta=5e5, softmax_scale=None, stream: int = 0, kv_scales=None) -> None:
+                  rms_eps=1e-5, rope_theta=5e5, softmax_scale=None, stream: int = 0, kv_scales=None,
+                  mtp: int = 1) -> None:
         """Attention-side decode layer; `w` holds bf16 device tensors
         in_norm, qkv, q_norm, q_up, o, post_norm (shapes as in include/afdk.h)."""
         hidden = x.shape[1]
@@ -270,9 +272,11 @@ class Context:
         scale = head_dim ** -0.5 if softmax_scale is None else softmax_scale
         mw = MfaWeights(hidden, q_lora, n_heads, head_dim, ptr(w["in_norm"]), ptr(w["qkv"]), ptr(w["q_norm"]),
                         ptr(w["q_up"]), ptr(w["o"]), ptr(w["post_norm"]), rms_eps, rope_theta, scale)
-        a = MfaLayerArgs(x.shape[0], ptr(x), ptr(k_cache), ptr(v_cache), k_cache.shape[0], k_cache.shape[1],
+        a = MfaLayerArgs(x.shape[0] // mtp, ptr(x), ptr(k_cache), ptr(v_cache), k_cache.shape[0], k_cache.shape[1],
                          ptr(block_table), block_table.shape[1], ptr(seq_lens), ptr(h_res), ptr(h_norm))
-        if kv_scales is None:
+        if mtp != 1:  # x / h_res / h_norm rows are (request, token)
+            check(self.lib.afdk_mfa_layer_mtp(self.handle, ctypes.byref(mw), ctypes.byref(a), mtp, c_void_p(stream)))
+        elif kv_scales is None:
             check(self.lib.afdk_mfa_layer(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
         else:  # e4m3 caches (uint8 codes) with per-tensor (k_scale, v_scale)
             check(self.lib.afdk_mfa_layer_fp8(self.handle, ctypes.byref(mw), ctypes.byref(a),

@@ -235,7 +235,7 @@ afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, 
 }
 
 static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
-                                   float k_scale, float v_scale, afdk_stream stream) {
+                                   float k_scale, float v_scale, afdk_stream stream, int mtp = 1) {
   if (!ctx || !w || !a) { set_error("afdk_mfa_layer: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }
   if (w->n_heads != 64 || w->head_dim != 256 || a->page_size != 64) {
     set_error("afdk_mfa_layer: n_heads/head_dim/page_size must be 64/256/64");
@@ -249,7 +249,10 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
     set_error("afdk_mfa_layer: hidden <= 16384 and q_lora <= 4096 (row epilogues span one 4-CTA cluster)");
     return AFDK_ERR_INVALID;
   }
-  if (a->batch < 1 || a->batch > 256) { set_error("afdk_mfa_layer: batch must be in [1, 256]"); return AFDK_ERR_INVALID; }
+  if (a->batch < 1 || a->batch * mtp > 256) {
+    set_error("afdk_mfa_layer: batch x mtp must be in [1, 256]");
+    return AFDK_ERR_INVALID;
+  }
   if (!a->x || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->h_res || !a->h_norm ||
       !w->in_norm || !w->w_qkv || !w->q_norm || !w->w_q_up || !w->w_o || !w->post_norm) {
     set_error("afdk_mfa_layer: NULL tensor pointer");
@@ -261,7 +264,7 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
                        w->in_norm, w->w_qkv, w->q_norm, w->w_q_up, w->w_o, w->post_norm,
                        w->rms_eps, w->rope_theta, w->softmax_scale, a->x, a->k_cache, a->v_cache,
                        a->num_pages, a->block_table, a->max_pages, a->seq_lens, a->h_res, a->h_norm,
-                       k_scale, v_scale};
+                       k_scale, v_scale, mtp};
   void* ws = afdk::workspace(c, afdk::mfa_layer_workspace_bytes(m, c.num_sms));
   if (!ws) { set_error("afdk_mfa_layer: workspace allocation failed"); return AFDK_ERR_CUDA; }
   const cudaError_t e = afdk::mfa_layer_launch(c, m, ws, static_cast<cudaStream_t>(stream));
@@ -272,6 +275,14 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
 afdk_status afdk_mfa_layer(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
                            afdk_stream stream) {
   return mfa_layer_entry(ctx, w, a, 0.0f, 0.0f, stream);
+}
+
+afdk_status afdk_mfa_layer_mtp(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a, int mtp,
+                               afdk_stream stream) {
+  if (mtp == 1) return mfa_layer_entry(ctx, w, a, 0.0f, 0.0f, stream);
+  if (mtp != 2) { set_error("afdk_mfa_layer_mtp: mtp must be 1 or 2"); return AFDK_ERR_INVALID; }
+  if (a && a->batch > 128) { set_error("afdk_mfa_layer_mtp: batch must be <= 128"); return AFDK_ERR_INVALID; }
+  return mfa_layer_entry(ctx, w, a, 0.0f, 0.0f, stream, mtp);
 }
 
 afdk_status afdk_mfa_layer_fp8(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,

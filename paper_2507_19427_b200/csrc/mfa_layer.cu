@@ -107,6 +107,7 @@ struct QkvEpi {
   const int32_t* seq_lens;
   const double* inv_freq;       // [head_dim/2]
   float k_scale, v_scale;       // > 0: caches are e4m3, store e4m3(bf16(x) / scale)
+  int mtp;                      // row r = token r % mtp of request r / mtp, position seq_len - mtp + j
 };
 
 __device__ __forceinline__ uint8_t kv_e4m3(float x, float scale) {
@@ -156,9 +157,10 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
     *reinterpret_cast<uint2*>(e.qa + (size_t)row * e.q_lora + f) = o;
   }
   if (f1 <= e.q_lora) return;  // this CTA holds no k/v features
-  const int pos = __ldg(e.seq_lens + row) - 1;
+  const int req = row / e.mtp;
+  const int pos = __ldg(e.seq_lens + req) - e.mtp + row % e.mtp;
   if (pos < 0) return;
-  const int pg = __ldg(e.block_table + (size_t)row * e.max_pages + pos / e.page);
+  const int pg = __ldg(e.block_table + (size_t)req * e.max_pages + pos / e.page);
   const size_t kslot = ((size_t)pg * e.page + pos % e.page) * e.head_dim;
   const int half = e.head_dim / 2;
   const float* k = kv_s;
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
 // grid (B, ceil(n_out/8/blockDim)): each thread rotates 4 consecutive pairs.
 __global__ void __launch_bounds__(256) qup_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
                                                             int G, int n_out, int head_dim,
-                                                            const int32_t* __restrict__ seq_lens,
+                                                            const int32_t* __restrict__ seq_lens, int mtp,
                                                             const double* __restrict__ inv_freq,
                                                             __nv_bfloat16* __restrict__ q) {
   __shared__ lin::SlotTable tab;
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(256) qup_epilogue_kernel(const LinearPlan P, c
   lin::build_slot_table(P, G, tab);
   const int row = blockIdx.x;
   const int half = head_dim / 2;
-  const int pos = max(__ldg(seq_lens + row) - 1, 0);
+  const int pos = max(__ldg(seq_lens + row / mtp) - mtp + row % mtp, 0);
   // every head shares the row's rotation: one double-precision sincos per
   // frequency per CTA (seq_lens / inv_freq are inputs: before griddep_wait)
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
@@ -301,7 +303,7 @@ const double* rope_inv_freq(Ctx& ctx, int head_dim, float theta) {
 }
 
 size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms) {
-  const int B = a.batch, Hd = a.hidden, QL = a.q_lora, NQ = a.n_heads * a.head_dim;
+  const int B = a.batch * a.mtp, Hd = a.hidden, QL = a.q_lora, NQ = a.n_heads * a.head_dim;
   size_t b = 0;
   b += align_up((size_t)B * Hd * 2, 256);                       // xn
   b += align_up((size_t)B * QL * 2, 256);                       // qa
@@ -310,7 +312,7 @@ size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms) {
   size_t part = linear_workspace_bytes(make_linear_plan(B, QL + 2 * a.head_dim, Hd), num_sms);
   const size_t p2 = linear_workspace_bytes(make_linear_plan(B, NQ, QL), num_sms);
   const size_t p3 = linear_workspace_bytes(make_linear_plan(B, Hd, NQ), num_sms);
-  const size_t p4 = mfa_decode_workspace_bytes(B, num_sms);
+  const size_t p4 = a.mtp > 1 ? mfa_decode_mtp_workspace_bytes(a.batch, num_sms) : mfa_decode_workspace_bytes(B, num_sms);
   part = part > p2 ? part : p2;
   part = part > p3 ? part : p3;
   part = part > p4 ? part : p4;
@@ -319,7 +321,8 @@ size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms) {
 
 cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cudaStream_t stream) {
   using namespace layer;
-  const int B = a.batch, Hd = a.hidden, QL = a.q_lora, D = a.head_dim, NQ = a.n_heads * a.head_dim;
+  // B = token rows (requests x mtp) for norms, projections and epilogues
+  const int B = a.batch * a.mtp, Hd = a.hidden, QL = a.q_lora, D = a.head_dim, NQ = a.n_heads * a.head_dim;
   uint8_t* ws = static_cast<uint8_t*>(ws_base);
   auto take = [&](size_t bytes) { void* p = ws; ws += align_up(bytes, 256); return p; };
   auto* xn = static_cast<__nv_bfloat16*>(take((size_t)B * Hd * 2));
@@ -341,7 +344,8 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   if ((e = linear_bf16_launch(ctx, p1, xn, a.w_qkv, part, stream)) != cudaSuccess) return e;
   QkvEpi qe{QL, D, a.page_size, a.max_pages, p1.n_out, a.rms_eps,
             static_cast<const __nv_bfloat16*>(a.w_q_norm), qa, static_cast<__nv_bfloat16*>(a.k_cache),
-            static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq, a.k_scale, a.v_scale};
+            static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq, a.k_scale, a.v_scale,
+            a.mtp};
   if ((e = launch_cluster_k(ctx.pdl, kRowCluster, qkv_epilogue_kernel, dim3(B * kRowCluster), dim3(512), 0, stream,
                             p1, (const float*)part, linear_grid(ctx, p1), qe)) != cudaSuccess)
     return e;
@@ -349,12 +353,13 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   const LinearPlan p2 = make_linear_plan(B, NQ, QL);
   if ((e = linear_bf16_launch(ctx, p2, qa, a.w_q_up, part, stream)) != cudaSuccess) return e;
   if ((e = launch_k(ctx.pdl, qup_epilogue_kernel, dim3(B, (NQ / 8 + 255) / 256), dim3(256), 0, stream, p2,
-                    (const float*)part, linear_grid(ctx, p2), NQ, D, a.seq_lens, inv_freq, q)) != cudaSuccess)
+                    (const float*)part, linear_grid(ctx, p2), NQ, D, a.seq_lens, a.mtp, inv_freq, q)) != cudaSuccess)
     return e;
   // K2/K3: MFA decode core over the paged cache (now including this token)
-  MfaDecodeArgs md{B, q, a.k_cache, a.v_cache, a.num_pages, a.block_table, a.max_pages, a.seq_lens,
+  MfaDecodeArgs md{a.batch, q, a.k_cache, a.v_cache, a.num_pages, a.block_table, a.max_pages, a.seq_lens,
                    a.softmax_scale, attn, nullptr, part, a.k_scale, a.v_scale};
-  if ((e = (a.k_scale > 0.0f ? mfa_decode_fp8_launch(ctx, md, stream) : mfa_decode_launch(ctx, md, stream))) !=
+  if ((e = (a.mtp > 1 ? mfa_decode_mtp_launch(ctx, md, stream)
+            : a.k_scale > 0.0f ? mfa_decode_fp8_launch(ctx, md, stream) : mfa_decode_launch(ctx, md, stream))) !=
       cudaSuccess)
     return e;
   // K4: o_proj, then residual + post-attention RMSNorm

@@ -103,3 +103,36 @@ def test_mfa_layer_fp8_kv(ctx, dims, seq_lens, seed):
     for b, L in enumerate(sl):
         mask[bt[b, (L - 1) // page], (L - 1) % page] = False
     np.testing.assert_array_equal(gk[mask], rk[mask])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,seq_lens,seed", [(mg.SMALL, [70, 130, 2, 64, 65], 21), (STEP3, [300, 4096, 66], 8)])
+def test_mfa_layer_mtp2(ctx, dims, seq_lens, seed):
+    """MTP layer: 2 token rows per request, each appending its own K/V, causal
+    attention among the new tokens.  The oracle runs the same rows as
+    independent decode rows (seq_len L-1 and L, the request's pages)."""
+    import torch
+
+    x1, w, kc, vc, bt, sl = mg.layer_inputs(dims, seq_lens, seed)
+    rng = np.random.default_rng(seed + 1)
+    B = len(seq_lens)
+    x = orc.bf16_round(rng.standard_normal((2 * B, dims["hidden"])).astype(np.float32))
+    dev = torch.device("cuda:0")
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(dev)
+    wd = {k: bf(v) for k, v in w.items()}
+    kd, vd, xd = bf(kc), bf(vc), bf(x)
+    h_res, h_norm = torch.empty_like(xd), torch.empty_like(xd)
+    ctx.mfa_layer(wd, xd, kd, vd, torch.from_numpy(bt).to(dev), torch.from_numpy(sl).to(dev), h_res, h_norm, mtp=2)
+    torch.cuda.synchronize()
+    bt_rows = np.repeat(bt, 2, axis=0)
+    sl_rows = np.stack([sl - 1, sl], axis=1).reshape(-1).astype(np.int32)
+    k1, v1 = kc.copy(), vc.copy()
+    r_res, r_norm = orc.mfa_layer(dims, x, w, k1, v1, bt_rows, sl_rows)
+    assert rel_err(h_res.float().cpu().numpy(), r_res) <= 2e-2, rel_err(h_res.float().cpu().numpy(), r_res)
+    assert rel_err(h_norm.float().cpu().numpy(), r_norm) <= 2e-2, rel_err(h_norm.float().cpu().numpy(), r_norm)
+    gk = kd.float().cpu().numpy()
+    page = dims["page"]
+    for b, L in enumerate(sl):
+        for j, pos in enumerate((L - 2, L - 1)):
+            pg, s = bt[b, pos // page], pos % page
+            assert rel_err(gk[pg, s], k1[pg, s]) <= 1e-2, (b, j)

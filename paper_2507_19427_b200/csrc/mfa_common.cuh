@@ -32,7 +32,16 @@ struct Params {
   float scale_log2;            // softmax scale * log2(e)
   float k_scale, v_scale;      // e4m3 KV cache dequantisation scales (fp8 kernel)
   int rows;                    // query rows per request: 64 heads x mtp (0 = 64)
+  int* sync;                   // [2][kMaxBatch] zeroed counters: split parts published / K3 CTAs done
 };
+
+// A split part of request `req` is in memory: each of the 4 epilogue warps of
+// the K2 CTA publishes its share (K3 waits for 4 x parts arrivals).
+__device__ __forceinline__ void publish_part(int* sync, int req, int lane) {
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) atomicAdd(sync + req, 1);
+}
 
 // Contiguous page range of CTA c out of G over T total pages.
 __device__ __forceinline__ void cta_range(int c, int G, int T, int& lo, int& hi) {

@@ -387,6 +387,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.o_free);
+      if (!whole) publish_part(prm.sync, req, lane);  // after o_free: the fence must not hold up PV
       ++seg;
     }
   }
@@ -401,73 +402,127 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
 
 constexpr int kMaxSplit = 160;  // CTAs one request may span (>= #SMs + 1)
 // K3: merge the split partials of requests that spanned several CTAs (fixed
-// CTA order => deterministic), zero-fill empty requests.  grid (B, 16): 4
-// heads per CTA, 64 threads per head, 4 dims (one float4) per thread.
-__global__ void __launch_bounds__(256) mfa_combine_kernel(const Params prm, int G) {
+// CTA order => deterministic), zero-fill empty requests.  grid (B, R/16): 16
+// rows per CTA, 32 threads per row, 8 dims per thread.
+//
+// K3 does not wait for the whole of K2: its CTAs become resident under PDL
+// while K2 runs (every K2 CTA is resident by then, so spinning cannot starve
+// it) and each waits only for its own request's parts (K2's publish_part
+// counters), so merges overlap K2's tail.  The page prefix is recomputed from
+// seq_lens (a caller input) because K2's copy is not final yet.  Every CTA
+// ends with griddepcontrol.wait, so K3 completes only after K2 has, and the
+// next kernel sees the whole-request outputs K2 wrote directly.
+constexpr int kK3Rows = 16;     // query rows per K3 CTA
+constexpr int kK3Threads = 512;  // 32 threads per row, 8 dims (16 B of bf16) per thread
+__global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params prm, int G) {
   __shared__ int s_slot[kMaxSplit];
-  __shared__ float s_w[4][kMaxSplit];
+  __shared__ float s_w[kK3Rows][kMaxSplit];
   __shared__ int s_n;
-  griddep_wait();
+  __shared__ int s_red[2][kK3Threads / 32];
   griddep_launch();
   const int R = prm.rows > 0 ? prm.rows : kHeads;  // query rows per request
   const int req = blockIdx.x;
-  const int T = prm.prefix_out[prm.batch];
-  const int p0 = prm.prefix_out[req], p1 = prm.prefix_out[req + 1];
-  const int hl = threadIdx.x >> 6, head = blockIdx.y * 4 + hl;
-  const int d = (threadIdx.x & 63) * 4;
-  if (p1 <= p0) {
-    *reinterpret_cast<uint2*>(prm.out + ((size_t)req * R + head) * kDim + d) = make_uint2(0, 0);
-    if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * R + head] = -INFINITY;
-    return;
+  const int hl = threadIdx.x >> 5, head = blockIdx.y * kK3Rows + hl;
+  const int d = (threadIdx.x & 31) * 8;
+  {  // p0 = pages before this request, T = all pages
+    int before = 0, all = 0;
+    for (int i = threadIdx.x; i < prm.batch; i += blockDim.x) {
+      const int pg = (max(__ldg(prm.seq_lens + i), 0) + kPage - 1) / kPage;
+      all += pg;
+      if (i < req) before += pg;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(0xffffffff, before, o);
+      all += __shfl_xor_sync(0xffffffff, all, o);
+    }
+    if ((threadIdx.x & 31) == 0) { s_red[0][threadIdx.x >> 5] = before; s_red[1][threadIdx.x >> 5] = all; }
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    int c = (int)(((long long)p0 * G) / T);
-    while (c > 0 && (((long long)c * T) / G) > p0) --c;
-    while ((((long long)(c + 1) * T) / G) <= p0) ++c;
+    int p0 = 0, T = 0;
+    for (int w = 0; w < kK3Threads / 32; ++w) { p0 += s_red[0][w]; T += s_red[1][w]; }
+    const int p1 = p0 + (max(__ldg(prm.seq_lens + req), 0) + kPage - 1) / kPage;
     int n = 0;
-    for (; c < G && n < kMaxSplit; ++c) {
-      const int lo = (int)(((long long)c * T) / G), hi = (int)(((long long)(c + 1) * T) / G);
-      if (lo >= p1) break;
-      if (hi > lo) s_slot[n++] = req + c;
+    if (p1 > p0) {
+      int c = (int)(((long long)p0 * G) / T);
+      while (c > 0 && (((long long)c * T) / G) > p0) --c;
+      while ((((long long)(c + 1) * T) / G) <= p0) ++c;
+      for (; c < G && n < kMaxSplit; ++c) {
+        const int lo = (int)(((long long)c * T) / G), hi = (int)(((long long)(c + 1) * T) / G);
+        if (lo >= p1) break;
+        if (hi > lo) s_slot[n++] = req + c;
+      }
     }
     s_n = n;
+    if (n > 1) {  // wait until K2 has published all n parts (bounded: trap rather than hang)
+      const int target = 4 * n;
+      const int* cnt = prm.sync + req;
+      unsigned ns = 128;
+      long long spins = 0;
+      while (ld_acquire_gpu(cnt) < target) {
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+        if (++spins > (1ll << 24)) __trap();
+      }
+    }
   }
   __syncthreads();
   const int n = s_n;
-  if (n == 1) return;  // whole request: written by the main kernel
-  for (int i = threadIdx.x; i < 4 * n; i += blockDim.x)
-    s_w[i / n][i % n] = __ldcg(prm.part_lse + (size_t)s_slot[i % n] * R + blockIdx.y * 4 + i / n);
-  __syncthreads();
-  float m = -INFINITY;
-  for (int k = 0; k < n; ++k) m = fmaxf(m, s_w[hl][k]);
-  if (m == -INFINITY) {  // a causal MTP row that sees no token in any part
-    *reinterpret_cast<uint2*>(prm.out + ((size_t)req * R + head) * kDim + d) = make_uint2(0, 0);
-    if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * R + head] = -INFINITY;
-    return;
-  }
-  float wsum = 0.0f;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  __nv_bfloat16* out = prm.out + ((size_t)req * R + head) * kDim + d;
+  const bool lse_lane = prm.lse && (threadIdx.x & 31) == 0;
+  if (n == 0) {  // empty request
+    *reinterpret_cast<uint4*>(out) = make_uint4(0, 0, 0, 0);
+    if (lse_lane) prm.lse[(size_t)req * R + head] = -INFINITY;
+  } else if (n > 1) {
+    for (int i = threadIdx.x; i < kK3Rows * n; i += blockDim.x)
+      s_w[i / n][i % n] = __ldcg(prm.part_lse + (size_t)s_slot[i % n] * R + blockIdx.y * kK3Rows + i / n);
+    __syncthreads();
+    float m = -INFINITY;
+    for (int k = 0; k < n; ++k) m = fmaxf(m, s_w[hl][k]);
+    if (m == -INFINITY) {  // a causal MTP row that sees no token in any part
+      *reinterpret_cast<uint4*>(out) = make_uint4(0, 0, 0, 0);
+      if (lse_lane) prm.lse[(size_t)req * R + head] = -INFINITY;
+    } else {
+      float wsum = 0.0f;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
-  for (int k = 0; k < n; ++k) {
-    const float w = exp2f(s_w[hl][k] - m);
-    wsum += w;
+      for (int k = 0; k < n; ++k) {
+        const float w = exp2f(s_w[hl][k] - m);
+        wsum += w;
 #if AFDK_MFA_BF16_PART
-    const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(prm.part_o) +
-                                                            ((size_t)s_slot[k] * R + head) * kDim + d));
-    const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-    const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-    const float4 v = make_float4(v01.x, v01.y, v23.x, v23.y);
+        const uint4 raw = __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(prm.part_o) +
+                                                                ((size_t)s_slot[k] * R + head) * kDim + d));
+        const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[j]));
+          acc[2 * j] += w * f.x;
+          acc[2 * j + 1] += w * f.y;
+        }
 #else
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(prm.part_o + ((size_t)s_slot[k] * R + head) * kDim + d));
+        const float4* src = reinterpret_cast<const float4*>(prm.part_o + ((size_t)s_slot[k] * R + head) * kDim + d);
+        const float4 a = __ldcg(src), b = __ldcg(src + 1);
+        acc[0] += w * a.x; acc[1] += w * a.y; acc[2] += w * a.z; acc[3] += w * a.w;
+        acc[4] += w * b.x; acc[5] += w * b.y; acc[6] += w * b.z; acc[7] += w * b.w;
 #endif
-    acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+      }
+      const float inv = 1.0f / wsum;
+      uint4 o;
+      o.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+      o.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+      o.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+      o.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+      *reinterpret_cast<uint4*>(out) = o;
+      if (lse_lane) prm.lse[(size_t)req * R + head] = (m + __log2f(wsum)) * 0.69314718055994531f;
+    }
+    // the last of this request's gridDim.y CTAs re-arms both counters
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(prm.sync + kMaxBatch + req, 1) == (int)gridDim.y - 1) {
+      prm.sync[req] = 0;
+      prm.sync[kMaxBatch + req] = 0;
+    }
   }
-  const float inv = 1.0f / wsum;
-  uint2 o;
-  o.x = pack_bf16x2(acc.x * inv, acc.y * inv);
-  o.y = pack_bf16x2(acc.z * inv, acc.w * inv);
-  *reinterpret_cast<uint2*>(prm.out + ((size_t)req * R + head) * kDim + d) = o;
-  if (prm.lse && (threadIdx.x & 63) == 0) prm.lse[(size_t)req * R + head] = (m + __log2f(wsum)) * 0.69314718055994531f;
+  griddep_wait();
 }
 
 }  // namespace mfa
@@ -497,6 +552,7 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
   prm.part_lse = reinterpret_cast<float*>(ws);
   prm.out = static_cast<__nv_bfloat16*>(a.out);
   prm.lse = a.lse;
+  prm.sync = ctx.counters + kCounterSlots / 2;
   prm.batch = a.batch;
   prm.max_pages = a.max_pages;
   prm.scale_log2 = a.softmax_scale * 1.4426950408889634f;
@@ -532,7 +588,8 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
 
 cudaError_t mfa_combine_launch(bool pdl, const mfa::Params& prm, int G, cudaStream_t stream) {
   const int R = prm.rows > 0 ? prm.rows : mfa::kHeads;
-  return launch_k(pdl, mfa::mfa_combine_kernel, dim3(prm.batch, R / 4), dim3(256), 0, stream, prm, G);
+  return launch_k(pdl, mfa::mfa_combine_kernel, dim3(prm.batch, R / mfa::kK3Rows), dim3(mfa::kK3Threads), 0, stream,
+                  prm, G);
 }
 
 }  // namespace afdk

@@ -337,6 +337,7 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.o_free);
+      if (!whole) publish_part(prm.sync, req, lane);  // after o_free: the fence must not hold up PV
       ++seg;
     }
   }
@@ -375,6 +376,7 @@ cudaError_t mfa_decode_mtp_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t
   prm.part_lse = reinterpret_cast<float*>(ws);
   prm.out = static_cast<__nv_bfloat16*>(a.out);
   prm.lse = a.lse;
+  prm.sync = ctx.counters + kCounterSlots / 2;
   prm.batch = a.batch;
   prm.max_pages = a.max_pages;
   prm.scale_log2 = a.softmax_scale * 1.4426950408889634f;

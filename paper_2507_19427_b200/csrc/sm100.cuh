@@ -112,6 +112,13 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 
 // --------------------------------------------------------------------- TMA
+// acquire load of a flag/counter published with __threadfence + atomic by another CTA
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }

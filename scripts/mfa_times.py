@@ -1,0 +1,32 @@
+"""Per-CTA timeline of one MFA decode core launch (diagnostic build with
+-DAFDK_MFA_TIMES=1): python scripts/mfa_times.py [B ctx]; AFDK_LIB=libafdk_times.so"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import bench
+from paper_2507_19427_b200 import Context
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+L = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+ctx = Context(0)
+lib = ctypes.CDLL(os.environ["AFDK_LIB"])
+dev = torch.device("cuda:0")
+w = bench.make_workload_attn(torch, dev, B, L)
+s = torch.cuda.current_stream()
+for i in range(6):
+    k, v = w["kv"][i % 2]
+    ctx.mfa_decode_attention(w["q"], k, v, w["block_table"], w["seq_lens"], w["out"], 0.0625, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    buf = (ctypes.c_ulonglong * 1024)()
+    lib.afdk_debug_mfa_times(buf)
+    t = np.array(buf[:4 * 148], dtype=np.int64).reshape(148, 4)
+    t0 = t[:, 0].min()
+    t = (t - t0) / 1e3
+    if i >= 3:
+        q = lambda c: np.percentile(t[:, c], [0, 50, 100]).round(2).tolist()
+        print(f"start {q(0)} after-wait {q(1)} first-S {q(2)} end {q(3)}  (us; min/median/max over CTAs)")

@@ -17,13 +17,29 @@ constexpr int kPage = 64;  // tokens per KV page == one tile
 #define AFDK_MFA_BF16_PART 1
 #endif
 
-constexpr int kMaxBatch = 2048;  // prefix of pages per request lives in smem
+constexpr int kMaxBatch = 2048;  // prefix of work units per request lives in smem
+
+// Work split: request r is kSegCost + pages_r units (0 when empty), and CTA c
+// of G takes the contiguous unit range [cU/G, (c+1)U/G).  The kSegCost units
+// at the head of each request carry no page: they charge a CTA that starts a
+// new request segment for its extra Q load, O epilogue and split partial
+// (~2-3 pages of streaming time measured per extra segment), so CTAs that
+// straddle a request boundary get fewer pages and all CTAs end together.
+#ifndef AFDK_MFA_SEG_COST
+#define AFDK_MFA_SEG_COST 3
+#endif
+constexpr int kSegCost = AFDK_MFA_SEG_COST;
+
+__device__ __forceinline__ int request_pages(int seq_len) { return (max(seq_len, 0) + kPage - 1) / kPage; }
+__device__ __forceinline__ int request_units(int seq_len) {
+  const int pg = request_pages(seq_len);
+  return pg > 0 ? pg + kSegCost : 0;
+}
 
 
 struct Params {
   const int32_t* block_table;  // [B, max_pages]
   const int32_t* seq_lens;     // [B]
-  int32_t* prefix_out;         // [B+1] pages-per-request prefix, written by CTA 0 for K3
   __nv_bfloat16* out;          // [B, 64, 256]
   float* lse;                  // [B, 64] natural log, optional
   float* part_o;               // [(B+G), 64, 256] split partials (bf16 when AFDK_MFA_BF16_PART)
@@ -43,14 +59,14 @@ __device__ __forceinline__ void publish_part(int* sync, int req, int lane) {
   if (lane == 0) atomicAdd(sync + req, 1);
 }
 
-// Contiguous page range of CTA c out of G over T total pages.
+// Contiguous unit range of CTA c out of G over T total units.
 __device__ __forceinline__ void cta_range(int c, int G, int T, int& lo, int& hi) {
   lo = (int)(((long long)c * T) / G);
   hi = (int)(((long long)(c + 1) * T) / G);
 }
 
-// First request whose page range contains global page index `t` (prefix is
-// non-decreasing; empty requests are skipped because prefix[r+1] > t fails).
+// First request whose unit range contains unit `t` (prefix is non-decreasing;
+// empty requests are skipped because prefix[r+1] > t fails).
 __device__ __forceinline__ int find_request(const int32_t* prefix, int B, int t) {
   int lo = 0, hi = B - 1;
   while (lo < hi) {
@@ -60,7 +76,7 @@ __device__ __forceinline__ int find_request(const int32_t* prefix, int B, int t)
   return lo;
 }
 
-// Walks the segments (request, [lo,hi) local pages) of one CTA in order.
+// Walks the segments (request, [lo,hi) local pages) of one CTA's unit range in order.
 struct SegmentWalker {
   const int32_t* prefix;
   int B, end, r, pos;
@@ -70,20 +86,25 @@ struct SegmentWalker {
   }
   // returns false when the range is exhausted
   __device__ bool next(int& req, int& lo, int& hi, bool& whole) {
-    if (pos >= end) return false;
-    while (prefix[r + 1] <= pos) ++r;
-    const int p0 = prefix[r], p1 = prefix[r + 1];
-    const int seg_hi = p1 < end ? p1 : end;
-    req = r;
-    lo = pos - p0;
-    hi = seg_hi - p0;
-    whole = (pos == p0) && (seg_hi == p1);
-    pos = seg_hi;
-    return true;
+    while (pos < end) {
+      while (prefix[r + 1] <= pos) ++r;
+      const int p0 = prefix[r] + kSegCost, p1 = prefix[r + 1];  // the request's page units
+      const int a = pos > p0 ? pos : p0;
+      const int b = p1 < end ? p1 : end;
+      pos = b;
+      if (a < b) {
+        req = r;
+        lo = a - p0;
+        hi = b - p0;
+        whole = (a == p0) && (b == p1);
+        return true;
+      }
+    }
+    return false;
   }
 };
 
-// pages per request -> exclusive prefix in smem (every CTA; B <= kMaxBatch).
+// work units per request -> exclusive prefix in smem (every CTA; B <= kMaxBatch).
 // seq_lens is a caller input (no kernel of this library writes it), so this
 // may run before griddepcontrol.wait.
 template <int kThreads>
@@ -95,7 +116,7 @@ __device__ __forceinline__ void build_page_prefix(int32_t* prefix, const int32_t
   if (threadIdx.x == 0) { s_carry = 0; prefix[0] = 0; }
   for (int base = 0; base < batch; base += kThreads) {
     const int i = base + threadIdx.x;
-    const int v = (i < batch) ? (max(__ldg(seq_lens + i), 0) + kPage - 1) / kPage : 0;
+    const int v = (i < batch) ? request_units(__ldg(seq_lens + i)) : 0;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -50,16 +50,12 @@ constexpr int kChunkBytes = 64 * 128;         // one 64-row x 128B swizzle panel
 #ifndef AFDK_MFA_NV
 #define AFDK_MFA_NV 3
 #endif
-#ifndef AFDK_MFA_PREFETCH
-#define AFDK_MFA_PREFETCH 0
-#endif
 constexpr int kNK = AFDK_MFA_NK;              // K ring depth
 constexpr int kNV = AFDK_MFA_NV;              // V ring depth
 constexpr int kThreads = 256;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColO = 0, kColS = 256;    // O: 256 cols, S: 2 x 64 cols
 constexpr float kRescaleThresh = 8.0f;        // lazy O rescale (log2 units)
-constexpr int kPrefetch = AFDK_MFA_PREFETCH;  // pages prefetched into L2 ahead of the rings (0: off)
 
 struct __align__(1024) Smem {
   uint8_t q[4 * kChunkBytes];       // 32 KB  Q of the current request
@@ -116,8 +112,6 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   const uint32_t tmem = sm.tmem_base;
   griddep_wait();  // q, the appended K/V row and the reused workspace belong to the predecessors
   griddep_launch();
-  if (cta == 0)
-    for (int i = threadIdx.x; i <= prm.batch; i += kThreads) prm.prefix_out[i] = prefix[i];
 
   if (warp == 0) {
     // ------------------------------------------------ Q + K TMA producer
@@ -125,20 +119,6 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
       SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
-      // L2 prefetch kPrefetch pages ahead of the smem rings (K and V): more
-      // bytes in flight per SM than the 5 x 32 KB of smem slots allow
-      int pf_pos = range_lo, pf_r = (range_lo < range_hi) ? find_request(prefix, prm.batch, range_lo) : 0;
-      auto prefetch_next = [&]() {
-        if (pf_pos >= range_hi) return;
-        while (prefix[pf_r + 1] <= pf_pos) ++pf_r;
-        const int pg = __ldg(prm.block_table + (size_t)pf_r * prm.max_pages + (pf_pos - prefix[pf_r]));
-        for (int c = 0; c < 4; ++c) {
-          tma_prefetch_l2_3d(&tm_k, c * 64, 0, pg);
-          tma_prefetch_l2_3d(&tm_v, c * 64, 0, pg);
-        }
-        ++pf_pos;
-      };
-      for (int i = 0; i < kPrefetch; ++i) prefetch_next();
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -147,7 +127,6 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
         for (int c = 0; c < 4; ++c)
           tma_load_2d(sm.q + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, req * kHeads, pol_keep);
         for (int t = lo; t < hi; ++t, ++g) {
-          prefetch_next();
           const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
           const int s = g % kNK, n = g / kNK;
           if (n > 0) mbar_wait(&sm.k_empty[s], (n & 1) ^ 1);
@@ -424,10 +403,10 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
   const int req = blockIdx.x;
   const int hl = threadIdx.x >> 5, head = blockIdx.y * kK3Rows + hl;
   const int d = (threadIdx.x & 31) * 8;
-  {  // p0 = pages before this request, T = all pages
+  {  // p0 = units before this request, T = all units
     int before = 0, all = 0;
     for (int i = threadIdx.x; i < prm.batch; i += blockDim.x) {
-      const int pg = (max(__ldg(prm.seq_lens + i), 0) + kPage - 1) / kPage;
+      const int pg = request_units(__ldg(prm.seq_lens + i));
       all += pg;
       if (i < req) before += pg;
     }
@@ -441,7 +420,8 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
   if (threadIdx.x == 0) {
     int p0 = 0, T = 0;
     for (int w = 0; w < kK3Threads / 32; ++w) { p0 += s_red[0][w]; T += s_red[1][w]; }
-    const int p1 = p0 + (max(__ldg(prm.seq_lens + req), 0) + kPage - 1) / kPage;
+    const int p1 = p0 + request_units(__ldg(prm.seq_lens + req));
+    p0 += kSegCost;  // the request's page units: [p0, p1)
     int n = 0;
     if (p1 > p0) {
       int c = (int)(((long long)p0 * G) / T);
@@ -544,7 +524,6 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
   Params prm{};
   prm.block_table = a.block_table;
   prm.seq_lens = a.seq_lens;
-  prm.prefix_out = reinterpret_cast<int32_t*>(ws);
   ws += align_up((size_t)(a.batch + 1) * sizeof(int32_t), 256);
   const size_t slots = (size_t)a.batch + G;
   prm.part_o = reinterpret_cast<float*>(ws);

@@ -96,8 +96,6 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   const uint32_t tmem = sm.tmem_base;
   griddep_wait();
   griddep_launch();
-  if (cta == 0)
-    for (int i = threadIdx.x; i <= prm.batch; i += kThreadsM) prm.prefix_out[i] = prefix[i];
 
   if (warp == 0) {
     // ------------------------------------------------ Q + K TMA producer
@@ -368,7 +366,6 @@ cudaError_t mfa_decode_mtp_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t
   Params prm{};
   prm.block_table = a.block_table;
   prm.seq_lens = a.seq_lens;
-  prm.prefix_out = reinterpret_cast<int32_t*>(ws);
   ws += align_up((size_t)(a.batch + 1) * sizeof(int32_t), 256);
   const size_t slots = (size_t)a.batch + G;
   prm.part_o = reinterpret_cast<float*>(ws);

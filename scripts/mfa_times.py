@@ -29,4 +29,18 @@ for i in range(6):
     t = (t - t0) / 1e3
     if i >= 3:
         q = lambda c: np.percentile(t[:, c], [0, 50, 100]).round(2).tolist()
-        print(f"start {q(0)} after-wait {q(1)} first-S {q(2)} end {q(3)}  (us; min/median/max over CTAs)")
+        print(f"start {q(0)} first-S {q(1)} last-PV {q(2)} end {q(3)}  (us; min/median/max over CTAs)")
+        pages = (w["seq_lens"].cpu().numpy() + 63) // 64
+        pre = np.concatenate([[0], np.cumsum(pages)])
+        T, G = pre[-1], 148
+        segs = []
+        for c in range(G):
+            lo, hi = c * T // G, (c + 1) * T // G
+            segs.append(int(((pre[1:] > lo) & (pre[:-1] < hi)).sum()))
+        segs = np.array(segs)
+        for k in sorted(set(segs.tolist())):
+            m = segs == k
+            print(f"  {k} segments: {m.sum()} CTAs, end median {np.median(t[m, 3]):.2f} max {t[m, 3].max():.2f}, "
+                  f"first-S median {np.median(t[m, 1]):.2f}")
+        slow = np.argsort(t[:, 3])[-8:]
+        print("  slowest CTAs:", slow.tolist(), "SM-order ends:", t[slow, 3].round(1).tolist())

@@ -202,11 +202,15 @@ struct MoeGemmMxArgs {
   uint8_t* hq;           // W13 outputs [rows_pad, I] + [rows_pad, I/32]
   uint8_t* hsf;
   float* y;              // W2 output [rows_pad, H]
+  int chunk = 0;         // rows per work item (pair kernels: > 256 selects the two-accumulator form)
 };
 cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream);
 cudaError_t moe_gemm_mx2_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream);
 // CTA-pair kernels once experts see enough rows (AFDK_MX_PAIR=0/1 forces)
 bool moe_mx_use_pair(int T, int k, int E);
+// rows per pair work item: 384 (two accumulators) when routed experts average
+// 200-352 rows, else 256 (AFDK_MX_CHUNK=256/384 forces)
+int moe_mx_pair_chunk(int T, int k, int E);
 struct MoeFfnMxArgs {
   int T, k, E, H, I;
   int expert_lo, expert_hi;

@@ -12,6 +12,7 @@ constexpr int kMaxTopK = 8;      // Step-3: 3
 constexpr int kChunk = 64;       // dispatched rows per GEMM work item (MMA N <= 64)
 constexpr int kChunkMX = 128;    // rows per work item of the MXFP8 (block-scaled MMA) GEMMs
 constexpr int kChunkMX2 = 256;   // rows per work item of the CTA-pair MXFP8 GEMMs
+constexpr int kChunkMX2Two = 384;  // ... in their two-accumulator form
 
 struct RouterArgs {
   const __nv_bfloat16* h;       // [T, H] post-attention RMSNorm output

@@ -93,6 +93,12 @@ bool moe_mx_use_pair(int T, int k, int E) {
   return (long)T * k >= 64L * E;  // >= 64 rows per routed expert on average
 }
 
+int moe_mx_pair_chunk(int T, int k, int E) {
+  if (const char* env = std::getenv("AFDK_MX_CHUNK")) return std::atoi(env) > moe::kChunkMX2 ? moe::kChunkMX2Two : moe::kChunkMX2;
+  const long avg = (long)T * k / E;
+  return (avg > 200 && avg <= 352) ? moe::kChunkMX2Two : moe::kChunkMX2;
+}
+
 cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cudaStream_t stream) {
   const int T = a.T, k = a.k, E = a.E, H = a.H, I = a.I;
   const int rp = moe::rows_pad_mx(T, k);
@@ -110,6 +116,7 @@ cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cu
   auto* y = static_cast<float*>(take((size_t)rp * H * 4));
   const bool shared_local = a.shared_hi > a.shared_lo;
   const bool pair = moe_mx_use_pair(T, k, E);
+  const int chunk = pair ? moe_mx_pair_chunk(T, k, E) : moe::kChunkMX;
   auto gemm = pair ? moe_gemm_mx2_launch : moe_gemm_mx_launch;
   cudaError_t e;
   static const bool dbg = std::getenv("AFDK_DEBUG_SYNC") != nullptr;
@@ -119,14 +126,15 @@ cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cu
     return err;
   };
   moe::PermuteArgs pa{a.ids, T, k, E, a.expert_lo, a.expert_hi, shared_local ? 1 : 0, a.shared_lo, a.shared_hi,
-                      offsets, perm, inv, work, n_work, pair ? moe::kChunkMX2 : moe::kChunkMX};
+                      offsets, perm, inv, work, n_work, chunk};
   if ((e = chk(permute_launch(pa, stream, ctx.pdl), "permute")) != cudaSuccess) return e;
   moe::GatherArgs ga{a.xq, nullptr, perm, T, k, H, rp, xp, nullptr, a.xsf, xsf_p};
   if ((e = chk(gather_launch(ga, stream, ctx.pdl), "gather")) != cudaSuccess) return e;
   const int n_local = a.expert_hi - a.expert_lo;
-  MoeGemmMxArgs g13{a.w13, a.sf13, xp, xsf_p, work, n_work, H, I, E, a.expert_lo, n_local, rp, hq, hsf, nullptr};
+  MoeGemmMxArgs g13{a.w13, a.sf13, xp, xsf_p, work, n_work, H, I, E, a.expert_lo, n_local, rp, hq, hsf, nullptr,
+                    chunk};
   if ((e = chk(gemm(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
-  MoeGemmMxArgs g2{a.w2, a.sf2, hq, hsf, work, n_work, H, I, E, a.expert_lo, n_local, rp, nullptr, nullptr, y};
+  MoeGemmMxArgs g2{a.w2, a.sf2, hq, hsf, work, n_work, H, I, E, a.expert_lo, n_local, rp, nullptr, nullptr, y, chunk};
   if ((e = chk(gemm(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
   moe::CombineArgs ca{y, a.ids, a.weights, inv, T, k, H, a.expert_lo, a.expert_hi, shared_local ? 1 : 0,
                       a.shared_lo, a.shared_hi, static_cast<__nv_bfloat16*>(a.out), a.dst, a.rows_per_dst};

@@ -10,15 +10,21 @@
 // k-block is now 32 KB per 8.4 MFLOP, and an expert with <= 256 rows fetches
 // its weights once per item instead of once per 128-row chunk.
 //
-// Item = (256-row dispatch chunk, pair m-tile).
+// Item = (dispatch chunk, pair m-tile).  Chunks are 256 rows, or 384 rows in
+// the two-accumulator form (kTwo, chosen when routed experts average 200-352
+// rows): one MMA covers at most N=256 tokens, so a chunk's first 256 rows
+// accumulate in TMEM columns [0,256) and the rest (<= 128) in [384,512) from
+// a second B panel; both MMAs of a k-step read the same weight panel, so an
+// expert with 257-384 rows streams its weights once instead of twice.  kTwo
+// costs one pipeline stage (40 KB stages), so it is not used elsewhere.
 //   W13: the pair covers 128 intermediate features; CTA r stages gate rows
 //        [f0+64r, +64) and the matching up rows as one 128-row A panel, so
 //        TMEM lanes 0-63 hold gate and 64-127 hold up for the same features;
 //        the epilogue parks both in smem, and each thread applies SiLU(gate)*up
 //        to one (token, 32-feature block) and re-quantises it to MXFP8.
 //   W2:  the pair covers 256 output features, 128 per CTA.
-// Scale factors: SFA = the CTA's own 128 rows (4 TMEM columns), SFB = all N
-// tokens replicated in both CTAs (8 columns), written per stage by four stager
+// Scale factors: SFA = the CTA's own 128 rows (4 TMEM columns), SFB = all
+// tokens replicated in both CTAs (8 + 4 columns), written per stage by four stager
 // warps per CTA from TMA-loaded smem groups (see moe_gemm_mx.cu for the TMEM
 // scale layout).
 //
@@ -45,11 +51,20 @@ using namespace sm100;
 
 constexpr int kPairThreads = 448;  // w0 TMA, w1 MMA (leader) + TMEM, w2-5 + w10-13 epilogue, w6-9 scale stagers
 constexpr uint32_t kPSfCol0 = 256;
-constexpr int kPSfCols = 4 + 8;    // SFA 4 + SFB 8 columns per stage
-constexpr int kPStage = 32768;     // A 16 KB + B 16 KB
-constexpr int kPSfGrp = 2048 + 4096;  // SFA 128 rows x 16 B + SFB 256 rows x 16 B
-constexpr int kPStages = 5;        // W13 (the epilogue exchange takes 35 KB of smem)
-constexpr int kPStagesW2 = 6;
+constexpr uint32_t kPAcc1Col = 384;     // kTwo: second accumulator, chunk rows 256..383
+// per form: SF columns per stage (SFA 4 + SFB 8 [+ SFB1 4]), stage bytes
+// (A 16 KB + B 16 KB [+ B1 8 KB]), scale-group bytes, stages (W13 / W2; the
+// W13 epilogue exchange takes 35 KB of smem)
+template <bool kTwo> struct PairCfg {
+  static constexpr int kSfCols = kTwo ? 16 : 12;
+  static constexpr int kStage = kTwo ? 40960 : 32768;
+  static constexpr int kSfGrp = kTwo ? 2048 + 4096 + 2048 : 2048 + 4096;
+  static constexpr int kStagesW13 = kTwo ? 4 : 5;
+  static constexpr int kStagesW2 = kTwo ? 5 : 6;
+};
+static_assert(kPSfCol0 + PairCfg<true>::kStagesW2 * PairCfg<true>::kSfCols <= kPAcc1Col,
+              "TMEM scale ring overlaps the second accumulator");
+static_assert(kChunkMX2Two <= 384, "two accumulators cover at most 384 rows");
 constexpr int kXRow = 68;          // padded smem row (floats) of the W13 epilogue exchange
 
 struct Mx2Params {
@@ -74,18 +89,25 @@ __device__ __forceinline__ int mx2_exp(float amax) {
   return max(-127, min(127, e));
 }
 
+// TMEM column of chunk row t (t % 32 == 0): rows 0-255 in the first
+// accumulator, 256-383 in the second
+__device__ __forceinline__ uint32_t acc_col(int t) { return t < 256 ? (uint32_t)t : kPAcc1Col + (uint32_t)(t - 256); }
+
 __device__ __forceinline__ void pair_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <bool kGLU>
+template <bool kGLU, bool kTwo>
 __global__ void __launch_bounds__(kPairThreads, 1)
 moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                    const __grid_constant__ CUtensorMap tm_wsf, const __grid_constant__ CUtensorMap tm_xsf,
+                    const __grid_constant__ CUtensorMap tm_x1, const __grid_constant__ CUtensorMap tm_wsf,
+                    const __grid_constant__ CUtensorMap tm_xsf, const __grid_constant__ CUtensorMap tm_xsf1,
                     const Mx2Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int S = kGLU ? kPStages : kPStagesW2;
+  using Cfg = PairCfg<kTwo>;
+  constexpr int S = kGLU ? Cfg::kStagesW13 : Cfg::kStagesW2;
+  constexpr int kPStage = Cfg::kStage, kPSfGrp = Cfg::kSfGrp, kPSfCols = Cfg::kSfCols;
   uint8_t* sfbuf = smem + S * kPStage;
   float* xchg = reinterpret_cast<float*>(sfbuf + 2 * kPSfGrp);  // W13: gate, up [64 tokens][kXRow]
   uint64_t* full = reinterpret_cast<uint64_t*>(xchg + (kGLU ? 2 * 64 * kXRow : 0));
@@ -104,8 +126,10 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_x1);
     tma_prefetch_desc(&tm_wsf);
     tma_prefetch_desc(&tm_xsf);
+    tma_prefetch_desc(&tm_xsf1);
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&sf_full[i], 8); mbar_init(&empty[i], 1); }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 16);
@@ -131,7 +155,8 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
         const ItemRef ir = item_of(p.work, it, p.m_tiles);
         const int mt = ir.mt;
         const Work wk = p.work[ir.chunk];
-        const int half = ((wk.rows + 31) & ~31) >> 1;
+        const int n0 = min((wk.rows + 31) & ~31, 256), n1 = kTwo ? max(((wk.rows + 31) & ~31) - 256, 0) : 0;
+        const int half = n0 >> 1, half1 = n1 >> 1;
         const int widx = (wk.group == p.E ? p.n_local : wk.group - p.expert_lo) * p.w_rows;
         const int arow = kGLU ? widx + mt * 128 + 64 * (int)rank : widx + mt * 256 + 128 * (int)rank;
         const int in_row0 = kGLU ? wk.xrow0 : wk.row0;  // W13 reads the token rows, W2 the intermediate
@@ -142,19 +167,21 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
             ++gi;
             if (ng > 0) mbar_wait(&sfg_empty[g], (ng & 1) ^ 1);
             uint8_t* dst = sfbuf + g * kPSfGrp;
-            mbar_expect_tx(&sfg_full[g], kPSfGrp);
+            mbar_expect_tx(&sfg_full[g], 2048 + 4096 + (n1 ? 2048 : 0));  // SFA + SFB [+ SFB1]
             tma_load_2d(dst, &tm_wsf, &sfg_full[g], kb * 4, arow, pol);
             if (kGLU) tma_load_2d(dst + 1024, &tm_wsf, &sfg_full[g], kb * 4, arow + p.up_offset, pol);
             tma_load_2d(dst + 2048, &tm_xsf, &sfg_full[g], kb * 4, in_row0, pol);
+            if (n1) tma_load_2d(dst + 6144, &tm_xsf1, &sfg_full[g], kb * 4, in_row0 + 256, pol);
           }
           const int s = i % S, n = i / S;
           if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
           uint8_t* st = smem + s * kPStage;
-          if (rank == 0) mbar_expect_tx(&full[s], 2 * kPStage);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * (32768 + (n1 ? 8192 : 0)));  // A + B [+ B1], both CTAs
           const uint32_t fb = full_l + 8u * s;
           tma_load_2d_pair(st, &tm_w, fb, kb * 128, arow, pol);
           if (kGLU) tma_load_2d_pair(st + 8192, &tm_w, fb, kb * 128, arow + p.up_offset, pol);
           tma_load_2d_pair(st + 16384, &tm_x, fb, kb * 128, brow, pol);
+          if (n1) tma_load_2d_pair(st + 32768, &tm_x1, fb, kb * 128, in_row0 + 256 + (int)rank * half1, pol);
         }
       }
     }
@@ -169,8 +196,9 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
 #endif
       for (int it = pair; it < n_items; it += n_pairs, ++li) {
         const Work wk = p.work[item_of(p.work, it, p.m_tiles).chunk];
-        const uint32_t N = (uint32_t)((wk.rows + 31) & ~31);
-        const uint32_t idesc = idesc_mxf8(256, N);
+        const uint32_t npad = (uint32_t)((wk.rows + 31) & ~31);
+        const uint32_t n0 = npad < 256u ? npad : 256u, n1 = (kTwo && npad > 256u) ? npad - 256u : 0u;
+        const uint32_t idesc = idesc_mxf8(256, n0), idesc1 = idesc_mxf8(256, n1 ? n1 : 32u);
 #ifdef AFDK_MX2_PROF
         t0 = clock64();
 #endif
@@ -196,6 +224,11 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
             const uint32_t sel = (uint32_t)kk << 30;
             mma_mxf8_pair(tmem, da, db, idesc | idesc_sf_ids(kk, kk), sf | sel, (sf + 4) | sel,
                           (kb > 0 || kk > 0) ? 1u : 0u);
+            if (n1) {
+              const uint64_t db1 = sdesc_sw128(base + 32768 + kk * 32, 0, 1024);
+              mma_mxf8_pair(tmem + kPAcc1Col, da, db1, idesc1 | idesc_sf_ids(kk, kk), sf | sel, (sf + 12) | sel,
+                            (kb > 0 || kk > 0) ? 1u : 0u);
+            }
           }
           mma_commit_pair(&empty[s], 0x3);
           if (kb == p.kblocks - 1) mma_commit_pair(acc_full, 0x3);
@@ -225,6 +258,7 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
         tmem_st4(col, ga[0], ga[128], ga[256], ga[384]);
         tmem_st4(col + 4, gb[0], gb[128], gb[256], gb[384]);
         tmem_st4(col + 8, gb[512], gb[640], gb[768], gb[896]);
+        if (kTwo) tmem_st4(col + 12, gb[1024], gb[1152], gb[1280], gb[1408]);  // rows 256-383 (stale when unused)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -261,7 +295,7 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
         for (int g0 = 0; g0 < n_chunks * 32; g0 += 64) {
           if (g0 + ehalf * 32 < n_chunks * 32) {
             uint32_t v[32];
-            tmem_ld32(t_lane + g0 + ehalf * 32, v);
+            tmem_ld32(t_lane + acc_col(g0 + ehalf * 32), v);
             tmem_wait_ld();
             float* dst = (sub < 2 ? xg : xu) + (ehalf * 32) * kXRow + (sub & 1) * 32 + lane;
 #pragma unroll
@@ -308,7 +342,7 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
       } else {
         for (int c = ehalf; c < n_chunks; c += 2) {
           uint32_t v[32];
-          tmem_ld32(t_lane + c * 32, v);
+          tmem_ld32(t_lane + acc_col(c * 32), v);
           tmem_wait_ld();
           const int feat = mt * 256 + 128 * (int)rank + sub * 32 + lane;
 #pragma unroll
@@ -339,7 +373,7 @@ cudaError_t moe_gemm_mx2_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cuda
   const int K = glu ? a.H : a.I;
   const int w_rows = glu ? 2 * a.I : a.H;
   const uint64_t wr = (uint64_t)(a.n_local + 1) * w_rows;
-  CUtensorMap tw, tx, twsf, txsf;
+  CUtensorMap tw, tx, tx1, twsf, txsf, txsf1;
   auto enc = [&](CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint32_t bi, uint32_t br,
                  CUtensorMapSwizzle sw) {
     const uint64_t dims[2] = {inner, rows};
@@ -349,8 +383,10 @@ cudaError_t moe_gemm_mx2_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cuda
   };
   if (!enc(&tw, a.w, K, wr, 128, glu ? 64 : 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !enc(&tx, a.x, K, a.rows_pad, 128, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !enc(&tx1, a.x, K, a.rows_pad, 128, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !enc(&twsf, a.w_sf, K / 32, wr, 16, glu ? 64 : 128, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !enc(&txsf, a.x_sf, K / 32, a.rows_pad, 16, 256, CU_TENSOR_MAP_SWIZZLE_NONE))
+      !enc(&txsf, a.x_sf, K / 32, a.rows_pad, 16, 256, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !enc(&txsf1, a.x_sf, K / 32, a.rows_pad, 16, 128, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   Mx2Params p{};
   p.work = a.work;
@@ -366,18 +402,20 @@ cudaError_t moe_gemm_mx2_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cuda
   p.hq = a.hq;
   p.hsf = a.hsf;
   p.y = a.y;
-  const size_t smem = (size_t)(glu ? kPStages : kPStagesW2) * kPStage + 2 * kPSfGrp + (glu ? 2 * 64 * kXRow * 4 : 0) +
-                      1024 + 512;
   const int grid = (ctx.num_sms / 2) * 2;
-  cudaError_t e;
-  if (glu) {
-    if ((e = ensure_smem(moe_gemm_mx2_kernel<true>, smem)) != cudaSuccess) return e;
-    return launch_cluster_k(ctx.pdl, 2, moe_gemm_mx2_kernel<true>, dim3(grid), dim3(kPairThreads), smem, stream, tw,
-                            tx, twsf, txsf, p);
-  }
-  if ((e = ensure_smem(moe_gemm_mx2_kernel<false>, smem)) != cudaSuccess) return e;
-  return launch_cluster_k(ctx.pdl, 2, moe_gemm_mx2_kernel<false>, dim3(grid), dim3(kPairThreads), smem, stream, tw,
-                          tx, twsf, txsf, p);
+  auto go = [&](auto kernel, auto cfg) {
+    using Cfg = decltype(cfg);
+    const size_t smem = (size_t)(glu ? Cfg::kStagesW13 : Cfg::kStagesW2) * Cfg::kStage + 2 * Cfg::kSfGrp +
+                        (glu ? 2 * 64 * kXRow * 4 : 0) + 1024 + 512;
+    if (const cudaError_t e = ensure_smem(kernel, smem); e != cudaSuccess) return e;
+    return launch_cluster_k(ctx.pdl, 2, kernel, dim3(grid), dim3(kPairThreads), smem, stream, tw, tx, tx1, twsf, txsf,
+                            txsf1, p);
+  };
+  const bool two = a.chunk > kChunkMX2;
+  if (glu) return two ? go(moe_gemm_mx2_kernel<true, true>, PairCfg<true>{})
+                      : go(moe_gemm_mx2_kernel<true, false>, PairCfg<false>{});
+  return two ? go(moe_gemm_mx2_kernel<false, true>, PairCfg<true>{})
+             : go(moe_gemm_mx2_kernel<false, false>, PairCfg<false>{});
 }
 
 }  // namespace afdk

@@ -79,7 +79,7 @@ def run_moe_mx(ctx, T, H, I, E, k, seed, ranges=None):
     return got, ref
 
 
-# "0": single-CTA kernels (128-row items), "1": CTA-pair kernels (256-row items)
+# "0": single-CTA kernels (128-row items), "1": CTA-pair kernels (items of up to 384 rows)
 KERNELS = ["0", "1"]
 
 
@@ -100,6 +100,14 @@ def test_moe_ffn_mx_small(ctx, mx_kernel):
 def test_moe_ffn_mx_many_rows_per_expert(ctx, mx_kernel):
     """> 256 rows for one expert (several work chunks) and a ragged last chunk."""
     got, ref = run_moe_mx(ctx, 300, 512, 1024, 4, 2, 3)
+    assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
+
+
+@pytest.mark.gpu
+def test_moe_ffn_mx_two_accumulator_chunks(ctx, mx_kernel):
+    """~350 rows per routed expert and 700 shared rows: pair items of 257-384
+    rows use the second TMEM accumulator; 700 = 384 + 316 splits the shared expert."""
+    got, ref = run_moe_mx(ctx, 700, 512, 1024, 4, 2, 6)
     assert rel_err(got, ref) <= 1e-2, rel_err(got, ref)
 
 

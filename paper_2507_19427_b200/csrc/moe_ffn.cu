@@ -90,7 +90,9 @@ bool moe_mx_use_pair(int T, int k, int E) {
   const char* env = std::getenv("AFDK_MX_PAIR");
   if (env && env[0] == '0') return false;
   if (env && env[0] == '1') return true;
-  return (long)T * k >= 64L * E;  // >= 64 rows per routed expert on average
+  // >= 32 rows per routed expert on average (Step-3, MoE layer ms single / pair:
+  // T=384 1.052 / 1.070, T=512 1.134 / 1.063, T=1024 1.356 / 1.169)
+  return (long)T * k >= 32L * E;
 }
 
 int moe_mx_pair_chunk(int T, int k, int E) {

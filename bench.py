@@ -76,6 +76,25 @@ def fp8_peak(fmt):
     return 2 * bf16, f"fp8 = 2 x {kind} bf16 cuBLAS"
 
 
+def fp8_peak_sustained(fmt):
+    """The same library GEMM run back to back for 4 s (power-limited clocks):
+    the denominator for kernels that run inside long steps (None if unmeasured)."""
+    path = os.path.join(ROOT, "profiles", "r01_fp8_peaks.json")
+    key = "mxfp8" if fmt == "mx" else "fp8_tensorwise"
+    if os.path.exists(path):
+        return json.load(open(path)).get(key, {}).get("sustained_tflops")
+    return None
+
+
+def tensor_roofline(flops, ms, fmt, bf16_peak):
+    tf = flops / (ms * 1e-3) / 1e12
+    peak, kind = fp8_peak(fmt)
+    sus = fp8_peak_sustained(fmt)
+    return {"achieved": tf, "unit": "TFLOP/s", "peak": peak, "peak_kind": kind, "frac": tf / peak,
+            "peak_sustained": sus, "frac_of_sustained": tf / sus if sus else None,
+            "frac_of_2x_bf16": tf / (2 * bf16_peak)}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -337,10 +356,7 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=No
             "hbm": {"achieved": wbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": wbytes / (ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": wbytes,
                     "experts_touched": touched},
-            "tensor": {"achieved": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                       "peak": fp8_peak(fmt)[0], "peak_kind": fp8_peak(fmt)[1],
-                       "frac": flops / (ms * 1e-3) / 1e12 / fp8_peak(fmt)[0],
-                       "frac_of_2x_bf16": flops / (ms * 1e-3) / 1e12 / (2 * tf_peak)},
+            "tensor": tensor_roofline(flops, ms, fmt, tf_peak),
             "gpu_launches_per_layer": 5}
 
 
@@ -380,10 +396,7 @@ def run_dense_bench(ctx, torch, dev, T, n_split, steps, warmup):
     return {"T": T, "n_split": n_split, "format": "mxfp8", "ms_per_layer": ms, "tokens_per_s": T / (ms * 1e-3),
             "hbm": {"achieved": wbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": wbytes / (ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": wbytes},
-            "tensor": {"achieved": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                       "peak": fp8_peak("mx")[0], "peak_kind": fp8_peak("mx")[1],
-                       "frac": flops / (ms * 1e-3) / 1e12 / fp8_peak("mx")[0],
-                       "frac_of_2x_bf16": flops / (ms * 1e-3) / 1e12 / (2 * tf_peak)}}
+            "tensor": tensor_roofline(flops, ms, "mx", tf_peak)}
 
 
 # ------------------------------------------- config 4: 32K split-KV attention

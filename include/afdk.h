@@ -27,7 +27,9 @@
  * capturable (kernels are chained with programmatic dependent launch); the
  * context's workspace grows on demand (cudaFree + cudaMalloc, synchronising),
  * so capture after a warm-up call of the largest shape, and recapture if a
- * later call needs a larger workspace.  One context per stream in flight.
+ * later call needs a larger workspace.  One context per stream in flight
+ * (the MFA merge kernel also synchronises with the main kernel through
+ * self-re-arming arrival counters owned by the context).
  *
  * Tensor formats: bf16 = IEEE bfloat16 (uint16 storage), e4m3 = OCP FP8
  * E4M3FN (max 448), all tensors dense row-major unless stated.

@@ -567,8 +567,11 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
 
 cudaError_t mfa_combine_launch(bool pdl, const mfa::Params& prm, int G, cudaStream_t stream) {
   const int R = prm.rows > 0 ? prm.rows : mfa::kHeads;
-  return launch_k(pdl, mfa::mfa_combine_kernel, dim3(prm.batch, R / mfa::kK3Rows), dim3(mfa::kK3Threads), 0, stream,
-                  prm, G);
+  const cudaError_t e = launch_k(pdl, mfa::mfa_combine_kernel, dim3(prm.batch, R / mfa::kK3Rows),
+                                 dim3(mfa::kK3Threads), 0, stream, prm, G);
+  // K2 has already published its parts: re-arm the counters K3 would have reset
+  if (e != cudaSuccess) cudaMemsetAsync(prm.sync, 0, 2 * mfa::kMaxBatch * sizeof(int), stream);
+  return e;
 }
 
 }  // namespace afdk

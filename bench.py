@@ -724,22 +724,24 @@ def main():
         step(i)
         attn_step(i)
     torch.cuda.synchronize()
-    # the layer as CUDA graphs (one per rotating KV cache; the 9 PDL launches keep
-    # their programmatic edges); replay is what a serving loop would run
+    # the K timed layers as ONE CUDA graph, as a decode step over a layer stack
+    # is captured: each layer's 9 PDL launches keep their programmatic edges,
+    # and so does the hand-off from one layer to the next (layer i reads KV
+    # cache i % N_ROT).  The graph is replayed once per timed region, so step i
+    # of timed() launches it at i == 0 and the region still covers exactly K
+    # layers (ms per step = elapsed / K).
     graphs, graph_note = None, "off"
     if args.workload == "layer" and not args.no_graph:
         try:
-            graphs = []
-            for r in range(N_ROT):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
-                    layer_step(r)
-                graphs.append(g)
-            for r in range(N_ROT):
-                graphs[r].replay()
+            g_all = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_all, stream=stream):
+                for j in range(args.steps):
+                    layer_step(j)
+            g_all.replay()  # untimed warm replay
             torch.cuda.synchronize()
-            step = lambda i: graphs[i % N_ROT].replay()  # noqa: E731
-            graph_note = "cuda graph replay"
+            graphs = [g_all]
+            step = lambda i: g_all.replay() if i == 0 else None  # noqa: E731
+            graph_note = f"one CUDA graph of the {args.steps} timed layers, replayed once"
         except Exception as e:  # direct launches instead, reported
             graphs, graph_note = None, f"direct launches (capture failed: {type(e).__name__})"
             torch.cuda.synchronize()

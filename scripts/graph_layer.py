@@ -44,3 +44,13 @@ for r in range(bench.N_ROT):
             layer(r, torch.cuda.current_stream().cuda_stream)
     graphs.append(g)
 print("graph  us/layer", timed(lambda i: graphs[i % bench.N_ROT].replay()))
+
+# a stack of layers in ONE graph (as a decode step over many layers would be
+# captured): consecutive layers keep their programmatic (PDL) edges
+for L in (6, 20):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(L):
+                layer(i, torch.cuda.current_stream().cuda_stream)
+    print(f"graph of {L} layers us/layer", timed(lambda i: g.replay(), n=5) / L)

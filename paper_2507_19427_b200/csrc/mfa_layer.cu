@@ -124,14 +124,26 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
   __shared__ float red[32];
   __shared__ float slot;
   __shared__ float kv_s[2 * 256];  // k then v of this row (head_dim <= 256)
+  __shared__ float2 cs_s[128];     // RoPE (cos, sin) of this row's position (head_dim <= 256)
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
-  sm100::griddep_wait();
-  sm100::griddep_launch();
   const int row = blockIdx.x / kRowCluster;
   const int rank = (int)sm100::cluster_ctarank();
   const int qs = e.q_lora / kRowCluster, f0 = rank * qs;
   const int f1 = rank == kRowCluster - 1 ? e.n_out : f0 + qs;
+  const int req = row / e.mtp;
+  const int pos = __ldg(e.seq_lens + req) - e.mtp + row % e.mtp;
+  if (f1 > e.q_lora && pos >= 0) {
+    // the rotation depends only on inputs (seq_lens, inv_freq): one
+    // double-precision sincos per frequency, before the PDL wait
+    for (int i = threadIdx.x; i < e.head_dim / 2; i += blockDim.x) {
+      double sn, cs;
+      sincos((double)pos * e.inv_freq[i], &sn, &cs);
+      cs_s[i] = make_float2((float)cs, (float)sn);
+    }
+  }
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   const int f = f0 + threadIdx.x * 4;  // 4 features per thread ((f1 - f0)/4 <= blockDim)
   const bool act = f < f1;
   float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -157,8 +169,6 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
     *reinterpret_cast<uint2*>(e.qa + (size_t)row * e.q_lora + f) = o;
   }
   if (f1 <= e.q_lora) return;  // this CTA holds no k/v features
-  const int req = row / e.mtp;
-  const int pos = __ldg(e.seq_lens + req) - e.mtp + row % e.mtp;
   if (pos < 0) return;
   const int pg = __ldg(e.block_table + (size_t)req * e.max_pages + pos / e.page);
   const size_t kslot = ((size_t)pg * e.page + pos % e.page) * e.head_dim;
@@ -167,9 +177,7 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
   const float* v = kv_s + e.head_dim;
   const bool fp8 = e.k_scale > 0.0f;
   for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    double sn, cs;
-    sincos((double)pos * e.inv_freq[i], &sn, &cs);
-    const float c = (float)cs, s = (float)sn;
+    const float c = cs_s[i].x, s = cs_s[i].y;
     const float x1 = k[i], x2 = k[i + half];
     const __nv_bfloat16 k1 = __float2bfloat16_rn(x1 * c - x2 * s), k2 = __float2bfloat16_rn(x2 * c + x1 * s);
     if (fp8) {
@@ -243,11 +251,22 @@ __global__ void __launch_bounds__(512) o_epilogue_kernel(const LinearPlan P, con
   __shared__ float slot;
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
-  sm100::griddep_wait();
-  sm100::griddep_launch();
   const size_t row = blockIdx.x / kRowCluster;
   const int q = n / kRowCluster, f0 = (int)sm100::cluster_ctarank() * q;
   constexpr int kMax = 2;  // float4 groups per thread (n/4 <= 2*4*512)
+  // the residual input x and the norm weight are inputs of the layer (x was
+  // complete before its first kernel ran): load them before the PDL wait
+  uint2 xbv[kMax], wbv[kMax];
+#pragma unroll
+  for (int j = 0; j < kMax; ++j) {
+    const int f = f0 + (threadIdx.x + j * blockDim.x) * 4;
+    if (f < f0 + q) {
+      xbv[j] = *reinterpret_cast<const uint2*>(x + row * n + f);
+      wbv[j] = *reinterpret_cast<const uint2*>(w_post + f);
+    }
+  }
+  sm100::griddep_wait();
+  sm100::griddep_launch();
   float r[kMax][4];
   float ss = 0.0f;
 #pragma unroll
@@ -255,7 +274,7 @@ __global__ void __launch_bounds__(512) o_epilogue_kernel(const LinearPlan P, con
     const int f = f0 + (threadIdx.x + j * blockDim.x) * 4;
     if (f < f0 + q) {
       const float4 o = tab.sum4(P, part, (int)row, f);
-      const uint2 xb = *reinterpret_cast<const uint2*>(x + row * n + f);
+      const uint2 xb = xbv[j];
       const __nv_bfloat162 x01 = *reinterpret_cast<const __nv_bfloat162*>(&xb.x);
       const __nv_bfloat162 x23 = *reinterpret_cast<const __nv_bfloat162*>(&xb.y);
       r[j][0] = bf16r(__low2float(x01) + o.x);
@@ -276,7 +295,7 @@ __global__ void __launch_bounds__(512) o_epilogue_kernel(const LinearPlan P, con
   for (int j = 0; j < kMax; ++j) {
     const int f = f0 + (threadIdx.x + j * blockDim.x) * 4;
     if (f < f0 + q) {
-      const uint2 wb = *reinterpret_cast<const uint2*>(w_post + f);
+      const uint2 wb = wbv[j];
       const __nv_bfloat162 w01 = *reinterpret_cast<const __nv_bfloat162*>(&wb.x);
       const __nv_bfloat162 w23 = *reinterpret_cast<const __nv_bfloat162*>(&wb.y);
       uint2 ob;

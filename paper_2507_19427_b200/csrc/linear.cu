@@ -194,6 +194,9 @@ int linear_grid(const Ctx& ctx, const LinearPlan& p) {
   const long long U = (long long)p.tiles * p.kblocks;
   if (g > U) g = U;
   if (g > (long long)(lin::kMaxSegs - 1) * p.tiles) g = (long long)(lin::kMaxSegs - 1) * p.tiles;
+  // nearly one tile per SM (q_up: 128 tiles on 148 SMs): one whole tile per
+  // CTA, no split partials — measured ~1 us faster per layer than stream-K
+  if (p.tiles <= ctx.num_sms && (long long)p.tiles * 20 >= (long long)ctx.num_sms * 17) g = p.tiles;
   return (int)(g < 1 ? 1 : g);
 }
 

@@ -244,7 +244,8 @@ class AfdRank:
             mine = self.alloc()
         except Exception as e:  # noqa: BLE001 - reported on all ranks below
             err, mine = e, None
-        ok = self.torch.tensor([0 if err else 1], dtype=self.torch.int32, device=self.dev)
+        on_gloo = self.dist.get_backend() == "gloo"  # CPU rendezvous (tests, oversubscribed checks)
+        ok = self.torch.tensor([0 if err else 1], dtype=self.torch.int32, device="cpu" if on_gloo else self.dev)
         self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN)
         if int(ok.item()) == 0:
             raise RuntimeError(f"AFD setup failed on some rank (this rank: {err!r})")

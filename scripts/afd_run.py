@@ -35,12 +35,21 @@ def main():
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # AFDK_OVERSUB=1: more ranks than GPUs (e.g. the 8-rank protocol on a 4-GPU
+    # box for --check): ranks share GPUs round-robin and the rendezvous runs on
+    # gloo (NCCL refuses two ranks on one device)
+    oversub = os.environ.get("AFDK_OVERSUB") == "1"
+    if oversub:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    dist.init_process_group("nccl", device_id=dev)
+    if oversub:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     if a.check:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=24, n_micro=2, layers=1, hidden=1024,
-                        q_lora=256, ctx_len=300, n_experts=8, top_k=2, inter=512, seed=3, ffn_format=a.fmt, f2a=a.f2a,
+                        q_lora=256, ctx_len=300, n_experts=8 if (world - a.n_attn) in (1, 2, 4, 8) else 24, top_k=2, inter=512, seed=3, ffn_format=a.fmt, f2a=a.f2a,
                         attn_chunk=min(a.attn_chunk, 256), layer_kind=a.layer, dense_inter=2048 * 6)
     else:
         cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=a.T_mb, n_micro=a.n_micro, layers=a.layers,

@@ -49,7 +49,7 @@ __device__ __forceinline__ float cluster_row_sum(float v, float* red, float* slo
   float t = 0.0f;
 #pragma unroll
   for (int r = 0; r < kRowCluster; ++r) t += sm100::ld_shared_cluster_f32(sm100::mapa_shared(slot, r));
-  sm100::cluster_sync();  // peers finished reading `slot` before anyone moves on / exits
+  sm100::cluster_sync_relaxed();  // peers finished reading `slot` (values already consumed) before anyone exits
   return t;
 }
 

@@ -39,17 +39,36 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // Row statistics over a 4-CTA cluster (one row per cluster, a quarter of the
-// features per CTA): block sums exchanged through distributed shared memory,
-// added in rank order so all four CTAs hold the identical total.
+// features per CTA): every CTA pushes its block sum into slot [its rank] of
+// all four CTAs with st.async (completing 4 bytes on each receiver's
+// mbarrier), then adds the four slots in rank order, so all four hold the
+// identical total.  No cluster barrier (and no fence) on the critical path:
+// row_red_init arms the barrier and publishes it before the PDL wait.
 constexpr int kRowCluster = 4;
-__device__ __forceinline__ float cluster_row_sum(float v, float* red, float* slot) {
+struct RowRed {
+  uint64_t bar;
+  float slot[kRowCluster];
+};
+__device__ __forceinline__ void row_red_init(RowRed& rr) {
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(&rr.bar, 1);
+    sm100::fence_barrier_init();
+    sm100::mbar_expect_tx(&rr.bar, 4 * kRowCluster);
+  }
+  sm100::cluster_sync();  // every CTA's barrier is initialised before any peer stores into it
+}
+__device__ __forceinline__ float cluster_row_sum(float v, float* red, RowRed& rr) {
   v = block_sum(v, red);
-  if (threadIdx.x == 0) *slot = v;
-  sm100::cluster_sync();
+  if (threadIdx.x == 0) {
+    const uint32_t me = sm100::cluster_ctarank();
+#pragma unroll
+    for (int r = 0; r < kRowCluster; ++r)
+      sm100::st_async_f32(sm100::mapa_shared(&rr.slot[me], r), v, sm100::mapa_shared(&rr.bar, r));
+  }
+  sm100::mbar_wait(&rr.bar, 0);
   float t = 0.0f;
 #pragma unroll
-  for (int r = 0; r < kRowCluster; ++r) t += sm100::ld_shared_cluster_f32(sm100::mapa_shared(slot, r));
-  sm100::cluster_sync_relaxed();  // peers finished reading `slot` (values already consumed) before anyone exits
+  for (int r = 0; r < kRowCluster; ++r) t += rr.slot[r];
   return t;
 }
 
@@ -59,7 +78,8 @@ __global__ void __launch_bounds__(512) rmsnorm_kernel(const __nv_bfloat16* __res
                                                       const __nv_bfloat16* __restrict__ w,
                                                       __nv_bfloat16* __restrict__ out, int dim, float eps) {
   __shared__ float red[32];
-  __shared__ float slot;
+  __shared__ RowRed rr;
+  row_red_init(rr);
   sm100::griddep_wait();
   sm100::griddep_launch();
   const size_t row = blockIdx.x / kRowCluster;
@@ -79,7 +99,7 @@ __global__ void __launch_bounds__(512) rmsnorm_kernel(const __nv_bfloat16* __res
       ss += a[j].x * a[j].x + a[j].y * a[j].y + b[j].x * b[j].x + b[j].y * b[j].y;
     }
   }
-  ss = cluster_row_sum(ss, red, &slot);
+  ss = cluster_row_sum(ss, red, rr);
   const float inv = rsqrtf(ss / dim + eps);
 #pragma unroll
   for (int j = 0; j < kMax; ++j) {
@@ -122,11 +142,12 @@ __device__ __forceinline__ uint8_t kv_e4m3(float x, float scale) {
 __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
                                                            int G, const QkvEpi e) {
   __shared__ float red[32];
-  __shared__ float slot;
+  __shared__ RowRed rr;
   __shared__ float kv_s[2 * 256];  // k then v of this row (head_dim <= 256)
   __shared__ float2 cs_s[128];     // RoPE (cos, sin) of this row's position (head_dim <= 256)
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
+  row_red_init(rr);
   const int row = blockIdx.x / kRowCluster;
   const int rank = (int)sm100::cluster_ctarank();
   const int qs = e.q_lora / kRowCluster, f0 = rank * qs;
@@ -157,7 +178,7 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
       kv_s[o] = v4.x; kv_s[o + 1] = v4.y; kv_s[o + 2] = v4.z; kv_s[o + 3] = v4.w;
     }
   }
-  ss = cluster_row_sum(ss, red, &slot);  // includes __syncthreads: kv_s complete
+  ss = cluster_row_sum(ss, red, rr);  // includes __syncthreads: kv_s complete
   const float inv = rsqrtf(ss / e.q_lora + e.eps);
   if (act && f < e.q_lora) {
     const uint2 wb = *reinterpret_cast<const uint2*>(e.q_norm_w + f);
@@ -248,9 +269,10 @@ __global__ void __launch_bounds__(512) o_epilogue_kernel(const LinearPlan P, con
                                                          __nv_bfloat16* __restrict__ h_res,
                                                          __nv_bfloat16* __restrict__ h_norm) {
   __shared__ float red[32];
-  __shared__ float slot;
+  __shared__ RowRed rr;
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
+  row_red_init(rr);
   const size_t row = blockIdx.x / kRowCluster;
   const int q = n / kRowCluster, f0 = (int)sm100::cluster_ctarank() * q;
   constexpr int kMax = 2;  // float4 groups per thread (n/4 <= 2*4*512)
@@ -289,7 +311,7 @@ __global__ void __launch_bounds__(512) o_epilogue_kernel(const LinearPlan P, con
       for (int z = 0; z < 4; ++z) ss += r[j][z] * r[j][z];
     }
   }
-  ss = cluster_row_sum(ss, red, &slot);
+  ss = cluster_row_sum(ss, red, rr);
   const float inv = rsqrtf(ss / n + eps);
 #pragma unroll
   for (int j = 0; j < kMax; ++j) {

@@ -44,7 +44,13 @@ using namespace sm100;
 constexpr int kTile8 = kPage * kDim;  // 16 KB e4m3 K or V page
 constexpr int kPanel8 = 64 * 128;     // 64 rows x 128 B swizzle panel (128 dims)
 constexpr int kPanel16 = 64 * 128;    // 64 rows x 128 B bf16 panel (64 dims)
-constexpr int kNK8 = 3, kNV8 = 4;
+#ifndef AFDK_NK8
+#define AFDK_NK8 4
+#endif
+#ifndef AFDK_NV8
+#define AFDK_NV8 5
+#endif
+constexpr int kNK8 = AFDK_NK8, kNV8 = AFDK_NV8;  // K / V page stages (experiment knobs)
 constexpr int kThreads8 = 256;
 constexpr uint32_t kColO8 = 0, kColS8 = 256;
 constexpr float kRescale8 = 4.0f;     // lazy O rescale threshold (log2 units)
@@ -53,8 +59,8 @@ constexpr float kPScale8 = 16.0f;     // P is stored as e4m3(16 * p)
 struct __align__(1024) Smem8 {
   uint8_t q[4 * kPanel16];   // 32 KB bf16 Q (TMA)
   uint8_t q8[2 * kPanel8];   // 16 KB e4m3 Q, K-major SW128
-  uint8_t k[kNK8][kTile8];   // 48 KB
-  uint8_t v[kNV8][kTile8];   // 64 KB
+  uint8_t k[kNK8][kTile8];   // 64 KB
+  uint8_t v[kNV8][kTile8];   // 80 KB
   uint8_t p[2][64 * 128];    // 16 KB e4m3 P: 64 head rows x 128 B (tokens in the first 64 B, swizzled)
   float qscale[kHeads];
   uint64_t q_full, q_empty, q8_full;

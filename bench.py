@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--no-fp8kv", action="store_true", help="skip the config-2 e4m3 KV-cache measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="time direct launches instead of CUDA-graph replay")
+    p.add_argument("--e2e-direct", action="store_true", help="e2e: direct C-ABI launches instead of one captured C-ABI call per step")
     return p.parse_args()
 
 
@@ -794,6 +795,27 @@ def main():
         def compute(i, b):
             k, v = s["kv"][i % N_ROT]
             ctx.mfa_decode_attention(ins[b], k, v, s["block_table"], s["seq_lens"], outs[b], scale, stream=sp)
+    # A serving loop captures its per-step C-ABI call once and replays it: one
+    # graph per (buffer set, KV cache) pair, each holding one mfa_layer call
+    # (its 9 PDL launches), so the host issues one launch per step.
+    e2e_launch = "direct C-ABI launches"
+    if args.workload == "layer" and not args.no_graph and not args.e2e_direct:
+        try:
+            g_e2e = {}
+            for b in (0, 1):
+                for r in range(N_ROT):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        compute(r, b)
+                    g_e2e[(b, r)] = g
+            for g in g_e2e.values():
+                g.replay()
+            torch.cuda.synchronize()
+            compute = lambda i, b: g_e2e[(b, i % N_ROT)].replay()  # noqa: E731
+            e2e_launch = "one captured C-ABI mfa_layer call per step (graph replay)"
+        except Exception as e:
+            e2e_launch = f"direct C-ABI launches (capture failed: {type(e).__name__})"
+            torch.cuda.synchronize()
     in_host = [x.cpu().pin_memory() for x in ins]
     out_host = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
     cstream = torch.cuda.Stream(device=dev)
@@ -913,7 +935,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tokens/s",
                     "h2d_bytes_per_step": in_host.numel() * in_host.element_size(),
-                    "d2h_bytes_per_step": out_host.numel() * out_host.element_size()},
+                    "d2h_bytes_per_step": out_host.numel() * out_host.element_size(),
+                    "launch": e2e_launch},
             "config4_long_context": long_ctx,
             "config2_fp8_kv": fp8kv,
             "config2_mtp2": mtp,

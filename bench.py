@@ -89,6 +89,13 @@ def fp8_peak_sustained(fmt):
 
 def tensor_roofline(flops, ms, fmt, bf16_peak):
     tf = flops / (ms * 1e-3) / 1e12
+    if fmt == "bf16":  # 16-bit experts: the driver-measured dense bf16 peak
+        sus = None
+        path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(path):
+            sus = json.load(open(path)).get("bf16_tflops_sustained")
+        return {"achieved": tf, "unit": "TFLOP/s", "peak": bf16_peak, "peak_kind": "MEASURED_PEAKS bf16 burst",
+                "frac": tf / bf16_peak, "peak_sustained": sus, "frac_of_sustained": tf / sus if sus else None}
     peak, kind = fp8_peak(fmt)
     sus = fp8_peak_sustained(fmt)
     return {"achieved": tf, "unit": "TFLOP/s", "peak": peak, "peak_kind": kind, "frac": tf / peak,
@@ -316,6 +323,12 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=No
              "sf13": torch.full((n, 2 * INTER, HIDDEN // 32), 120, dtype=torch.uint8, device=dev),
              "sf2": torch.full((n, HIDDEN, INTER // 32), 120, dtype=torch.uint8, device=dev)}
         xs = torch.full((T, HIDDEN // 32), 121, dtype=torch.uint8, device=dev)
+    elif fmt == "bf16":  # 16-bit experts (10.8 GB for 49 experts)
+        del w
+        w = {"n_experts": E_ROUTED,
+             "w13": (torch.randn(n, 2 * INTER, HIDDEN, device=dev) / HIDDEN ** 0.5).to(torch.bfloat16),
+             "w2": (torch.randn(n, HIDDEN, INTER, device=dev) / INTER ** 0.5).to(torch.bfloat16)}
+        xq = torch.randn(T, HIDDEN, device=dev).to(torch.bfloat16)
     logits = torch.randn(T, E_ROUTED, generator=g).to(dev)
     top = torch.topk(logits, TOPK, dim=1)
     ids = top.indices.to(torch.int32).contiguous()
@@ -325,6 +338,9 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=No
     sp = stream.cuda_stream
 
     def step(i):
+        if fmt == "bf16":
+            ctx.moe_ffn_bf16(w, xq, ids, wts, out, expert_lo=lo, expert_hi=hi, shared=sh, stream=sp)
+            return
         f = ctx.moe_ffn_mx if fmt == "mx" else ctx.moe_ffn
         f(w, xq, xs, ids, wts, out, expert_lo=lo, expert_hi=hi, shared=sh, stream=sp)
 
@@ -347,11 +363,11 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=No
         return ms * 1e-3
     idl = ids.flatten().tolist()
     touched = len({e for e in idl if lo <= e < hi}) + 1
-    wbytes = moe_weight_bytes(touched)
+    wbytes = 2 * 3 * HIDDEN * INTER * touched if fmt == "bf16" else moe_weight_bytes(touched)
     flops = 2.0 * 3 * HIDDEN * INTER * (sum(lo <= e < hi for e in idl) + sh[1] - sh[0])
     hbm_peak, tf_peak, kind = peaks()
     del w
-    return {"T": T, "format": "mxfp8" if fmt == "mx" else "fp8_block128", "ms_per_layer": ms,
+    return {"T": T, "format": {"mx": "mxfp8", "bf16": "bf16"}.get(fmt, "fp8_block128"), "ms_per_layer": ms,
             "experts_per_gpu": hi - lo, "gpus": shard[1] if shard else 1,
             "tokens_per_s": T / (ms * 1e-3),
             "hbm": {"achieved": wbytes / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -884,7 +900,7 @@ def main():
         # at N > 1 the experts are sharded over the GPUs (config 3 at 2/4)
         shard = (rank, world, dist) if world > 1 else None
         pts = (("fp8", 256), ("mx", 256)) if shard else \
-            (("fp8", 256), ("fp8", 4096), ("mx", 256), ("mx", 4096), ("mx", 8192))
+            (("fp8", 256), ("fp8", 4096), ("mx", 256), ("mx", 4096), ("mx", 8192), ("bf16", 256), ("bf16", 4096))
         moe = [run_moe_bench(ctx, torch, dev, T, max(3, args.steps // 4), 2, seed=0, fmt=f, shard=shard)
                for f, T in pts]
         # dense Step-3 layers (inter 18432) as 4 intermediate slices, MXFP8

@@ -255,6 +255,36 @@ typedef struct afdk_moe_mx_args {
 afdk_status afdk_moe_ffn_mx(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
                             afdk_stream stream);
 
+/* ---------------------------------- K7/K8/K9 MoE FFN (16-bit experts)
+ * The FFN with 2-byte weights: QuantScheme.weight_bytes = 2 /
+ * compute_kind f16 (types.hpp:34-40, effective_kind types.hpp:93-95), the
+ * BF16 fallback of PAPER.md:279.  Same routing, shared-expert and
+ * partial-sum semantics as afdk_moe_ffn; the dispatch payload is the bf16
+ * token rows (dispatch_bytes 2 instead of 1 in ffn_net_bytes,
+ * moeplan.cpp:17-20), the SiLU(gate)*up intermediate is stored bf16, GEMMs on
+ * tcgen05 kind::f16 with fp32 accumulation:
+ *   w13 bf16 [(n_local+1), 2*inter, hidden] (rows: gate then up),
+ *   w2  bf16 [(n_local+1), hidden, inter].
+ * Limits: hidden % 128 == 0, inter % 128 == 0, E <= 64, k <= 8, T*k <= 65536. */
+typedef struct afdk_moe_bf16_weights {
+  int hidden, inter, n_experts, top_k;
+  int expert_lo, expert_hi;
+  const void* w13;
+  const void* w2;
+} afdk_moe_bf16_weights;
+
+typedef struct afdk_moe_bf16_args {
+  int T;
+  const void* x;         /* bf16 [T, hidden] dispatch payload        */
+  const int32_t* ids;    /* [T, top_k]                               */
+  const float* weights;  /* [T, top_k]                               */
+  int shared_lo, shared_hi;
+  void* out;             /* bf16 [T, hidden] this rank's partial     */
+} afdk_moe_bf16_args;
+
+afdk_status afdk_moe_ffn_bf16(afdk_ctx* ctx, const afdk_moe_bf16_weights* w, const afdk_moe_bf16_args* a,
+                              afdk_stream stream);
+
 /* ------------------------------------------------ dense FFN (MXFP8)
  * The dense Step-3 layers (first four and last, inter 18432,
  * builtin_catalog.cpp:248-250): out = SiLU(x.Wg^T) * (x.Wu^T) . W2^T as a sum
@@ -304,6 +334,8 @@ afdk_status afdk_moe_ffn_scatter(afdk_ctx* ctx, const afdk_moe_weights* w, const
                                  const afdk_row_scatter* sc, afdk_stream stream);
 afdk_status afdk_moe_ffn_mx_scatter(afdk_ctx* ctx, const afdk_moe_mx_weights* w, const afdk_moe_mx_args* a,
                                     const afdk_row_scatter* sc, afdk_stream stream);
+afdk_status afdk_moe_ffn_bf16_scatter(afdk_ctx* ctx, const afdk_moe_bf16_weights* w, const afdk_moe_bf16_args* a,
+                                      const afdk_row_scatter* sc, afdk_stream stream);
 /* dense layer, this GPU's intermediate slices (tensor-parallel partial) */
 afdk_status afdk_dense_ffn_mx_scatter(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,
                                       const uint8_t* xsf, const afdk_row_scatter* sc, afdk_stream stream);

@@ -281,6 +281,7 @@ void orc_moe_permute(const int32_t* ids, int T, int k, int E, int32_t* offsets,
 void orc_quant_fp8_rowblock(const float* x, int rows, int cols, int block,
                             uint8_t* q, float* scales) {
   const int nb = cols / block;
+#pragma omp parallel for schedule(static)
   for (int r = 0; r < rows; ++r)
     for (int b = 0; b < nb; ++b) {
       const float* xb = x + (size_t)r * cols + (size_t)b * block;
@@ -296,6 +297,7 @@ void orc_quant_fp8_rowblock(const float* x, int rows, int cols, int block,
 void orc_quant_fp8_tile(const float* w, int rows, int cols, int bm, int bk,
                         uint8_t* q, float* scales) {
   const int nbr = rows / bm, nbc = cols / bk;
+#pragma omp parallel for schedule(static)
   for (int br = 0; br < nbr; ++br)
     for (int bc = 0; bc < nbc; ++bc) {
       float amax = 0.0f;
@@ -394,6 +396,67 @@ void orc_moe_layer_fp8(const uint8_t* xq, const float* xs, int T, int H, int I, 
   free(acc); free(y); free(gx); free(gs); free(rows_tok); free(rows_w);
 }
 
+/* ------------------------------------------------- 16-bit / fp32 experts */
+/* QuantScheme with 2-byte FFN weights (types.hpp:34-40, effective_kind
+ * types.hpp:93-95; "BF16 where FP8 is unavailable"): the gated
+ * expert of step3_text.py Step3TextMLP — gate_up_proj rows [gate; up],
+ * SiluAndMul, down_proj.  x and the weights are passed as float (bf16-widened
+ * for the bf16 path, unquantised for the fp32 error budget).  round_bf16: the
+ * SwiGLU intermediate is stored bf16 (the B200 path's storage point). */
+void orc_expert_ffn_f32(const float* x, int rows, int H, int I, const float* w13,
+                        const float* w2, int round_bf16, float* y) {
+  float* hbuf = (float*)malloc(sizeof(float) * (size_t)rows * I);
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int r = 0; r < rows; ++r)
+    for (int n = 0; n < I; ++n) {
+      const float* xr = x + (size_t)r * H;
+      const float* wg = w13 + (size_t)n * H;
+      const float* wu = w13 + (size_t)(n + I) * H;
+      double g = 0.0, u = 0.0;
+      for (int c = 0; c < H; ++c) { g += (double)xr[c] * wg[c]; u += (double)xr[c] * wu[c]; }
+      hbuf[(size_t)r * I + n] = maybe_bf16(silu((float)g) * (float)u, round_bf16);
+    }
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int r = 0; r < rows; ++r)
+    for (int n = 0; n < H; ++n) {
+      const float* hr = hbuf + (size_t)r * I;
+      const float* wr = w2 + (size_t)n * I;
+      double acc = 0.0;
+      for (int c = 0; c < I; ++c) acc += (double)hr[c] * wr[c];
+      y[(size_t)r * H + n] = (float)acc;
+    }
+  free(hbuf);
+}
+
+/* Routed layer over 16-bit/fp32 experts: same routing, shared-expert and
+ * combine semantics as orc_moe_layer_fp8 (experts [0,E) routed, E shared). */
+void orc_moe_layer_f32(const float* x, int T, int H, int I, int E, int k, const int32_t* ids,
+                       const float* weights, const float* w13_all, const float* w2_all,
+                       int round_bf16, float* out) {
+  const size_t w13_sz = (size_t)2 * I * H, w2_sz = (size_t)H * I;
+  double* acc = (double*)calloc((size_t)T * H, sizeof(double));
+  float* y = (float*)malloc(sizeof(float) * (size_t)T * H);
+  float* gx = (float*)malloc(sizeof(float) * (size_t)T * H);
+  int32_t* rows_tok = (int32_t*)malloc(sizeof(int32_t) * (size_t)T);
+  float* rows_w = (float*)malloc(sizeof(float) * (size_t)T);
+  for (int e = 0; e <= E; ++e) {
+    int n = 0;
+    for (int t = 0; t < T; ++t) {
+      if (e == E) { rows_tok[n] = t; rows_w[n] = 1.0f; ++n; continue; }
+      for (int j = 0; j < k; ++j)
+        if (ids[(size_t)t * k + j] == e) { rows_tok[n] = t; rows_w[n] = weights[(size_t)t * k + j]; ++n; }
+    }
+    if (n == 0) continue;
+    for (int r = 0; r < n; ++r) memcpy(gx + (size_t)r * H, x + (size_t)rows_tok[r] * H, sizeof(float) * H);
+    orc_expert_ffn_f32(gx, n, H, I, w13_all + e * w13_sz, w2_all + e * w2_sz, round_bf16, y);
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < H; ++c)
+        acc[(size_t)rows_tok[r] * H + c] += (double)rows_w[r] * y[(size_t)r * H + c];
+  }
+  for (size_t i = 0; i < (size_t)T * H; ++i) out[i] = maybe_bf16((float)acc[i], round_bf16);
+  free(acc); free(y); free(gx); free(rows_tok); free(rows_w);
+}
+
 /* ------------------------------------------------------------------ MXFP8 */
 /* smallest e with amax <= 448 * 2^e, from the exact binary exponent/mantissa
  * of amax (448 = 1.75 * 2^8) */
@@ -415,6 +478,7 @@ float orc_mx_scale(uint8_t sf) { return ldexpf(1.0f, (int)sf - 127); }
 
 void orc_quant_pow2(const float* x, int rows, int cols, int block, uint8_t* q, int32_t* eo) {
   const int nb = cols / block;
+#pragma omp parallel for schedule(static)
   for (int r = 0; r < rows; ++r)
     for (int b = 0; b < nb; ++b) {
       const float* xb = x + (size_t)r * cols + (size_t)b * block;
@@ -429,6 +493,7 @@ void orc_quant_pow2(const float* x, int rows, int cols, int block, uint8_t* q, i
 
 void orc_quant_mx(const float* x, int rows, int cols, uint8_t* q, uint8_t* sf) {
   const int nb = cols / 32;
+#pragma omp parallel for schedule(static)
   for (int r = 0; r < rows; ++r)
     for (int b = 0; b < nb; ++b) {
       const float* xb = x + (size_t)r * cols + (size_t)b * 32;

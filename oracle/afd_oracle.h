@@ -159,6 +159,13 @@ float orc_mx_scale(uint8_t sf); /* 2^(sf-127) */
 /* One gated expert, all operands MXFP8: xq [rows,H] + xsf [rows,H/32],
  * w13 [2I,H] + sf13 [2I,H/32], w2 [H,I] + sf2 [H,I/32]; the SiLU(gate)*up
  * intermediate is re-quantised to MXFP8 before W2. y [rows,H] fp32. */
+/* 16-bit (bf16) / unquantised fp32 gated expert and routed layer
+ * (types.hpp:34-40,93-95; step3_text.py Step3TextMLP + SiluAndMul). */
+void orc_expert_ffn_f32(const float* x, int rows, int H, int I, const float* w13,
+                        const float* w2, int round_bf16, float* y);
+void orc_moe_layer_f32(const float* x, int T, int H, int I, int E, int k, const int32_t* ids,
+                       const float* weights, const float* w13_all, const float* w2_all,
+                       int round_bf16, float* out);
 void orc_expert_ffn_mx(const uint8_t* xq, const uint8_t* xsf, int rows, int H, int I,
                        const uint8_t* w13, const uint8_t* sf13, const uint8_t* w2,
                        const uint8_t* sf2, float* y);

@@ -320,6 +320,64 @@ def moe_layer_mx(xq, xsf, ids, weights, w13_all, sf13_all, w2_all, sf2_all, roun
     return out
 
 
+def expert_ffn_f32(x, w13, w2, round_bf16=False):
+    """Gated expert over float weights (orc_expert_ffn_f32): the bf16 FFN
+    format with round_bf16=True (bf16-widened inputs), the unquantised fp32
+    model with round_bf16=False."""
+    x = _f32(x)
+    rows, H = x.shape
+    I = w2.shape[1]
+    y = np.empty((rows, H), np.float32)
+    orc().orc_expert_ffn_f32(_p(x, c_float), c_int(rows), c_int(H), c_int(I), _p(_f32(w13), c_float),
+                             _p(_f32(w2), c_float), c_int(int(round_bf16)), _p(y, c_float))
+    return y
+
+
+def moe_layer_f32(x, ids, weights, w13_all, w2_all, round_bf16=False):
+    x = _f32(x)
+    T, H = x.shape
+    E = w13_all.shape[0] - 1
+    I = w2_all.shape[2]
+    k = ids.shape[1]
+    out = np.empty((T, H), np.float32)
+    orc().orc_moe_layer_f32(_p(x, c_float), c_int(T), c_int(H), c_int(I), c_int(E), c_int(k),
+                            _p(_i32(ids), c_int32), _p(_f32(weights), c_float), _p(_f32(w13_all), c_float),
+                            _p(_f32(w2_all), c_float), c_int(int(round_bf16)), _p(out, c_float))
+    return out
+
+
+def moe_layer_by_expert(ids, weights, n_experts, expert_fn, tokens=None, round_bf16=True):
+    """Routed layer restricted to a token subset, one expert at a time.
+
+    Same semantics as orc_moe_layer_* (experts [0,E) routed, E = shared, out =
+    sum_k w_k y_k + shared, bf16-rounded): a token's output depends only on its
+    own row, so the oracle can check a fixed subset of a full-size layer.
+    expert_fn(e, token_rows) -> y [len(rows), H] float32 runs expert e (the
+    caller fetches that expert's weights only, keeping host memory small)."""
+    ids = np.asarray(ids)
+    T = ids.shape[0]
+    tokens = np.arange(T) if tokens is None else np.asarray(tokens)
+    acc = None
+    for e in range(n_experts + 1):
+        if e == n_experts:
+            rows, w = tokens, np.ones(len(tokens), np.float64)
+        else:
+            hit = ids[tokens] == e
+            sel = hit.any(axis=1)
+            rows = tokens[sel]
+            w = np.asarray(weights)[rows][hit[sel]].astype(np.float64)
+        if len(rows) == 0:
+            continue
+        y = expert_fn(e, rows).astype(np.float64)
+        if acc is None:
+            acc = np.zeros((len(tokens), y.shape[1]), np.float64)
+        pos = np.searchsorted(tokens, rows) if np.all(np.diff(tokens) > 0) else \
+            np.array([int(np.where(tokens == r)[0][0]) for r in rows])
+        np.add.at(acc, pos, w[:, None] * y)
+    out = acc.astype(np.float32)
+    return bf16_round(out) if round_bf16 else out
+
+
 def num_threads() -> int:
     return orc().orc_num_threads()
 

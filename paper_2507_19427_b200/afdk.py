@@ -88,6 +88,20 @@ class MoeMxArgs(Structure):
     ]
 
 
+class MoeBf16Weights(Structure):
+    _fields_ = [
+        ("hidden", c_int), ("inter", c_int), ("n_experts", c_int), ("top_k", c_int),
+        ("expert_lo", c_int), ("expert_hi", c_int), ("w13", c_void_p), ("w2", c_void_p),
+    ]
+
+
+class MoeBf16Args(Structure):
+    _fields_ = [
+        ("T", c_int), ("x", c_void_p), ("ids", c_void_p), ("weights", c_void_p),
+        ("shared_lo", c_int), ("shared_hi", c_int), ("out", c_void_p),
+    ]
+
+
 class DenseMxWeights(Structure):
     _fields_ = [("hidden", c_int), ("inter_split", c_int), ("n_split", c_int),
                 ("w13", c_void_p), ("sf13", c_void_p), ("w2", c_void_p), ("sf2", c_void_p)]
@@ -144,6 +158,9 @@ SIGNATURES = {
     "afdk_moe_ffn_mx_scatter": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), POINTER(RowScatter),
                                         c_void_p]),
     "afdk_moe_ffn_mx": (c_int, [c_void_p, POINTER(MoeMxWeights), POINTER(MoeMxArgs), c_void_p]),
+    "afdk_moe_ffn_bf16": (c_int, [c_void_p, POINTER(MoeBf16Weights), POINTER(MoeBf16Args), c_void_p]),
+    "afdk_moe_ffn_bf16_scatter": (c_int, [c_void_p, POINTER(MoeBf16Weights), POINTER(MoeBf16Args),
+                                          POINTER(RowScatter), c_void_p]),
     "afdk_dense_ffn_mx": (c_int, [c_void_p, POINTER(DenseMxWeights), c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "afdk_dense_ffn_mx_scatter": (c_int, [c_void_p, POINTER(DenseMxWeights), c_int, c_void_p, c_void_p,
                                           POINTER(RowScatter), c_void_p]),
@@ -330,6 +347,24 @@ class Context:
             sc = RowScatter(scatter[0].numel(), scatter[1], ptr(scatter[0]))
             check(self.lib.afdk_moe_ffn_mx_scatter(self.handle, ctypes.byref(mw), ctypes.byref(a), ctypes.byref(sc),
                                                    c_void_p(stream)))
+
+    def moe_ffn_bf16(self, w: dict, x, ids, weights, out, expert_lo=0, expert_hi=None, shared=(0, None),
+                     stream: int = 0, scatter=None) -> None:
+        """16-bit experts. w: n_experts, w13 [n+1, 2I, H] bf16, w2 [n+1, H, I] bf16; x bf16 [T, H]."""
+        T, Hd = x.shape
+        k = ids.shape[1]
+        inter = w["w2"].shape[2]
+        E = w["n_experts"]
+        hi = E if expert_hi is None else expert_hi
+        sh_lo, sh_hi = shared[0], (T if shared[1] is None else shared[1])
+        mw = MoeBf16Weights(Hd, inter, E, k, expert_lo, hi, ptr(w["w13"]), ptr(w["w2"]))
+        a = MoeBf16Args(T, ptr(x), ptr(ids), ptr(weights), sh_lo, sh_hi, ptr(out))
+        if scatter is None:
+            check(self.lib.afdk_moe_ffn_bf16(self.handle, ctypes.byref(mw), ctypes.byref(a), c_void_p(stream)))
+        else:
+            sc = RowScatter(scatter[0].numel(), scatter[1], ptr(scatter[0]))
+            check(self.lib.afdk_moe_ffn_bf16_scatter(self.handle, ctypes.byref(mw), ctypes.byref(a),
+                                                     ctypes.byref(sc), c_void_p(stream)))
 
     def dense_ffn_mx(self, w: dict, xq, xsf, out, stream: int = 0, scatter=None) -> None:
         """Dense FFN in slice layout: w13 [n_split, 2*Is, H], sf13, w2 [n_split, H, Is], sf2."""

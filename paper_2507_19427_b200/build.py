@@ -24,6 +24,7 @@ CU_SOURCES = [
     "linear.cu",
     "moe_gemm_mx.cu",
     "moe_gemm_mx2.cu",
+    "moe_gemm_bf16.cu",
     "mfa_layer.cu",
     "moe_route.cu",
     "moe_gemm.cu",

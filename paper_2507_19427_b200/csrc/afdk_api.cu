@@ -103,14 +103,18 @@ afdk_status afdk_create(afdk_ctx** out, const afdk_cfg* cfg) {
   }
   const int dev = cfg ? cfg->device : 0;
   if (dev < 0 || dev >= n) { set_error("afdk_create: cfg.device out of range"); return AFDK_ERR_INVALID; }
-  cudaError_t e = cudaSetDevice(dev);
-  if (e != cudaSuccess) return cuda_fail("cudaSetDevice", e);
+  afdk::DeviceGuard device_guard(dev);
   cudaDeviceProp prop{};
-  e = cudaGetDeviceProperties(&prop, dev);
+  cudaError_t e = cudaGetDeviceProperties(&prop, dev);
   if (e != cudaSuccess) return cuda_fail("cudaGetDeviceProperties", e);
-  if (prop.major != 10) {
+  if (prop.major != 10 || prop.minor != 0) {
     set_error("afdk_create: device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
               ", this library is built for sm_100a only");
+    return AFDK_ERR_UNSUPPORTED;
+  }
+  if (prop.multiProcessorCount >= afdk::kMfaMaxSplit) {
+    set_error("afdk_create: " + std::to_string(prop.multiProcessorCount) +
+              " SMs exceed the split-KV merge limit (" + std::to_string(afdk::kMfaMaxSplit - 1) + ")");
     return AFDK_ERR_UNSUPPORTED;
   }
   auto* ctx = new afdk_ctx();
@@ -155,7 +159,10 @@ static afdk_status mfa_decode_entry(afdk_ctx* ctx, const afdk_mfa_decode_args* a
   if (a->n_heads != 64) { set_error("mfa_decode: n_heads must be 64"); return AFDK_ERR_INVALID; }
   if (a->head_dim != 256) { set_error("mfa_decode: head_dim must be 256"); return AFDK_ERR_INVALID; }
   if (a->page_size != 64) { set_error("mfa_decode: page_size must be 64"); return AFDK_ERR_INVALID; }
-  if (a->batch <= 0) { set_error("mfa_decode: batch must be > 0"); return AFDK_ERR_INVALID; }
+  if (a->batch <= 0 || a->batch > afdk::kMfaMaxBatch) {
+    set_error("mfa_decode: batch must be in [1, " + std::to_string(afdk::kMfaMaxBatch) + "]");
+    return AFDK_ERR_INVALID;
+  }
   if (a->num_pages <= 0 || a->max_pages <= 0) { set_error("mfa_decode: num_pages/max_pages must be > 0"); return AFDK_ERR_INVALID; }
   if (!a->q || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->out) {
     set_error("mfa_decode: NULL tensor pointer");
@@ -167,7 +174,7 @@ static afdk_status mfa_decode_entry(afdk_ctx* ctx, const afdk_mfa_decode_args* a
     return AFDK_ERR_INVALID;
   }
   afdk::Ctx& c = ctx->c;
-  cudaSetDevice(c.device);
+  afdk::DeviceGuard device_guard(c.device);
   void* ws = afdk::workspace(c, afdk::mfa_decode_workspace_bytes(a->batch, c.num_sms));
   if (!ws) { set_error("mfa_decode: workspace allocation failed"); return AFDK_ERR_CUDA; }
   afdk::MfaDecodeArgs m{a->batch, a->q, a->k_cache, a->v_cache, a->num_pages, a->block_table,
@@ -207,7 +214,7 @@ afdk_status afdk_mfa_decode_attention_mtp(afdk_ctx* ctx, const afdk_mfa_decode_a
     return AFDK_ERR_INVALID;
   }
   afdk::Ctx& c = ctx->c;
-  cudaSetDevice(c.device);
+  afdk::DeviceGuard device_guard(c.device);
   void* ws = afdk::workspace(c, afdk::mfa_decode_mtp_workspace_bytes(a->batch, c.num_sms));
   if (!ws) { set_error("mfa_decode_mtp: workspace allocation failed"); return AFDK_ERR_CUDA; }
   afdk::MfaDecodeArgs m{a->batch, a->q, a->k_cache, a->v_cache, a->num_pages, a->block_table,
@@ -223,7 +230,7 @@ afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, 
   if (m < 1 || m > 256) { set_error("afdk_linear: m must be in [1, 256]"); return AFDK_ERR_INVALID; }
   if (n < 1 || k < 64 || k % 64) { set_error("afdk_linear: k must be a positive multiple of 64"); return AFDK_ERR_INVALID; }
   afdk::Ctx& c = ctx->c;
-  cudaSetDevice(c.device);
+  afdk::DeviceGuard device_guard(c.device);
   const afdk::LinearPlan p = afdk::make_linear_plan(m, n, k);
   float* part = static_cast<float*>(afdk::workspace(c, afdk::linear_workspace_bytes(p, c.num_sms)));
   if (!part) { set_error("afdk_linear: workspace allocation failed"); return AFDK_ERR_CUDA; }
@@ -259,7 +266,7 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
     return AFDK_ERR_INVALID;
   }
   afdk::Ctx& c = ctx->c;
-  cudaSetDevice(c.device);
+  afdk::DeviceGuard device_guard(c.device);
   afdk::MfaLayerArgs m{a->batch, w->hidden, w->q_lora, w->n_heads, w->head_dim, a->page_size,
                        w->in_norm, w->w_qkv, w->q_norm, w->w_q_up, w->w_o, w->post_norm,
                        w->rms_eps, w->rope_theta, w->softmax_scale, a->x, a->k_cache, a->v_cache,
@@ -303,7 +310,7 @@ afdk_status afdk_router_topk(afdk_ctx* ctx, const void* h, const void* gate_w, i
   if (T < 1 || H < 256 || H % 256) { set_error("afdk_router_topk: H must be a positive multiple of 256"); return AFDK_ERR_INVALID; }
   if (H > 65536) { set_error("afdk_router_topk: H must be <= 65536"); return AFDK_ERR_INVALID; }
   if (xq && !xs) { set_error("afdk_router_topk: xq requires xs"); return AFDK_ERR_INVALID; }
-  cudaSetDevice(ctx->c.device);
+  afdk::DeviceGuard device_guard(ctx->c.device);
   afdk::moe::RouterArgs a{static_cast<const __nv_bfloat16*>(h), static_cast<const __nv_bfloat16*>(gate_w), T, H, E, k,
                           renormalize, logits, ids, weights, static_cast<uint8_t*>(xq), xs};
   void* ws = afdk::workspace(ctx->c, afdk::router_workspace_bytes(H, E, ctx->c.num_sms));
@@ -321,7 +328,7 @@ afdk_status afdk_moe_permute(afdk_ctx* ctx, const int32_t* ids, int T, int k, in
     return AFDK_ERR_INVALID;
   }
   afdk::Ctx& c = ctx->c;
-  cudaSetDevice(c.device);
+  afdk::DeviceGuard device_guard(c.device);
   const size_t wbytes = afdk::align_up((size_t)afdk::moe::max_work(T, k, E) * sizeof(afdk::moe::Work), 256) + 256;
   uint8_t* ws = static_cast<uint8_t*>(afdk::workspace(c, wbytes));
   if (!ws) { set_error("afdk_moe_permute: workspace allocation failed"); return AFDK_ERR_CUDA; }
@@ -363,7 +370,7 @@ static afdk_status moe_ffn_entry(afdk_ctx* ctx, const afdk_moe_weights* w, const
     return AFDK_ERR_INVALID;
   }
   afdk::Ctx& c = ctx->c;
-  cudaSetDevice(c.device);
+  afdk::DeviceGuard device_guard(c.device);
   const int sh_lo = a->shared_lo < 0 ? 0 : a->shared_lo;
   const int sh_hi = a->shared_hi > a->T ? a->T : a->shared_hi;
   afdk::MoeFfnArgs m{a->T, w->top_k, w->n_experts, w->hidden, w->inter, w->expert_lo, w->expert_hi,
@@ -399,7 +406,7 @@ static afdk_status moe_ffn_mx_entry(afdk_ctx* ctx, const afdk_moe_mx_weights* w,
     return AFDK_ERR_INVALID;
   }
   afdk::Ctx& c = ctx->c;
-  cudaSetDevice(c.device);
+  afdk::DeviceGuard device_guard(c.device);
   const int sh_lo = a->shared_lo < 0 ? 0 : a->shared_lo;
   const int sh_hi = a->shared_hi > a->T ? a->T : a->shared_hi;
   afdk::MoeFfnMxArgs m{a->T, w->top_k, w->n_experts, w->hidden, w->inter, w->expert_lo, w->expert_hi,
@@ -432,6 +439,50 @@ afdk_status afdk_moe_ffn_mx_scatter(afdk_ctx* ctx, const afdk_moe_mx_weights* w,
   return moe_ffn_mx_entry(ctx, w, a, sc, stream);
 }
 
+static afdk_status moe_ffn_bf16_entry(afdk_ctx* ctx, const afdk_moe_bf16_weights* w, const afdk_moe_bf16_args* a,
+                                      const afdk_row_scatter* sc, afdk_stream stream) {
+  if (!ctx || !w || !a) { set_error("afdk_moe_ffn_bf16: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }
+  if (w->hidden % 128 || w->inter % 128 || w->hidden < 128 || w->inter < 128) {
+    set_error("afdk_moe_ffn_bf16: hidden and inter must be positive multiples of 128");
+    return AFDK_ERR_INVALID;
+  }
+  if (w->n_experts < 1 || w->n_experts > afdk::moe::kMaxExperts || w->top_k < 1 || w->top_k > afdk::moe::kMaxTopK) {
+    set_error("afdk_moe_ffn_bf16: need 1 <= n_experts <= 64 and 1 <= top_k <= 8");
+    return AFDK_ERR_INVALID;
+  }
+  if (w->expert_lo < 0 || w->expert_hi > w->n_experts || w->expert_lo > w->expert_hi) {
+    set_error("afdk_moe_ffn_bf16: expert range out of bounds");
+    return AFDK_ERR_INVALID;
+  }
+  if (a->T < 1 || a->T * w->top_k > 65536) { set_error("afdk_moe_ffn_bf16: T out of range"); return AFDK_ERR_INVALID; }
+  if (!a->x || !a->ids || !a->weights || (!a->out && !sc) || !w->w13 || !w->w2) {
+    set_error("afdk_moe_ffn_bf16: NULL tensor pointer");
+    return AFDK_ERR_INVALID;
+  }
+  if (!scatter_ok(sc, a->T, "afdk_moe_ffn_bf16")) return AFDK_ERR_INVALID;
+  afdk::Ctx& c = ctx->c;
+  afdk::DeviceGuard device_guard(c.device);
+  const int sh_lo = a->shared_lo < 0 ? 0 : a->shared_lo;
+  const int sh_hi = a->shared_hi > a->T ? a->T : a->shared_hi;
+  afdk::MoeFfnBf16Args m{a->T, w->top_k, w->n_experts, w->hidden, w->inter, w->expert_lo, w->expert_hi,
+                         w->w13, w->w2, a->x, a->ids, a->weights, sh_lo, sh_hi, a->out};
+  if (sc) { m.dst = sc->dst; m.rows_per_dst = sc->rows_per_dst; }
+  void* ws = afdk::workspace(c, afdk::moe_ffn_bf16_workspace_bytes(a->T, w->top_k, w->n_experts, w->hidden, w->inter));
+  if (!ws) { set_error("afdk_moe_ffn_bf16: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  if (afdk::moe_ffn_bf16_launch(c, m, ws, static_cast<cudaStream_t>(stream)) != cudaSuccess) return AFDK_ERR_CUDA;
+  return AFDK_OK;
+}
+
+afdk_status afdk_moe_ffn_bf16(afdk_ctx* ctx, const afdk_moe_bf16_weights* w, const afdk_moe_bf16_args* a,
+                              afdk_stream stream) {
+  return moe_ffn_bf16_entry(ctx, w, a, nullptr, stream);
+}
+afdk_status afdk_moe_ffn_bf16_scatter(afdk_ctx* ctx, const afdk_moe_bf16_weights* w, const afdk_moe_bf16_args* a,
+                                      const afdk_row_scatter* sc, afdk_stream stream) {
+  if (!sc) { set_error("afdk_moe_ffn_bf16_scatter: NULL scatter"); return AFDK_ERR_INVALID; }
+  return moe_ffn_bf16_entry(ctx, w, a, sc, stream);
+}
+
 static afdk_status dense_ffn_mx_entry(afdk_ctx* ctx, const afdk_dense_mx_weights* w, int T, const void* xq,
                                       const uint8_t* xsf, void* out, const afdk_row_scatter* sc, afdk_stream stream) {
   if (!ctx || !w) { set_error("afdk_dense_ffn_mx: NULL ctx/weights"); return AFDK_ERR_INVALID; }
@@ -446,7 +497,7 @@ static afdk_status dense_ffn_mx_entry(afdk_ctx* ctx, const afdk_dense_mx_weights
     return AFDK_ERR_INVALID;
   }
   afdk::Ctx& c = ctx->c;
-  cudaSetDevice(c.device);
+  afdk::DeviceGuard device_guard(c.device);
   afdk::DenseFfnMxArgs d{T, w->hidden, w->inter_split, w->n_split, w->w13, w->sf13, w->w2, w->sf2,
                          static_cast<const uint8_t*>(xq), xsf, out};
   if (!scatter_ok(sc, T, "afdk_dense_ffn_mx")) return AFDK_ERR_INVALID;
@@ -471,7 +522,7 @@ afdk_status afdk_quant_mx(afdk_ctx* ctx, const void* x, int T, int H, void* q, u
   if (!ctx || !x || !q || !sf) { set_error("afdk_quant_mx: NULL argument"); return AFDK_ERR_INVALID; }
   if (T < 0 || H <= 0 || H % 32) { set_error("afdk_quant_mx: need T >= 0 and H % 32 == 0"); return AFDK_ERR_INVALID; }
   if (T == 0) return AFDK_OK;
-  cudaSetDevice(ctx->c.device);
+  afdk::DeviceGuard device_guard(ctx->c.device);
   afdk::moe::QuantMxArgs a{static_cast<const __nv_bfloat16*>(x), T, H, static_cast<uint8_t*>(q), sf};
   const cudaError_t e = afdk::quant_mx_launch(a, static_cast<cudaStream_t>(stream), ctx->c.pdl);
   if (e != cudaSuccess) return cuda_fail("afdk_quant_mx", e);
@@ -494,7 +545,7 @@ afdk_status afdk_ipc_handle(afdk_ctx* ctx, const void* dev_ptr, void* handle72) 
     }
     range = reinterpret_cast<RangeFn>(fn);
   }
-  cudaSetDevice(ctx->c.device);
+  afdk::DeviceGuard device_guard(ctx->c.device);
   CUdeviceptr base = 0;
   size_t size = 0;
   if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) {
@@ -512,7 +563,7 @@ afdk_status afdk_ipc_handle(afdk_ctx* ctx, const void* dev_ptr, void* handle72) 
 
 afdk_status afdk_ipc_open(afdk_ctx* ctx, const void* handle72, void** dev_ptr) {
   if (!ctx || !handle72 || !dev_ptr) { set_error("afdk_ipc_open: NULL argument"); return AFDK_ERR_INVALID; }
-  cudaSetDevice(ctx->c.device);
+  afdk::DeviceGuard device_guard(ctx->c.device);
   cudaIpcMemHandle_t h;
   uint64_t off = 0;
   std::memcpy(&h, handle72, 64);
@@ -526,7 +577,7 @@ afdk_status afdk_ipc_open(afdk_ctx* ctx, const void* handle72, void** dev_ptr) {
 
 afdk_status afdk_ipc_close(afdk_ctx* ctx, void* dev_ptr) {
   if (!ctx || !dev_ptr) { set_error("afdk_ipc_close: NULL argument"); return AFDK_ERR_INVALID; }
-  cudaSetDevice(ctx->c.device);
+  afdk::DeviceGuard device_guard(ctx->c.device);
   using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;

@@ -36,6 +36,29 @@ struct Ctx {
   float rope_theta = 0.0f;
 };
 
+// Entry points run on the context's device and hand the caller's current
+// device back on return (a process may drive several GPUs from one thread).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Shape limits of the decode kernels, checked at the C-ABI (AFDK_ERR_INVALID):
+// the per-request work prefix lives in shared memory (mfa_common.cuh
+// kMaxBatch) and K3 merges at most kMfaMaxSplit parts per request
+// (mfa_decode.cu), which must exceed the SM count.
+constexpr int kMfaMaxBatch = 2048;
+constexpr int kMfaMaxSplit = 160;
+
 // Returns a device workspace of at least `bytes` (grows; not graph-capturable
 // the first time a larger size is requested).
 void* workspace(Ctx& ctx, size_t bytes);
@@ -229,6 +252,34 @@ struct MoeFfnMxArgs {
 };
 size_t moe_ffn_mx_workspace_bytes(int T, int k, int E, int H, int I);
 cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws, cudaStream_t stream);
+
+// 16-bit experts (moe_gemm_bf16.cu, moe_ffn.cu): bf16 dispatch rows, bf16
+// weights, bf16 SwiGLU intermediate, fp32 W2 outputs
+struct MoeGemmBf16Args {
+  const void* w;         // bf16 [(n_local+1) * w_rows, K]
+  const void* x;         // bf16 [rows_pad, K]
+  const moe::Work* work;
+  const int* n_work;
+  int H, I, E, expert_lo, n_local, rows_pad;
+  __nv_bfloat16* h;      // W13 output [rows_pad, I]
+  float* y;              // W2 output [rows_pad, H]
+};
+cudaError_t moe_gemm_bf16_launch(Ctx& ctx, bool glu, const MoeGemmBf16Args& a, cudaStream_t stream);
+struct MoeFfnBf16Args {
+  int T, k, E, H, I;
+  int expert_lo, expert_hi;
+  const void* w13;
+  const void* w2;
+  const void* x;         // bf16 [T, H]
+  const int32_t* ids;
+  const float* weights;
+  int shared_lo, shared_hi;
+  void* out;
+  const uint64_t* dst = nullptr;
+  int rows_per_dst = 0;
+};
+size_t moe_ffn_bf16_workspace_bytes(int T, int k, int E, int H, int I);
+cudaError_t moe_ffn_bf16_launch(Ctx& ctx, const MoeFfnBf16Args& a, void* ws, cudaStream_t stream);
 
 // Dense FFN as n_split slices of the intermediate dimension ("virtual
 // experts" every token visits with weight 1), MXFP8 (moe_ffn.cu)

@@ -380,6 +380,8 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
 }
 
 constexpr int kMaxSplit = 160;  // CTAs one request may span (>= #SMs + 1)
+static_assert(kMaxSplit == kMfaMaxSplit, "afdk_create checks the SM count against kMfaMaxSplit");
+static_assert(kMaxBatch == kMfaMaxBatch, "the C-ABI checks batch against kMfaMaxBatch");
 // K3: merge the split partials of requests that spanned several CTAs (fixed
 // CTA order => deterministic), zero-fill empty requests.  grid (B, R/16): 16
 // rows per CTA, 32 threads per row, 8 dims per thread.

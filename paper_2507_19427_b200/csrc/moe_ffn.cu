@@ -143,6 +143,59 @@ cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cu
   return chk(combine_launch(ca, stream, ctx.pdl), "combine");
 }
 
+// 16-bit variant (QuantScheme with 2-byte FFN weights, types.hpp:34-40):
+// bf16 dispatch rows gathered as 2H-byte rows, bf16 grouped GEMMs, the same
+// permute / combine and partial semantics.
+size_t moe_ffn_bf16_workspace_bytes(int T, int k, int E, int H, int I) {
+  const int rp = moe::rows_pad_mx(T, k);
+  size_t b = 0;
+  b += align_up((size_t)(E + 1) * 4, 256);
+  b += 2 * align_up((size_t)T * k * 4, 256);
+  b += align_up((size_t)moe::max_work(T, k, E) * sizeof(moe::Work), 256);
+  b += 256;
+  b += align_up((size_t)rp * H * 2, 256);  // xp
+  b += align_up((size_t)rp * I * 2, 256);  // h
+  b += align_up((size_t)rp * H * 4, 256);  // y
+  return b;
+}
+
+cudaError_t moe_ffn_bf16_launch(Ctx& ctx, const MoeFfnBf16Args& a, void* ws_base, cudaStream_t stream) {
+  const int T = a.T, k = a.k, E = a.E, H = a.H, I = a.I;
+  const int rp = moe::rows_pad_mx(T, k);
+  uint8_t* ws = static_cast<uint8_t*>(ws_base);
+  auto take = [&](size_t bytes) { void* p = ws; ws += align_up(bytes, 256); return p; };
+  auto* offsets = static_cast<int32_t*>(take((size_t)(E + 1) * 4));
+  auto* perm = static_cast<int32_t*>(take((size_t)T * k * 4));
+  auto* inv = static_cast<int32_t*>(take((size_t)T * k * 4));
+  auto* work = static_cast<moe::Work*>(take((size_t)moe::max_work(T, k, E) * sizeof(moe::Work)));
+  auto* n_work = static_cast<int*>(take(256));
+  auto* xp = static_cast<uint8_t*>(take((size_t)rp * H * 2));
+  auto* h = static_cast<__nv_bfloat16*>(take((size_t)rp * I * 2));
+  auto* y = static_cast<float*>(take((size_t)rp * H * 4));
+  const bool shared_local = a.shared_hi > a.shared_lo;
+  cudaError_t e;
+  static const bool dbg = std::getenv("AFDK_DEBUG_SYNC") != nullptr;
+  auto chk = [&](cudaError_t err, const char* what) {
+    if (err == cudaSuccess && dbg) err = cudaStreamSynchronize(stream);
+    if (err != cudaSuccess) set_error(std::string("moe_ffn_bf16/") + what + ": " + cudaGetErrorString(err));
+    return err;
+  };
+  moe::PermuteArgs pa{a.ids, T, k, E, a.expert_lo, a.expert_hi, shared_local ? 1 : 0, a.shared_lo, a.shared_hi,
+                      offsets, perm, inv, work, n_work, moe::kChunkMX};
+  if ((e = chk(permute_launch(pa, stream, ctx.pdl), "permute")) != cudaSuccess) return e;
+  // rows of 2H bytes, no scales
+  moe::GatherArgs ga{static_cast<const uint8_t*>(a.x), nullptr, perm, T, k, 2 * H, rp, xp, nullptr, nullptr, nullptr};
+  if ((e = chk(gather_launch(ga, stream, ctx.pdl), "gather")) != cudaSuccess) return e;
+  const int n_local = a.expert_hi - a.expert_lo;
+  MoeGemmBf16Args g13{a.w13, xp, work, n_work, H, I, E, a.expert_lo, n_local, rp, h, nullptr};
+  if ((e = chk(moe_gemm_bf16_launch(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
+  MoeGemmBf16Args g2{a.w2, h, work, n_work, H, I, E, a.expert_lo, n_local, rp, nullptr, y};
+  if ((e = chk(moe_gemm_bf16_launch(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
+  moe::CombineArgs ca{y, a.ids, a.weights, inv, T, k, H, a.expert_lo, a.expert_hi, shared_local ? 1 : 0,
+                      a.shared_lo, a.shared_hi, static_cast<__nv_bfloat16*>(a.out), a.dst, a.rows_per_dst};
+  return chk(combine_launch(ca, stream, ctx.pdl), "combine");
+}
+
 // ------------------------------------------------------------- dense FFN
 // The 5 dense Step-3 layers (inter 18432, builtin_catalog.cpp:248-250) run
 // through the grouped MXFP8 GEMMs: slice j of the intermediate dimension is a

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
   if (a.xs) {
     const int nb = a.H / 128;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) a.xs_t[(size_t)b * a.rows_pad + s] = __ldg(a.xs + (size_t)src * nb + b);
-  } else {
+  } else if (a.xsf) {
     const int nb = a.H / 32;  // MXFP8: copy the row's UE8M0 scales
     for (int b = threadIdx.x; b < nb; b += blockDim.x) a.xsf_p[(size_t)s * nb + b] = __ldg(a.xsf + (size_t)src * nb + b);
   }

@@ -24,3 +24,22 @@ def rel_err(got, ref):
     got = np.asarray(got, np.float64)
     ref = np.asarray(ref, np.float64)
     return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-12))
+
+
+def rel_fro(got, ref):
+    """normwise relative error ||got-ref||_2 / ||ref||_2 (accuracy of a format)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+def record(name, **vals):
+    """Append a measured parity figure to $PARITY_LOG (JSON lines) when set, so
+    the errors behind DESIGN.md's parity table come from the GPU run itself."""
+    import json
+    import os
+
+    path = os.environ.get("PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"test": name, **{k: float(v) for k, v in vals.items()}}) + "\n")

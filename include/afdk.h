@@ -68,6 +68,8 @@ afdk_status afdk_create(afdk_ctx** out, const afdk_cfg* cfg);
 void afdk_destroy(afdk_ctx* ctx);
 /* SMs the persistent kernels of this context are sized for */
 int afdk_num_sms(const afdk_ctx* ctx);
+/* the CUDA device the context was created on (-1 for NULL) */
+int afdk_ctx_device(const afdk_ctx* ctx);
 
 /* ---------------------------------------------------------------- K2 + K3
  * MFA decode attention core.  One shared K head and one shared V head of
@@ -363,6 +365,130 @@ afdk_status afdk_wait(afdk_ctx* ctx, const uint32_t* flag, uint32_t value, afdk_
  * base may be NULL; count % 8 == 0.                                        */
 afdk_status afdk_add_partials(afdk_ctx* ctx, const void* base, const void* const* parts_dev, int n, size_t count,
                               void* out, afdk_stream stream);
+
+/* --------------------------------------------- AFD pipeline runtime (C++)
+ * The A -> link -> F -> link schedule of a decode layer that
+ * pipesim.cpp:155-237 models (ping-pong micro-batches, PAPER.md:690-724:
+ * StepMesh's pattern, here on NVLink inside one box), as a host runtime in
+ * C++ behind this C-ABI.  One afdk_afd per GPU (one process per GPU):
+ * attention ranks [0, n_attn) hold their requests (DP attention,
+ * PAPER.md:649), FFN ranks [n_attn, n_attn+n_ffn) hold experts
+ * [f*E/nF, (f+1)*E/nF) and a 1/nF share of the shared expert's tokens
+ * (expert parallel; dense layers: intermediate slices, tensor parallel).
+ *
+ * Ownership: the runtime owns the exchange buffers (A->F payload, F->A
+ * partial rows, sequence flags), the h_res/h_norm scratch, its streams (one
+ * per micro-batch + one copy stream) and the peer mappings; the caller owns
+ * weights, KV caches and the layer activations x (read and overwritten by
+ * afdk_afd_attn_layer).
+ *
+ * Rendezvous: afdk_afd_create calls allgather(user, mine, bytes, all) — any
+ * transport (torch.distributed, MPI, sockets) that concatenates every rank's
+ * `bytes` in rank order into `all` and returns 0 on success.  It is called
+ * twice (allocation status + IPC handles; then a barrier once the peers are
+ * mapped).  A rank that failed to allocate makes EVERY rank's create fail
+ * before any peer is mapped, instead of leaving peers waiting on flags.
+ *
+ * Schedule of one layer at sequence number s (afdk_afd_plan returns the op
+ * list the runtime executes; host only, no GPU needed):
+ *   attention rank a, micro-batch m (stream m):
+ *     ATTN(m) [mfa_layer in attn_chunk pieces; router + dispatch payload]
+ *     -> SIGNAL(FFN f, slot a*n_micro+m, s) for every f
+ *     -> WAIT(slot f*n_micro+m, s) [+ PULL f's partial rows if f2a=pull]
+ *     -> REDUCE(m) [x = h_res + sum_f partial_f]
+ *   FFN rank f, micro-batch m:
+ *     copy stream: WAIT(slot a*n_micro+m, s) + PULL a's payload, every a
+ *     -> JOIN(m) (compute stream waits for the copy stream)
+ *     -> FFN(m) [push: its combine stores rows into the attention GPUs]
+ *     -> SIGNAL(attention a, slot f*n_micro+m, s) for every a
+ * Flags are monotone (s = 1, 2, ...), so every cross-layer buffer reuse is
+ * ordered by a flag of the next layer (a payload is rewritten only after
+ * the FFN signalled that it consumed it, and so on).                      */
+#define AFDK_AFD_MAX_MICRO 4
+enum { AFDK_FFN_FP8 = 0, AFDK_FFN_MX = 1, AFDK_FFN_BF16 = 2 };
+enum { AFDK_LAYER_MOE = 0, AFDK_LAYER_DENSE = 1 };
+enum { AFDK_F2A_PUSH = 0, AFDK_F2A_PULL = 1 };
+
+typedef struct afdk_afd_cfg {
+  int n_attn, n_ffn, n_micro;  /* n_micro <= AFDK_AFD_MAX_MICRO (2 = ping-pong)        */
+  int T_mb;                    /* decode requests per micro-batch per attention rank  */
+  int hidden, top_k, n_experts, inter;
+  int dense_inter, dense_slices;  /* dense layers: inter and slices per FFN rank      */
+  int ffn_format;              /* AFDK_FFN_*                                          */
+  int layer_kind;              /* AFDK_LAYER_* (dense layers: MXFP8 slices)           */
+  int f2a;                     /* AFDK_F2A_*                                          */
+  int attn_chunk;              /* requests per attention-layer call, 1..256           */
+} afdk_afd_cfg;
+
+enum { AFDK_OP_ATTN = 0, AFDK_OP_SIGNAL = 1, AFDK_OP_WAIT = 2, AFDK_OP_PULL = 3, AFDK_OP_REDUCE = 4,
+       AFDK_OP_JOIN = 5, AFDK_OP_FFN = 6 };
+enum { AFDK_BUF_SEND = 0, AFDK_BUF_RECV = 1, AFDK_BUF_RX = 2, AFDK_BUF_OUT = 3 };
+
+typedef struct afdk_afd_op {
+  int kind;        /* AFDK_OP_*                                                  */
+  int stream;      /* 0..n_micro-1: micro-batch streams; n_micro: copy stream    */
+  int mb;          /* micro-batch                                                */
+  int peer;        /* SIGNAL target / PULL source rank, else -1                  */
+  int slot;        /* flag slot (on the peer for SIGNAL, local for WAIT)         */
+  uint32_t value;  /* sequence number                                            */
+  int src_buf, dst_buf;            /* PULL: peer buffer kind -> local buffer kind */
+  size_t src_off, dst_off, bytes;  /* PULL byte range                            */
+} afdk_afd_op;
+
+/* payload section offsets/sizes of one A->F message (xq, scales, ids, wts;
+ * 256-B aligned) and of the FFN's receive buffer (n_attn messages). */
+typedef struct afdk_afd_layout {
+  size_t off[4], size[4], total;        /* one attention rank's payload     */
+  size_t rx_off[4], rx_total;           /* FFN receive buffer (n_attn each) */
+  size_t part_bytes;                    /* one T_mb x hidden bf16 partial   */
+} afdk_afd_layout;
+
+afdk_status afdk_afd_check_cfg(const afdk_afd_cfg* cfg);
+afdk_status afdk_afd_get_layout(const afdk_afd_cfg* cfg, afdk_afd_layout* out);
+afdk_status afdk_afd_plan(const afdk_afd_cfg* cfg, int rank, uint32_t seq, afdk_afd_op* ops, int cap,
+                          int* n_ops);
+
+typedef int (*afdk_allgather_fn)(void* user, const void* mine, size_t bytes, void* all);
+typedef struct afdk_afd afdk_afd;
+
+/* ctxs: n_micro contexts on this rank's device (each micro-batch stream uses
+ * its own workspace); rank in [0, n_attn + n_ffn). */
+afdk_status afdk_afd_create(afdk_ctx* const* ctxs, const afdk_afd_cfg* cfg, int rank, afdk_allgather_fn allgather,
+                            void* user, afdk_afd** out);
+void afdk_afd_destroy(afdk_afd* afd);
+
+/* attention rank: one layer for every micro-batch (enqueue only) */
+typedef struct afdk_afd_attn_mb {
+  void* x;                  /* bf16 [T_mb, hidden] in: layer input, out: next layer input */
+  void* k_cache;            /* bf16 or e4m3 (k_scale > 0) [num_pages, page, head_dim]     */
+  void* v_cache;
+  int num_pages, page_size, max_pages;
+  const int32_t* block_table;  /* [T_mb, max_pages] */
+  const int32_t* seq_lens;     /* [T_mb]            */
+  float k_scale, v_scale;      /* 0: bf16 KV; > 0: e4m3 KV with these per-tensor scales   */
+} afdk_afd_attn_mb;
+afdk_status afdk_afd_attn_layer(afdk_afd* afd, const afdk_mfa_weights* w, const void* gate_w,
+                                const afdk_afd_attn_mb* mbs);
+
+/* FFN rank: one layer for every micro-batch.  MoE: the local routed experts
+ * then the shared expert (the afdk_moe_ffn* layouts of the format); dense:
+ * this rank's dense_slices intermediate slices (afdk_dense_ffn_mx layout). */
+typedef struct afdk_afd_ffn_weights {
+  const void* w13;
+  const void* s13;  /* fp8: fp32 128x128 scales; mx: UE8M0; bf16: NULL */
+  const void* w2;
+  const void* s2;
+} afdk_afd_ffn_weights;
+afdk_status afdk_afd_ffn_layer(afdk_afd* afd, const afdk_afd_ffn_weights* w);
+
+/* the runtime's streams (i in [0, n_micro]: micro-batch streams, then the
+ * copy stream) for event timing / joins; a runtime buffer (AFDK_BUF_*, or
+ * 4 = h_res, 5 = h_norm) of micro-batch mb for inspection; sequence number
+ * of the last enqueued layer; block the host until every stream is idle. */
+afdk_stream afdk_afd_stream(afdk_afd* afd, int i);
+void* afdk_afd_buffer(afdk_afd* afd, int which, int mb);
+uint32_t afdk_afd_seq(const afdk_afd* afd);
+afdk_status afdk_afd_sync(afdk_afd* afd);
 
 /* ------------------------------------------------ measured stage times
  * The measured counterpart of derive_stage_times (pipesim.cpp:59-127): runs

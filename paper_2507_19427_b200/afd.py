@@ -1,30 +1,36 @@
-"""Attention-FFN Disaggregation runtime inside one B200 box (config 5).
+"""Attention-FFN Disaggregation inside one B200 box (config 5): Python binding
+of the C++ AFD runtime (csrc/afd_runtime.cu, include/afdk.h afdk_afd_*).
 
 nA attention GPUs each own their decode requests (DP attention)
 and run the attention-side layer + router; nF FFN GPUs each hold 48/nF routed
-experts (expert parallel) and a share of the shared expert's tokens.  Per
-layer and micro-batch (pipesim.cpp:155-237 models it):
+experts (expert parallel) and a share of the shared expert's tokens.  The
+per-layer schedule (pipesim.cpp:155-237 models it) — op
+list, flags, transfers, streams and peer mappings — lives in the C++ runtime
+(afdk_afd_plan / afdk_afd_attn_layer / afdk_afd_ffn_layer).  This module
+holds only:
 
-  A: mfa_layer -> router/quant into its send buffer -> signal every F
-  F: wait all A -> DMA-pull payloads (fp8 tokens, scales, top-k) -> moe_ffn(_mx)
-     whose combine kernel stores each token's bf16 partial row straight into
-     the owning attention GPU's receive buffer over NVLink -> signal every A
-     (f2a="pull": local partial, the attention GPU DMA-pulls its rows)
-  A: wait all F -> x = h_res + sum partials
+  * AfdConfig: the validated configuration (mirrored into afdk_afd_cfg);
+  * the shard arithmetic and wire accounting the bench and tests report;
+  * AfdRank: synthetic weights / KV caches for one rank (caller-owned data
+    in the C-ABI's ownership model) and the rendezvous callback that hands
+    the runtime's 72-byte IPC handles to torch.distributed.
 
-n_micro micro-batches per attention GPU run on their own streams (ping-pong),
-so the attention of one overlaps the exchange/FFN of the other.  All data
-moves with copy-engine DMA over NVLink and stream-ordered flags
-(csrc/exchange.cu): no SM is spent on communication and no host round trip
-sits on the per-message path.  One process per GPU; torch.distributed is used
-only to exchange IPC handles, for barriers and to reduce the timing.
-
-The shard/layout helpers are pure Python and are exercised by the CPU suite
-(tests/test_afd_cpu.py, gloo world size 2-3).
+One process per GPU; torch.distributed only exchanges handles, runs
+barriers and reduces timings.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+import ctypes
+from ctypes import c_int, c_void_p
+from dataclasses import dataclass
+
+from . import afdk as _k
+
+FFN_FORMATS = {"fp8": 0, "mx": 1, "bf16": 2}
+LAYER_KINDS = {"moe": 0, "dense": 1}
+F2A = {"push": 0, "pull": 1}
+OP_NAMES = {0: "ATTN", 1: "SIGNAL", 2: "WAIT", 3: "PULL", 4: "REDUCE", 5: "JOIN", 6: "FFN"}
+BUF_SEND, BUF_RECV, BUF_RX, BUF_OUT, BUF_H_RES, BUF_H_NORM = 0, 1, 2, 3, 4, 5
 
 
 @dataclass
@@ -44,39 +50,28 @@ class AfdConfig:
     top_k: int = 3
     inter: int = 5120
     seed: int = 0
-    ffn_format: str = "fp8"   # "fp8": 1x128/128x128 fp32 scales; "mx": MXFP8 (UE8M0 per 32)
+    ffn_format: str = "fp8"   # "fp8": 1x128/128x128 fp32 scales; "mx": MXFP8; "bf16": 16-bit experts
     f2a: str = "push"         # "push": the FFN combine writes into the attention GPUs' receive
                               # buffers over NVLink (fused); "pull": attention DMA-pulls
     layer_kind: str = "moe"   # "moe": routed experts (EP over FFN GPUs); "dense": the dense Step-3
-                              # FFN (inter dense_inter) as intermediate slices, tensor-parallel over FFN GPUs
+                              # FFN (inter dense_inter) as intermediate slices, tensor-parallel
     dense_inter: int = 18432
     attn_chunk: int = 256     # requests per attention-layer call (its GEMM N limit); a larger
-                              # T_mb runs the attention side in chunks and ships ONE payload,
-                              # so the FFN tier streams its expert weights once per micro-batch
+                              # T_mb runs the attention side in chunks and ships ONE payload
+    kv: str = "bf16"          # attention KV cache: "bf16" or "e4m3" (per-tensor scales)
 
     def __post_init__(self):
-        # validated identically on every rank before any buffer exchange: a rank
-        # that failed mid-pipeline would leave its peers waiting on a flag
-        if not 1 <= self.attn_chunk <= 256:
-            raise ValueError(f"attn_chunk={self.attn_chunk}: the attention-side layer takes 1..256 requests per call")
-        if not 1 <= self.T_mb <= 4096:
-            raise ValueError(f"T_mb={self.T_mb}: expected 1..4096 requests per micro-batch")
-        if self.f2a not in ("push", "pull"):
-            raise ValueError(f"f2a={self.f2a!r}: expected 'push' or 'pull'")
-        if self.ffn_format not in ("fp8", "mx"):
-            raise ValueError(f"ffn_format={self.ffn_format!r}: expected 'fp8' or 'mx'")
-        if self.ffn_format == "mx" and (self.hidden % 512 or self.inter % 512):
-            raise ValueError("ffn_format='mx' needs hidden and inter to be multiples of 512")
-        if self.layer_kind not in ("moe", "dense"):
+        # validated identically on every rank before any buffer exchange
+        if self.ffn_format not in FFN_FORMATS:
+            raise ValueError(f"ffn_format={self.ffn_format!r}: expected one of {sorted(FFN_FORMATS)}")
+        if self.layer_kind not in LAYER_KINDS:
             raise ValueError(f"layer_kind={self.layer_kind!r}: expected 'moe' or 'dense'")
-        if self.layer_kind == "dense":
-            if self.ffn_format != "mx":
-                raise ValueError("layer_kind='dense' runs the MXFP8 dense FFN (ffn_format='mx')")
-            if self.dense_inter % (self.dense_slices_total * 512):
-                raise ValueError(f"dense_inter={self.dense_inter} is not a multiple of "
-                                 f"{self.dense_slices_total} slices x 512")
-        if self.n_attn < 1 or self.n_ffn < 1 or self.n_ffn > self.n_experts:
-            raise ValueError("need at least one attention and one FFN GPU, n_ffn <= n_experts")
+        if self.f2a not in F2A:
+            raise ValueError(f"f2a={self.f2a!r}: expected 'push' or 'pull'")
+        if self.kv not in ("bf16", "e4m3"):
+            raise ValueError(f"kv={self.kv!r}: expected 'bf16' or 'e4m3'")
+        if _k.load().afdk_afd_check_cfg(ctypes.byref(self.c_cfg())) != 0:
+            raise ValueError(_k.load().afdk_last_error().decode())
 
     @property
     def dense_slices_per_gpu(self) -> int:
@@ -98,6 +93,48 @@ class AfdConfig:
         """tokens one FFN GPU sees per micro-batch (broadcast from every attention GPU)"""
         return self.n_attn * self.T_mb
 
+    def c_cfg(self) -> "AfdCfg":
+        return AfdCfg(self.n_attn, self.n_ffn, self.n_micro, self.T_mb, self.hidden, self.top_k, self.n_experts,
+                      self.inter, self.dense_inter, self.dense_slices_per_gpu, FFN_FORMATS[self.ffn_format],
+                      LAYER_KINDS[self.layer_kind], F2A[self.f2a], self.attn_chunk)
+
+
+AfdCfg, AfdOp, AfdLayout, AfdAttnMb, AfdFfnWeights, ALLGATHER = (
+    _k.AfdCfg, _k.AfdOp, _k.AfdLayout, _k.AfdAttnMb, _k.AfdFfnWeights, _k.ALLGATHER)
+
+
+def layout(cfg: AfdConfig) -> AfdLayout:
+    """Payload / receive-buffer layout the runtime uses (afdk_afd_get_layout)."""
+    L = AfdLayout()
+    _k.check(_k.load().afdk_afd_get_layout(ctypes.byref(cfg.c_cfg()), ctypes.byref(L)))
+    return L
+
+
+def plan(cfg: AfdConfig, rank: int, seq: int) -> list[AfdOp]:
+    """The op list the runtime executes for one layer on `rank` (host only)."""
+    lib, c = _k.load(), cfg.c_cfg()
+    n = c_int(0)
+    _k.check(lib.afdk_afd_plan(ctypes.byref(c), rank, seq, None, 0, ctypes.byref(n)))
+    ops = (AfdOp * n.value)()
+    _k.check(lib.afdk_afd_plan(ctypes.byref(c), rank, seq, ctypes.cast(ops, c_void_p), n.value, ctypes.byref(n)))
+    return list(ops)
+
+
+class PayloadLayout:
+    """Python view of one A->F message's sections (xq, xs, ids, wts)."""
+
+    NAMES = ("xq", "xs", "ids", "wts")
+
+    def __init__(self, cfg: AfdConfig):
+        L = layout(cfg)
+        self.off = {n: L.off[i] for i, n in enumerate(self.NAMES)}
+        self._size = {n: L.size[i] for i, n in enumerate(self.NAMES)}
+        self.rx_off = {n: L.rx_off[i] for i, n in enumerate(self.NAMES)}
+        self.nbytes, self.rx_total, self.part_bytes = L.total, L.rx_total, L.part_bytes
+
+    def size(self, name: str) -> int:
+        return self._size[name]
+
 
 def shard(i: int, n: int, total: int) -> tuple[int, int]:
     """Contiguous split of `total` items over `n` owners (owner i's [lo, hi))."""
@@ -112,40 +149,16 @@ def shared_token_shard(f: int, cfg: AfdConfig) -> tuple[int, int]:
     return shard(f, cfg.n_ffn, cfg.T_ffn)
 
 
-@dataclass
-class PayloadLayout:
-    """A->F message of one micro-batch, one contiguous buffer per attention GPU:
-    e4m3 tokens | scales | int32 top-k ids | fp32 top-k weights.  The scale
-    section is T*H/32 bytes in both formats (fp32 per 1x128 block, or one
-    UE8M0 byte per 32 elements for MXFP8)."""
-
-    T: int
-    H: int
-    k: int
-    off: dict = field(default_factory=dict)
-    nbytes: int = 0
-
-    def __post_init__(self):
-        o = 0
-        for name, n in (("xq", self.T * self.H), ("xs", self.T * (self.H // 128) * 4), ("ids", self.T * self.k * 4),
-                        ("wts", self.T * self.k * 4)):
-            self.off[name] = o
-            o += (n + 255) // 256 * 256
-        self.nbytes = o
-
-    def size(self, name: str) -> int:
-        return {"xq": self.T * self.H, "xs": self.T * (self.H // 128) * 4, "ids": self.T * self.k * 4,
-                "wts": self.T * self.k * 4}[name]
-
-
 def wire_bytes(cfg: AfdConfig) -> dict:
     """Bytes crossing NVLink per layer per micro-batch (the moeplan.cpp:17-20
-    accounting (1+2)*H*T plus the scale/top-k metadata)."""
+    accounting (dispatch + combine)*H*T plus the scale/top-k metadata,
+    PAPER.md:655; dispatch = 1 byte for the FP8 formats, 2 for bf16)."""
     T = cfg.n_attn * cfg.T_mb
-    lay = PayloadLayout(cfg.T_mb, cfg.hidden, cfg.top_k)
-    a2f = cfg.n_ffn * cfg.n_attn * sum(lay.size(n) for n in ("xq", "xs", "ids", "wts"))
+    L = PayloadLayout(cfg)
+    a2f = cfg.n_ffn * cfg.n_attn * sum(L.size(n) for n in PayloadLayout.NAMES)
     f2a = cfg.n_ffn * T * cfg.hidden * 2
-    return {"a2f": a2f, "f2a": f2a, "payload_a2f": cfg.n_ffn * T * cfg.hidden, "payload_f2a": f2a}
+    disp = 2 if cfg.ffn_format == "bf16" else 1
+    return {"a2f": a2f, "f2a": f2a, "payload_a2f": cfg.n_ffn * T * cfg.hidden * disp, "payload_f2a": f2a}
 
 
 def flag_index(peer: int, mb: int, cfg: AfdConfig) -> int:
@@ -153,9 +166,10 @@ def flag_index(peer: int, mb: int, cfg: AfdConfig) -> int:
     return peer * cfg.n_micro + mb
 
 
-# ---------------------------------------------------------------- GPU runtime
+# ---------------------------------------------------------------- GPU rank
 class AfdRank:
-    """One GPU of the AFD group.  Call setup() once (collective), then step()."""
+    """One GPU of the AFD group: synthetic caller-owned data + the C++ runtime.
+    Call setup() once (collective), then step()."""
 
     def __init__(self, ctxs, cfg: AfdConfig, rank: int, torch, dist, dev):
         """ctxs: one afdk Context per micro-batch stream (each owns its workspace)."""
@@ -164,16 +178,10 @@ class AfdRank:
         self.cfg, self.rank, self.torch, self.dist, self.dev = cfg, rank, torch, dist, dev
         self.role = cfg.role(rank)
         self.idx = rank if self.role == "attn" else rank - cfg.n_attn
-        self.lay = PayloadLayout(cfg.T_mb, cfg.hidden, cfg.top_k)
-        self.epoch = 0
-        self.streams = [torch.cuda.Stream(device=dev) for _ in range(cfg.n_micro)]
-        self.copy_stream = torch.cuda.Stream(device=dev)
-        self.flags = torch.zeros(256, dtype=torch.int32, device=dev)
-        self.peer_flags = {}
-        self.peer_bufs = {}
-        self.peer_recv = {}
+        self.lay = PayloadLayout(cfg)
+        self.handle = None
 
-    # ---------------------------------------------------------------- setup
+    # ---------------------------------------------------------------- data
     def _weights_attn(self, g):
         t, c = self.torch, self.cfg
         bf = lambda x: x.to(t.bfloat16).to(self.dev)
@@ -186,14 +194,18 @@ class AfdRank:
                 "gate": bf(t.randn(c.n_experts, c.hidden, generator=g) / c.hidden ** 0.5)}
 
     def expert_weights(self, lo, hi, with_shared=True):
-        """Deterministic e4m3 expert weights: expert e's tensors depend only on
-        (seed, e), so every GPU materialises identical shards."""
+        """Deterministic expert weights in cfg.ffn_format: expert e's tensors
+        depend only on (seed, e), so every GPU materialises identical shards."""
         t, c = self.torch, self.cfg
         ids = list(range(lo, hi)) + ([c.n_experts] if with_shared else [])
-        mx = c.ffn_format == "mx"
         w13, w2, s13, s2 = [], [], [], []
         for e in ids:
             g = t.Generator(device=self.dev).manual_seed(c.seed * 1000 + e + 1)
+            if c.ffn_format == "bf16":
+                w13.append((t.randn(2 * c.inter, c.hidden, generator=g, device=self.dev) / c.hidden ** 0.5)
+                           .to(t.bfloat16))
+                w2.append((t.randn(c.hidden, c.inter, generator=g, device=self.dev) / c.inter ** 0.5).to(t.bfloat16))
+                continue
 
             def e4m3(shape):
                 mag = t.randint(0x18, 0x40, shape, generator=g, dtype=t.int32, device=self.dev)
@@ -202,17 +214,18 @@ class AfdRank:
 
             w13.append(e4m3((2 * c.inter, c.hidden)))
             w2.append(e4m3((c.hidden, c.inter)))
-            if mx:  # UE8M0 2^-7: |w| ~ 2^-6..2^-3 like the 1x128 recipe below
+            if c.ffn_format == "mx":  # UE8M0 2^-7: |w| ~ 2^-6..2^-3 like the 1x128 recipe below
                 s13.append(t.full((2 * c.inter, c.hidden // 32), 120, dtype=t.uint8, device=self.dev))
                 s2.append(t.full((c.hidden, c.inter // 32), 120, dtype=t.uint8, device=self.dev))
             else:
                 s13.append(t.full((2 * c.inter // 128, c.hidden // 128), 0.5 / c.hidden ** 0.5, device=self.dev))
                 s2.append(t.full((c.hidden // 128, c.inter // 128), 0.5 / c.inter ** 0.5, device=self.dev))
-        if mx:
-            return {"n_experts": c.n_experts, "w13": t.stack(w13), "w2": t.stack(w2), "sf13": t.stack(s13),
-                    "sf2": t.stack(s2)}
-        return {"n_experts": c.n_experts, "w13": t.stack(w13), "w2": t.stack(w2), "s13": t.stack(s13),
-                "s2": t.stack(s2)}
+        w = {"n_experts": c.n_experts, "w13": t.stack(w13), "w2": t.stack(w2)}
+        if c.ffn_format == "mx":
+            w.update(sf13=t.stack(s13), sf2=t.stack(s2))
+        elif c.ffn_format == "fp8":
+            w.update(s13=t.stack(s13), s2=t.stack(s2))
+        return w
 
     def dense_weights(self, lo, hi):
         """MXFP8 slices [lo, hi) of the dense FFN (slice layout of afdk_dense_ffn_mx);
@@ -235,24 +248,8 @@ class AfdRank:
                 "sf13": t.full((n, 2 * Is, c.hidden // 32), 120, dtype=t.uint8, device=self.dev),
                 "sf2": t.full((n, c.hidden, Is // 32), 120, dtype=t.uint8, device=self.dev)}
 
-    def setup(self):
-        """alloc() on every rank, agree that all succeeded, then connect().
-        A rank that failed to allocate makes EVERY rank raise here, before any
-        buffer exchange, instead of leaving its peers waiting on a flag."""
-        err = None
-        try:
-            mine = self.alloc()
-        except Exception as e:  # noqa: BLE001 - reported on all ranks below
-            err, mine = e, None
-        on_gloo = self.dist.get_backend() == "gloo"  # CPU rendezvous (tests, oversubscribed checks)
-        ok = self.torch.tensor([0 if err else 1], dtype=self.torch.int32, device="cpu" if on_gloo else self.dev)
-        self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN)
-        if int(ok.item()) == 0:
-            raise RuntimeError(f"AFD setup failed on some rank (this rank: {err!r})")
-        self.connect(mine)
-
-    def alloc(self) -> dict:
-        """Local allocations and IPC handle export (no collectives)."""
+    def alloc(self) -> None:
+        """Caller-owned data of this rank (weights, KV caches, activations)."""
         t, c, dev = self.torch, self.cfg, self.dev
         g = t.Generator().manual_seed(c.seed)
         if self.role == "attn":
@@ -261,13 +258,6 @@ class AfdRank:
             gx = t.Generator().manual_seed(c.seed + 7 + self.idx)
             self.x0 = [t.randn(c.T_mb, c.hidden, generator=gx).to(t.bfloat16).to(dev) for _ in range(c.n_micro)]
             self.x = [x.clone() for x in self.x0]
-            self.h_res = [t.empty_like(x) for x in self.x0]
-            self.h_norm = [t.empty_like(x) for x in self.x0]
-            self.send = [t.empty(self.lay.nbytes, dtype=t.uint8, device=dev) for _ in range(c.n_micro)]
-            self.recv_part = [t.empty(c.n_ffn, c.T_mb, c.hidden, dtype=t.bfloat16, device=dev)
-                              for _ in range(c.n_micro)]
-            self.part_ptrs = [t.tensor([rp[f].data_ptr() for f in range(c.n_ffn)], dtype=t.int64, device=dev)
-                              for rp in self.recv_part]
             self.kv = []
             for _ in range(c.layers):
                 per_mb = []
@@ -275,13 +265,28 @@ class AfdRank:
                     n_pages = c.T_mb * pages
                     k = t.empty(n_pages, c.page, c.head_dim, dtype=t.bfloat16, device=dev).normal_()
                     v = t.empty(n_pages, c.page, c.head_dim, dtype=t.bfloat16, device=dev).normal_()
+                    if c.kv == "e4m3":  # per-tensor scales (amax / 448)
+                        ks, vs = float(k.abs().max()) / 448.0, float(v.abs().max()) / 448.0
+                        k = (k.float() / ks).to(t.float8_e4m3fn).view(t.uint8)
+                        v = (v.float() / vs).to(t.float8_e4m3fn).view(t.uint8)
+                    else:
+                        ks = vs = 0.0
                     bt = t.randperm(n_pages, device=dev).to(t.int32).view(c.T_mb, pages).contiguous()
-                    per_mb.append((k, v, bt))
+                    per_mb.append((k, v, bt, ks, vs))
                 self.kv.append(per_mb)
             self.seq_lens = t.full((c.T_mb,), c.ctx_len, dtype=t.int32, device=dev)
-            mine = {"flags": self.ctx.ipc_handle(self.flags),
-                    "send": [self.ctx.ipc_handle(b) for b in self.send],
-                    "recv": [self.ctx.ipc_handle(b) for b in self.recv_part]}
+            w = self.w
+            self.c_w = _k.MfaWeights(c.hidden, c.q_lora, c.n_heads, c.head_dim, _k.ptr(w["in_norm"]), _k.ptr(w["qkv"]),
+                                     _k.ptr(w["q_norm"]), _k.ptr(w["q_up"]), _k.ptr(w["o"]), _k.ptr(w["post_norm"]),
+                                     1e-5, 5e5, c.head_dim ** -0.5)
+            self.c_mbs = []
+            for layer in range(c.layers):
+                arr = (AfdAttnMb * c.n_micro)()
+                for mb in range(c.n_micro):
+                    k, v, bt, ks, vs = self.kv[layer][mb]
+                    arr[mb] = AfdAttnMb(_k.ptr(self.x[mb]), _k.ptr(k), _k.ptr(v), k.shape[0], c.page, bt.shape[1],
+                                        _k.ptr(bt), _k.ptr(self.seq_lens), ks, vs)
+                self.c_mbs.append(arr)
         else:
             lo, hi = expert_shard(self.idx, c)
             if c.layer_kind == "dense":
@@ -291,110 +296,62 @@ class AfdRank:
                 self.moe_w = self.expert_weights(lo, hi)
             self.expert_lo, self.expert_hi = lo, hi
             self.shared = shared_token_shard(self.idx, c)
-            Tf = c.T_ffn
-            xs_shape, xs_dtype = ((Tf, c.hidden // 32), t.uint8) if c.ffn_format == "mx" else \
-                ((Tf, c.hidden // 128), t.float32)
-            self.rx = [{"xq": t.empty(Tf, c.hidden, dtype=t.uint8, device=dev),
-                        "xs": t.empty(*xs_shape, dtype=xs_dtype, device=dev),
-                        "ids": t.empty(Tf, c.top_k, dtype=t.int32, device=dev),
-                        "wts": t.empty(Tf, c.top_k, dtype=t.float32, device=dev)} for _ in range(c.n_micro)]
-            self.out = [t.empty(Tf, c.hidden, dtype=t.bfloat16, device=dev) for _ in range(c.n_micro)]
-            self.copied = [t.cuda.Event() for _ in range(c.n_micro)]
-            mine = {"flags": self.ctx.ipc_handle(self.flags), "out": [self.ctx.ipc_handle(b) for b in self.out]}
-        return mine
+            mw = self.moe_w
+            s13 = mw.get("sf13", mw.get("s13"))
+            s2 = mw.get("sf2", mw.get("s2"))
+            self.c_ffn_w = AfdFfnWeights(_k.ptr(mw["w13"]), _k.ptr(s13), _k.ptr(mw["w2"]), _k.ptr(s2))
 
-    def connect(self, mine: dict) -> None:
-        """Collective: exchange IPC handles and open the peers' buffers."""
-        t, c, dev = self.torch, self.cfg, self.dev
-        allh = [None] * c.world
-        self.dist.all_gather_object(allh, (self.rank, mine))
-        for r, h in allh:
-            if r == self.rank:
-                continue
-            peer_role = c.role(r)
-            if peer_role == self.role:
-                continue  # attention GPUs never talk to each other, nor FFN GPUs
-            self.peer_flags[r] = self.ctx.ipc_open(h["flags"])
-            key = "send" if peer_role == "attn" else "out"
-            self.peer_bufs[r] = [self.ctx.ipc_open(x) for x in h[key]]
-            if peer_role == "attn" and c.f2a == "push":
-                self.peer_recv[r] = [self.ctx.ipc_open(x) for x in h["recv"]]
-        if self.role == "ffn" and c.f2a == "push":
-            # my slot f of every attention GPU's [n_ffn, T_mb, H] receive buffer
-            slot = self.idx * c.T_mb * c.hidden * 2
-            self.dst = [t.tensor([self.peer_recv[a][mb] + slot for a in range(c.n_attn)], dtype=t.int64,
-                                 device=dev) for mb in range(c.n_micro)]
-        t.cuda.synchronize()
-        self.dist.barrier()
+    def _allgather(self, user, mine, nbytes, out):
+        """Rendezvous callback of afdk_afd_create (torch.distributed transport)."""
+        try:
+            blob = ctypes.string_at(mine, nbytes)
+            got = [None] * self.cfg.world
+            self.dist.all_gather_object(got, blob)
+            for r, b in enumerate(got):
+                ctypes.memmove(out + r * nbytes, b, nbytes)
+            return 0
+        except Exception:  # noqa: BLE001 - reported as the runtime's create failure
+            return 1
+
+    def setup(self):
+        """alloc() on every rank, agree that all succeeded, then create the
+        runtime (which allocates the exchange buffers, agrees again and maps
+        the peers).  A failing rank makes EVERY rank raise, before any buffer
+        exchange, instead of leaving its peers waiting on a flag."""
+        err = None
+        try:
+            self.alloc()
+        except Exception as e:  # noqa: BLE001 - reported on all ranks below
+            err = e
+        on_gloo = self.dist.get_backend() == "gloo"
+        ok = self.torch.tensor([0 if err else 1], dtype=self.torch.int32, device="cpu" if on_gloo else self.dev)
+        self.dist.all_reduce(ok, op=self.dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            raise RuntimeError(f"AFD setup failed on some rank (this rank: {err!r})")
+        self.torch.cuda.synchronize(self.dev)
+        lib = _k.load()
+        ctx_arr = (c_void_p * self.cfg.n_micro)(*[c.handle for c in self.ctxs])
+        self._cb = ALLGATHER(self._allgather)  # keep alive while the runtime exists
+        h = c_void_p()
+        _k.check(lib.afdk_afd_create(ctx_arr, ctypes.byref(self.cfg.c_cfg()), self.rank, self._cb, None,
+                                     ctypes.byref(h)))
+        self.handle = h
+        self._streams = [self.torch.cuda.ExternalStream(lib.afdk_afd_stream(h, i), device=self.dev)
+                         for i in range(self.cfg.n_micro + 1)]
 
     # ----------------------------------------------------------------- step
-    def _attn_layer(self, layer, mb, seq):
-        c, ctx, t = self.cfg, self.ctxs[mb], self.torch
-        st = self.streams[mb]
-        sp = st.cuda_stream
-        k, v, bt = self.kv[layer][mb]
-        for c0 in range(0, c.T_mb, c.attn_chunk):
-            c1 = min(c.T_mb, c0 + c.attn_chunk)
-            ctx.mfa_layer(self.w, self.x[mb][c0:c1], k, v, bt[c0:c1], self.seq_lens[c0:c1], self.h_res[mb][c0:c1],
-                          self.h_norm[mb][c0:c1], stream=sp)
-        buf, L = self.send[mb], self.lay
-        view = lambda name, shape, dtype: buf[L.off[name]:L.off[name] + L.size(name)].view(dtype).view(*shape)
-        if c.ffn_format == "mx":
-            if c.layer_kind == "moe":
-                ctx.router_topk(self.h_norm[mb], self.w["gate"], c.top_k, view("ids", (c.T_mb, c.top_k), t.int32),
-                                view("wts", (c.T_mb, c.top_k), t.float32), stream=sp)
-            ctx.quant_mx(self.h_norm[mb], view("xq", (c.T_mb, c.hidden), t.uint8),
-                         view("xs", (c.T_mb, c.hidden // 32), t.uint8), stream=sp)
-        else:
-            ctx.router_topk(self.h_norm[mb], self.w["gate"], c.top_k, view("ids", (c.T_mb, c.top_k), t.int32),
-                            view("wts", (c.T_mb, c.top_k), t.float32), xq=view("xq", (c.T_mb, c.hidden), t.uint8),
-                            xs=view("xs", (c.T_mb, c.hidden // 128), t.float32), stream=sp)
-        for f in range(c.n_ffn):
-            r = c.n_attn + f
-            ctx.signal(self.peer_flags[r] + 4 * flag_index(self.idx, mb, c), seq, stream=sp)
-        # F -> A: pull this GPU's rows of every FFN partial, then residual + EP reduction
-        row_bytes = c.T_mb * c.hidden * 2
-        for f in range(c.n_ffn):
-            r = c.n_attn + f
-            ctx.wait(self.flags.data_ptr() + 4 * flag_index(f, mb, c), seq, stream=sp)
-            if c.f2a == "pull":
-                ctx.copy(self.recv_part[mb][f].data_ptr(), self.peer_bufs[r][mb] + self.idx * row_bytes, row_bytes,
-                         stream=sp)
-        ctx.add_partials(self.h_res[mb], self.part_ptrs[mb], c.n_ffn, self.x[mb], stream=sp)
-
-    def _ffn_layer(self, mb, seq):
-        c, ctx, t = self.cfg, self.ctx, self.torch
-        cs = self.copy_stream.cuda_stream
-        rx, L = self.rx[mb], self.lay
-        for a in range(c.n_attn):
-            ctx.wait(self.flags.data_ptr() + 4 * flag_index(a, mb, c), seq, stream=cs)
-            src = self.peer_bufs[a][mb]
-            for name in ("xq", "xs", "ids", "wts"):
-                n = L.size(name)
-                ctx.copy(rx[name].data_ptr() + a * n, src + L.off[name], n, stream=cs)
-        self.copied[mb].record(self.copy_stream)
-        st = self.streams[0]
-        st.wait_event(self.copied[mb])
-        scatter = (self.dst[mb], c.T_mb) if c.f2a == "push" else None
-        if c.layer_kind == "dense":  # this GPU's slices of the dense FFN: a tensor-parallel partial
-            ctx.dense_ffn_mx(self.moe_w, rx["xq"], rx["xs"], self.out[mb], stream=st.cuda_stream, scatter=scatter)
-        else:
-            ffn = ctx.moe_ffn_mx if c.ffn_format == "mx" else ctx.moe_ffn
-            ffn(self.moe_w, rx["xq"], rx["xs"], rx["ids"], rx["wts"], self.out[mb], expert_lo=self.expert_lo,
-                expert_hi=self.expert_hi, shared=self.shared, stream=st.cuda_stream, scatter=scatter)
-        for a in range(c.n_attn):
-            ctx.signal(self.peer_flags[a] + 4 * flag_index(self.idx, mb, c), seq, stream=st.cuda_stream)
-
     def step(self):
         """One decode step over cfg.layers layers for every micro-batch (enqueue only)."""
-        c = self.cfg
-        for layer in range(c.layers):
-            self.epoch += 1
-            for mb in range(c.n_micro):
-                if self.role == "attn":
-                    self._attn_layer(layer, mb, self.epoch)
-                else:
-                    self._ffn_layer(mb, self.epoch)
+        lib = _k.load()
+        for layer in range(self.cfg.layers):
+            if self.role == "attn":
+                _k.check(lib.afdk_afd_attn_layer(self.handle, ctypes.byref(self.c_w), _k.ptr(self.w["gate"]),
+                                                 self.c_mbs[layer]))
+            else:
+                _k.check(lib.afdk_afd_ffn_layer(self.handle, ctypes.byref(self.c_ffn_w)))
+
+    def buffer(self, which: int, mb: int) -> int:
+        return _k.load().afdk_afd_buffer(self.handle, which, mb) or 0
 
     def reset_inputs(self):
         if self.role == "attn":
@@ -402,16 +359,12 @@ class AfdRank:
                 self.x[mb].copy_(self.x0[mb])
 
     def streams_all(self):
-        return self.streams + [self.copy_stream]
+        return list(self._streams)
+
+    def sync(self):
+        _k.check(_k.load().afdk_afd_sync(self.handle))
 
     def close(self):
-        for r, bufs in self.peer_recv.items():
-            for p in bufs:
-                self.ctx.ipc_close(p)
-        self.peer_recv = {}
-        for r, p in self.peer_flags.items():
-            self.ctx.ipc_close(p)
-        for r, bufs in self.peer_bufs.items():
-            for p in bufs:
-                self.ctx.ipc_close(p)
-        self.peer_flags, self.peer_bufs = {}, {}
+        if self.handle is not None:
+            _k.load().afdk_afd_destroy(self.handle)
+            self.handle = None

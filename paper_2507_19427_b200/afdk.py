@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, Structure, c_char_p, c_float, c_int, c_int32, c_size_t, c_void_p
+from ctypes import POINTER, Structure, c_char_p, c_float, c_int, c_int32, c_size_t, c_uint32, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AFDK_LIB") or os.path.join(HERE, "libafdk.so")
@@ -141,6 +141,7 @@ SIGNATURES = {
     "afdk_create": (c_int, [POINTER(c_void_p), POINTER(Cfg)]),
     "afdk_destroy": (None, [c_void_p]),
     "afdk_num_sms": (c_int, [c_void_p]),
+    "afdk_ctx_device": (c_int, [c_void_p]),
     "afdk_mfa_decode_attention": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_void_p]),
     "afdk_linear": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]),
     "afdk_mfa_layer": (c_int, [c_void_p, POINTER(MfaWeights), POINTER(MfaLayerArgs), c_void_p]),
@@ -176,6 +177,54 @@ SIGNATURES = {
                                          POINTER(LayerTimes)]),
     "afdk_simulate": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, POINTER(SimPlan), POINTER(SimResult)]),
 }
+
+# ------------------------------------------------ AFD runtime (afdk_afd_*)
+class AfdCfg(Structure):
+    _fields_ = [("n_attn", c_int), ("n_ffn", c_int), ("n_micro", c_int), ("T_mb", c_int), ("hidden", c_int),
+                ("top_k", c_int), ("n_experts", c_int), ("inter", c_int), ("dense_inter", c_int),
+                ("dense_slices", c_int), ("ffn_format", c_int), ("layer_kind", c_int), ("f2a", c_int),
+                ("attn_chunk", c_int)]
+
+
+class AfdOp(Structure):
+    _fields_ = [("kind", c_int), ("stream", c_int), ("mb", c_int), ("peer", c_int), ("slot", c_int),
+                ("value", c_uint32), ("src_buf", c_int), ("dst_buf", c_int), ("src_off", c_size_t),
+                ("dst_off", c_size_t), ("bytes", c_size_t)]
+
+
+class AfdLayout(Structure):
+    _fields_ = [("off", c_size_t * 4), ("size", c_size_t * 4), ("total", c_size_t), ("rx_off", c_size_t * 4),
+                ("rx_total", c_size_t), ("part_bytes", c_size_t)]
+
+
+class AfdAttnMb(Structure):
+    _fields_ = [("x", c_void_p), ("k_cache", c_void_p), ("v_cache", c_void_p), ("num_pages", c_int),
+                ("page_size", c_int), ("max_pages", c_int), ("block_table", c_void_p), ("seq_lens", c_void_p),
+                ("k_scale", c_float), ("v_scale", c_float)]
+
+
+class AfdFfnWeights(Structure):
+    _fields_ = [("w13", c_void_p), ("s13", c_void_p), ("w2", c_void_p), ("s2", c_void_p)]
+
+
+ALLGATHER = ctypes.CFUNCTYPE(c_int, c_void_p, c_void_p, c_size_t, c_void_p)
+
+_SIGS = {
+    "afdk_afd_check_cfg": (c_int, [POINTER(AfdCfg)]),
+    "afdk_afd_get_layout": (c_int, [POINTER(AfdCfg), POINTER(AfdLayout)]),
+    "afdk_afd_plan": (c_int, [POINTER(AfdCfg), c_int, c_uint32, c_void_p, c_int, POINTER(c_int)]),
+    "afdk_afd_create": (c_int, [POINTER(c_void_p), POINTER(AfdCfg), c_int, ALLGATHER, c_void_p, POINTER(c_void_p)]),
+    "afdk_afd_destroy": (None, [c_void_p]),
+    "afdk_afd_attn_layer": (c_int, [c_void_p, POINTER(MfaWeights), c_void_p, POINTER(AfdAttnMb)]),
+    "afdk_afd_ffn_layer": (c_int, [c_void_p, POINTER(AfdFfnWeights)]),
+    "afdk_afd_stream": (c_void_p, [c_void_p, c_int]),
+    "afdk_afd_buffer": (c_void_p, [c_void_p, c_int, c_int]),
+    "afdk_afd_seq": (c_uint32, [c_void_p]),
+    "afdk_afd_sync": (c_int, [c_void_p]),
+}
+SIGNATURES.update(_SIGS)
+
+
 
 _lib = None
 

@@ -32,6 +32,7 @@ CU_SOURCES = [
     "exchange.cu",
     "afd_measured.cu",
     "pipeline_model.cpp",
+    "afd_runtime.cu",
 ]
 CXX_SOURCES: list[str] = []
 

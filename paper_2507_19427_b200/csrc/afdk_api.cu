@@ -152,6 +152,7 @@ void afdk_destroy(afdk_ctx* ctx) {
 }
 
 int afdk_num_sms(const afdk_ctx* ctx) { return ctx ? ctx->c.num_sms : 0; }
+int afdk_ctx_device(const afdk_ctx* ctx) { return ctx ? ctx->c.device : -1; }
 
 static afdk_status mfa_decode_entry(afdk_ctx* ctx, const afdk_mfa_decode_args* a, bool fp8, float k_scale,
                                     float v_scale, afdk_stream stream) {

@@ -1,8 +1,8 @@
-"""AFD pipeline driver: torchrun --nproc-per-node N scripts/afd_run.py --n-attn A [--check]
+"""AFD pipeline timing driver: torchrun --nproc-per-node N scripts/afd_run.py --n-attn A
 
---check: small dims, one layer; attention rank 0 recomputes the whole layer
-(attention + router + all experts) on its own GPU and compares.
-Prints one JSON line (rank 0) with the measured layer period and throughput.
+Runs the C++ AFD runtime (through paper_2507_19427_b200.afd) at full Step-3
+dims and prints one JSON line (rank 0) with the measured layer period and
+throughput.  Correctness: tests/afd_gpu_check.py (pytest tests/test_afd_gpu.py).
 """
 import argparse
 import json
@@ -21,8 +21,8 @@ def main():
     ap.add_argument("--ctx-len", type=int, default=4096)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--check", action="store_true")
-    ap.add_argument("--fmt", default="fp8", choices=["fp8", "mx"])
+    ap.add_argument("--fmt", default="fp8", choices=["fp8", "mx", "bf16"])
+    ap.add_argument("--kv", default="bf16", choices=["bf16", "e4m3"])
     ap.add_argument("--f2a", default="push", choices=["push", "pull"])
     ap.add_argument("--attn-chunk", type=int, default=256)
     ap.add_argument("--layer", default="moe", choices=["moe", "dense"])
@@ -35,9 +35,8 @@ def main():
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    # AFDK_OVERSUB=1: more ranks than GPUs (e.g. the 8-rank protocol on a 4-GPU
-    # box for --check): ranks share GPUs round-robin and the rendezvous runs on
-    # gloo (NCCL refuses two ranks on one device)
+    # AFDK_OVERSUB=1: more ranks than GPUs: ranks share GPUs round-robin and the
+    # rendezvous runs on gloo (NCCL refuses two ranks on one device)
     oversub = os.environ.get("AFDK_OVERSUB") == "1"
     if oversub:
         local %= torch.cuda.device_count()
@@ -47,14 +46,9 @@ def main():
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=dev)
-    if a.check:
-        cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=24, n_micro=2, layers=1, hidden=1024,
-                        q_lora=256, ctx_len=300, n_experts=8 if (world - a.n_attn) in (1, 2, 4, 8) else 24, top_k=2, inter=512, seed=3, ffn_format=a.fmt, f2a=a.f2a,
-                        attn_chunk=min(a.attn_chunk, 256), layer_kind=a.layer, dense_inter=2048 * 6)
-    else:
-        cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=a.T_mb, n_micro=a.n_micro, layers=a.layers,
-                        ctx_len=a.ctx_len, ffn_format=a.fmt, f2a=a.f2a, attn_chunk=a.attn_chunk,
-                        layer_kind=a.layer)
+    cfg = AfdConfig(n_attn=a.n_attn, n_ffn=world - a.n_attn, T_mb=a.T_mb, n_micro=a.n_micro, layers=a.layers,
+                    ctx_len=a.ctx_len, ffn_format=a.fmt, f2a=a.f2a, attn_chunk=a.attn_chunk, layer_kind=a.layer,
+                    kv=a.kv)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -80,54 +74,6 @@ def main():
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
-
-    if a.check:
-        run(1)
-        ok = True
-        if rank == 0:
-            from tests.helpers import rel_err
-            c = cfg
-            wall = r.expert_weights(0, c.n_experts)
-            errs = []
-            for mb in range(c.n_micro):
-                k, v, bt = r.kv[0][mb]
-                h_res = torch.empty_like(r.x0[mb])
-                h_norm = torch.empty_like(r.x0[mb])
-                ctxs[0].mfa_layer(r.w, r.x0[mb], k, v, bt, r.seq_lens, h_res, h_norm)
-                ids = torch.empty(c.T_mb, c.top_k, dtype=torch.int32, device=dev)
-                wts = torch.empty(c.T_mb, c.top_k, device=dev)
-                xq = torch.empty(c.T_mb, c.hidden, dtype=torch.uint8, device=dev)
-                part = torch.empty_like(h_res)
-                if c.layer_kind == "dense":
-                    xs = torch.empty(c.T_mb, c.hidden // 32, dtype=torch.uint8, device=dev)
-                    ctxs[0].quant_mx(h_norm, xq, xs)
-                    ctxs[0].dense_ffn_mx(r.dense_weights(0, c.dense_slices_total), xq, xs, part)
-                elif c.ffn_format == "mx":
-                    xs = torch.empty(c.T_mb, c.hidden // 32, dtype=torch.uint8, device=dev)
-                    ctxs[0].router_topk(h_norm, r.w["gate"], c.top_k, ids, wts)
-                    ctxs[0].quant_mx(h_norm, xq, xs)
-                    ctxs[0].moe_ffn_mx(wall, xq, xs, ids, wts, part)
-                else:
-                    xs = torch.empty(c.T_mb, c.hidden // 128, device=dev)
-                    ctxs[0].router_topk(h_norm, r.w["gate"], c.top_k, ids, wts, xq=xq, xs=xs)
-                    ctxs[0].moe_ffn(wall, xq, xs, ids, wts, part)
-                torch.cuda.synchronize()
-                ref = (h_res.float() + part.float())
-                errs.append(rel_err(r.x[mb].float().cpu().numpy(), ref.cpu().numpy()))
-                L = r.lay
-                sb = r.send[mb]
-                sent_xq = sb[L.off["xq"]:L.off["xq"] + L.size("xq")].view(c.T_mb, c.hidden)
-                sent_ids = sb[L.off["ids"]:L.off["ids"] + L.size("ids")].view(torch.int32).view(c.T_mb, c.top_k)
-                print("mb", mb, "x err", errs[-1], "h_res err", rel_err(r.h_res[mb].float().cpu().numpy(), h_res.float().cpu().numpy()),
-                      "part err", rel_err(r.recv_part[mb][0].float().cpu().numpy(), part.float().cpu().numpy()),
-                      "xq eq", bool(torch.equal(sent_xq, xq)), "ids eq", bool(torch.equal(sent_ids, ids)), flush=True)
-            ok = max(errs) <= 2e-2
-            print(json.dumps({"afd_check": "ok" if ok else "FAIL", "layer": c.layer_kind, "fmt": c.ffn_format, "f2a": c.f2a, "rel_err": errs, "world": world,
-                              "n_attn": cfg.n_attn}), flush=True)
-        dist.barrier()
-        r.close()
-        dist.destroy_process_group()
-        sys.exit(0 if ok else 1)
 
     for _ in range(a.warmup):
         r.reset_inputs()

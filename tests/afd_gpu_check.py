@@ -1,0 +1,130 @@
+"""Multi-process check of the C++ AFD runtime on the GPU (TEST HARNESS).
+
+    torchrun --nproc-per-node N tests/afd_gpu_check.py --n-attn A [--fmt fp8|mx|bf16] [--f2a push|pull]
+             [--kv bf16|e4m3] [--layer moe|dense] [--attn-chunk C] [--out result.json]
+
+Runs the real runtime (afdk_afd_create / attn_layer / ffn_layer, IPC-mapped
+buffers, flags, copy-engine pulls, fused F->A scatter) for STEPS steps x
+LAYERS layers x 2 micro-batches at small dims, buffers reused across
+sequence numbers.  After every step, EVERY attention rank recomputes the
+step's layers on its own GPU from the step's input — attention layer,
+router / dispatch quantisation and the whole MoE (all experts, no
+expert parallelism) through the single-GPU C-ABI calls — and compares its
+activations (rel = max|afd - ref| / max|ref|; bar 2e-2: the runtime sums
+bf16-rounded EP partials where the recompute rounds the whole layer once).
+
+Ranks beyond the visible GPU count share GPUs round-robin (IPC between
+processes on one device works), with a gloo rendezvous.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+STEPS, LAYERS = 3, 2
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n-attn", type=int, default=1)
+    ap.add_argument("--fmt", default="fp8", choices=["fp8", "mx", "bf16"])
+    ap.add_argument("--f2a", default="push", choices=["push", "pull"])
+    ap.add_argument("--kv", default="bf16", choices=["bf16", "e4m3"])
+    ap.add_argument("--layer", default="moe", choices=["moe", "dense"])
+    ap.add_argument("--attn-chunk", type=int, default=256)
+    ap.add_argument("--T-mb", type=int, default=24)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_19427_b200 import Context
+    from paper_2507_19427_b200.afd import AfdConfig, AfdRank
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    shared_gpu = world > torch.cuda.device_count()
+    dist.init_process_group("gloo" if shared_gpu else "nccl", **({} if shared_gpu else {"device_id": dev}))
+    nf = world - a.n_attn
+    cfg = AfdConfig(n_attn=a.n_attn, n_ffn=nf, T_mb=a.T_mb, n_micro=2, layers=LAYERS, hidden=1024, q_lora=256,
+                    ctx_len=300, n_experts=8 if nf in (1, 2, 4, 8) else 24, top_k=2, inter=512, seed=3,
+                    ffn_format=a.fmt, f2a=a.f2a, kv=a.kv, layer_kind=a.layer, attn_chunk=a.attn_chunk,
+                    dense_inter=2048 * 6)
+    ctxs = [Context(local) for _ in range(cfg.n_micro)]
+    r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
+    r.setup()
+    errs = []
+    if r.role == "attn":
+        wall = r.dense_weights(0, cfg.dense_slices_total) if cfg.layer_kind == "dense" else \
+            r.expert_weights(0, cfg.n_experts)
+    c0 = ctxs[0]
+    for step in range(STEPS):
+        x_in = [x.clone() for x in r.x] if r.role == "attn" else None
+        r.step()
+        r.sync()
+        dist.barrier()
+        if r.role != "attn":
+            continue
+        for mb in range(cfg.n_micro):
+            x = x_in[mb]
+            for layer in range(cfg.layers):
+                k, v, bt, ks, vs = r.kv[layer][mb]
+                h_res, h_norm = torch.empty_like(x), torch.empty_like(x)
+                for s0 in range(0, cfg.T_mb, cfg.attn_chunk):
+                    s1 = min(cfg.T_mb, s0 + cfg.attn_chunk)
+                    c0.mfa_layer(r.w, x[s0:s1], k, v, bt[s0:s1], r.seq_lens[s0:s1], h_res[s0:s1], h_norm[s0:s1],
+                                 **({"kv_scales": (ks, vs)} if cfg.kv == "e4m3" else {}))
+                T = cfg.T_mb
+                ids = torch.empty(T, cfg.top_k, dtype=torch.int32, device=dev)
+                wts = torch.empty(T, cfg.top_k, device=dev)
+                part = torch.empty_like(h_res)
+                if cfg.layer_kind == "dense":
+                    xq = torch.empty(T, cfg.hidden, dtype=torch.uint8, device=dev)
+                    xs = torch.empty(T, cfg.hidden // 32, dtype=torch.uint8, device=dev)
+                    c0.quant_mx(h_norm, xq, xs)
+                    c0.dense_ffn_mx(wall, xq, xs, part)
+                elif cfg.ffn_format == "mx":
+                    xq = torch.empty(T, cfg.hidden, dtype=torch.uint8, device=dev)
+                    xs = torch.empty(T, cfg.hidden // 32, dtype=torch.uint8, device=dev)
+                    c0.router_topk(h_norm, r.w["gate"], cfg.top_k, ids, wts)
+                    c0.quant_mx(h_norm, xq, xs)
+                    c0.moe_ffn_mx(wall, xq, xs, ids, wts, part)
+                elif cfg.ffn_format == "bf16":
+                    c0.router_topk(h_norm, r.w["gate"], cfg.top_k, ids, wts)
+                    c0.moe_ffn_bf16(wall, h_norm, ids, wts, part)
+                else:
+                    xq = torch.empty(T, cfg.hidden, dtype=torch.uint8, device=dev)
+                    xs = torch.empty(T, cfg.hidden // 128, device=dev)
+                    c0.router_topk(h_norm, r.w["gate"], cfg.top_k, ids, wts, xq=xq, xs=xs)
+                    c0.moe_ffn(wall, xq, xs, ids, wts, part)
+                x = (h_res.float() + part.float()).to(torch.bfloat16)
+            torch.cuda.synchronize()
+            ref, got = x.float(), r.x[mb].float()
+            errs.append(float((got - ref).abs().max() / ref.abs().max().clamp_min(1e-12)))
+    allerr = [None] * world
+    dist.all_gather_object(allerr, errs)
+    flat = [e for es in allerr for e in es]
+    ok = len(flat) == cfg.n_attn * cfg.n_micro * STEPS and max(flat) <= 2e-2
+    if rank == 0:
+        res = {"afd_check": "ok" if ok else "FAIL", "world": world, "n_attn": cfg.n_attn, "fmt": cfg.ffn_format,
+               "f2a": cfg.f2a, "kv": cfg.kv, "layer": cfg.layer_kind, "T_mb": cfg.T_mb, "attn_chunk": cfg.attn_chunk,
+               "steps": STEPS, "layers": LAYERS, "seq": STEPS * LAYERS, "max_rel_err": max(flat), "rel_err": flat,
+               "shared_gpu": shared_gpu}
+        print(json.dumps(res), flush=True)
+        if a.out:
+            with open(a.out, "w") as f:
+                json.dump(res, f)
+    dist.barrier()
+    r.close()
+    for c in ctxs:
+        c.close()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,46 @@
+"""The C++ AFD runtime end to end on the GPU (tests/afd_gpu_check.py under
+torchrun): 3 steps x 2 layers x 2 micro-batches, buffers reused across
+sequence numbers, every attention rank compared after every step with a
+one-GPU recompute (bar 2e-2, stated in the harness).  With fewer GPUs than
+ranks the ranks share GPUs (CUDA IPC between processes on one device), so
+the protocol runs even on a 1-GPU lease; with >= world GPUs it crosses
+NVLink."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = [
+    # (world, n_attn, extra args)
+    (2, 1, ["--fmt", "fp8", "--f2a", "push"]),
+    (2, 1, ["--fmt", "mx", "--f2a", "pull", "--kv", "e4m3"]),
+    (2, 1, ["--fmt", "bf16", "--f2a", "push", "--T-mb", "40", "--attn-chunk", "16"]),  # T_mb > attn_chunk
+    (3, 1, ["--fmt", "mx", "--f2a", "push"]),
+    (3, 2, ["--fmt", "fp8", "--f2a", "push", "--kv", "e4m3"]),
+    (3, 1, ["--layer", "dense", "--fmt", "mx", "--f2a", "push"]),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,n_attn,extra", CASES,
+                         ids=[f"{w}r-{a}A-{'-'.join(x[1::2])}" for w, a, x in CASES])
+def test_afd_runtime_multi_process(tmp_path, world, n_attn, extra):
+    out = tmp_path / "res.json"
+    port = 29500 + (os.getpid() % 1000)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "afd_gpu_check.py"),
+           "--n-attn", str(n_attn), "--out", str(out), *extra]
+    env = dict(os.environ, PYTHONPATH=ROOT, OMP_NUM_THREADS="1")
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    got = json.load(open(out))
+    assert got["afd_check"] == "ok" and got["max_rel_err"] <= 2e-2, got
+    try:
+        from tests.helpers import record
+        record(f"afd_{world}r_{n_attn}A_{'_'.join(extra[1::2])}", max_rel_err=got["max_rel_err"])
+    except Exception:  # noqa: BLE001
+        pass

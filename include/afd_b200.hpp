@@ -57,6 +57,17 @@ LayerMeasurement measure_layer(const ModelSpec& model, const DeploymentPlan& pla
                                const Catalog& catalog);
 void clear_measurement_cache();
 
+// vet_plan's stage_ok (planner.cpp:124-131) evaluated on any StageTimes —
+// measured ones in particular: every layer's attention and FFN time within
+// stage_budget(w, model) = tpot_sla / pipeline_stages / n_layers
+// (sizing.cpp:9-11).
+struct StageCheck {
+  bool stage_ok = true;
+  int first_bad_layer = -1;
+  double budget = 0, worst_attn = 0, worst_ffn = 0;
+};
+StageCheck vet_stages(const StageTimes& times, const Workload& w, const ModelSpec& model);
+
 // Pipeline model on measured times (semantics of pipesim.cpp:155-237).
 SimResult simulate(const StageTimes& times, const DeploymentPlan& plan, const SimOptions& opts = {});
 std::string trace_csv(const SimResult& result);

@@ -538,6 +538,23 @@ typedef struct afdk_sim_result {
 afdk_status afdk_simulate(const double* attn, const double* comm_fwd, const double* ffn, const double* comm_bwd,
                           int layers, const afdk_sim_plan* plan, afdk_sim_result* out);
 
+/* trace_csv of the simulated run (pipesim.cpp:239-260 schema
+ * "time_s,resource,layer,micro_batch,stage,duration_s", %.9f); *len = the
+ * full text length; buf (may be NULL) receives up to cap-1 bytes + NUL. */
+afdk_status afdk_trace_csv(const double* attn, const double* comm_fwd, const double* ffn, const double* comm_bwd,
+                           int layers, const afdk_sim_plan* plan, char* buf, size_t cap, size_t* len);
+
+/* vet_plan's stage check (planner.cpp:124-131) on given (typically measured)
+ * per-layer attention / FFN stage times: stage_ok iff every layer's attn and
+ * ffn <= budget = tpot_sla / pipeline_stages / n_model_layers
+ * (stage_budget, sizing.cpp:9-11).  CPU only. */
+typedef struct afdk_stage_check {
+  int stage_ok, first_bad_layer;
+  double budget_s, worst_attn_s, worst_ffn_s;
+} afdk_stage_check;
+afdk_status afdk_vet_stages(const double* attn, const double* ffn, int layers, double tpot_sla, int pipeline_stages,
+                            int n_model_layers, afdk_stage_check* out);
+
 #ifdef __cplusplus
 }
 #endif

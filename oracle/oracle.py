@@ -448,6 +448,17 @@ def ref_trace_csv(attn, fwd, ffn, bwd, n_micro, total_batch, total_gpus) -> str:
     return s
 
 
+def ref_vet_plan(hw: dict, attn_inst, ffn_inst, micro_batch, n_micro, ctx, tpot=0.05, stages=3, model=STEP3):
+    """The reference's vet_plan flags (planner.cpp:111-137)."""
+    flags = (c_int * 3)()
+    _ref_check(ref().ref_vet_plan(
+        c_char_p(model), c_char_p(hw["name"].encode()), c_double(hw["f16"]), c_double(hw.get("f8", 0.0)),
+        c_double(hw["bw"]), c_double(hw["net"]), c_int(hw.get("gps", 1)), c_double(hw.get("net_eff", 1.0)),
+        c_int(attn_inst), c_int(ffn_inst), c_longlong(micro_batch), c_int(n_micro), c_longlong(ctx),
+        c_double(tpot), c_int(stages), flags))
+    return dict(sparsity_ok=bool(flags[0]), net_ok=bool(flags[1]), stage_ok=bool(flags[2]))
+
+
 def ref_stage_budget(tpot, stages, layers):
     out = c_double()
     _ref_check(ref().ref_stage_budget(c_double(tpot), c_int(stages), c_int(layers), ctypes.byref(out)))

@@ -16,6 +16,7 @@
 #include "afdsim/costmodel.hpp"
 #include "afdsim/moeplan.hpp"
 #include "afdsim/pipesim.hpp"
+#include "afdsim/planner.hpp"
 #include "afdsim/sizing.hpp"
 
 namespace {
@@ -205,6 +206,34 @@ char* ref_trace_csv(const double* attn, const double* fwd, const double* ffn,
     std::memcpy(res, s.c_str(), s.size() + 1);
   });
   return res;
+}
+
+// vet_plan (planner.cpp:111-137) of an AFD plan on one accelerator used for
+// both tiers; flags = {sparsity_ok, net_ok, stage_ok}
+int ref_vet_plan(const char* model, const char* hw, double f16, double f8, double bw, double net, int gps,
+                 double net_eff, int attn_inst, int ffn_inst, long long micro_batch, int n_micro, long long ctx,
+                 double tpot, int stages, int flags[3]) {
+  return guarded([&] {
+    auto cat = afd::builtin_catalog();
+    cat.accelerators.push_back(make_accel(hw, f16, f8, bw, net, gps, net_eff));
+    afd::DeploymentPlan p;
+    p.attn_hw = hw;
+    p.ffn_hw = hw;
+    p.attn_instances = attn_inst;
+    p.ffn_instances = ffn_inst;
+    p.micro_batch = micro_batch;
+    p.n_micro = n_micro;
+    p.total_batch = micro_batch * n_micro;
+    p.total_gpus = (attn_inst + ffn_inst) * gps;
+    afd::Workload w;
+    w.avg_ctx = ctx;
+    w.tpot_sla = tpot;
+    w.pipeline_stages = stages;
+    const auto f = afd::vet_plan(p, cat.model(model), w, cat);
+    flags[0] = f.sparsity_ok;
+    flags[1] = f.net_ok;
+    flags[2] = f.stage_ok;
+  });
 }
 
 void ref_free(void* p) { std::free(p); }

@@ -128,6 +128,11 @@ class SimPlan(Structure):
                 ("token_steps", c_int), ("shared_link", c_int)]
 
 
+class StageCheck(Structure):
+    _fields_ = [("stage_ok", c_int), ("first_bad_layer", c_int), ("budget_s", ctypes.c_double),
+                ("worst_attn_s", ctypes.c_double), ("worst_ffn_s", ctypes.c_double)]
+
+
 class SimResult(Structure):
     _fields_ = [("tpot", ctypes.c_double), ("tgs", ctypes.c_double), ("utilization", ctypes.c_double * 4),
                 ("bubble_fraction", ctypes.c_double * 4)]
@@ -176,6 +181,9 @@ SIGNATURES = {
     "afdk_measure_stage_times": (c_int, [c_void_p, POINTER(StagePlan), c_void_p, c_void_p, c_void_p, c_void_p,
                                          POINTER(LayerTimes)]),
     "afdk_simulate": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, POINTER(SimPlan), POINTER(SimResult)]),
+    "afdk_trace_csv": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, POINTER(SimPlan), c_void_p, c_size_t,
+                               POINTER(c_size_t)]),
+    "afdk_vet_stages": (c_int, [c_void_p, c_void_p, c_int, ctypes.c_double, c_int, c_int, POINTER(StageCheck)]),
 }
 
 # ------------------------------------------------ AFD runtime (afdk_afd_*)
@@ -263,6 +271,29 @@ def simulate(attn, fwd, ffn, bwd, n_micro, total_batch, total_gpus, token_steps=
                                ctypes.byref(SimPlan(n_micro, total_batch, total_gpus, token_steps, int(shared_link))),
                                ctypes.byref(out)))
     return dict(tpot=out.tpot, tgs=out.tgs, utilization=list(out.utilization), bubble=list(out.bubble_fraction))
+
+
+def trace_csv(attn, fwd, ffn, bwd, n_micro, total_batch, total_gpus, token_steps=3, shared_link=False) -> str:
+    """trace_csv (pipesim.cpp:239-260 schema) of the product's simulate; CPU only."""
+    L = len(attn)
+    arrs = [ctypes.cast((ctypes.c_double * L)(*map(float, v)), c_void_p) for v in (attn, fwd, ffn, bwd)]
+    plan = SimPlan(n_micro, total_batch, total_gpus, token_steps, int(shared_link))
+    n = c_size_t(0)
+    check(load().afdk_trace_csv(*arrs, L, ctypes.byref(plan), None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    check(load().afdk_trace_csv(*arrs, L, ctypes.byref(plan), buf, n.value + 1, ctypes.byref(n)))
+    return buf.value.decode()
+
+
+def vet_stages(attn, ffn, tpot_sla=0.05, pipeline_stages=3, n_model_layers=None) -> dict:
+    """vet_plan's stage_ok (planner.cpp:124-131) on given per-layer attn/ffn stage seconds; CPU only."""
+    L = len(attn)
+    a = (ctypes.c_double * L)(*map(float, attn))
+    f = (ctypes.c_double * L)(*map(float, ffn))
+    out = StageCheck()
+    check(load().afdk_vet_stages(a, f, L, tpot_sla, pipeline_stages, n_model_layers or L, ctypes.byref(out)))
+    return dict(stage_ok=bool(out.stage_ok), first_bad_layer=out.first_bad_layer, budget_s=out.budget_s,
+                worst_attn_s=out.worst_attn_s, worst_ffn_s=out.worst_ffn_s)
 
 
 class Context:

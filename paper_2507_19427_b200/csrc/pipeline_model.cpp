@@ -13,6 +13,7 @@
 // reference library (oracle/_ref) bit for bit on random instances.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -138,8 +139,88 @@ std::string trace_csv(const SimResult& r) {
   return os.str();
 }
 
+// vet_plan's stage check (planner.cpp:124-131) on any StageTimes: every
+// layer's attention and FFN stage must fit stage_budget = tpot_sla /
+// pipeline_stages / n_layers (sizing.cpp:9-11).
+StageCheck vet_stages(const StageTimes& t, const Workload& w, const ModelSpec& model) {
+  if (model.n_layers < 1 || w.pipeline_stages < 1 || !(w.tpot_sla > 0.0))
+    throw SpecError("vet_stages: need n_layers >= 1, pipeline_stages >= 1, tpot_sla > 0");
+  StageCheck c;
+  c.budget = w.tpot_sla / w.pipeline_stages / model.n_layers;
+  c.stage_ok = true;
+  for (int l = 0; l < t.layers(); ++l) {
+    c.worst_attn = std::max(c.worst_attn, t.attn[l]);
+    c.worst_ffn = std::max(c.worst_ffn, t.ffn[l]);
+    if ((t.attn[l] > c.budget || t.ffn[l] > c.budget) && c.stage_ok) {
+      c.stage_ok = false;
+      c.first_bad_layer = l;
+    }
+  }
+  return c;
+}
+
 }  // namespace b200
 }  // namespace afd
+
+static afd::StageTimes stage_times(const double* attn, const double* fwd, const double* ffn, const double* bwd,
+                                   int layers) {
+  afd::StageTimes st;
+  st.attn.assign(attn, attn + layers);
+  st.comm_fwd.assign(fwd, fwd + layers);
+  st.ffn.assign(ffn, ffn + layers);
+  st.comm_bwd.assign(bwd, bwd + layers);
+  return st;
+}
+
+extern "C" afdk_status afdk_trace_csv(const double* attn, const double* fwd, const double* ffn, const double* bwd,
+                                      int layers, const afdk_sim_plan* p, char* buf, size_t cap, size_t* len) {
+  if (!attn || !fwd || !ffn || !bwd || !p || !len || layers < 1) return AFDK_ERR_INVALID;
+  try {
+    afd::DeploymentPlan plan;
+    plan.n_micro = p->n_micro;
+    plan.total_batch = p->total_batch;
+    plan.total_gpus = p->total_gpus;
+    afd::SimOptions o;
+    o.token_steps = p->token_steps;
+    o.shared_link = p->shared_link != 0;
+    const std::string csv = afd::b200::trace_csv(afd::b200::simulate(stage_times(attn, fwd, ffn, bwd, layers), plan, o));
+    *len = csv.size();
+    if (buf && cap > 0) {
+      const size_t n = std::min(cap - 1, csv.size());
+      std::memcpy(buf, csv.data(), n);
+      buf[n] = '\0';
+    }
+    return AFDK_OK;
+  } catch (const std::exception&) {
+    return AFDK_ERR_INVALID;
+  }
+}
+
+extern "C" afdk_status afdk_vet_stages(const double* attn, const double* ffn, int layers, double tpot_sla,
+                                       int pipeline_stages, int n_model_layers, afdk_stage_check* out) {
+  if (!attn || !ffn || !out || layers < 1) return AFDK_ERR_INVALID;
+  try {
+    afd::StageTimes st;
+    st.attn.assign(attn, attn + layers);
+    st.ffn.assign(ffn, ffn + layers);
+    st.comm_fwd.assign(layers, 0.0);
+    st.comm_bwd.assign(layers, 0.0);
+    afd::Workload w;
+    w.tpot_sla = tpot_sla;
+    w.pipeline_stages = pipeline_stages;
+    afd::ModelSpec m;
+    m.n_layers = n_model_layers;
+    const afd::b200::StageCheck c = afd::b200::vet_stages(st, w, m);
+    out->stage_ok = c.stage_ok ? 1 : 0;
+    out->first_bad_layer = c.first_bad_layer;
+    out->budget_s = c.budget;
+    out->worst_attn_s = c.worst_attn;
+    out->worst_ffn_s = c.worst_ffn;
+    return AFDK_OK;
+  } catch (const std::exception&) {
+    return AFDK_ERR_INVALID;
+  }
+}
 
 extern "C" afdk_status afdk_simulate(const double* attn, const double* fwd, const double* ffn, const double* bwd,
                                      int layers, const afdk_sim_plan* p, afdk_sim_result* out) {

@@ -54,3 +54,34 @@ def test_reference_stage_times_feed_product_simulator():
     mine = afdk.simulate(*st, n_micro=3, total_batch=768, total_gpus=8)
     ref = orc.ref_simulate(*st, n_micro=3, total_batch=768, total_gpus=8)
     assert mine == ref
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_trace_csv_matches_reference_bytes(seed):
+    """The product's trace_csv (afdk_trace_csv) == the reference's trace_csv
+    (pipesim.cpp:239-260) byte for byte on random stage times."""
+    rng = np.random.default_rng(77 + seed)
+    L, n = int(rng.integers(1, 20)), int(rng.integers(1, 4))
+    t = rand_times(rng, L)
+    mine = afdk.trace_csv(*t, n_micro=n, total_batch=100 * n, total_gpus=4)
+    ref = orc.ref_trace_csv(*t, n_micro=n, total_batch=100 * n, total_gpus=4)
+    assert mine == ref
+    assert mine.splitlines()[0] == "time_s,resource,layer,micro_batch,stage,duration_s"
+
+
+HW = dict(name="B200", f16=2.25e15, f8=4.5e15, bw=8e12, net=9e11, gps=1)
+
+
+@pytest.mark.parametrize("plan", [(2, 6, 256, 3, 4096), (1, 1, 4096, 3, 4096), (2, 2, 2048, 3, 8192),
+                                  (1, 3, 512, 2, 32768), (4, 4, 8192, 4, 4096)])
+@pytest.mark.parametrize("tpot,stages", [(0.05, 3), (0.2, 3), (0.01, 3)])
+def test_vet_stages_matches_reference_vet_plan(plan, tpot, stages):
+    """stage_ok of the product's vet_stages == the reference's vet_plan
+    stage_ok (planner.cpp:124-131) on the reference's own derived stage times:
+    the same check can then run on MEASURED stage times."""
+    na, nf, mb, nm, ctx = plan
+    st = orc.ref_derive_stage_times(HW, attn_inst=na, ffn_inst=nf, micro_batch=mb, n_micro=nm, ctx=ctx)
+    ref = orc.ref_vet_plan(HW, na, nf, mb, nm, ctx, tpot=tpot, stages=stages)
+    mine = afdk.vet_stages(st[0], st[2], tpot_sla=tpot, pipeline_stages=stages, n_model_layers=61)
+    assert mine["stage_ok"] == ref["stage_ok"], (mine, ref)
+    assert mine["budget_s"] == orc.ref_stage_budget(tpot, stages, 61)

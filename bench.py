@@ -493,27 +493,60 @@ def afd_roles(world):
 
 
 def afd_runs(world):
-    """(plan, ffn format, T_mb) points measured at this world size: the survey's
-    plan (1A1F / 1A3F / 2A6F, config 5 at 8) at the 192-token baseline, then
-    MXFP8 at the largest micro-batch the attention layer takes, and the
-    balanced attention/FFN split."""
+    """(plan, ffn format, T_mb, layer kind, kv) points measured at this world
+    size: the survey's plan (1A1F / 1A3F / 2A6F, config 5 at 8) at the
+    192-token baseline, MXFP8 / bf16 FFN tiers, the e4m3 KV cache (the paper's
+    FP8 attention) and micro-batches sized for the 50 ms TPOT SLA, the
+    balanced attention/FFN split, and one dense layer."""
     base = {2: (1, 1), 4: (1, 3), 8: (2, 6)}.get(world, (1, world - 1))
-    runs = [(base, "fp8", 192, "moe"), (base, "mx", 256, "moe"), (base, "mx", 512, "moe")]
     bal = (world // 2, world - world // 2)
+    runs = [(base, "fp8", 192, "moe", "bf16"), (base, "mx", 256, "moe", "bf16"), (base, "mx", 256, "moe", "e4m3"),
+            (base, "mx", 512, "moe", "e4m3"), (base, "bf16", 256, "moe", "e4m3")]
     if bal != base:
-        runs += [(bal, "mx", 256, "moe"), (bal, "mx", 512, "moe")]
-    runs.append((bal, "mx", 512, "dense"))  # a dense layer: FFN tier tensor-parallel over intermediate slices
+        runs += [(bal, "mx", 128, "moe", "e4m3"), (bal, "mx", 192, "moe", "e4m3"), (bal, "mx", 256, "moe", "e4m3"),
+                 (bal, "mx", 512, "moe", "e4m3")]
+    runs.append((bal, "mx", 512, "dense", "bf16"))  # dense layer: FFN tier tensor-parallel over intermediate slices
     return runs
 
 
-def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt="fp8", plan=None, kind="moe"):
-    """Real pipeline on all ranks: nA attention GPUs + nF FFN GPUs, 2 ping-pong
-    micro-batches, 2 layers per step (distinct KV caches), copy-engine NVLink."""
-    from paper_2507_19427_b200 import Context
+TPOT_SLA, PIPE_STAGES, N_LAYERS = 0.05, 3, 61  # Workload defaults (types.hpp:99-104), Step-3 layers
+
+
+def stages_from_traces(traces, n_micro):
+    """Per-(layer, micro-batch) stage seconds from every rank's measured trace
+    (trace_csv schema): attention = attention-resource time of the micro-batch
+    on its attention GPU (max over attention GPUs), ffn = FFN op time (max over
+    FFN GPUs), fwd = the payload pulls (max over FFN GPUs), bwd = attention-side
+    pulls (0 with the fused push return, which runs inside the FFN op)."""
+    acc = {}
+    for csv in traces:
+        per = {}
+        for ln in csv.strip().splitlines()[1:]:
+            t, res, layer, mb, _, d = ln.split(",")
+            k = (res, int(layer), int(mb))
+            per[k] = per.get(k, 0.0) + float(d)
+        for k, d in per.items():
+            acc[k] = max(acc.get(k, 0.0), d)
+    out = {}
+    for res in ("attention", "fwd_link", "ffn", "bwd_link"):
+        v = [d for (r, _, _), d in acc.items() if r == res]
+        out[res] = (sum(v) / len(v)) if v else 0.0
+    return out
+
+
+def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt="fp8", plan=None, kind="moe",
+                     kv="bf16"):
+    """Real pipeline on all ranks through the C++ AFD runtime: nA attention
+    GPUs + nF FFN GPUs, 2 ping-pong micro-batches, 2 layers per step (distinct
+    KV caches), copy-engine NVLink.  One more traced step gives the measured
+    stage times (trace_csv schema) that feed vet_plan's stage check; the
+    measured layer period gives TPOT = 61 x period against the 50 ms SLA."""
+    from paper_2507_19427_b200 import Context, afdk
     from paper_2507_19427_b200.afd import AfdConfig, AfdRank, wire_bytes
 
     na, nf = plan if plan else afd_roles(world)
-    cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=T_mb, n_micro=2, layers=2, ctx_len=CTX, ffn_format=fmt, layer_kind=kind)
+    cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=T_mb, n_micro=2, layers=2, ctx_len=CTX, ffn_format=fmt, layer_kind=kind,
+                    kv=kv)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -541,6 +574,13 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
 
     run(2)
     ms = run(steps)
+    # one traced step (after the timed region): measured stage times
+    dist.barrier()
+    r.trace_start()
+    r.step()
+    csv = r.trace_csv()
+    traces = [None] * world
+    dist.all_gather_object(traces, csv)
     period = ms / (steps * cfg.layers)
     tokens = na * cfg.n_micro * cfg.T_mb
     wb = wire_bytes(cfg)
@@ -549,33 +589,67 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
         c.close()
     del r
     torch.cuda.empty_cache()
-    return {"plan": f"{na}A{nf}F", "layer": kind, "ffn_format": fmt, "T_mb": cfg.T_mb, "n_micro": cfg.n_micro,
-            "ctx": cfg.ctx_len,
-            "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
-            "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
-            "nvlink_bytes_per_layer": {k: v * cfg.n_micro for k, v in wb.items()},
-            "transport": ("A->F copy-engine DMA pulls; F->A partial rows stored over NVLink by the combine kernel "
-                          "(fused); cuStreamWrite/WaitValue32 flags"), "measured": True}
+    st = stages_from_traces(traces, cfg.n_micro)
+    vet = afdk.vet_stages([st["attention"]] * N_LAYERS, [st["ffn"]] * N_LAYERS, tpot_sla=TPOT_SLA,
+                          pipeline_stages=PIPE_STAGES, n_model_layers=N_LAYERS)
+    tpot = N_LAYERS * period * 1e-3
+    res = {"plan": f"{na}A{nf}F", "layer": kind, "ffn_format": fmt, "kv": kv, "T_mb": cfg.T_mb,
+           "n_micro": cfg.n_micro, "ctx": cfg.ctx_len,
+           "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
+           "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
+           "tpot_ms_61_layers": tpot * 1e3, "sla_ok": tpot <= TPOT_SLA,
+           "tgs_tok_per_gpu_s": tokens / (tpot * world),
+           "measured_stage_us": {k: v * 1e6 for k, v in st.items()},
+           "vet_stages": vet,
+           "nvlink_bytes_per_layer": {k: v * cfg.n_micro for k, v in wb.items()},
+           "transport": ("A->F copy-engine DMA pulls; F->A partial rows stored over NVLink by the combine kernel "
+                         "(fused); cuStreamWrite/WaitValue32 flags"), "runtime": "C++ afdk_afd_*", "measured": True}
+    tdir = os.environ.get("AFDK_TRACE_DIR")
+    if tdir and rank == 0:
+        os.makedirs(tdir, exist_ok=True)
+        name = f"afd_{res['plan']}_{fmt}_{kind}_{kv}_T{T_mb}"
+        with open(os.path.join(tdir, name + ".csv"), "w") as f:
+            for q, csv in enumerate(traces):
+                body = csv.strip().splitlines()
+                f.write(("rank," + body[0] + "\n") if q == 0 else "")
+                f.writelines(f"{q},{ln}\n" for ln in body[1:])
+        res["trace_file"] = name + ".csv"
+    return res
 
 
 def run_afd_modeled(ctx):
-    """Config 5 (2A6F @ 4K) on 1 GPU: measured per-layer stage times
-    (afdk_measure_stage_times: attention-tier layer at 192 requests, FFN tier at
-    8 local experts + shared share over 384 tokens) fed to the pipeline model
-    (afdk_simulate, pipesim.cpp:155 semantics) -> modeled 8-GPU TPOT/TGS."""
+    """Config 5 (2A6F @ 4K) on 1 GPU: per-layer stage times measured by
+    afdk_measure_stage_times (attention-tier layer at micro_batch/2 requests,
+    FFN tier at 8 local experts + shared share over micro_batch tokens, the
+    dense layers as the tier's tensor-parallel share) fed to the pipeline
+    model (afdk_simulate, pipesim.cpp:155 semantics) -> modeled 8-GPU TPOT /
+    TGS, and vet_plan's stage check on the measured times.  The survey plan
+    (fp8 1x128 FFN, bf16 KV, 384 x 3) and the paper's production formats
+    (FP8 attention = e4m3 KV, MXFP8 FFN) over a micro-batch sweep."""
     from paper_2507_19427_b200 import afdk
 
-    mb, n_micro = 384, 3
-    st = ctx.measure_stage_times(attn_gpus=2, ffn_gpus=6, micro_batch=mb, avg_ctx=CTX)
-    sim = afdk.simulate(st["attn"], st["comm_fwd"], st["ffn"], st["comm_bwd"], n_micro=n_micro,
-                        total_batch=mb * n_micro, total_gpus=8)
-    d = st["detail"]
-    return {"plan": "2A6F", "micro_batch": mb, "n_micro": n_micro, "ctx": CTX, "modeled": True,
-            "stage_us": {"attn": 1e6 * d["attn_s"], "moe_ffn": 1e6 * d["moe_ffn_s"], "dense_ffn": 1e6 * d["dense_ffn_s"],
-                         "comm_fwd": 1e6 * d["comm_fwd_s"], "comm_bwd": 1e6 * d["comm_bwd_s"]},
-            "link": {"gbs": d["link_gbs"], "measured": bool(d["link_measured"])},
-            "tpot_ms": 1e3 * sim["tpot"], "tgs_tok_per_gpu_s": sim["tgs"],
-            "tokens_per_s_per_gpu_per_layer": sim["tgs"] * 61, "utilization": sim["utilization"]}
+    def one(mb, n_micro, fmt, kv):
+        st = ctx.measure_stage_times(attn_gpus=2, ffn_gpus=6, micro_batch=mb, avg_ctx=CTX, ffn_format=fmt, kv=kv)
+        sim = afdk.simulate(st["attn"], st["comm_fwd"], st["ffn"], st["comm_bwd"], n_micro=n_micro,
+                            total_batch=mb * n_micro, total_gpus=8)
+        vet = afdk.vet_stages(st["attn"], st["ffn"], tpot_sla=TPOT_SLA, pipeline_stages=PIPE_STAGES,
+                              n_model_layers=N_LAYERS)
+        d = st["detail"]
+        return {"plan": "2A6F", "ffn_format": fmt, "kv": kv, "micro_batch": mb, "n_micro": n_micro, "ctx": CTX,
+                "modeled": True,
+                "stage_us": {"attn": 1e6 * d["attn_s"], "moe_ffn": 1e6 * d["moe_ffn_s"],
+                             "dense_ffn": 1e6 * d["dense_ffn_s"], "comm_fwd": 1e6 * d["comm_fwd_s"],
+                             "comm_bwd": 1e6 * d["comm_bwd_s"]},
+                "link": {"gbs": d["link_gbs"], "measured": bool(d["link_measured"])},
+                "tpot_ms": 1e3 * sim["tpot"], "tgs_tok_per_gpu_s": sim["tgs"], "sla_ok": sim["tpot"] <= TPOT_SLA,
+                "vet_stages": vet, "tokens_per_s_per_gpu_per_layer": sim["tgs"] * N_LAYERS,
+                "utilization": sim["utilization"]}
+
+    survey = one(384, 3, "fp8", "bf16")
+    sweep = [one(mb, 3, "mx", "e4m3") for mb in (256, 384, 512, 768, 1024)]
+    ok = [x for x in sweep if x["sla_ok"] and x["vet_stages"]["stage_ok"]]
+    return dict(survey, production_sweep=sweep,
+                best_within_sla=max(ok, key=lambda x: x["tgs_tok_per_gpu_s"]) if ok else None)
 
 
 def run_afd_modeled_mx(ctx, torch, dev, plans=((2, 6), (4, 4)), T_mb=512, n_micro=2, link_gbs=770.0):
@@ -915,10 +989,14 @@ def main():
             else:
                 # micro-batch sweep: per-layer throughput depends on balancing the
                 # attention tier (grows with T_mb) against expert weight streaming
-                runs = [run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4), T, f, plan, kind)
-                        for plan, f, T, kind in afd_runs(world)]
+                runs = [run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4), T, f, plan, kind,
+                                         kv) for plan, f, T, kind, kv in afd_runs(world)]
                 moe_runs = [x for x in runs if x["layer"] == "moe"]
-                afd = {"runs": runs, "best": max(moe_runs, key=lambda x: x["tokens_per_s_per_gpu_per_layer"])}
+                sla = [x for x in moe_runs if x["sla_ok"]]
+                afd = {"runs": runs, "best": max(moe_runs, key=lambda x: x["tokens_per_s_per_gpu_per_layer"]),
+                       "best_within_sla": max(sla, key=lambda x: x["tgs_tok_per_gpu_s"]) if sla else None,
+                       "sla": {"tpot_s": TPOT_SLA, "pipeline_stages": PIPE_STAGES, "layers": N_LAYERS,
+                               "paper_tgs_hopper": 4039}}
         except Exception as e:  # reported, never silently replaced
             afd = {"error": f"{type(e).__name__}: {e}"}
 

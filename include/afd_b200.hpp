@@ -37,7 +37,9 @@ namespace afd {
 // kernels on the current CUDA device, later calls are pure lookups (safe to
 // call from the planner's OpenMP loop once warmed).
 // Supports the Step-3 geometry (MFA 64x256, hidden from the model card) on
-// an sm_100 device; throws SpecError otherwise.
+// an sm_100 device; throws SpecError otherwise.  Formats follow the model
+// card's QuantScheme (types.hpp:34-40): weight_bytes 1 -> MXFP8 experts,
+// 2 -> bf16 experts; kv_store_bytes 1 -> e4m3 KV cache, 2 -> bf16.
 StageTimes measure_stage_times(const ModelSpec& model, const DeploymentPlan& plan, const Workload& w,
                                const Catalog& catalog);
 
@@ -49,7 +51,7 @@ struct LayerMeasurement {
   std::int64_t ffn_tokens = 0;   // tokens per FFN GPU per micro-batch
   int local_experts = 0;
   double link_gbs = 0;           // per-direction NVLink bandwidth used for comm
-  std::string link_source;       // "measured peer copy" or the pool figure
+  std::string link_source;       // "measured peer DMA of the payload" or the pool figure
 };
 
 // The measurement behind measure_stage_times (exposed for reporting).

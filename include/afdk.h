@@ -490,15 +490,32 @@ void* afdk_afd_buffer(afdk_afd* afd, int which, int mb);
 uint32_t afdk_afd_seq(const afdk_afd* afd);
 afdk_status afdk_afd_sync(afdk_afd* afd);
 
+/* Measured trace of the layers enqueued after afdk_afd_trace_start: CUDA
+ * events around every op that occupies a resource (ATTN / REDUCE ->
+ * attention, FFN -> ffn, the payload pulls of one (layer, micro-batch) ->
+ * fwd_link on FFN ranks, partial pulls -> bwd_link on attention ranks; with
+ * f2a = push the return transfer is inside the FFN op).  afdk_afd_trace_csv
+ * (host-blocking) stops tracing and writes this rank's events in the
+ * reference's trace_csv schema (pipesim.cpp:239-260: time_s relative to the
+ * trace start, resource, layer, micro_batch, stage, duration_s; %.9f). */
+afdk_status afdk_afd_trace_start(afdk_afd* afd);
+afdk_status afdk_afd_trace_csv(afdk_afd* afd, char* buf, size_t cap, size_t* len);
+
 /* ------------------------------------------------ measured stage times
  * The measured counterpart of derive_stage_times (pipesim.cpp:59-127): runs
- * one attention-tier layer (afdk_mfa_layer + router/dispatch) at
- * ceil(micro_batch / attn_gpus) requests and avg_ctx tokens, one FFN-tier MoE
- * layer (48/ffn_gpus local experts + the shared expert's token share) and one
- * dense FFN layer at micro_batch tokens, and the NVLink transfers, then fills
- * per-layer seconds for n_layers Step-3 layers (layers 0-3 and n_layers-1
- * dense, builtin_catalog.cpp:248-250).  link_gbs <= 0 measures a peer copy
- * when a second GPU is visible, else uses the pool's measured 770 GB/s.   */
+ * one attention-tier layer (afdk_mfa_layer[_fp8] + router/dispatch in the FFN
+ * format) at ceil(micro_batch / attn_gpus) requests and avg_ctx tokens, one
+ * FFN-tier MoE layer (48/ffn_gpus local experts + the shared expert's token
+ * share over micro_batch tokens) and one dense FFN layer as this GPU's
+ * tensor-parallel share (dense_inter/ffn_gpus intermediate columns over all
+ * micro_batch tokens, the AFD runtime's split), and the NVLink transfers,
+ * then fills per-layer seconds for n_layers Step-3 layers (layers 0-3 and
+ * n_layers-1 dense, builtin_catalog.cpp:248-250).
+ *   ffn_format: AFDK_FFN_* (QuantScheme.weight_bytes 1 -> FP8, 2 -> BF16)
+ *   kv_bytes:   1 = e4m3 KV cache, 2 (or 0) = bf16 (QuantScheme.kv_store_bytes)
+ *   link_gbs <= 0: when a second GPU is visible, the A->F payload and the
+ *   F->A partial of this plan are each timed as a real peer DMA of their
+ *   byte count; otherwise bytes / the pool's measured 770 GB/s.           */
 typedef struct afdk_stage_plan {
   int attn_gpus, ffn_gpus;
   long long micro_batch;
@@ -506,6 +523,8 @@ typedef struct afdk_stage_plan {
   int n_layers;
   int hidden;
   double link_gbs;
+  int ffn_format;
+  int kv_bytes;
 } afdk_stage_plan;
 
 typedef struct afdk_layer_times {

@@ -361,6 +361,18 @@ class AfdRank:
     def streams_all(self):
         return list(self._streams)
 
+    def trace_start(self):
+        """Record CUDA events around every resource-occupying op from now on."""
+        _k.check(_k.load().afdk_afd_trace_start(self.handle))
+
+    def trace_csv(self) -> str:
+        """This rank's measured trace (trace_csv schema), host-blocking; stops tracing."""
+        lib, n = _k.load(), ctypes.c_size_t(0)
+        _k.check(lib.afdk_afd_trace_csv(self.handle, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _k.check(lib.afdk_afd_trace_csv(self.handle, buf, n.value + 1, ctypes.byref(n)))
+        return buf.value.decode()
+
     def sync(self):
         _k.check(_k.load().afdk_afd_sync(self.handle))
 

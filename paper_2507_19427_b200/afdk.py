@@ -113,7 +113,8 @@ class RowScatter(Structure):
 
 class StagePlan(Structure):
     _fields_ = [("attn_gpus", c_int), ("ffn_gpus", c_int), ("micro_batch", ctypes.c_longlong),
-                ("avg_ctx", ctypes.c_longlong), ("n_layers", c_int), ("hidden", c_int), ("link_gbs", ctypes.c_double)]
+                ("avg_ctx", ctypes.c_longlong), ("n_layers", c_int), ("hidden", c_int), ("link_gbs", ctypes.c_double),
+                ("ffn_format", c_int), ("kv_bytes", c_int)]
 
 
 class LayerTimes(Structure):
@@ -229,6 +230,8 @@ _SIGS = {
     "afdk_afd_buffer": (c_void_p, [c_void_p, c_int, c_int]),
     "afdk_afd_seq": (c_uint32, [c_void_p]),
     "afdk_afd_sync": (c_int, [c_void_p]),
+    "afdk_afd_trace_start": (c_int, [c_void_p]),
+    "afdk_afd_trace_csv": (c_int, [c_void_p, c_void_p, c_size_t, POINTER(c_size_t)]),
 }
 SIGNATURES.update(_SIGS)
 
@@ -516,12 +519,15 @@ class Context:
 
     # -------------------------------------------------- measured stage times
     def measure_stage_times(self, attn_gpus, ffn_gpus, micro_batch, avg_ctx, n_layers=61, hidden=7168,
-                            link_gbs=0.0) -> dict:
+                            link_gbs=0.0, ffn_format="fp8", kv="bf16") -> dict:
+        """ffn_format: fp8 (1x128) / mx / bf16; kv: bf16 / e4m3 (afdk_stage_plan)."""
         L = n_layers
         arrs = [(ctypes.c_double * L)() for _ in range(4)]
         det = LayerTimes()
+        fmt = {"fp8": 0, "mx": 1, "bf16": 2}[ffn_format]
+        sp = StagePlan(attn_gpus, ffn_gpus, micro_batch, avg_ctx, L, hidden, link_gbs, fmt, 1 if kv == "e4m3" else 2)
         check(self.lib.afdk_measure_stage_times(
-            self.handle, ctypes.byref(StagePlan(attn_gpus, ffn_gpus, micro_batch, avg_ctx, L, hidden, link_gbs)),
+            self.handle, ctypes.byref(sp),
             *[ctypes.cast(a, c_void_p) for a in arrs], ctypes.byref(det)))
         names = ["attn", "comm_fwd", "ffn", "comm_bwd"]
         res = {n: list(a) for n, a in zip(names, arrs)}

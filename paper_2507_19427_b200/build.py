@@ -79,6 +79,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
             raise RuntimeError("link failed")
     build_demo(force)
+    build_ref_demo(force)
     return OUT
 
 
@@ -97,6 +98,33 @@ def build_demo(force: bool = False) -> str:
             sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
             raise RuntimeError("demo build failed")
     return DEMO_OUT
+
+
+REF_INCLUDE = os.environ.get("AFD_REFERENCE_INCLUDE", "/root/reference/proj/include")
+REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libafdref.so")
+REF_DEMO_SRC = os.path.join(ROOT, "tests", "cpp", "stage_times_ref_demo.cpp")
+REF_DEMO_OUT = os.path.join(ROOT, "tests", "cpp", "stage_times_ref_demo")
+
+
+def build_ref_demo(force: bool = False) -> str | None:
+    """The drop-in proof: the C++ host API compiled against the REFERENCE's own
+    headers (AFD_B200_USE_REFERENCE_HEADERS) and linked with the reference's
+    own library (oracle/_ref/libafdref.so) + libafdk.so.  Built only where the
+    reference tree is present (this container); the binary travels to the GPU
+    box with the snapshot (rpaths are $ORIGIN-relative)."""
+    if not (os.path.isdir(REF_INCLUDE) and os.path.exists(REF_LIB)):
+        return None
+    deps = [REF_DEMO_SRC, OUT, REF_LIB, os.path.join(ROOT, "include", "afd_b200.hpp")]
+    if force or _stale(REF_DEMO_OUT, deps):
+        cmd = ["g++", "-std=c++20", "-O2", "-DAFD_B200_USE_REFERENCE_HEADERS", "-I", REF_INCLUDE, "-I",
+               os.path.join(ROOT, "include"), REF_DEMO_SRC, "-o", REF_DEMO_OUT, "-L", HERE, "-lafdk",
+               "-L", os.path.dirname(REF_LIB), "-lafdref",
+               "-Wl,-rpath,$ORIGIN/../../paper_2507_19427_b200", "-Wl,-rpath,$ORIGIN/../../oracle/_ref"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+            raise RuntimeError("reference-headers demo build failed")
+    return REF_DEMO_OUT
 
 
 if __name__ == "__main__":

@@ -9,7 +9,9 @@
 // DMA over NVLink, stream-ordered sequence flags).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -177,6 +179,17 @@ struct afdk_afd {
   std::vector<std::vector<uint8_t*>> peer_recv;  // attn peer: recv[mb] (push)
   std::vector<void*> opened;
   uint32_t seq = 0;
+  // measured trace (afdk_afd_trace_start / afdk_afd_trace_csv)
+  struct Rec {
+    cudaEvent_t a, b;
+    int kind, seq, mb;
+  };
+  bool tracing = false;
+  uint32_t trace_seq0 = 0;
+  cudaEvent_t t0 = nullptr;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 };
 
 namespace {
@@ -313,6 +326,8 @@ void release(afdk_afd* r) {
   if (!r->ctxs.empty())
     for (void* p : r->opened) afdk_ipc_close(r->ctxs[0], p);
   for (cudaEvent_t e : r->joins) cudaEventDestroy(e);
+  for (cudaEvent_t e : r->ev_pool) cudaEventDestroy(e);
+  if (r->t0) cudaEventDestroy(r->t0);
   for (cudaStream_t s : r->streams) cudaStreamDestroy(s);
   for (void* p : r->own) cudaFree(p);
   delete r;
@@ -322,6 +337,17 @@ inline uint8_t* sect(uint8_t* base, const afdk_afd_layout& L, int s) { return ba
 
 // Executes the shared ops (SIGNAL / WAIT / PULL / JOIN); ATTN / REDUCE / FFN
 // are role callbacks.
+afdk_status trace_event(afdk_afd* r, cudaEvent_t* ev) {
+  if (r->ev_used == r->ev_pool.size()) {
+    cudaEvent_t e;
+    const cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) return cuda_err("trace event", err);
+    r->ev_pool.push_back(e);
+  }
+  *ev = r->ev_pool[r->ev_used++];
+  return AFDK_OK;
+}
+
 template <typename Compute>
 afdk_status run_plan(afdk_afd* r, Compute&& compute) {
   const uint32_t seq = ++r->seq;
@@ -330,6 +356,17 @@ afdk_status run_plan(afdk_afd* r, Compute&& compute) {
   for (const afdk_afd_op& o : ops) {
     cudaStream_t s = r->streams[o.stream];
     afdk_status st = AFDK_OK;
+    // measured trace: an event pair around every op that occupies a resource
+    const bool traced = r->tracing && (o.kind == AFDK_OP_ATTN || o.kind == AFDK_OP_REDUCE ||
+                                       o.kind == AFDK_OP_FFN || o.kind == AFDK_OP_PULL);
+    afdk_afd::Rec rec{};
+    if (traced) {
+      if ((st = trace_event(r, &rec.a)) != AFDK_OK || (st = trace_event(r, &rec.b)) != AFDK_OK) return st;
+      rec.kind = o.kind;
+      rec.seq = (int)seq;
+      rec.mb = o.mb;
+      cudaEventRecord(rec.a, s);
+    }
     switch (o.kind) {
       case AFDK_OP_SIGNAL:
         st = afdk_signal(ctx0, r->peer_flags[o.peer] + o.slot, o.value, s);
@@ -353,6 +390,10 @@ afdk_status run_plan(afdk_afd* r, Compute&& compute) {
         st = compute(o, s);
     }
     if (st != AFDK_OK) return st;
+    if (traced) {
+      cudaEventRecord(rec.b, s);
+      r->recs.push_back(rec);
+    }
   }
   return AFDK_OK;
 }
@@ -463,6 +504,77 @@ void* afdk_afd_buffer(afdk_afd* afd, int which, int mb) {
 }
 
 uint32_t afdk_afd_seq(const afdk_afd* afd) { return afd ? afd->seq : 0; }
+
+afdk_status afdk_afd_trace_start(afdk_afd* afd) {
+  if (!afd) { set_error("afdk_afd_trace_start: NULL"); return AFDK_ERR_INVALID; }
+  afdk::DeviceGuard g(afd->device);
+  cudaError_t e = cudaSuccess;
+  if (!afd->t0 && (e = cudaEventCreate(&afd->t0)) != cudaSuccess) return cuda_err("trace t0", e);
+  afd->recs.clear();
+  afd->ev_used = 0;
+  afd->trace_seq0 = afd->seq;
+  afd->tracing = true;
+  // t0 on stream 0; every other stream starts after it
+  if ((e = cudaEventRecord(afd->t0, afd->streams[0])) != cudaSuccess) return cuda_err("trace t0", e);
+  for (size_t i = 1; i < afd->streams.size(); ++i)
+    if ((e = cudaStreamWaitEvent(afd->streams[i], afd->t0, 0)) != cudaSuccess) return cuda_err("trace t0", e);
+  return AFDK_OK;
+}
+
+afdk_status afdk_afd_trace_csv(afdk_afd* afd, char* buf, size_t cap, size_t* len) {
+  if (!afd || !len) { set_error("afdk_afd_trace_csv: NULL argument"); return AFDK_ERR_INVALID; }
+  if (!afd->t0) { set_error("afdk_afd_trace_csv: tracing never started"); return AFDK_ERR_INVALID; }
+  afdk::DeviceGuard g(afd->device);
+  afd->tracing = false;
+  struct Row {
+    double t, d;
+    const char* res;
+    const char* stage;
+    int layer, mb;
+  };
+  std::vector<Row> rows;
+  for (const auto& rc : afd->recs) {
+    float ms_a = 0.f, ms_b = 0.f;
+    cudaError_t e = cudaEventSynchronize(rc.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms_a, afd->t0, rc.a);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms_b, afd->t0, rc.b);
+    if (e != cudaSuccess) return cuda_err("trace timing", e);
+    const char* res = "attention";
+    const char* stage = "attention";
+    if (rc.kind == AFDK_OP_FFN) res = stage = "ffn";
+    if (rc.kind == AFDK_OP_PULL) { res = afd->attn ? "bwd_link" : "fwd_link"; stage = "comm"; }
+    rows.push_back({ms_a * 1e-3, (ms_b - ms_a) * 1e-3, res, stage, rc.seq - (int)afd->trace_seq0 - 1, rc.mb});
+  }
+  // the pulls of one (layer, micro-batch) form one link interval
+  std::vector<Row> merged;
+  for (const Row& r : rows) {
+    bool folded = false;
+    if (std::strcmp(r.stage, "comm") == 0)
+      for (Row& m : merged)
+        if (m.res == r.res && m.layer == r.layer && m.mb == r.mb) {
+          const double end = std::max(m.t + m.d, r.t + r.d);
+          m.t = std::min(m.t, r.t);
+          m.d = end - m.t;
+          folded = true;
+          break;
+        }
+    if (!folded) merged.push_back(r);
+  }
+  std::stable_sort(merged.begin(), merged.end(), [](const Row& a, const Row& b) { return a.t < b.t; });
+  std::string csv = "time_s,resource,layer,micro_batch,stage,duration_s\n";
+  char line[256];
+  for (const Row& r : merged) {
+    std::snprintf(line, sizeof(line), "%.9f,%s,%d,%d,%s,%.9f\n", r.t, r.res, r.layer, r.mb, r.stage, r.d);
+    csv += line;
+  }
+  *len = csv.size();
+  if (buf && cap > 0) {
+    const size_t n = std::min(cap - 1, csv.size());
+    std::memcpy(buf, csv.data(), n);
+    buf[n] = '\0';
+  }
+  return AFDK_OK;
+}
 
 afdk_status afdk_afd_sync(afdk_afd* afd) {
   if (!afd) { set_error("afdk_afd_sync: NULL"); return AFDK_ERR_INVALID; }

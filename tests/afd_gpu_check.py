@@ -105,10 +105,25 @@ def main():
             torch.cuda.synchronize()
             ref, got = x.float(), r.x[mb].float()
             errs.append(float((got - ref).abs().max() / ref.abs().max().clamp_min(1e-12)))
+    # measured trace of one more step (afdk_afd_trace_start / _trace_csv)
+    r.trace_start()
+    r.step()
+    csv = r.trace_csv()
+    rows = [ln.split(",") for ln in csv.strip().splitlines()]
+    want = {"attention"} if r.role == "attn" else {"ffn", "fwd_link"}
+    if r.role == "attn" and cfg.f2a == "pull":
+        want.add("bwd_link")
+    got_res = {row[1] for row in rows[1:]}
+    trace_ok = (rows[0] == ["time_s", "resource", "layer", "micro_batch", "stage", "duration_s"] and
+                want <= got_res and {int(row[2]) for row in rows[1:]} == set(range(LAYERS)) and
+                all(float(row[5]) >= 0 for row in rows[1:]))
+    if not trace_ok:
+        print("bad trace on rank", rank, csv[:2000], flush=True)
+        errs.append(1.0)
     allerr = [None] * world
     dist.all_gather_object(allerr, errs)
     flat = [e for es in allerr for e in es]
-    ok = len(flat) == cfg.n_attn * cfg.n_micro * STEPS and max(flat) <= 2e-2
+    ok = len(flat) == cfg.n_attn * cfg.n_micro * STEPS and max(flat) <= 2e-2  # a bad trace adds an entry
     if rank == 0:
         res = {"afd_check": "ok" if ok else "FAIL", "world": world, "n_attn": cfg.n_attn, "fmt": cfg.ffn_format,
                "f2a": cfg.f2a, "kv": cfg.kv, "layer": cfg.layer_kind, "T_mb": cfg.T_mb, "attn_chunk": cfg.attn_chunk,

@@ -39,3 +39,40 @@ def test_cpp_host_api_demo():
     assert out.returncode == 0, out.stderr
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["plan"] == "2A6F" and d["tgs"] > 0 and d["attn_us"] > 0 and d["moe_ffn_us"] > 0
+
+
+@pytest.mark.gpu
+def test_reference_headers_build_drop_in():
+    """The host API compiled against the reference's OWN headers and linked
+    with the reference's own library (tests/cpp/stage_times_ref_demo, built by
+    build() where /root/reference exists): the reference's catalog card feeds
+    measure_stage_times, and the reference's own simulate() consumes the
+    measured StageTimes — bit-identical to the product's pipeline model."""
+    exe = os.path.join(ROOT, "tests", "cpp", "stage_times_ref_demo")
+    if not os.path.exists(exe):
+        pytest.skip("reference-headers demo not built (reference tree absent at build time)")
+    out = subprocess.run([exe, "2", "6", "256", "4096", "3"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["model"] == "step3" and d["layers"] == 61
+    assert d["ref_simulate_tpot_ms"] == d["product_simulate_tpot_ms"] > 0
+    assert d["ref_simulate_tgs"] == d["product_simulate_tgs"]
+    assert d["ref_tpot_bound_ms"] <= d["ref_simulate_tpot_ms"] * (1 + 1e-12)
+    assert d["attn_us"] > 0 and d["ffn_moe_us"] > 0 and d["ffn_dense_us"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt,kv", [("fp8", "bf16"), ("mx", "e4m3"), ("bf16", "e4m3")])
+def test_measured_provider_formats(ctx, fmt, kv):
+    """Formats honoured: e4m3 KV makes the attention stage faster than bf16 KV
+    (half the KV bytes), bf16 experts make the FFN stage slower than MXFP8
+    (twice the weight bytes); the dense stage is this GPU's TP share."""
+    st = ctx.measure_stage_times(attn_gpus=2, ffn_gpus=6, micro_batch=256, avg_ctx=4096, ffn_format=fmt, kv=kv)
+    d = st["detail"]
+    assert d["attn_s"] > 0 and d["moe_ffn_s"] > 0 and d["dense_ffn_s"] > 0
+    base = ctx.measure_stage_times(attn_gpus=2, ffn_gpus=6, micro_batch=256, avg_ctx=4096, ffn_format="mx",
+                                   kv="bf16")["detail"]
+    if kv == "e4m3":
+        assert d["attn_s"] < base["attn_s"]
+    if fmt == "bf16":
+        assert d["moe_ffn_s"] > base["moe_ffn_s"]

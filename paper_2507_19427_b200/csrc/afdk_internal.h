@@ -147,6 +147,12 @@ size_t linear_workspace_bytes(const LinearPlan& p, int num_sms);
 // partials of y = x . w^T into `part` (linear_workspace_bytes); reduce with a
 // SlotTable epilogue or linear_store_launch.  linear_grid = CTAs the GEMM uses.
 int linear_grid(const Ctx& ctx, const LinearPlan& p);
+// q_up with NeoX RoPE fused into the epilogue (one whole tile per CTA; pairs
+// (i, i + head_dim/2) of a head in one tile): bf16 q out, no partials.
+bool linear_rope_fusable(const Ctx& ctx, const LinearPlan& p, int head_dim);
+cudaError_t linear_bf16_rope_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w,
+                                    __nv_bfloat16* q_out, const float2* rope_cs, int head_dim,
+                                    cudaStream_t stream);
 cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
                                cudaStream_t stream);
 cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,

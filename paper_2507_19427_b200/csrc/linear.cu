@@ -38,6 +38,13 @@ struct KParams {
   LinearPlan plan;
   float* part;  // [(tiles + G)][m_tok][128] fp32 segment partials
   int stage_bytes, stages;
+  // kRope mode (q_up with NeoX RoPE fused, one whole tile per CTA): tile t
+  // holds the 64 pairs [j*64, j*64+64) of head h (h = t / tph, j = t % tph,
+  // tph = head_dim/128): weight rows x1 = h*head_dim + j*64 + [0,64) in TMEM
+  // lanes 0-63, x2 = x1 + head_dim/2 in lanes 64-127
+  __nv_bfloat16* q_out;   // [m_tok, n_out] bf16, rotated
+  const float2* rope_cs;  // [m_tok, head_dim/2] (cos, sin) of each row's position
+  int head_dim;
 };
 
 __device__ __forceinline__ void unit_range(int c, int G, int U, int& lo, int& hi) {
@@ -45,6 +52,7 @@ __device__ __forceinline__ void unit_range(int c, int G, int U, int& lo, int& hi
   hi = (int)(((long long)(c + 1) * U) / G);
 }
 
+template <bool kRope>
 __global__ void __launch_bounds__(kThreads, 1)
 linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                    const KParams kp) {
@@ -84,13 +92,24 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       const uint32_t bytes = kABytes + n_mma * 128;
+      // kRope: the panel's rows 0-63 are the pairs' x1 rows, 64-127 their x2 rows
+      const int tph = kRope ? kp.head_dim / 128 : 1;
+      auto load_w = [&](uint8_t* dst, uint64_t* bar, int kb, int tile) {
+        if (kRope) {
+          const int r1 = (tile / tph) * kp.head_dim + (tile % tph) * 64;
+          tma_load_2d(dst, &tm_w, bar, kb * 64, r1, pol_w);
+          tma_load_2d(dst + kABytes / 2, &tm_w, bar, kb * 64, r1 + kp.head_dim / 2, pol_w);
+        } else {
+          tma_load_2d(dst, &tm_w, bar, kb * 64, tile * kBM, pol_w);
+        }
+      };
       // weights never depend on the previous kernel: fill the first S stages'
       // weight panels before waiting for the predecessor (PDL), then the X panels
       const int pro = min(S, u_hi - u_lo);
       for (int i = 0; i < pro; ++i) {
         const int u = u_lo + i, tile = u / P.kblocks, kb = u % P.kblocks;
         mbar_expect_tx(&full[i], bytes);
-        tma_load_2d(smem + i * kp.stage_bytes, &tm_w, &full[i], kb * 64, tile * kBM, pol_w);
+        load_w(smem + i * kp.stage_bytes, &full[i], kb, tile);
       }
       griddep_wait();
       for (int i = 0; i < pro; ++i) {
@@ -103,7 +122,7 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
         const int tile = u / P.kblocks, kb = u % P.kblocks;
         uint8_t* st = smem + s * kp.stage_bytes;
         mbar_expect_tx(&full[s], bytes);
-        tma_load_2d(st, &tm_w, &full[s], kb * 64, tile * kBM, pol_w);
+        load_w(st, &full[s], kb, tile);
         tma_load_2d(st + kABytes, &tm_x, &full[s], kb * 64, 0, pol_x);
       }
     }
@@ -134,6 +153,42 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
         }
         mma_commit(&acc_full[ab]);
       }
+    }
+  } else if (kRope) {
+    // epilogue (one whole tile): bf16-round the q_up output (the oracle's
+    // storage point), exchange x1 / x2 of each pair through smem between the
+    // warp pairs (sub 0 <-> 2, 1 <-> 3: lane l of both is pair i = j*64 +
+    // (sub&1)*32 + l), rotate with the row's (cos, sin) — the qkv epilogue's
+    // double-precision table — and store bf16 q.
+    const int sub = warp & 3, pair = sub & 1, hi = sub >> 1;
+    const int tile = u_lo / P.kblocks, tph = kp.head_dim / 128, half = kp.head_dim / 2;
+    const int fi = (tile % tph) * 64 + pair * 32 + lane;  // frequency / pair index in the head
+    const int col = (tile / tph) * kp.head_dim + fi + (hi ? half : 0);
+    float* xch = reinterpret_cast<float*>(tmem_slot + 4) + pair * 2 * 32 * 33;  // [2 halves][32 tok][33]
+    griddep_wait();  // the (cos, sin) table comes from the qkv epilogue
+    mbar_wait(&acc_full[0], 0);
+    tc_fence_after();
+    const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
+    for (int c = 0; c < n_mma; c += 32) {
+      uint32_t v[32];
+      tmem_ld32(t_row + c, v);
+      tmem_wait_ld();
+      float* mine = xch + hi * 32 * 33;
+      const float* other = xch + (hi ^ 1) * 32 * 33;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) mine[j * 33 + lane] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[j])));
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair));
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const int t = c + j;
+        if (t >= P.m_tok) break;
+        const float2 cs = __ldg(kp.rope_cs + (size_t)t * half + fi);
+        const float x = mine[j * 33 + lane], y = other[j * 33 + lane];
+        // x1' = x1 c - x2 s ; x2' = x2 c + x1 s
+        const float o = hi ? (x * cs.x + y * cs.y) : (x * cs.x - y * cs.y);
+        kp.q_out[(size_t)t * P.n_out + col] = __float2bfloat16_rn(o);
+      }
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pair));
     }
   } else {
     // epilogue: TMEM lane = weight row = output feature, column = token;
@@ -223,14 +278,16 @@ size_t linear_workspace_bytes(const LinearPlan& p, int num_sms) {
   return align_up((size_t)(p.tiles + num_sms) * p.m_tok * lin::kBM * sizeof(float), 256);
 }
 
-cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
-                               cudaStream_t stream) {
+static cudaError_t linear_launch_impl(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
+                                      __nv_bfloat16* q_out, const float2* rope_cs, int head_dim,
+                                      cudaStream_t stream) {
   using namespace lin;
+  const bool rope = q_out != nullptr;
   CUtensorMap tw, tx;
   {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.n_out};
     const uint64_t strides[1] = {(uint64_t)p.k * 2};
-    const uint32_t box[2] = {64, kBM};
+    const uint32_t box[2] = {64, rope ? (uint32_t)(kBM / 2) : (uint32_t)kBM};
     if (!encode_tma(ctx, &tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box,
                     CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
@@ -246,13 +303,38 @@ cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, con
   KParams kp{};
   kp.plan = p;
   kp.part = part;
+  kp.q_out = q_out;
+  kp.rope_cs = rope_cs;
+  kp.head_dim = head_dim;
   kp.stage_bytes = kABytes + p.n_mma * 128;
-  const int budget = 200 * 1024;
+  const int xch_bytes = rope ? 2 * 2 * 32 * 33 * 4 : 0;  // x1/x2 exchange of the two warp pairs
+  const int budget = 200 * 1024 - xch_bytes;
   kp.stages = budget / kp.stage_bytes;
   if (kp.stages > 8) kp.stages = 8;
-  const size_t smem = (size_t)kp.stages * kp.stage_bytes + 1024 + 256;
-  if (const cudaError_t e = ensure_smem(linear_bf16_kernel, smem); e != cudaSuccess) return e;
-  return launch_k(ctx.pdl, linear_bf16_kernel, dim3(linear_grid(ctx, p)), dim3(kThreads), smem, stream, tw, tx, kp);
+  const size_t smem = (size_t)kp.stages * kp.stage_bytes + 1024 + 256 + xch_bytes;
+  const int grid = linear_grid(ctx, p);
+  if (rope) {
+    if (const cudaError_t e = ensure_smem(linear_bf16_kernel<true>, smem); e != cudaSuccess) return e;
+    return launch_k(ctx.pdl, linear_bf16_kernel<true>, dim3(grid), dim3(kThreads), smem, stream, tw, tx, kp);
+  }
+  if (const cudaError_t e = ensure_smem(linear_bf16_kernel<false>, smem); e != cudaSuccess) return e;
+  return launch_k(ctx.pdl, linear_bf16_kernel<false>, dim3(grid), dim3(kThreads), smem, stream, tw, tx, kp);
+}
+
+cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
+                               cudaStream_t stream) {
+  return linear_launch_impl(ctx, p, x, w, part, nullptr, nullptr, 0, stream);
+}
+
+bool linear_rope_fusable(const Ctx& ctx, const LinearPlan& p, int head_dim) {
+  return head_dim % 128 == 0 && p.n_out % head_dim == 0 && linear_grid(ctx, p) == p.tiles;
+}
+
+cudaError_t linear_bf16_rope_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w,
+                                    __nv_bfloat16* q_out, const float2* rope_cs, int head_dim,
+                                    cudaStream_t stream) {
+  if (!linear_rope_fusable(ctx, p, head_dim)) return cudaErrorInvalidValue;
+  return linear_launch_impl(ctx, p, x, w, nullptr, q_out, rope_cs, head_dim, stream);
 }
 
 

@@ -16,6 +16,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "afdk_internal.h"
@@ -128,6 +129,8 @@ struct QkvEpi {
   const double* inv_freq;       // [head_dim/2]
   float k_scale, v_scale;       // > 0: caches are e4m3, store e4m3(bf16(x) / scale)
   int mtp;                      // row r = token r % mtp of request r / mtp, position seq_len - mtp + j
+  float2* rope_cs;              // out (optional): [B, head_dim/2] (cos, sin) of each row's position,
+                                // for the RoPE(q) fused into the q_up GEMM
 };
 
 __device__ __forceinline__ uint8_t kv_e4m3(float x, float scale) {
@@ -154,17 +157,23 @@ __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, c
   const int f1 = rank == kRowCluster - 1 ? e.n_out : f0 + qs;
   const int req = row / e.mtp;
   const int pos = __ldg(e.seq_lens + req) - e.mtp + row % e.mtp;
-  if (f1 > e.q_lora && pos >= 0) {
+  if (f1 > e.q_lora) {
     // the rotation depends only on inputs (seq_lens, inv_freq): one
-    // double-precision sincos per frequency, before the PDL wait
+    // double-precision sincos per frequency, before the PDL wait (rows with
+    // no position yet, L < mtp, rotate q by position 0 like the oracle)
+    const int p0 = max(pos, 0);
     for (int i = threadIdx.x; i < e.head_dim / 2; i += blockDim.x) {
       double sn, cs;
-      sincos((double)pos * e.inv_freq[i], &sn, &cs);
+      sincos((double)p0 * e.inv_freq[i], &sn, &cs);
       cs_s[i] = make_float2((float)cs, (float)sn);
     }
   }
   sm100::griddep_wait();
   sm100::griddep_launch();
+  if (f1 > e.q_lora && e.rope_cs) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < e.head_dim / 2; i += blockDim.x) e.rope_cs[(size_t)row * (e.head_dim / 2) + i] = cs_s[i];
+  }
   const int f = f0 + threadIdx.x * 4;  // 4 features per thread ((f1 - f0)/4 <= blockDim)
   const bool act = f < f1;
   float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -350,6 +359,7 @@ size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms) {
   b += align_up((size_t)B * QL * 2, 256);                       // qa
   b += align_up((size_t)B * NQ * 2, 256);                       // q
   b += align_up((size_t)B * NQ * 2, 256);                       // attn
+  b += align_up((size_t)B * (a.head_dim / 2) * 8, 256);         // rope (cos, sin)
   size_t part = linear_workspace_bytes(make_linear_plan(B, QL + 2 * a.head_dim, Hd), num_sms);
   const size_t p2 = linear_workspace_bytes(make_linear_plan(B, NQ, QL), num_sms);
   const size_t p3 = linear_workspace_bytes(make_linear_plan(B, Hd, NQ), num_sms);
@@ -370,6 +380,7 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   auto* qa = static_cast<__nv_bfloat16*>(take((size_t)B * QL * 2));
   auto* q = static_cast<__nv_bfloat16*>(take((size_t)B * NQ * 2));
   auto* attn = static_cast<__nv_bfloat16*>(take((size_t)B * NQ * 2));
+  auto* rope_cs = static_cast<float2*>(take((size_t)B * (D / 2) * 8));
   float* part = reinterpret_cast<float*>(ws);
   const double* inv_freq = rope_inv_freq(ctx, D, a.rope_theta);
   if (!inv_freq) return cudaErrorMemoryAllocation;
@@ -386,16 +397,24 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   QkvEpi qe{QL, D, a.page_size, a.max_pages, p1.n_out, a.rms_eps,
             static_cast<const __nv_bfloat16*>(a.w_q_norm), qa, static_cast<__nv_bfloat16*>(a.k_cache),
             static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq, a.k_scale, a.v_scale,
-            a.mtp};
+            a.mtp, nullptr};
+  const LinearPlan p2 = make_linear_plan(B, NQ, QL);
+  const bool fused_rope = linear_rope_fusable(ctx, p2, D) && !std::getenv("AFDK_NO_ROPE_FUSION");
+  if (fused_rope) qe.rope_cs = rope_cs;
   if ((e = launch_cluster_k(ctx.pdl, kRowCluster, qkv_epilogue_kernel, dim3(B * kRowCluster), dim3(512), 0, stream,
                             p1, (const float*)part, linear_grid(ctx, p1), qe)) != cudaSuccess)
     return e;
-  // K1c: q_up projection + RoPE(q)
-  const LinearPlan p2 = make_linear_plan(B, NQ, QL);
-  if ((e = linear_bf16_launch(ctx, p2, qa, a.w_q_up, part, stream)) != cudaSuccess) return e;
-  if ((e = launch_k(ctx.pdl, qup_epilogue_kernel, dim3(B, (NQ / 8 + 255) / 256), dim3(256), 0, stream, p2,
-                    (const float*)part, linear_grid(ctx, p2), NQ, D, a.seq_lens, a.mtp, inv_freq, q)) != cudaSuccess)
-    return e;
+  // K1c: q_up projection + RoPE(q): fused into the GEMM's epilogue when every
+  // CTA owns a whole tile (the layer's shape on 148 SMs), else a row epilogue
+  if (fused_rope) {
+    if ((e = linear_bf16_rope_launch(ctx, p2, qa, a.w_q_up, q, rope_cs, D, stream)) != cudaSuccess) return e;
+  } else {
+    if ((e = linear_bf16_launch(ctx, p2, qa, a.w_q_up, part, stream)) != cudaSuccess) return e;
+    if ((e = launch_k(ctx.pdl, qup_epilogue_kernel, dim3(B, (NQ / 8 + 255) / 256), dim3(256), 0, stream, p2,
+                      (const float*)part, linear_grid(ctx, p2), NQ, D, a.seq_lens, a.mtp, inv_freq, q)) !=
+        cudaSuccess)
+      return e;
+  }
   // K2/K3: MFA decode core over the paged cache (now including this token)
   MfaDecodeArgs md{a.batch, q, a.k_cache, a.v_cache, a.num_pages, a.block_table, a.max_pages, a.seq_lens,
                    a.softmax_scale, attn, nullptr, part, a.k_scale, a.v_scale};

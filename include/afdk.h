@@ -366,6 +366,29 @@ afdk_status afdk_wait(afdk_ctx* ctx, const uint32_t* flag, uint32_t value, afdk_
 afdk_status afdk_add_partials(afdk_ctx* ctx, const void* base, const void* const* parts_dev, int n, size_t count,
                               void* out, afdk_stream stream);
 
+/* -------------------------------------- NVLS in-switch reduction groups
+ * The FFN-tier reduction of PAPER.md:651,654 (EP / TP partials summed for the
+ * attention side) done by the NVSwitch: n_members GPUs (one process each)
+ * bind one buffer each to a multicast object; afdk_nvls_reduce_bf16 reads
+ * the element-wise sum over all members' buffers through the multicast
+ * address (multimem.ld_reduce, fp32 accumulation in the switch).
+ *   creator (creator_pid <= 0): creates the object and returns *export_fd;
+ *   the others pass the creator's pid and export_fd (exchanged through the
+ *   caller's rendezvous; imported with pidfd_getfd).  Every member then calls
+ *   afdk_nvls_bind (blocks until all members were created/imported): uc_ptr
+ *   = this member's buffer (write your contribution), mc_ptr = the multicast
+ *   view (the reduce's input).  Order contributions before the reduce with
+ *   the exchange flags (afdk_signal / afdk_wait).  AFDK_ERR_UNSUPPORTED when
+ *   the device or system has no NVLS.                                      */
+typedef struct afdk_nvls afdk_nvls;
+int afdk_nvls_supported(afdk_ctx* ctx);
+afdk_status afdk_nvls_create(afdk_ctx* ctx, int n_members, size_t bytes, int creator_pid, int creator_fd,
+                             afdk_nvls** out, int* export_fd);
+afdk_status afdk_nvls_bind(afdk_nvls* g, void** uc_ptr, void** mc_ptr);
+size_t afdk_nvls_size(const afdk_nvls* g);
+void afdk_nvls_destroy(afdk_nvls* g);
+afdk_status afdk_nvls_reduce_bf16(afdk_ctx* ctx, const void* mc_ptr, void* out, size_t count, afdk_stream stream);
+
 /* --------------------------------------------- AFD pipeline runtime (C++)
  * The A -> link -> F -> link schedule of a decode layer that
  * pipesim.cpp:155-237 models (ping-pong micro-batches, PAPER.md:690-724:

@@ -219,6 +219,12 @@ class AfdFfnWeights(Structure):
 ALLGATHER = ctypes.CFUNCTYPE(c_int, c_void_p, c_void_p, c_size_t, c_void_p)
 
 _SIGS = {
+    "afdk_nvls_supported": (c_int, [c_void_p]),
+    "afdk_nvls_create": (c_int, [c_void_p, c_int, c_size_t, c_int, c_int, POINTER(c_void_p), POINTER(c_int)]),
+    "afdk_nvls_bind": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p)]),
+    "afdk_nvls_size": (c_size_t, [c_void_p]),
+    "afdk_nvls_destroy": (None, [c_void_p]),
+    "afdk_nvls_reduce_bf16": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "afdk_afd_check_cfg": (c_int, [POINTER(AfdCfg)]),
     "afdk_afd_get_layout": (c_int, [POINTER(AfdCfg), POINTER(AfdLayout)]),
     "afdk_afd_plan": (c_int, [POINTER(AfdCfg), c_int, c_uint32, c_void_p, c_int, POINTER(c_int)]),

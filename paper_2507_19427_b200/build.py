@@ -33,6 +33,7 @@ CU_SOURCES = [
     "afd_measured.cu",
     "pipeline_model.cpp",
     "afd_runtime.cu",
+    "nvls.cu",
 ]
 CXX_SOURCES: list[str] = []
 

@@ -269,6 +269,7 @@ struct MoeGemmBf16Args {
   int H, I, E, expert_lo, n_local, rows_pad;
   __nv_bfloat16* h;      // W13 output [rows_pad, I]
   float* y;              // W2 output [rows_pad, H]
+  int chunk = 128;       // token rows per work item (128 or 256)
 };
 cudaError_t moe_gemm_bf16_launch(Ctx& ctx, bool glu, const MoeGemmBf16Args& a, cudaStream_t stream);
 struct MoeFfnBf16Args {

@@ -166,29 +166,37 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     const int col = (tile / tph) * kp.head_dim + fi + (hi ? half : 0);
     float* xch = reinterpret_cast<float*>(tmem_slot + 4) + pair * 2 * 32 * 33;  // [2 halves][32 tok][33]
     griddep_wait();  // the (cos, sin) table comes from the qkv epilogue
+    // this lane's (cos, sin) for 32 tokens, loaded as one batch (independent
+    // L2 loads in flight); chunk 0's before the accumulator is ready
+    float2 cs[32];
+    auto load_cs = [&](int c) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        cs[j] = (c + j < P.m_tok) ? __ldg(kp.rope_cs + (size_t)(c + j) * half + fi) : make_float2(0.f, 0.f);
+    };
+    load_cs(0);
     mbar_wait(&acc_full[0], 0);
     tc_fence_after();
     const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
+    float* mine = xch + hi * 32 * 33;
+    const float* other = xch + (hi ^ 1) * 32 * 33;
     for (int c = 0; c < n_mma; c += 32) {
       uint32_t v[32];
       tmem_ld32(t_row + c, v);
       tmem_wait_ld();
-      float* mine = xch + hi * 32 * 33;
-      const float* other = xch + (hi ^ 1) * 32 * 33;
 #pragma unroll
       for (int j = 0; j < 32; ++j) mine[j * 33 + lane] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(v[j])));
       asm volatile("bar.sync %0, 64;" ::"r"(1 + pair));
-#pragma unroll 4
+#pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int t = c + j;
-        if (t >= P.m_tok) break;
-        const float2 cs = __ldg(kp.rope_cs + (size_t)t * half + fi);
         const float x = mine[j * 33 + lane], y = other[j * 33 + lane];
         // x1' = x1 c - x2 s ; x2' = x2 c + x1 s
-        const float o = hi ? (x * cs.x + y * cs.y) : (x * cs.x - y * cs.y);
-        kp.q_out[(size_t)t * P.n_out + col] = __float2bfloat16_rn(o);
+        const float o = hi ? (x * cs[j].x + y * cs[j].y) : (x * cs[j].x - y * cs[j].y);
+        if (t < P.m_tok) kp.q_out[(size_t)t * P.n_out + col] = __float2bfloat16_rn(o);
       }
       asm volatile("bar.sync %0, 64;" ::"r"(1 + pair));
+      if (c + 32 < n_mma) load_cs(c + 32);
     }
   } else {
     // epilogue: TMEM lane = weight row = output feature, column = token;

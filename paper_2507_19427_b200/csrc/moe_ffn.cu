@@ -146,8 +146,15 @@ cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cu
 // 16-bit variant (QuantScheme with 2-byte FFN weights, types.hpp:34-40):
 // bf16 dispatch rows gathered as 2H-byte rows, bf16 grouped GEMMs, the same
 // permute / combine and partial semantics.
+// 256-row items once routed experts average >= 128 rows (AFDK_BF16_CHUNK=128/256 forces)
+static int moe_bf16_chunk(int T, int k, int E) {
+  if (const char* env = std::getenv("AFDK_BF16_CHUNK")) return std::atoi(env) > 128 ? 256 : 128;
+  return (long)T * k >= 128L * E ? 256 : 128;
+}
+static int rows_pad_bf16(int T, int k, int E) { return moe::rows_pad(T, k) + moe_bf16_chunk(T, k, E); }
+
 size_t moe_ffn_bf16_workspace_bytes(int T, int k, int E, int H, int I) {
-  const int rp = moe::rows_pad_mx(T, k);
+  const int rp = rows_pad_bf16(T, k, E);
   size_t b = 0;
   b += align_up((size_t)(E + 1) * 4, 256);
   b += 2 * align_up((size_t)T * k * 4, 256);
@@ -161,7 +168,8 @@ size_t moe_ffn_bf16_workspace_bytes(int T, int k, int E, int H, int I) {
 
 cudaError_t moe_ffn_bf16_launch(Ctx& ctx, const MoeFfnBf16Args& a, void* ws_base, cudaStream_t stream) {
   const int T = a.T, k = a.k, E = a.E, H = a.H, I = a.I;
-  const int rp = moe::rows_pad_mx(T, k);
+  const int rp = rows_pad_bf16(T, k, E);
+  const int chunk = moe_bf16_chunk(T, k, E);
   uint8_t* ws = static_cast<uint8_t*>(ws_base);
   auto take = [&](size_t bytes) { void* p = ws; ws += align_up(bytes, 256); return p; };
   auto* offsets = static_cast<int32_t*>(take((size_t)(E + 1) * 4));
@@ -181,15 +189,15 @@ cudaError_t moe_ffn_bf16_launch(Ctx& ctx, const MoeFfnBf16Args& a, void* ws_base
     return err;
   };
   moe::PermuteArgs pa{a.ids, T, k, E, a.expert_lo, a.expert_hi, shared_local ? 1 : 0, a.shared_lo, a.shared_hi,
-                      offsets, perm, inv, work, n_work, moe::kChunkMX};
+                      offsets, perm, inv, work, n_work, chunk};
   if ((e = chk(permute_launch(pa, stream, ctx.pdl), "permute")) != cudaSuccess) return e;
   // rows of 2H bytes, no scales
   moe::GatherArgs ga{static_cast<const uint8_t*>(a.x), nullptr, perm, T, k, 2 * H, rp, xp, nullptr, nullptr, nullptr};
   if ((e = chk(gather_launch(ga, stream, ctx.pdl), "gather")) != cudaSuccess) return e;
   const int n_local = a.expert_hi - a.expert_lo;
-  MoeGemmBf16Args g13{a.w13, xp, work, n_work, H, I, E, a.expert_lo, n_local, rp, h, nullptr};
+  MoeGemmBf16Args g13{a.w13, xp, work, n_work, H, I, E, a.expert_lo, n_local, rp, h, nullptr, chunk};
   if ((e = chk(moe_gemm_bf16_launch(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
-  MoeGemmBf16Args g2{a.w2, h, work, n_work, H, I, E, a.expert_lo, n_local, rp, nullptr, y};
+  MoeGemmBf16Args g2{a.w2, h, work, n_work, H, I, E, a.expert_lo, n_local, rp, nullptr, y, chunk};
   if ((e = chk(moe_gemm_bf16_launch(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
   moe::CombineArgs ca{y, a.ids, a.weights, inv, T, k, H, a.expert_lo, a.expert_hi, shared_local ? 1 : 0,
                       a.shared_lo, a.shared_hi, static_cast<__nv_bfloat16*>(a.out), a.dst, a.rows_per_dst};

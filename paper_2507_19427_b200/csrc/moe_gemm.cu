@@ -239,7 +239,7 @@ moe_gemm_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
             for (int j = 0; j < 16; ++j) {
               const int n = g16 * 16 + j;
               const float g = accg[n];
-              h[n] = (g / (1.0f + __expf(-g))) * accu[kGLU ? n : 0];
+              h[n] = sm100::silu_fast(g) * accu[kGLU ? n : 0];
               float m = fabsf(h[n]);
 #pragma unroll
               for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));

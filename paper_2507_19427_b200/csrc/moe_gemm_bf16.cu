@@ -19,6 +19,10 @@
 // Items are ordered (expert, m-tile, chunk) (moe.cuh item_of), so an expert's
 // chunks share each weight tile while it is in L2.
 //
+// Items carry up to 128 token rows, or 256 once experts average >= 128 rows
+// (MMA N = 256 halves the L2->smem bytes per FLOP, the limit of the 128-row
+// form at large batches; gate | up then fill all 512 TMEM columns).
+//
 // Roles (192 threads): w0 TMA producer, w1 MMA issuer + TMEM owner, w2-5
 // epilogue (one TMEM subpartition each).
 #include <cuda.h>
@@ -50,6 +54,8 @@ struct BfGemmParams {
   __nv_bfloat16* h;      // W13 out: [rows_pad, I] bf16
   float* y;              // W2 out:  [rows_pad, H] fp32
   int stage_bytes, stages;
+  int chunk;             // token rows per item: 128, or 256 at large batches (MMA N = 256:
+                         // half the L2->smem bytes per FLOP; accumulators use all 512 TMEM columns)
 };
 
 template <bool kGLU>
@@ -60,7 +66,8 @@ moe_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kA = 128 * 128;  // 128 weight rows x 64 bf16
   constexpr int kAOps = kGLU ? 2 : 1;
-  constexpr int kB = kChunkMX * 128;
+  const int kB = p.chunk * 128;
+  const int acc_cols = p.chunk;  // one accumulator's TMEM columns
   const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * p.stage_bytes);
   uint64_t* empty = full + S;
@@ -78,7 +85,7 @@ moe_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -129,7 +136,7 @@ moe_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
           const uint32_t b_base = base + kAOps * kA;
 #pragma unroll
           for (int op = 0; op < kAOps; ++op) {
-            const uint32_t d = tmem + (kGLU ? op * 128 : b * 128);
+            const uint32_t d = tmem + (uint32_t)((kGLU ? op : b) * acc_cols);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)  // K = 16 bf16 = 32 bytes per MMA
               mma_bf16(d, sdesc_sw128(base + op * kA + kk * 32, 0, 1024), sdesc_sw128(b_base + kk * 32, 0, 1024),
@@ -154,20 +161,20 @@ moe_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
       tc_fence_after();
       const int col = ir.mt * 128 + feat;
 #pragma unroll 1
-      for (int c = 0; c < kChunkMX / 32; ++c) {
+      for (int c = 0; c < p.chunk / 32; ++c) {
         if (c * 32 >= wk.rows) break;
         uint32_t v[32];
-        tmem_ld32(t_lane + b * 128 + c * 32, v);
+        tmem_ld32(t_lane + b * acc_cols + c * 32, v);
         if (kGLU) {
           uint32_t u[32];
-          tmem_ld32(t_lane + 128 + c * 32, u);
+          tmem_ld32(t_lane + acc_cols + c * 32, u);
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int r = c * 32 + j;
             if (r < wk.rows) {
               const float g = __uint_as_float(v[j]);
-              const float hv = (g / (1.0f + __expf(-g))) * __uint_as_float(u[j]);
+              const float hv = silu_fast(g) * __uint_as_float(u[j]);
               p.h[((size_t)wk.row0 + r) * p.out_cols + col] = __float2bfloat16_rn(hv);
             }
           }
@@ -189,7 +196,7 @@ moe_gemm_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<512>(tmem);
   }
 }
 
@@ -211,7 +218,7 @@ cudaError_t moe_gemm_bf16_launch(Ctx& ctx, bool glu, const MoeGemmBf16Args& a, c
   {
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)a.rows_pad};
     const uint64_t strides[1] = {(uint64_t)K * 2};
-    const uint32_t box[2] = {64, kChunkMX};
+    const uint32_t box[2] = {64, (uint32_t)a.chunk};
     if (!encode_tma(ctx, &tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.x), dims, strides, box,
                     CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
@@ -229,7 +236,8 @@ cudaError_t moe_gemm_bf16_launch(Ctx& ctx, bool glu, const MoeGemmBf16Args& a, c
   p.out_cols = glu ? a.I : a.H;
   p.h = a.h;
   p.y = a.y;
-  p.stage_bytes = (glu ? 2 : 1) * 128 * 128 + kChunkMX * 128;
+  p.chunk = a.chunk;
+  p.stage_bytes = (glu ? 2 : 1) * 128 * 128 + a.chunk * 128;
   p.stages = (200 * 1024) / p.stage_bytes;
   if (p.stages > 8) p.stages = 8;
   const size_t smem = (size_t)p.stages * p.stage_bytes + 1024 + 256;

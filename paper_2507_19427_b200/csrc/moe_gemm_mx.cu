@@ -259,7 +259,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float g = __uint_as_float(v[j]);
-            const float h = (g / (1.0f + __expf(-g))) * __uint_as_float(u[j]);
+            const float h = silu_fast(g) * __uint_as_float(u[j]);
             float m = fabsf(h);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));

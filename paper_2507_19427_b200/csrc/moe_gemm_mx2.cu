@@ -314,7 +314,7 @@ moe_gemm_mx2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_const
             const float ga[4] = {a.x, a.y, a.z, a.w}, ub[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
             for (int z = 0; z < 4; ++z) {
-              h[q * 4 + z] = __fdividef(ga[z], 1.0f + __expf(-ga[z])) * ub[z];
+              h[q * 4 + z] = silu_fast(ga[z]) * ub[z];
               amax = fmaxf(amax, fabsf(h[q * 4 + z]));
             }
           }

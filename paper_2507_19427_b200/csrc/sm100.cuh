@@ -189,6 +189,25 @@ __device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* m, int c0,
                : "memory");
 }
 
+// ------------------------------------------------------------- activations
+// SiLU(g) = g * sigmoid(g) = h + h * tanh(h), h = g / 2: one MUFU.TANH per
+// element instead of MUFU.EX2 + MUFU.RCP (the SwiGLU epilogues are MUFU-bound);
+// tanh.approx.f32 is accurate to ~2^-11 relative, far below the bf16 / e4m3
+// rounding of the stored intermediate.
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float silu_fast(float g) {
+#ifdef AFDK_SILU_EXP  // A/B variant: the exp + reciprocal form
+  return __fdividef(g, 1.0f + __expf(-g));
+#else
+  const float h = 0.5f * g;
+  return fmaf(h, tanh_approx(h), h);
+#endif
+}
+
 // ------------------------------------------------------------------- TMEM
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

@@ -430,7 +430,15 @@ afdk_status afdk_nvls_reduce_bf16(afdk_ctx* ctx, const void* mc_ptr, void* out, 
 #define AFDK_AFD_MAX_MICRO 4
 enum { AFDK_FFN_FP8 = 0, AFDK_FFN_MX = 1, AFDK_FFN_BF16 = 2 };
 enum { AFDK_LAYER_MOE = 0, AFDK_LAYER_DENSE = 1 };
-enum { AFDK_F2A_PUSH = 0, AFDK_F2A_PULL = 1 };
+enum { AFDK_F2A_PUSH = 0, AFDK_F2A_PULL = 1, AFDK_F2A_NVLS = 2 };
+/* f2a: PUSH — each FFN rank's combine stores its partial rows into the
+ * attention rank's receive buffer over NVLink, the attention side adds them;
+ * PULL — the attention rank DMA-pulls them; NVLS — each FFN rank's combine
+ * writes its rows into its OWN member buffer of an NVLS group per
+ * (attention rank, micro-batch) whose attention member is h_res, and the
+ * attention side reads x = h_res + sum of partials with one in-switch
+ * multimem.ld_reduce (afdk_nvls_*; needs >= 1 GPU per rank on an NVSwitch
+ * box and pidfd_getfd permission between the ranks' processes). */
 
 typedef struct afdk_afd_cfg {
   int n_attn, n_ffn, n_micro;  /* n_micro <= AFDK_AFD_MAX_MICRO (2 = ping-pong)        */

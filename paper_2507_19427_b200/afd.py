@@ -28,7 +28,7 @@ from . import afdk as _k
 
 FFN_FORMATS = {"fp8": 0, "mx": 1, "bf16": 2}
 LAYER_KINDS = {"moe": 0, "dense": 1}
-F2A = {"push": 0, "pull": 1}
+F2A = {"push": 0, "pull": 1, "nvls": 2}
 OP_NAMES = {0: "ATTN", 1: "SIGNAL", 2: "WAIT", 3: "PULL", 4: "REDUCE", 5: "JOIN", 6: "FFN"}
 BUF_SEND, BUF_RECV, BUF_RX, BUF_OUT, BUF_H_RES, BUF_H_NORM = 0, 1, 2, 3, 4, 5
 
@@ -52,7 +52,8 @@ class AfdConfig:
     seed: int = 0
     ffn_format: str = "fp8"   # "fp8": 1x128/128x128 fp32 scales; "mx": MXFP8; "bf16": 16-bit experts
     f2a: str = "push"         # "push": the FFN combine writes into the attention GPUs' receive
-                              # buffers over NVLink (fused); "pull": attention DMA-pulls
+                              # buffers over NVLink (fused); "pull": attention DMA-pulls;
+                              # "nvls": partials reduced in the NVSwitch (multimem.ld_reduce)
     layer_kind: str = "moe"   # "moe": routed experts (EP over FFN GPUs); "dense": the dense Step-3
                               # FFN (inter dense_inter) as intermediate slices, tensor-parallel
     dense_inter: int = 18432
@@ -67,7 +68,7 @@ class AfdConfig:
         if self.layer_kind not in LAYER_KINDS:
             raise ValueError(f"layer_kind={self.layer_kind!r}: expected 'moe' or 'dense'")
         if self.f2a not in F2A:
-            raise ValueError(f"f2a={self.f2a!r}: expected 'push' or 'pull'")
+            raise ValueError(f"f2a={self.f2a!r}: expected one of {sorted(F2A)}")
         if self.kv not in ("bf16", "e4m3"):
             raise ValueError(f"kv={self.kv!r}: expected 'bf16' or 'e4m3'")
         if _k.load().afdk_afd_check_cfg(ctypes.byref(self.c_cfg())) != 0:

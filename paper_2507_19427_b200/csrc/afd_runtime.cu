@@ -8,6 +8,7 @@
 // library's own kernels and zero-SM transport (csrc/exchange.cu: copy-engine
 // DMA over NVLink, stream-ordered sequence flags).
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -43,7 +44,7 @@ std::string check_cfg(const afdk_afd_cfg* c) {
   if (c->attn_chunk < 1 || c->attn_chunk > 256) return "attn_chunk must be in [1, 256]";
   if (c->hidden < 512 || c->hidden % 512) return "hidden must be a positive multiple of 512";
   if (c->ffn_format < AFDK_FFN_FP8 || c->ffn_format > AFDK_FFN_BF16) return "unknown ffn_format";
-  if (c->f2a != AFDK_F2A_PUSH && c->f2a != AFDK_F2A_PULL) return "unknown f2a";
+  if (c->f2a != AFDK_F2A_PUSH && c->f2a != AFDK_F2A_PULL && c->f2a != AFDK_F2A_NVLS) return "unknown f2a";
   if (c->layer_kind == AFDK_LAYER_MOE) {
     if (c->n_experts < 1 || c->n_experts > 64 || c->n_ffn > c->n_experts) return "need 1 <= n_ffn <= n_experts <= 64";
     if (c->top_k < 1 || c->top_k > 8) return "top_k must be in [1, 8]";
@@ -178,6 +179,10 @@ struct afdk_afd {
   std::vector<std::vector<uint8_t*>> peer_bufs;  // attn peer: send[mb]; FFN peer: out[mb]
   std::vector<std::vector<uint8_t*>> peer_recv;  // attn peer: recv[mb] (push)
   std::vector<void*> opened;
+  // NVLS return (f2a = AFDK_F2A_NVLS): groups [n_attn][n_micro] (an attention
+  // rank holds only its own row a), unicast / multicast views
+  std::vector<afdk_nvls*> nvls;
+  std::vector<uint8_t*> nv_uc, nv_mc;  // index a * n_micro + mb
   uint32_t seq = 0;
   // measured trace (afdk_afd_trace_start / afdk_afd_trace_csv)
   struct Rec {
@@ -260,6 +265,8 @@ afdk_status alloc_local(afdk_afd* r) {
 struct Blob {
   int32_t ok;
   int32_t rank;
+  int32_t pid;                            // NVLS: the group creator's process ...
+  int32_t nvls_fd[AFDK_AFD_MAX_MICRO];    // ... and its exported descriptors (attention ranks)
   uint8_t flags[afdk::kHandle];
   uint8_t bufs[AFDK_AFD_MAX_MICRO][afdk::kHandle];  // attn: send; FFN: out
   uint8_t recv[AFDK_AFD_MAX_MICRO][afdk::kHandle];  // attn: recv
@@ -268,6 +275,21 @@ struct Blob {
 afdk_status export_handles(afdk_afd* r, Blob* b) {
   afdk_ctx* ctx = r->ctxs[0];
   afdk_status s;
+  const afdk_afd_cfg& c = r->cfg;
+  if (c.f2a == AFDK_F2A_NVLS) {
+    r->nvls.assign((size_t)c.n_attn * c.n_micro, nullptr);
+    r->nv_uc.assign(r->nvls.size(), nullptr);
+    r->nv_mc.assign(r->nvls.size(), nullptr);
+    b->pid = (int32_t)getpid();
+    if (r->attn)  // this attention rank creates its groups: members = itself + every FFN rank
+      for (int m = 0; m < c.n_micro; ++m) {
+        int fd = -1;
+        if ((s = afdk_nvls_create(ctx, 1 + c.n_ffn, r->lay.part_bytes, 0, -1, &r->nvls[(size_t)r->idx * c.n_micro + m],
+                                  &fd)) != AFDK_OK)
+          return s;
+        b->nvls_fd[m] = fd;
+      }
+  }
   if ((s = afdk_ipc_handle(ctx, r->flags, b->flags)) != AFDK_OK) return s;
   for (int m = 0; m < r->cfg.n_micro; ++m) {
     if ((s = afdk_ipc_handle(ctx, r->attn ? r->send[m] : r->out[m], b->bufs[m])) != AFDK_OK) return s;
@@ -306,6 +328,32 @@ afdk_status connect(afdk_afd* r, const std::vector<Blob>& all) {
       }
     }
   }
+  if (c.f2a == AFDK_F2A_NVLS) {
+    afdk_status s;
+    if (!r->attn)  // join every attention rank's groups (all joins before any bind)
+      for (int a = 0; a < c.n_attn; ++a)
+        for (int m = 0; m < c.n_micro; ++m)
+          if ((s = afdk_nvls_create(ctx, 1 + c.n_ffn, r->lay.part_bytes, all[a].pid, all[a].nvls_fd[m],
+                                    &r->nvls[(size_t)a * c.n_micro + m], nullptr)) != AFDK_OK)
+            return s;
+    for (size_t i = 0; i < r->nvls.size(); ++i) {
+      if (!r->nvls[i]) continue;
+      void *uc = nullptr, *mc = nullptr;
+      if ((s = afdk_nvls_bind(r->nvls[i], &uc, &mc)) != AFDK_OK) return s;
+      r->nv_uc[i] = static_cast<uint8_t*>(uc);
+      r->nv_mc[i] = static_cast<uint8_t*>(mc);
+    }
+    if (r->attn) {  // h_res IS this rank's member buffer: x = ld_reduce(h_res + partials)
+      for (int m = 0; m < c.n_micro; ++m) r->h_res[m] = r->nv_uc[(size_t)r->idx * c.n_micro + m];
+    } else {  // the combine writes token rows of attention rank a into my member buffer of group (a, mb)
+      for (int m = 0; m < c.n_micro; ++m) {
+        std::vector<uint64_t> d(c.n_attn);
+        for (int a = 0; a < c.n_attn; ++a) d[a] = reinterpret_cast<uint64_t>(r->nv_uc[(size_t)a * c.n_micro + m]);
+        const cudaError_t e = cudaMemcpy(r->dst[m], d.data(), d.size() * 8, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_err("nvls scatter pointers", e);
+      }
+    }
+  }
   if (!r->attn && c.f2a == AFDK_F2A_PUSH) {
     // my slot idx of every attention rank's [n_ffn, T_mb, hidden] receive buffer
     const size_t slot = (size_t)r->idx * r->lay.part_bytes;
@@ -325,6 +373,7 @@ void release(afdk_afd* r) {
   for (cudaStream_t s : r->streams) cudaStreamSynchronize(s);
   if (!r->ctxs.empty())
     for (void* p : r->opened) afdk_ipc_close(r->ctxs[0], p);
+  for (afdk_nvls* g : r->nvls) afdk_nvls_destroy(g);
   for (cudaEvent_t e : r->joins) cudaEventDestroy(e);
   for (cudaEvent_t e : r->ev_pool) cudaEventDestroy(e);
   if (r->t0) cudaEventDestroy(r->t0);
@@ -601,6 +650,9 @@ afdk_status afdk_afd_attn_layer(afdk_afd* afd, const afdk_mfa_weights* w, const 
     afdk_ctx* ctx = afd->ctxs[m];
     afdk_status st = AFDK_OK;
     if (o.kind == AFDK_OP_REDUCE) {
+      if (c.f2a == AFDK_F2A_NVLS)  // x = h_res + sum of the FFN partials, summed in the switch
+        return afdk_nvls_reduce_bf16(ctx, afd->nv_mc[(size_t)afd->idx * c.n_micro + m], in.x,
+                                     (size_t)c.T_mb * c.hidden, s);
       return afdk_add_partials(ctx, afd->h_res[m], const_cast<const void* const*>(afd->part_ptrs[m]), c.n_ffn,
                                (size_t)c.T_mb * c.hidden, in.x, s);
     }
@@ -646,7 +698,7 @@ afdk_status afdk_afd_ffn_layer(afdk_afd* afd, const afdk_afd_ffn_weights* w) {
     const int m = o.mb;
     afdk_ctx* ctx = afd->ctxs[0];
     uint8_t* rx = afd->rx[m];
-    const bool push = c.f2a == AFDK_F2A_PUSH;
+    const bool push = c.f2a != AFDK_F2A_PULL;  // NVLS: the scatter targets are local member buffers
     afdk_row_scatter sc{c.n_attn, c.T_mb, afd->dst[m]};
     void* out = afd->out[m];
     const auto* ids = reinterpret_cast<const int32_t*>(rx + L.rx_off[2]);

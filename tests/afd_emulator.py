@@ -191,7 +191,7 @@ class Rank:
             elif k == "SIGNAL":
                 if self.attn:  # release my payload to the FFN rank
                     self._send(o.peer, o.slot, o.value, SEND, o.mb, self.send[o.mb])
-                elif cfg.f2a == "push":  # the rows my combine stored into attention rank a
+                elif cfg.f2a in ("push", "nvls"):  # the rows my combine stored for attention rank a
                     a, pb = o.peer, self.L.part_bytes
                     self._send(o.peer, o.slot, o.value, RECV, o.mb, self.out[o.mb][a * pb:(a + 1) * pb])
                 else:  # pull: expose my whole partial buffer

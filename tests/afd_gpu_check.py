@@ -30,7 +30,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n-attn", type=int, default=1)
     ap.add_argument("--fmt", default="fp8", choices=["fp8", "mx", "bf16"])
-    ap.add_argument("--f2a", default="push", choices=["push", "pull"])
+    ap.add_argument("--f2a", default="push", choices=["push", "pull", "nvls"])
     ap.add_argument("--kv", default="bf16", choices=["bf16", "e4m3"])
     ap.add_argument("--layer", default="moe", choices=["moe", "dense"])
     ap.add_argument("--attn-chunk", type=int, default=256)

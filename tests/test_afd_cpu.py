@@ -60,6 +60,7 @@ CASES = {
     "1A2F-fp8-push": (1, 2, "fp8", "push"),
     "2A1F-mx-pull": (2, 1, "mx", "pull"),
     "1A1F-bf16-push": (1, 1, "bf16", "push"),
+    "1A2F-mx-nvls": (1, 2, "mx", "nvls"),
 }
 STEPS, LAYERS = 3, 2
 

@@ -500,12 +500,15 @@ def afd_runs(world):
     balanced attention/FFN split, and one dense layer."""
     base = {2: (1, 1), 4: (1, 3), 8: (2, 6)}.get(world, (1, world - 1))
     bal = (world // 2, world - world // 2)
-    runs = [(base, "fp8", 192, "moe", "bf16"), (base, "mx", 256, "moe", "bf16"), (base, "mx", 256, "moe", "e4m3"),
-            (base, "mx", 512, "moe", "e4m3"), (base, "bf16", 256, "moe", "e4m3")]
+    runs = [(base, "fp8", 192, "moe", "bf16", "push"), (base, "mx", 256, "moe", "bf16", "push"),
+            (base, "mx", 256, "moe", "e4m3", "push"), (base, "mx", 512, "moe", "e4m3", "push"),
+            (base, "bf16", 256, "moe", "e4m3", "push")]
     if bal != base:
-        runs += [(bal, "mx", 128, "moe", "e4m3"), (bal, "mx", 192, "moe", "e4m3"), (bal, "mx", 256, "moe", "e4m3"),
-                 (bal, "mx", 512, "moe", "e4m3")]
-    runs.append((bal, "mx", 512, "dense", "bf16"))  # dense layer: FFN tier tensor-parallel over intermediate slices
+        runs += [(bal, "mx", 128, "moe", "e4m3", "push"), (bal, "mx", 192, "moe", "e4m3", "push"),
+                 (bal, "mx", 256, "moe", "e4m3", "push"), (bal, "mx", 512, "moe", "e4m3", "push")]
+    # the FFN partials reduced in the NVSwitch (multimem.ld_reduce) instead of on the attention SMs
+    runs += [(base, "mx", 256, "moe", "e4m3", "nvls")]
+    runs.append((bal, "mx", 512, "dense", "bf16", "push"))  # dense layer: FFN tier tensor-parallel over slices
     return runs
 
 
@@ -535,7 +538,7 @@ def stages_from_traces(traces, n_micro):
 
 
 def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt="fp8", plan=None, kind="moe",
-                     kv="bf16"):
+                     kv="bf16", f2a="push"):
     """Real pipeline on all ranks through the C++ AFD runtime: nA attention
     GPUs + nF FFN GPUs, 2 ping-pong micro-batches, 2 layers per step (distinct
     KV caches), copy-engine NVLink.  One more traced step gives the measured
@@ -546,7 +549,7 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
 
     na, nf = plan if plan else afd_roles(world)
     cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=T_mb, n_micro=2, layers=2, ctx_len=CTX, ffn_format=fmt, layer_kind=kind,
-                    kv=kv)
+                    kv=kv, f2a=f2a)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -590,10 +593,11 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
     del r
     torch.cuda.empty_cache()
     st = stages_from_traces(traces, cfg.n_micro)
+    # stage budget of this pipeline: tpot / n_micro / L (ping-pong: 2 stages per layer period)
     vet = afdk.vet_stages([st["attention"]] * N_LAYERS, [st["ffn"]] * N_LAYERS, tpot_sla=TPOT_SLA,
-                          pipeline_stages=PIPE_STAGES, n_model_layers=N_LAYERS)
+                          pipeline_stages=cfg.n_micro, n_model_layers=N_LAYERS)
     tpot = N_LAYERS * period * 1e-3
-    res = {"plan": f"{na}A{nf}F", "layer": kind, "ffn_format": fmt, "kv": kv, "T_mb": cfg.T_mb,
+    res = {"plan": f"{na}A{nf}F", "layer": kind, "ffn_format": fmt, "kv": kv, "f2a": f2a, "T_mb": cfg.T_mb,
            "n_micro": cfg.n_micro, "ctx": cfg.ctx_len,
            "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
            "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
@@ -607,7 +611,7 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
     tdir = os.environ.get("AFDK_TRACE_DIR")
     if tdir and rank == 0:
         os.makedirs(tdir, exist_ok=True)
-        name = f"afd_{res['plan']}_{fmt}_{kind}_{kv}_T{T_mb}"
+        name = f"afd_{res['plan']}_{fmt}_{kind}_{kv}_{f2a}_T{T_mb}"
         with open(os.path.join(tdir, name + ".csv"), "w") as f:
             for q, csv in enumerate(traces):
                 body = csv.strip().splitlines()
@@ -989,9 +993,16 @@ def main():
             else:
                 # micro-batch sweep: per-layer throughput depends on balancing the
                 # attention tier (grows with T_mb) against expert weight streaming
-                runs = [run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4), T, f, plan, kind,
-                                         kv) for plan, f, T, kind, kv in afd_runs(world)]
-                moe_runs = [x for x in runs if x["layer"] == "moe"]
+                runs = []
+                for plan, f, T, kind, kv, f2a in afd_runs(world):
+                    try:
+                        runs.append(run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4), T,
+                                                     f, plan, kind, kv, f2a))
+                    except Exception as e:  # e.g. no NVLS on this system: reported, the sweep goes on
+                        runs.append({"plan": f"{plan[0]}A{plan[1]}F", "ffn_format": f, "T_mb": T, "layer": kind,
+                                     "kv": kv, "f2a": f2a, "error": f"{type(e).__name__}: {e}"})
+                runs_ok = [x for x in runs if "error" not in x]
+                moe_runs = [x for x in runs_ok if x["layer"] == "moe"]
                 sla = [x for x in moe_runs if x["sla_ok"]]
                 afd = {"runs": runs, "best": max(moe_runs, key=lambda x: x["tokens_per_s_per_gpu_per_layer"]),
                        "best_within_sla": max(sla, key=lambda x: x["tgs_tok_per_gpu_s"]) if sla else None,

@@ -5,6 +5,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <utility>
 
@@ -57,6 +58,12 @@ struct DeviceGuard {
 // kMaxBatch) and K3 merges at most kMfaMaxSplit parts per request
 // (mfa_decode.cu), which must exceed the SM count.
 constexpr int kMfaMaxBatch = 2048;
+// CTAs of the decode core: every SM, or AFDK_MFA_GRID (experiments)
+inline int mfa_grid(const Ctx& ctx, int batch) {
+  static const int env = [] { const char* e = std::getenv("AFDK_MFA_GRID"); return e ? std::atoi(e) : 0; }();
+  (void)batch;
+  return (env > 0 && env < ctx.num_sms) ? env : ctx.num_sms;
+}
 constexpr int kMfaMaxSplit = 160;
 
 // Returns a device workspace of at least `bytes` (grows; not graph-capturable

@@ -520,7 +520,7 @@ size_t mfa_decode_workspace_bytes(int batch, int num_sms) {
 
 cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream) {
   using namespace mfa;
-  const int G = ctx.num_sms;
+  const int G = mfa_grid(ctx, a.batch);
   if (a.batch > kMaxBatch) return cudaErrorInvalidValue;
   uint8_t* ws = static_cast<uint8_t*>(a.workspace);
   Params prm{};

@@ -425,7 +425,7 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
 
 cudaError_t mfa_decode_fp8_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream) {
   using namespace mfa;
-  const int G = ctx.num_sms;
+  const int G = mfa_grid(ctx, a.batch);
   if (a.batch > kMaxBatch) return cudaErrorInvalidValue;
   uint8_t* ws = static_cast<uint8_t*>(a.workspace);
   Params prm{};

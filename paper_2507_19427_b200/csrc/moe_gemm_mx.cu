@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "afdk_internal.h"
 #include "moe.cuh"
@@ -65,6 +66,7 @@ struct MxGemmParams {
   uint8_t* hsf;         // W13 out: [rows_pad, I/32] UE8M0
   float* y;             // W2 out:  [rows_pad, H] fp32
   int stage_bytes, stages;
+  int prefetch;         // L2-prefetch the first item's weights before the PDL wait
 };
 
 __device__ __forceinline__ int mx_weight_index(const MxGemmParams& p, int group) {
@@ -128,6 +130,24 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (p.prefetch && warp == 0 && lane == 0) {
+    // Before the PDL wait: weights never depend on the predecessor, and the
+    // work list was written by the permute kernel, which completed before
+    // this grid could launch (the predecessor launches us only after its own
+    // griddepcontrol.wait).  CTAs that start on SMs the predecessor's last,
+    // partial wave left idle stream their first item's weight tile into L2
+    // while HBM is under-used, instead of idling at the wait.
+    const int n0 = *p.n_work * p.m_tiles;
+    if (cta < n0) {
+      const ItemRef ir = item_of(p.work, cta, p.m_tiles);
+      const Work wk = p.work[ir.chunk];
+      const int wrow = mx_weight_index(p, wk.group) * p.w_rows + ir.mt * 128;
+      for (int kb = 0; kb < p.kblocks; ++kb) {
+        tma_prefetch_l2_2d(&tm_w, kb * 128, wrow);
+        if (kGLU) tma_prefetch_l2_2d(&tm_w, kb * 128, wrow + p.up_offset);
+      }
+    }
+  }
   griddep_wait();
   griddep_launch();
   const uint32_t tmem = *tmem_slot;
@@ -352,6 +372,8 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
   p.hsf = a.hsf;
   p.y = a.y;
   p.stage_bytes = (glu ? 2 : 1) * 128 * 128 + kChunkMX * 128;
+  static const int prefetch = [] { const char* e = std::getenv("AFDK_MX_PREFETCH"); return e ? std::atoi(e) : 1; }();
+  p.prefetch = ctx.pdl ? prefetch : 0;
   p.stages = (196 * 1024) / p.stage_bytes;
   if (p.stages > 6) p.stages = 6;
   const size_t smem = (size_t)p.stages * p.stage_bytes + 2 * (glu ? 3 : 2) * 2048 + 1024 + 512;

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(256) dense_combine_kernel(const float* y, int 
   __nv_bfloat16* orow = dst ? reinterpret_cast<__nv_bfloat16*>(__ldg(dst + t / rows_per_dst)) +
                                   (size_t)(t % rows_per_dst) * H
                             : out + (size_t)t * H;
-  for (int f = (blockIdx.y * blockDim.x + threadIdx.x) * 4; f < H; f += gridDim.y * blockDim.x * 4) {
+  for (int f = threadIdx.x * 4; f < H; f += blockDim.x * 4) {
     float4 acc = __ldcg(reinterpret_cast<const float4*>(y + (size_t)t * H + f));
     for (int j = 1; j < n_split; ++j) {
       const float4 v = __ldcg(reinterpret_cast<const float4*>(y + ((size_t)j * T + t) * H + f));
@@ -300,8 +300,7 @@ cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws_base
   if ((e = chk(gemm(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
   MoeGemmMxArgs g2{a.w2, a.sf2, hq, hsf, work, n_work, a.H, a.Is, a.n_split, 0, a.n_split, rp, nullptr, nullptr, y};
   if ((e = chk(gemm(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
-  return chk(launch_k(ctx.pdl, moe::dense_combine_kernel, dim3(a.T, (a.H + 1023) / 1024), dim3(256), 0, stream,
-                      (const float*)y, a.T,
+  return chk(launch_k(ctx.pdl, moe::dense_combine_kernel, dim3(a.T), dim3(256), 0, stream, (const float*)y, a.T,
                       a.n_split, a.H, static_cast<__nv_bfloat16*>(a.out), a.dst, a.rows_per_dst),
              "combine");
 }

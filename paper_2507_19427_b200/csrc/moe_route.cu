@@ -320,9 +320,7 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   __nv_bfloat16* orow = a.dst ? reinterpret_cast<__nv_bfloat16*>(__ldg(a.dst + t / a.rows_per_dst)) +
                                     (size_t)(t % a.rows_per_dst) * a.H
                               : a.out + (size_t)t * a.H;
-  // blockIdx.y splits the row: (T, ceil(H/1024)) CTAs keep enough loads in
-  // flight at decode T (one 256-thread CTA per token left it latency-bound)
-  for (int f = (blockIdx.y * blockDim.x + threadIdx.x) * 4; f < a.H; f += gridDim.y * blockDim.x * 4) {
+  for (int f = threadIdx.x * 4; f < a.H; f += blockDim.x * 4) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (sh) acc = __ldcg(reinterpret_cast<const float4*>(a.y + sh_row * a.H + f));
     for (int j = 0; j < a.k; ++j) {
@@ -377,7 +375,7 @@ cudaError_t quant_mx_launch(const moe::QuantMxArgs& a, cudaStream_t stream, bool
 }
 
 cudaError_t combine_launch(const moe::CombineArgs& a, cudaStream_t stream, bool pdl) {
-  return launch_k(pdl, moe::combine_kernel, dim3(a.T, (a.H + 1023) / 1024), dim3(256), 0, stream, a);
+  return launch_k(pdl, moe::combine_kernel, dim3(a.T), dim3(256), 0, stream, a);
 }
 
 }  // namespace afdk

@@ -45,46 +45,51 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // mbarrier), then adds the four slots in rank order, so all four hold the
 // identical total.  No cluster barrier (and no fence) on the critical path:
 // row_red_init arms the barrier and publishes it before the PDL wait.
-constexpr int kRowCluster = 4;
+// kC = CTAs per row (4 at decode batches; 2 from 128 token rows, where 4
+// would launch 4 x B CTAs, several waves of the latency-bound kernel).
+template <int kC>
 struct RowRed {
   uint64_t bar;
-  float slot[kRowCluster];
+  float slot[kC];
 };
-__device__ __forceinline__ void row_red_init(RowRed& rr) {
+template <int kC>
+__device__ __forceinline__ void row_red_init(RowRed<kC>& rr) {
   if (threadIdx.x == 0) {
     sm100::mbar_init(&rr.bar, 1);
     sm100::fence_barrier_init();
-    sm100::mbar_expect_tx(&rr.bar, 4 * kRowCluster);
+    sm100::mbar_expect_tx(&rr.bar, 4 * kC);
   }
   sm100::cluster_sync();  // every CTA's barrier is initialised before any peer stores into it
 }
-__device__ __forceinline__ float cluster_row_sum(float v, float* red, RowRed& rr) {
+template <int kC>
+__device__ __forceinline__ float cluster_row_sum(float v, float* red, RowRed<kC>& rr) {
   v = block_sum(v, red);
   if (threadIdx.x == 0) {
     const uint32_t me = sm100::cluster_ctarank();
 #pragma unroll
-    for (int r = 0; r < kRowCluster; ++r)
+    for (int r = 0; r < kC; ++r)
       sm100::st_async_f32(sm100::mapa_shared(&rr.slot[me], r), v, sm100::mapa_shared(&rr.bar, r));
   }
   sm100::mbar_wait(&rr.bar, 0);
   float t = 0.0f;
 #pragma unroll
-  for (int r = 0; r < kRowCluster; ++r) t += rr.slot[r];
+  for (int r = 0; r < kC; ++r) t += rr.slot[r];
   return t;
 }
 
 // xn = RMSNorm(x) * w, bf16 out (input_layernorm); grid B*4 in 4-CTA clusters,
 // CTA r of a row's cluster owns features [r*dim/4, (r+1)*dim/4); dim % 16 == 0
+template <int kC>
 __global__ void __launch_bounds__(512) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
                                                       const __nv_bfloat16* __restrict__ w,
                                                       __nv_bfloat16* __restrict__ out, int dim, float eps) {
   __shared__ float red[32];
-  __shared__ RowRed rr;
+  __shared__ RowRed<kC> rr;
   row_red_init(rr);
   sm100::griddep_wait();
   sm100::griddep_launch();
-  const size_t row = blockIdx.x / kRowCluster;
-  const int q = dim / kRowCluster, f0 = (int)sm100::cluster_ctarank() * q;
+  const size_t row = blockIdx.x / kC;
+  const int q = dim / kC, f0 = (int)sm100::cluster_ctarank() * q;
   const __nv_bfloat16* xr = x + row * dim;
   constexpr int kMax = 4;  // float4 groups per thread (dim/4 <= 4*4*512)
   float2 a[kMax], b[kMax];
@@ -142,19 +147,20 @@ __device__ __forceinline__ uint8_t kv_e4m3(float x, float scale) {
 // grid B*4 in 4-CTA clusters: CTA r < 3 owns q features [r*QL/4, (r+1)*QL/4),
 // CTA 3 the last quarter of q plus all of k and v (q RMSNorm statistics over
 // the cluster; CTA 3 does the RoPE + KV append).  QL/4 + 2*head_dim <= 2048.
+template <int kC>
 __global__ void __launch_bounds__(512) qkv_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
                                                            int G, const QkvEpi e) {
   __shared__ float red[32];
-  __shared__ RowRed rr;
+  __shared__ RowRed<kC> rr;
   __shared__ float kv_s[2 * 256];  // k then v of this row (head_dim <= 256)
   __shared__ float2 cs_s[128];     // RoPE (cos, sin) of this row's position (head_dim <= 256)
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
   row_red_init(rr);
-  const int row = blockIdx.x / kRowCluster;
+  const int row = blockIdx.x / kC;
   const int rank = (int)sm100::cluster_ctarank();
-  const int qs = e.q_lora / kRowCluster, f0 = rank * qs;
-  const int f1 = rank == kRowCluster - 1 ? e.n_out : f0 + qs;
+  const int qs = e.q_lora / kC, f0 = rank * qs;
+  const int f1 = rank == kC - 1 ? e.n_out : f0 + qs;
   const int req = row / e.mtp;
   const int pos = __ldg(e.seq_lens + req) - e.mtp + row % e.mtp;
   if (f1 > e.q_lora) {
@@ -272,18 +278,19 @@ __global__ void __launch_bounds__(256) qup_epilogue_kernel(const LinearPlan P, c
 
 // y = o_proj (fp32); h_res = bf16(x + y); h_norm = RMSNorm(h_res) (post_attention_layernorm)
 // grid B*4 in 4-CTA clusters, CTA r owns features [r*n/4, (r+1)*n/4); n % 16 == 0
+template <int kC>
 __global__ void __launch_bounds__(512) o_epilogue_kernel(const LinearPlan P, const float* __restrict__ part,
                                                          int G, int n, const __nv_bfloat16* __restrict__ x,
                                                          const __nv_bfloat16* __restrict__ w_post, float eps,
                                                          __nv_bfloat16* __restrict__ h_res,
                                                          __nv_bfloat16* __restrict__ h_norm) {
   __shared__ float red[32];
-  __shared__ RowRed rr;
+  __shared__ RowRed<kC> rr;
   __shared__ lin::SlotTable tab;
   lin::build_slot_table(P, G, tab);
   row_red_init(rr);
-  const size_t row = blockIdx.x / kRowCluster;
-  const int q = n / kRowCluster, f0 = (int)sm100::cluster_ctarank() * q;
+  const size_t row = blockIdx.x / kC;
+  const int q = n / kC, f0 = (int)sm100::cluster_ctarank() * q;
   constexpr int kMax = 2;  // float4 groups per thread (n/4 <= 2*4*512)
   // the residual input x and the norm weight are inputs of the layer (x was
   // complete before its first kernel ran): load them before the PDL wait
@@ -386,10 +393,17 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   if (!inv_freq) return cudaErrorMemoryAllocation;
   cudaError_t e;
 
+  // row epilogues: 4-CTA clusters per token row at decode batches, 2-CTA
+  // clusters from 128 rows (AFDK_ROW_CLUSTER=2/4 forces)
+  static const int env_c = [] { const char* v = std::getenv("AFDK_ROW_CLUSTER"); return v ? std::atoi(v) : 0; }();
+  const bool wide = env_c ? env_c == 2 : B >= 128;
+  auto row_launch = [&](auto k2, auto k4, auto&&... args) {
+    return wide ? launch_cluster_k(ctx.pdl, 2, k2, dim3(B * 2), dim3(512), 0, stream, args...)
+                : launch_cluster_k(ctx.pdl, 4, k4, dim3(B * 4), dim3(512), 0, stream, args...);
+  };
   // K1a: input RMSNorm
-  if ((e = launch_cluster_k(ctx.pdl, kRowCluster, rmsnorm_kernel, dim3(B * kRowCluster), dim3(512), 0, stream,
-                            static_cast<const __nv_bfloat16*>(a.x), static_cast<const __nv_bfloat16*>(a.w_in_norm),
-                            xn, Hd, a.rms_eps)) != cudaSuccess)
+  if ((e = row_launch(rmsnorm_kernel<2>, rmsnorm_kernel<4>, static_cast<const __nv_bfloat16*>(a.x),
+                      static_cast<const __nv_bfloat16*>(a.w_in_norm), xn, Hd, a.rms_eps)) != cudaSuccess)
     return e;
   // K1b: [q_down | k | v] projection, then q RMSNorm + RoPE(k) + paged KV append
   const LinearPlan p1 = make_linear_plan(B, QL + 2 * D, Hd);
@@ -405,8 +419,8 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   // epilogue is faster (B=256: 308 vs 302 us, e4m3 KV 240 vs 230 us)
   const bool fused_rope = linear_rope_fusable(ctx, p2, D) && B <= 64 && !std::getenv("AFDK_NO_ROPE_FUSION");
   if (fused_rope) qe.rope_cs = rope_cs;
-  if ((e = launch_cluster_k(ctx.pdl, kRowCluster, qkv_epilogue_kernel, dim3(B * kRowCluster), dim3(512), 0, stream,
-                            p1, (const float*)part, linear_grid(ctx, p1), qe)) != cudaSuccess)
+  if ((e = row_launch(qkv_epilogue_kernel<2>, qkv_epilogue_kernel<4>, p1, (const float*)part, linear_grid(ctx, p1),
+                      qe)) != cudaSuccess)
     return e;
   // K1c: q_up projection + RoPE(q): fused into the GEMM's epilogue when every
   // CTA owns a whole tile (the layer's shape on 148 SMs), else a row epilogue
@@ -429,10 +443,9 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   // K4: o_proj, then residual + post-attention RMSNorm
   const LinearPlan p3 = make_linear_plan(B, Hd, NQ);
   if ((e = linear_bf16_launch(ctx, p3, attn, a.w_o, part, stream)) != cudaSuccess) return e;
-  if ((e = launch_cluster_k(ctx.pdl, kRowCluster, o_epilogue_kernel, dim3(B * kRowCluster), dim3(512), 0, stream, p3,
-                            (const float*)part, linear_grid(ctx, p3), Hd, static_cast<const __nv_bfloat16*>(a.x),
-                            static_cast<const __nv_bfloat16*>(a.w_post_norm), a.rms_eps,
-                            static_cast<__nv_bfloat16*>(a.h_res), static_cast<__nv_bfloat16*>(a.h_norm))) !=
+  if ((e = row_launch(o_epilogue_kernel<2>, o_epilogue_kernel<4>, p3, (const float*)part, linear_grid(ctx, p3), Hd,
+                      static_cast<const __nv_bfloat16*>(a.x), static_cast<const __nv_bfloat16*>(a.w_post_norm),
+                      a.rms_eps, static_cast<__nv_bfloat16*>(a.h_res), static_cast<__nv_bfloat16*>(a.h_norm))) !=
       cudaSuccess)
     return e;
   return cudaGetLastError();

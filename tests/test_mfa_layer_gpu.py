@@ -136,3 +136,18 @@ def test_mfa_layer_mtp2(ctx, dims, seq_lens, seed):
         for j, pos in enumerate((L - 2, L - 1)):
             pg, s = bt[b, pos // page], pos % page
             assert rel_err(gk[pg, s], k1[pg, s]) <= 1e-2, (b, j)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kv", ["bf16", "e4m3"])
+def test_mfa_layer_wide_batch(ctx, kv):
+    """256 requests (the AFD micro-batch): the 2-CTA-cluster row epilogues, the
+    separate RoPE(q) row epilogue and the N=256 projections; ragged contexts."""
+    rng = np.random.default_rng(77)
+    seq_lens = rng.integers(1, 700, size=256).tolist()
+    if kv == "bf16":
+        check(run_layer(ctx, STEP3, seq_lens, 31), 64)
+    else:
+        g_res, g_norm, gk, gv, r_res, r_norm, rk, rv, bt, sl, _ = run_layer_fp8(ctx, STEP3, seq_lens, 32)
+        assert rel_err(g_res, r_res) <= 3e-2, rel_err(g_res, r_res)
+        assert rel_err(g_norm, r_norm) <= 3e-2, rel_err(g_norm, r_norm)

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "afdk_internal.h"
 #include "linear.cuh"
@@ -52,7 +53,7 @@ __device__ __forceinline__ void unit_range(int c, int G, int U, int& lo, int& hi
   hi = (int)(((long long)(c + 1) * U) / G);
 }
 
-template <bool kRope>
+template <bool kRope, bool kM2>
 __global__ void __launch_bounds__(kThreads, 1)
 linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                    const KParams kp) {
@@ -91,7 +92,7 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      const uint32_t bytes = kABytes + n_mma * 128;
+      const uint32_t bytes = (kM2 ? 2 : 1) * kABytes + n_mma * 128;
       // kRope: the panel's rows 0-63 are the pairs' x1 rows, 64-127 their x2 rows
       const int tph = kRope ? kp.head_dim / 128 : 1;
       auto load_w = [&](uint8_t* dst, uint64_t* bar, int kb, int tile) {
@@ -99,6 +100,9 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
           const int r1 = (tile / tph) * kp.head_dim + (tile % tph) * 64;
           tma_load_2d(dst, &tm_w, bar, kb * 64, r1, pol_w);
           tma_load_2d(dst + kABytes / 2, &tm_w, bar, kb * 64, r1 + kp.head_dim / 2, pol_w);
+        } else if (kM2) {  // two 128-row panels of a 256-row tile
+          tma_load_2d(dst, &tm_w, bar, kb * 64, tile * 256, pol_w);
+          tma_load_2d(dst + kABytes, &tm_w, bar, kb * 64, tile * 256 + kBM, pol_w);
         } else {
           tma_load_2d(dst, &tm_w, bar, kb * 64, tile * kBM, pol_w);
         }
@@ -114,7 +118,7 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       griddep_wait();
       for (int i = 0; i < pro; ++i) {
         const int u = u_lo + i, kb = u % P.kblocks;
-        tma_load_2d(smem + i * kp.stage_bytes + kABytes, &tm_x, &full[i], kb * 64, 0, pol_x);
+        tma_load_2d(smem + i * kp.stage_bytes + (kM2 ? 2 : 1) * kABytes, &tm_x, &full[i], kb * 64, 0, pol_x);
       }
       for (int u = u_lo + pro, i = pro; u < u_hi; ++u, ++i) {
         const int s = i % S, n = i / S;
@@ -123,31 +127,36 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
         uint8_t* st = smem + s * kp.stage_bytes;
         mbar_expect_tx(&full[s], bytes);
         load_w(st, &full[s], kb, tile);
-        tma_load_2d(st + kABytes, &tm_x, &full[s], kb * 64, 0, pol_x);
+        tma_load_2d(st + (kM2 ? 2 : 1) * kABytes, &tm_x, &full[s], kb * 64, 0, pol_x);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(128, (uint32_t)n_mma, false, false);
+      // kM2: two accumulators (panel 0 / 1) of n_mma columns per segment; they
+      // double-buffer across segments only while 4 x n_mma fits TMEM
+      const bool dbuf = !kM2 || n_mma <= 128;
       int seg = 0;
       for (int u = u_lo, i = 0; u < u_hi; ++seg) {
         const int tile = u / P.kblocks;
         const int seg_end = min(u_hi, (tile + 1) * P.kblocks);
-        const int ab = seg & 1, na = seg >> 1;
-        if (seg >= 2) mbar_wait(&acc_empty[ab], (na & 1) ^ 1);
+        const int ab = dbuf ? (seg & 1) : 0, na = dbuf ? (seg >> 1) : seg;
+        if (dbuf ? seg >= 2 : seg >= 1) mbar_wait(&acc_empty[ab], (na & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + ab * 256;
+        const uint32_t d = tmem + (kM2 ? ab * 2 * n_mma : ab * 256);
         for (bool first = true; u < seg_end; ++u, ++i, first = false) {
           const int s = i % S, n = i / S;
           mbar_wait(&full[s], n & 1);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem + s * kp.stage_bytes);
-          const uint32_t b_base = a_base + kABytes;
+          const uint32_t b_base = a_base + (kM2 ? 2 : 1) * kABytes;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t a = sdesc_sw128(a_base + kk * 32, 0, 1024);
             const uint64_t b = sdesc_sw128(b_base + kk * 32, 0, 1024);
-            mma_bf16(d, a, b, idesc, (first && kk == 0) ? 0u : 1u);
+            mma_bf16(d, sdesc_sw128(a_base + kk * 32, 0, 1024), b, idesc, (first && kk == 0) ? 0u : 1u);
+            if (kM2)
+              mma_bf16(d + n_mma, sdesc_sw128(a_base + kABytes + kk * 32, 0, 1024), b, idesc,
+                       (first && kk == 0) ? 0u : 1u);
           }
           mma_commit(&empty[s]);
         }
@@ -203,23 +212,27 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     // each (tile, k-range) segment writes its fp32 partial to slot tile + cta.
     const int sub = warp & 3;
     const int feat = sub * 32 + lane;
+    const bool dbuf = !kM2 || n_mma <= 128;
     int seg = 0;
     for (int u = u_lo; u < u_hi; ++seg) {
       const int tile = u / P.kblocks;
       const int seg_end = min(u_hi, (tile + 1) * P.kblocks);
       u = seg_end;
-      const int ab = seg & 1, na = seg >> 1;
+      const int ab = dbuf ? (seg & 1) : 0, na = dbuf ? (seg >> 1) : seg;
       mbar_wait(&acc_full[ab], na & 1);
       tc_fence_after();
-      float* dst = kp.part + ((size_t)(tile + cta) * P.m_tok) * kBM + feat;
-      const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16) + ab * 256;
-      for (int c = 0; c < n_mma; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(t_row + c, v);
-        tmem_wait_ld();
+#pragma unroll 1
+      for (int pnl = 0; pnl < (kM2 ? 2 : 1); ++pnl) {
+        float* dst = kp.part + ((size_t)(tile + cta) * P.m_tok) * P.mtile + pnl * kBM + feat;
+        const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16) + (kM2 ? (ab * 2 + pnl) * n_mma : ab * 256);
+        for (int c = 0; c < n_mma; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(t_row + c, v);
+          tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (c + j < P.m_tok) dst[(size_t)(c + j) * kBM] = __uint_as_float(v[j]);
+          for (int j = 0; j < 32; ++j)
+            if (c + j < P.m_tok) dst[(size_t)(c + j) * P.mtile] = __uint_as_float(v[j]);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -277,13 +290,18 @@ LinearPlan make_linear_plan(int m_tok, int n_out, int k) {
   if (p.n_mma < 16) p.n_mma = 16;
   p.n_out = n_out;
   p.k = k;
-  p.tiles = (n_out + lin::kBM - 1) / lin::kBM;
+  // 256-row tiles (two MMA panels per token panel) once the token panel is
+  // wide: at N > 64 the 128-row form moves more L2->smem bytes per FLOP than
+  // the SMs can be fed (AFDK_LIN_MTILE=128/256 forces; projections only)
+  static const int env = [] { const char* e = std::getenv("AFDK_LIN_MTILE"); return e ? std::atoi(e) : 0; }();
+  p.mtile = (n_out >= 2048 && (env ? env == 256 : m_tok > 64)) ? 256 : lin::kBM;
+  p.tiles = (n_out + p.mtile - 1) / p.mtile;
   p.kblocks = k / 64;
   return p;
 }
 
 size_t linear_workspace_bytes(const LinearPlan& p, int num_sms) {
-  return align_up((size_t)(p.tiles + num_sms) * p.m_tok * lin::kBM * sizeof(float), 256);
+  return align_up((size_t)(p.tiles + num_sms) * p.m_tok * p.mtile * sizeof(float), 256);
 }
 
 static cudaError_t linear_launch_impl(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
@@ -314,19 +332,20 @@ static cudaError_t linear_launch_impl(Ctx& ctx, const LinearPlan& p, const void*
   kp.q_out = q_out;
   kp.rope_cs = rope_cs;
   kp.head_dim = head_dim;
-  kp.stage_bytes = kABytes + p.n_mma * 128;
+  const bool m2 = p.mtile == 256 && !rope;
+  kp.stage_bytes = (m2 ? 2 : 1) * kABytes + p.n_mma * 128;
   const int xch_bytes = rope ? 2 * 2 * 32 * 33 * 4 : 0;  // x1/x2 exchange of the two warp pairs
   const int budget = 200 * 1024 - xch_bytes;
   kp.stages = budget / kp.stage_bytes;
   if (kp.stages > 8) kp.stages = 8;
   const size_t smem = (size_t)kp.stages * kp.stage_bytes + 1024 + 256 + xch_bytes;
   const int grid = linear_grid(ctx, p);
-  if (rope) {
-    if (const cudaError_t e = ensure_smem(linear_bf16_kernel<true>, smem); e != cudaSuccess) return e;
-    return launch_k(ctx.pdl, linear_bf16_kernel<true>, dim3(grid), dim3(kThreads), smem, stream, tw, tx, kp);
-  }
-  if (const cudaError_t e = ensure_smem(linear_bf16_kernel<false>, smem); e != cudaSuccess) return e;
-  return launch_k(ctx.pdl, linear_bf16_kernel<false>, dim3(grid), dim3(kThreads), smem, stream, tw, tx, kp);
+  auto go = [&](auto kernel) -> cudaError_t {
+    if (const cudaError_t e = ensure_smem(kernel, smem); e != cudaSuccess) return e;
+    return launch_k(ctx.pdl, kernel, dim3(grid), dim3(kThreads), smem, stream, tw, tx, kp);
+  };
+  if (rope) return go(linear_bf16_kernel<true, false>);
+  return m2 ? go(linear_bf16_kernel<false, true>) : go(linear_bf16_kernel<false, false>);
 }
 
 cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
@@ -335,7 +354,7 @@ cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, con
 }
 
 bool linear_rope_fusable(const Ctx& ctx, const LinearPlan& p, int head_dim) {
-  return head_dim % 128 == 0 && p.n_out % head_dim == 0 && linear_grid(ctx, p) == p.tiles;
+  return p.mtile == lin::kBM && head_dim % 128 == 0 && p.n_out % head_dim == 0 && linear_grid(ctx, p) == p.tiles;
 }
 
 cudaError_t linear_bf16_rope_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w,

@@ -12,8 +12,10 @@ struct LinearPlan {
   int n_mma;    // m_tok rounded up to the MMA N granularity (16)
   int n_out;    // output features (rows of W)
   int k;        // reduction dim, multiple of 64
-  int tiles;    // ceil(n_out / 128)
+  int tiles;    // ceil(n_out / mtile)
   int kblocks;  // k / 64
+  int mtile;    // weight rows per work tile: 128, or 256 (two MMA panels sharing the
+                // token panel) once the token panel is wide (L2->smem bytes per FLOP)
 };
 
 namespace lin {
@@ -28,9 +30,9 @@ struct SlotTable {
   int n[kMaxTiles];
   __device__ __forceinline__ float sum(const LinearPlan& P, const float* __restrict__ part, int row,
                                        int f) const {
-    const int t = f / kBM, c0 = c_lo[t], nn = n[t];
-    const float* base = part + ((size_t)(t + c0) * P.m_tok + row) * kBM + (f % kBM);
-    const size_t stride = (size_t)P.m_tok * kBM;
+    const int t = f / P.mtile, c0 = c_lo[t], nn = n[t];
+    const float* base = part + ((size_t)(t + c0) * P.m_tok + row) * P.mtile + (f % P.mtile);
+    const size_t stride = (size_t)P.m_tok * P.mtile;
     float acc = 0.0f;
 #pragma unroll 4
     for (int k = 0; k < nn; ++k) acc += __ldcg(base + (size_t)k * stride);
@@ -39,9 +41,10 @@ struct SlotTable {
   // features f..f+3 (f % 4 == 0, one tile): one 16-byte load per segment
   __device__ __forceinline__ float4 sum4(const LinearPlan& P, const float* __restrict__ part, int row,
                                          int f) const {
-    const int t = f / kBM, c0 = c_lo[t], nn = n[t];
-    const float4* base = reinterpret_cast<const float4*>(part + ((size_t)(t + c0) * P.m_tok + row) * kBM + (f % kBM));
-    const size_t stride = (size_t)P.m_tok * kBM / 4;
+    const int t = f / P.mtile, c0 = c_lo[t], nn = n[t];
+    const float4* base =
+        reinterpret_cast<const float4*>(part + ((size_t)(t + c0) * P.m_tok + row) * P.mtile + (f % P.mtile));
+    const size_t stride = (size_t)P.m_tok * P.mtile / 4;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 4
     for (int k = 0; k < nn; ++k) {

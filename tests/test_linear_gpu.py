@@ -19,7 +19,7 @@ from tests.helpers import rel_err
     (256, 7168, 16384), # o_proj at the AFD micro-batch: 256-row tiles, single-buffered accumulators
     (128, 16384, 2048), # q_up at 128 rows: 256-row tiles, double-buffered (N = 128)
     (100, 2560, 7168),  # qkv, ragged N (112) on 256-row tiles
-    (96, 2304, 512),    # n_out not a multiple of 256: the last tile's second panel is TMA zero-filled
+    (96, 2176, 512),    # n_out not a multiple of 256: the last tile's second panel is TMA zero-filled
 ])
 def test_linear_vs_torch(ctx, m, n, k):
     import torch

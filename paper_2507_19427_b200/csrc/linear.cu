@@ -290,11 +290,13 @@ LinearPlan make_linear_plan(int m_tok, int n_out, int k) {
   if (p.n_mma < 16) p.n_mma = 16;
   p.n_out = n_out;
   p.k = k;
-  // 256-row tiles (two MMA panels per token panel) once the token panel is
-  // wide: at N > 64 the 128-row form moves more L2->smem bytes per FLOP than
-  // the SMs can be fed (AFDK_LIN_MTILE=128/256 forces; projections only)
+  // 256-row tiles (two MMA panels sharing each token panel; AFDK_LIN_MTILE=256)
+  // halve the L2->smem bytes per FLOP at wide token panels but were slower
+  // end to end: attention layer B=256 317.5 vs 295.0 us, B=128 185.6 vs
+  // 177.2 us (3 pipeline stages instead of 4, single-buffered accumulators,
+  // half the stream-K tiles), so 128-row tiles stay the default
   static const int env = [] { const char* e = std::getenv("AFDK_LIN_MTILE"); return e ? std::atoi(e) : 0; }();
-  p.mtile = (n_out >= 2048 && (env ? env == 256 : m_tok > 64)) ? 256 : lin::kBM;
+  p.mtile = (n_out >= 2048 && env == 256) ? 256 : lin::kBM;
   p.tiles = (n_out + p.mtile - 1) / p.mtile;
   p.kblocks = k / 64;
   return p;

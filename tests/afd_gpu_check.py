@@ -23,7 +23,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-STEPS, LAYERS = 3, 2
+LAYERS = 2
 
 
 def main():
@@ -35,8 +35,10 @@ def main():
     ap.add_argument("--layer", default="moe", choices=["moe", "dense"])
     ap.add_argument("--attn-chunk", type=int, default=256)
     ap.add_argument("--T-mb", type=int, default=24)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    STEPS = a.steps
     import torch
     import torch.distributed as dist
 

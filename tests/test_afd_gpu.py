@@ -23,6 +23,7 @@ CASES = [
     (3, 2, ["--fmt", "fp8", "--f2a", "push", "--kv", "e4m3"]),
     (3, 1, ["--layer", "dense", "--fmt", "mx", "--f2a", "push"]),
     (8, 2, ["--fmt", "mx", "--f2a", "push", "--kv", "e4m3"]),  # config 5's 2A6F layout (8 ranks; GPUs shared)
+    (3, 1, ["--fmt", "fp8", "--f2a", "pull", "--steps", "12"]),  # soak: 24 sequence numbers of flag reuse
     (2, 1, ["--fmt", "mx", "--f2a", "nvls"]),       # NVLS return: one GPU per rank
     (3, 1, ["--fmt", "bf16", "--f2a", "nvls"]),
 ]

@@ -71,6 +71,20 @@ struct __align__(1024) Smem {
   uint32_t tmem_base;
 };
 
+#ifdef AFDK_MFA_TIMES
+// diagnostic build: per-CTA %globaltimer stamps {after the PDL wait, first
+// S consumed, last page of the last segment done, CTA end}
+__device__ unsigned long long g_mfa_times[4 * 256];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MFA_STAMP(i) g_mfa_times[4 * blockIdx.x + (i)] = gtimer()
+#else
+#define MFA_STAMP(i)
+#endif
+
 __global__ void __launch_bounds__(kThreads, 1)
 mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
                   const __grid_constant__ CUtensorMap tm_k,
@@ -112,6 +126,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   const uint32_t tmem = sm.tmem_base;
   griddep_wait();  // q, the appended K/V row and the reused workspace belong to the predecessors
   griddep_launch();
+  if (threadIdx.x == 0) MFA_STAMP(0);
 
   if (warp == 0) {
     // ------------------------------------------------ Q + K TMA producer
@@ -241,6 +256,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
       for (int j = 0; j < n; ++j, ++g) {
         const int sb = g & 1, pb = g & 1;
         mbar_wait(&sm.s_full[sb], (g >> 1) & 1);
+        if (g == 0 && warp == 2 && lane == 0) MFA_STAMP(1);
         tc_fence_after();
         uint32_t sr[32];
         tmem_ld16x2_32(t_row + kColS + sb * 64, sr);
@@ -322,6 +338,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
         if (lane == 0) mbar_arrive(&sm.p_full[pb]);
       }
       // ---------------- epilogue of this segment: O / l -> global
+      if (warp == 2 && lane == 0) MFA_STAMP(2);
       const int gl = g - 1;
       mbar_wait(&sm.p_empty[gl & 1], (gl >> 1) & 1);
       tc_fence_after();
@@ -373,6 +390,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) MFA_STAMP(3);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -508,6 +526,12 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
 }
 
 }  // namespace mfa
+
+#ifdef AFDK_MFA_TIMES
+extern "C" void afdk_debug_mfa_times(unsigned long long* host) {
+  cudaMemcpyFromSymbol(host, mfa::g_mfa_times, sizeof(mfa::g_mfa_times));
+}
+#endif
 
 // ------------------------------------------------------------------ host side
 size_t mfa_decode_workspace_bytes(int batch, int num_sms) {

@@ -22,16 +22,19 @@ for i in range(6):
     k, v = w["kv"][i % 2]
     ctx.mfa_decode_attention(w["q"], k, v, w["block_table"], w["seq_lens"], w["out"], 0.0625, stream=s.cuda_stream)
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * 1024)()
+    buf = (ctypes.c_ulonglong * 1024)()  # 4 stamps x 256 CTAs
     lib.afdk_debug_mfa_times(buf)
     t = np.array(buf[:4 * 148], dtype=np.int64).reshape(148, 4)
     t0 = t[:, 0].min()
     t = (t - t0) / 1e3
     if i >= 3:
         q = lambda c: np.percentile(t[:, c], [0, 50, 100]).round(2).tolist()
-        print(f"start {q(0)} first-S {q(1)} last-PV {q(2)} end {q(3)}  (us; min/median/max over CTAs)")
+        print(f"start {q(0)} first-S {q(1)} last-seg-done {q(2)} end {q(3)}  (us; min/median/max over CTAs)")
+        ends = np.sort(t[:, 3])
+        print("  end deciles:", np.percentile(t[:, 3], [10, 25, 50, 75, 90, 100]).round(2).tolist())
         pages = (w["seq_lens"].cpu().numpy() + 63) // 64
-        pre = np.concatenate([[0], np.cumsum(pages)])
+        units = np.where(pages > 0, pages + 3, 0)  # kSegCost = 3 page-less units per request (mfa_common.cuh)
+        pre = np.concatenate([[0], np.cumsum(units)])
         T, G = pre[-1], 148
         segs = []
         for c in range(G):

@@ -813,14 +813,16 @@ def main():
         ctx.mfa_layer(s["w"], s["x"], k, v, s["block_table"], s["seq_lens"], s["h_res"], s["h_norm"], stream=sp)
 
     step = layer_step if args.workload == "layer" else attn_step
-    launches_per_step = 9 if args.workload == "layer" else 2  # rmsnorm, 3 x (GEMM + row epilogue), K2, K3
+    # layer: rmsnorm, qkv GEMM + epilogue, q_up GEMM (RoPE(q) fused in its epilogue up to 64 rows, else a
+    # row epilogue), K2, K3, o_proj GEMM + epilogue
+    launches_per_step = (8 if args.batch <= 64 else 9) if args.workload == "layer" else 2
 
     for i in range(max(args.warmup, 3)):
         step(i)
         attn_step(i)
     torch.cuda.synchronize()
     # the K timed layers as ONE CUDA graph, as a decode step over a layer stack
-    # is captured: each layer's 9 PDL launches keep their programmatic edges,
+    # is captured: each layer's 8 PDL launches keep their programmatic edges,
     # and so does the hand-off from one layer to the next (layer i reads KV
     # cache i % N_ROT).  The graph is replayed once per timed region, so step i
     # of timed() launches it at i == 0 and the region still covers exactly K
@@ -891,7 +893,7 @@ def main():
             ctx.mfa_decode_attention(ins[b], k, v, s["block_table"], s["seq_lens"], outs[b], scale, stream=sp)
     # A serving loop captures its per-step C-ABI call once and replays it: one
     # graph per (buffer set, KV cache) pair, each holding one mfa_layer call
-    # (its 9 PDL launches), so the host issues one launch per step.
+    # (its 8 PDL launches), so the host issues one launch per step.
     e2e_launch = "direct C-ABI launches"
     if args.workload == "layer" and not args.no_graph and not args.e2e_direct:
         try:

@@ -67,7 +67,6 @@ struct MxGemmParams {
   float* y;             // W2 out:  [rows_pad, H] fp32
   int stage_bytes, stages;
   int prefetch;         // L2-prefetch the first item's weights before the PDL wait
-  int full_box;         // always fetch 128-row token panels (A/B switch AFDK_MX_FULLBOX=1)
 };
 
 __device__ __forceinline__ int mx_weight_index(const MxGemmParams& p, int group) {
@@ -90,8 +89,6 @@ template <bool kGLU>
 __global__ void __launch_bounds__(kMxThreads, 1)
 moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                    const __grid_constant__ CUtensorMap tm_wsf, const __grid_constant__ CUtensorMap tm_xsf,
-                   const __grid_constant__ CUtensorMap tm_x32, const __grid_constant__ CUtensorMap tm_xsf32,
-                   const __grid_constant__ CUtensorMap tm_x64, const __grid_constant__ CUtensorMap tm_xsf64,
                    const MxGemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -120,10 +117,6 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     tma_prefetch_desc(&tm_x);
     tma_prefetch_desc(&tm_wsf);
     tma_prefetch_desc(&tm_xsf);
-    tma_prefetch_desc(&tm_x32);
-    tma_prefetch_desc(&tm_xsf32);
-    tma_prefetch_desc(&tm_x64);
-    tma_prefetch_desc(&tm_xsf64);
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&sf_full[i], 4); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -175,30 +168,24 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
         const int mt = ir.mt;
         const Work wk = p.work[ir.chunk];
         const int wrow = mx_weight_index(p, wk.group) * p.w_rows + mt * 128;
-        // the token panel is fetched for the item's rows only (32 / 64 / 128-row
-        // boxes): at decode batches a chunk holds ~16 rows, and a full 128-row
-        // box would double each SM's TMA ingest per k-block for padding
-        const int brow = p.full_box ? 128 : wk.rows <= 32 ? 32 : wk.rows <= 64 ? 64 : 128;
-        const CUtensorMap* mx = brow == 32 ? &tm_x32 : brow == 64 ? &tm_x64 : &tm_x;
-        const CUtensorMap* msf = brow == 32 ? &tm_xsf32 : brow == 64 ? &tm_xsf64 : &tm_xsf;
         for (int kb = 0; kb < p.kblocks; ++kb, ++i) {
           if ((kb & 3) == 0) {  // scale group of k-blocks kb..kb+3
             const int g = gi & 1, ng = gi >> 1;
             ++gi;
             if (ng > 0) mbar_wait(&sfg_empty[g], (ng & 1) ^ 1);
             uint8_t* dst = sfbuf + g * kSfGrp;
-            mbar_expect_tx(&sfg_full[g], kAOps * kSfOp + brow * 16);
+            mbar_expect_tx(&sfg_full[g], kSfGrp);
             tma_load_2d(dst, &tm_wsf, &sfg_full[g], kb * 4, wrow, pol);
             if (kGLU) tma_load_2d(dst + kSfOp, &tm_wsf, &sfg_full[g], kb * 4, wrow + p.up_offset, pol);
-            tma_load_2d(dst + kAOps * kSfOp, msf, &sfg_full[g], kb * 4, kGLU ? wk.xrow0 : wk.row0, pol_x);
+            tma_load_2d(dst + kAOps * kSfOp, &tm_xsf, &sfg_full[g], kb * 4, kGLU ? wk.xrow0 : wk.row0, pol_x);
           }
           const int s = i % S, n = i / S;
           if (n > 0) mbar_wait(&empty[s], (n & 1) ^ 1);
           uint8_t* st = smem + s * p.stage_bytes;
-          mbar_expect_tx(&full[s], kAOps * kA + brow * 128);
+          mbar_expect_tx(&full[s], kAOps * kA + kB);
           tma_load_2d(st, &tm_w, &full[s], kb * 128, wrow, pol);
           if (kGLU) tma_load_2d(st + kA, &tm_w, &full[s], kb * 128, wrow + p.up_offset, pol);
-          tma_load_2d(st + kAOps * kA, mx, &full[s], kb * 128, kGLU ? wk.xrow0 : wk.row0, pol_x);
+          tma_load_2d(st + kAOps * kA, &tm_x, &full[s], kb * 128, kGLU ? wk.xrow0 : wk.row0, pol_x);
         }
       }
     }
@@ -368,22 +355,6 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
                     CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
   }
-  // token-panel maps with 32 / 64-row boxes for small work items
-  CUtensorMap tx32, tx64, txsf32, txsf64;
-  for (int r : {32, 64}) {
-    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)a.rows_pad};
-    const uint64_t strides[1] = {(uint64_t)K};
-    const uint32_t box[2] = {128, (uint32_t)r};
-    if (!encode_tma(ctx, r == 32 ? &tx32 : &tx64, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(a.x), dims,
-                    strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
-      return cudaErrorInvalidValue;
-    const uint64_t sdims[2] = {(uint64_t)(K / 32), (uint64_t)a.rows_pad};
-    const uint64_t sstrides[1] = {(uint64_t)(K / 32)};
-    const uint32_t sbox[2] = {16, (uint32_t)r};
-    if (!encode_tma(ctx, r == 32 ? &txsf32 : &txsf64, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.x_sf),
-                    sdims, sstrides, sbox, CU_TENSOR_MAP_SWIZZLE_NONE))
-      return cudaErrorInvalidValue;
-  }
   MxGemmParams p{};
   p.work = a.work;
   p.n_work = a.n_work;
@@ -405,20 +376,16 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
   // (16 / 8 experts, the AFD FFN GPUs) 0.381 vs 0.374 and 0.238 vs 0.228 ms
   static const int prefetch = [] { const char* e = std::getenv("AFDK_MX_PREFETCH"); return e ? std::atoi(e) : 0; }();
   p.prefetch = ctx.pdl ? prefetch : 0;
-  static const int full_box = [] { const char* e = std::getenv("AFDK_MX_FULLBOX"); return e ? std::atoi(e) : 0; }();
-  p.full_box = full_box;
   p.stages = (196 * 1024) / p.stage_bytes;
   if (p.stages > 6) p.stages = 6;
   const size_t smem = (size_t)p.stages * p.stage_bytes + 2 * (glu ? 3 : 2) * 2048 + 1024 + 512;
   cudaError_t e;
   if (glu) {
     if ((e = ensure_smem(moe_gemm_mx_kernel<true>, smem)) != cudaSuccess) return e;
-    return launch_k(ctx.pdl, moe_gemm_mx_kernel<true>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, twsf,
-                    txsf, tx32, txsf32, tx64, txsf64, p);
+    return launch_k(ctx.pdl, moe_gemm_mx_kernel<true>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, twsf, txsf, p);
   }
   if ((e = ensure_smem(moe_gemm_mx_kernel<false>, smem)) != cudaSuccess) return e;
-  return launch_k(ctx.pdl, moe_gemm_mx_kernel<false>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, twsf,
-                  txsf, tx32, txsf32, tx64, txsf64, p);
+  return launch_k(ctx.pdl, moe_gemm_mx_kernel<false>, dim3(ctx.num_sms), dim3(kMxThreads), smem, stream, tw, tx, twsf, txsf, p);
 }
 
 }  // namespace afdk

@@ -118,12 +118,7 @@ cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cu
   auto* y = static_cast<float*>(take((size_t)rp * H * 4));
   const bool shared_local = a.shared_hi > a.shared_lo;
   const bool pair = moe_mx_use_pair(T, k, E);
-  // single-CTA items: 32 token rows at decode batches (<= 32 rows per routed
-  // expert on average: the 4 KB token panel leaves smem for a deeper weight
-  // ring), 128 above (AFDK_MX_SMALL_CHUNK=0/1 forces)
-  static const int small_env = [] { const char* v = std::getenv("AFDK_MX_SMALL_CHUNK"); return v ? std::atoi(v) : -1; }();
-  const bool small = small_env >= 0 ? small_env == 1 : (long)T * k <= 32L * E;
-  const int chunk = pair ? moe_mx_pair_chunk(T, k, E) : small ? 32 : moe::kChunkMX;
+  const int chunk = pair ? moe_mx_pair_chunk(T, k, E) : moe::kChunkMX;
   auto gemm = pair ? moe_gemm_mx2_launch : moe_gemm_mx_launch;
   cudaError_t e;
   static const bool dbg = std::getenv("AFDK_DEBUG_SYNC") != nullptr;

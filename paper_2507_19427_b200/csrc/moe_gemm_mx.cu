@@ -67,8 +67,6 @@ struct MxGemmParams {
   float* y;             // W2 out:  [rows_pad, H] fp32
   int stage_bytes, stages;
   int prefetch;         // L2-prefetch the first item's weights before the PDL wait
-  int chunk;            // token rows per work item / token-panel box: 128, or 32 at decode
-                        // batches (4 KB token panels leave smem for deeper weight rings)
 };
 
 __device__ __forceinline__ int mx_weight_index(const MxGemmParams& p, int group) {
@@ -96,7 +94,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kA = 128 * 128;
   constexpr int kAOps = kGLU ? 2 : 1;
-  const int kB = p.chunk * 128;
+  constexpr int kB = kChunkMX * 128;
   constexpr int kSfCols = 4 * kAOps + 4;       // scale columns per ring slot
   constexpr int kSfOp = 128 * 16;              // one operand's scales for 4 k-blocks
   constexpr int kSfGrp = (kAOps + 1) * kSfOp;  // smem scale group (4 k-blocks)
@@ -176,7 +174,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
             ++gi;
             if (ng > 0) mbar_wait(&sfg_empty[g], (ng & 1) ^ 1);
             uint8_t* dst = sfbuf + g * kSfGrp;
-            mbar_expect_tx(&sfg_full[g], kAOps * kSfOp + p.chunk * 16);
+            mbar_expect_tx(&sfg_full[g], kSfGrp);
             tma_load_2d(dst, &tm_wsf, &sfg_full[g], kb * 4, wrow, pol);
             if (kGLU) tma_load_2d(dst + kSfOp, &tm_wsf, &sfg_full[g], kb * 4, wrow + p.up_offset, pol);
             tma_load_2d(dst + kAOps * kSfOp, &tm_xsf, &sfg_full[g], kb * 4, kGLU ? wk.xrow0 : wk.row0, pol_x);
@@ -268,7 +266,7 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       mbar_wait(&acc_full[b], nb & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < p.chunk / 32; ++c) {
+      for (int c = 0; c < kChunkMX / 32; ++c) {
         if (c * 32 >= wk.rows) break;
         uint32_t v[32];
         tmem_ld32(t_lane + b * 128 + c * 32, v);
@@ -321,7 +319,6 @@ moe_gemm_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
 
 cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream) {
   using namespace moe;
-  const int chunk = a.chunk == 32 ? 32 : kChunkMX;
   CUtensorMap tw, tx;
   const int K = glu ? a.H : a.I;
   const int w_rows = glu ? 2 * a.I : a.H;
@@ -336,7 +333,7 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
   {
     const uint64_t dims[2] = {(uint64_t)K, (uint64_t)a.rows_pad};
     const uint64_t strides[1] = {(uint64_t)K};
-    const uint32_t box[2] = {128, (uint32_t)chunk};
+    const uint32_t box[2] = {128, kChunkMX};
     if (!encode_tma(ctx, &tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(a.x), dims, strides, box,
                     CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
@@ -353,7 +350,7 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
   {
     const uint64_t dims[2] = {(uint64_t)(K / 32), (uint64_t)a.rows_pad};
     const uint64_t strides[1] = {(uint64_t)(K / 32)};
-    const uint32_t box[2] = {16, (uint32_t)chunk};
+    const uint32_t box[2] = {16, 128};
     if (!encode_tma(ctx, &txsf, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(a.x_sf), dims, strides, box,
                     CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
@@ -374,14 +371,13 @@ cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaS
   p.hq = a.hq;
   p.hsf = a.hsf;
   p.y = a.y;
-  p.chunk = chunk;
-  p.stage_bytes = (glu ? 2 : 1) * 128 * 128 + chunk * 128;
+  p.stage_bytes = (glu ? 2 : 1) * 128 * 128 + kChunkMX * 128;
   // off by default: 48 local experts 0.969 vs 0.987 ms, but expert shards
   // (16 / 8 experts, the AFD FFN GPUs) 0.381 vs 0.374 and 0.238 vs 0.228 ms
   static const int prefetch = [] { const char* e = std::getenv("AFDK_MX_PREFETCH"); return e ? std::atoi(e) : 0; }();
   p.prefetch = ctx.pdl ? prefetch : 0;
   p.stages = (196 * 1024) / p.stage_bytes;
-  if (p.stages > 8) p.stages = 8;
+  if (p.stages > 6) p.stages = 6;
   const size_t smem = (size_t)p.stages * p.stage_bytes + 2 * (glu ? 3 : 2) * 2048 + 1024 + 512;
   cudaError_t e;
   if (glu) {

@@ -468,3 +468,21 @@ def ref_stage_budget(tpot, stages, layers):
 def _ref_check(rc):
     if rc != 0:
         raise RuntimeError(ref().ref_last_error().decode())
+
+
+def ref_dump_builtin_catalog() -> str:
+    ref().ref_dump_builtin_catalog.restype = c_void_p
+    p = ref().ref_dump_builtin_catalog()
+    if not p:
+        raise RuntimeError(ref().ref_last_error().decode())
+    s = ctypes.string_at(p).decode()
+    ref().ref_free(ctypes.c_void_p(p))
+    return s
+
+
+def ref_catalog_accel(text: str, name: str) -> dict:
+    """The reference's own catalog loader (parse_catalog + validate) on `text`."""
+    out = (c_double * 6)()
+    _ref_check(ref().ref_catalog_accel(c_char_p(text.encode()), c_char_p(name.encode()), out))
+    keys = ["flops_16bit", "flops_8bit", "mem_bw", "net_bw_per_server", "gpus_per_server", "net_efficiency"]
+    return dict(zip(keys, list(out)))

@@ -236,6 +236,33 @@ int ref_vet_plan(const char* model, const char* hw, double f16, double f8, doubl
   });
 }
 
+// the builtin catalog in the reference's own TOML schema (dump_catalog)
+char* ref_dump_builtin_catalog() {
+  char* res = nullptr;
+  guarded([&] {
+    const std::string t = afd::dump_catalog(afd::builtin_catalog());
+    res = static_cast<char*>(std::malloc(t.size() + 1));
+    std::memcpy(res, t.c_str(), t.size() + 1);
+  });
+  return res;
+}
+
+// parse a catalog text with the reference's loader (parse_catalog validates
+// every entry) and return accelerator `name`'s fields:
+// {flops_16bit, flops_8bit (0 if absent), mem_bw, net_bw_per_server, gpus_per_server, net_efficiency}
+int ref_catalog_accel(const char* text, const char* name, double out[6]) {
+  return guarded([&] {
+    const afd::Catalog cat = afd::parse_catalog(text, "b200_catalog");
+    const afd::AcceleratorSpec& a = cat.accelerator(name);
+    out[0] = a.flops_16bit;
+    out[1] = a.flops_8bit.value_or(0.0);
+    out[2] = a.mem_bw;
+    out[3] = a.net_bw_per_server;
+    out[4] = a.gpus_per_server;
+    out[5] = a.net_efficiency;
+  });
+}
+
 void ref_free(void* p) { std::free(p); }
 
 }  // extern "C"

@@ -606,8 +606,11 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
            "measured_stage_us": {k: v * 1e6 for k, v in st.items()},
            "vet_stages": vet,
            "nvlink_bytes_per_layer": {k: v * cfg.n_micro for k, v in wb.items()},
-           "transport": ("A->F copy-engine DMA pulls; F->A partial rows stored over NVLink by the combine kernel "
-                         "(fused); cuStreamWrite/WaitValue32 flags"), "runtime": "C++ afdk_afd_*", "measured": True}
+           "transport": "A->F copy-engine DMA pulls; " + {
+               "push": "F->A partial rows stored over NVLink by the combine kernel (fused)",
+               "pull": "F->A partial rows DMA-pulled by the attention GPU",
+               "nvls": "F->A partials summed in the NVSwitch (NVLS multimem.ld_reduce over per-rank member buffers)",
+           }[f2a] + "; cuStreamWrite/WaitValue32 flags", "runtime": "C++ afdk_afd_*", "measured": True}
     tdir = os.environ.get("AFDK_TRACE_DIR")
     if tdir and rank == 0:
         os.makedirs(tdir, exist_ok=True)

@@ -80,6 +80,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
             raise RuntimeError("link failed")
     build_demo(force)
+    build_afd_demo(force)
     build_ref_demo(force)
     return OUT
 
@@ -99,6 +100,27 @@ def build_demo(force: bool = False) -> str:
             sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
             raise RuntimeError("demo build failed")
     return DEMO_OUT
+
+
+AFD_DEMO_SRC = os.path.join(ROOT, "tests", "cpp", "afd_cpp_demo.cpp")
+AFD_DEMO_OUT = os.path.join(ROOT, "tests", "cpp", "afd_cpp_demo")
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+
+
+def build_afd_demo(force: bool = False) -> str:
+    """The AFD runtime driven from C++ alone (fork per rank, file rendezvous),
+    linked against libafdk.so and the static CUDA runtime for its own buffers."""
+    deps = [AFD_DEMO_SRC, OUT, os.path.join(ROOT, "include", "afdk.h")]
+    if force or _stale(AFD_DEMO_OUT, deps):
+        cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I",
+               os.path.join(CUDA_HOME, "include"), AFD_DEMO_SRC, "-o", AFD_DEMO_OUT, "-L", HERE, "-lafdk",
+               "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart_static", "-lrt", "-ldl", "-lpthread",
+               f"-Wl,-rpath,{HERE}", "-Wl,-rpath,$ORIGIN/../../paper_2507_19427_b200"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+            raise RuntimeError("AFD C++ demo build failed")
+    return AFD_DEMO_OUT
 
 
 REF_INCLUDE = os.environ.get("AFD_REFERENCE_INCLUDE", "/root/reference/proj/include")

@@ -37,6 +37,26 @@ __device__ __forceinline__ int request_units(int seq_len) {
 }
 
 
+#ifdef AFDK_MFA_TIMES
+// diagnostic build: launch timeline over back-to-back launches, one record of
+// 8 stamps per launch (%globaltimer, ns): K2 {first entry, first / last PDL
+// release, last end}, K3 {first entry, last wait done, last exit}.  Launch
+// index = arrival count / grid size.  One copy per translation unit (static).
+constexpr int kTlLaunches = 64;
+static __device__ unsigned long long g_tl[kTlLaunches * 8];
+static __device__ unsigned int g_tl_arrive[2];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int tl_launch(int which, unsigned grid) {
+  return (int)(atomicAdd(&g_tl_arrive[which], 1u) / grid) % kTlLaunches;
+}
+__device__ __forceinline__ void tl_min(int launch, int i) { atomicMin(&g_tl[launch * 8 + i], tl_now()); }
+__device__ __forceinline__ void tl_max(int launch, int i) { atomicMax(&g_tl[launch * 8 + i], tl_now()); }
+#endif
+
 struct Params {
   const int32_t* block_table;  // [B, max_pages]
   const int32_t* seq_lens;     // [B]

@@ -93,6 +93,10 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   int32_t* prefix = reinterpret_cast<int32_t*>(&sm + 1);  // [B+1] after the Smem block
   // (seq_lens is a caller input: no kernel of this library writes it, so it may be read before griddep_wait)
+#ifdef AFDK_MFA_TIMES
+  __shared__ int s_tl;
+  if (threadIdx.x == 0) { s_tl = tl_launch(0, gridDim.x); tl_min(s_tl, 0); }
+#endif
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -127,6 +131,9 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   griddep_wait();  // q, the appended K/V row and the reused workspace belong to the predecessors
   griddep_launch();
   if (threadIdx.x == 0) MFA_STAMP(0);
+#ifdef AFDK_MFA_TIMES
+  if (threadIdx.x == 0) { tl_min(s_tl, 1); tl_max(s_tl, 2); }
+#endif
 
   if (warp == 0) {
     // ------------------------------------------------ Q + K TMA producer
@@ -391,6 +398,9 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) MFA_STAMP(3);
+#ifdef AFDK_MFA_TIMES
+  if (threadIdx.x == 0) tl_max(s_tl, 3);
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
@@ -419,6 +429,10 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
   __shared__ int s_n;
   __shared__ int s_red[2][kK3Threads / 32];
   griddep_launch();
+#ifdef AFDK_MFA_TIMES
+  __shared__ int s_tl;
+  if (threadIdx.x == 0) { s_tl = tl_launch(1, gridDim.x * gridDim.y); tl_min(s_tl, 4); }
+#endif
   const int R = prm.rows > 0 ? prm.rows : kHeads;  // query rows per request
   const int req = blockIdx.x;
   const int hl = threadIdx.x >> 5, head = blockIdx.y * kK3Rows + hl;
@@ -465,6 +479,9 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
         if (++spins > (1ll << 24)) __trap();
       }
     }
+#ifdef AFDK_MFA_TIMES
+    tl_max(s_tl, 5);
+#endif
   }
   __syncthreads();
   const int n = s_n;
@@ -522,6 +539,9 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
       prm.sync[kMaxBatch + req] = 0;
     }
   }
+#ifdef AFDK_MFA_TIMES
+  if (threadIdx.x == 0) tl_max(s_tl, 6);
+#endif
   griddep_wait();
 }
 
@@ -530,6 +550,19 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
 #ifdef AFDK_MFA_TIMES
 extern "C" void afdk_debug_mfa_times(unsigned long long* host) {
   cudaMemcpyFromSymbol(host, mfa::g_mfa_times, sizeof(mfa::g_mfa_times));
+}
+// timeline of the bf16 K2 + K3 (host: kTlLaunches x 8); reset = re-arm before a run
+extern "C" void afdk_debug_mfa_tl(unsigned long long* host, int reset) {
+  using namespace mfa;
+  if (reset) {
+    static unsigned long long init[kTlLaunches * 8];
+    for (int i = 0; i < kTlLaunches * 8; ++i) init[i] = (i % 8 == 0 || i % 8 == 1 || i % 8 == 4) ? ~0ull : 0ull;
+    cudaMemcpyToSymbol(g_tl, init, sizeof(init));
+    const unsigned z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_tl_arrive, z, sizeof(z));
+    return;
+  }
+  cudaMemcpyFromSymbol(host, g_tl, sizeof(g_tl));
 }
 #endif
 

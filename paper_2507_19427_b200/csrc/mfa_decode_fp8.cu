@@ -84,6 +84,10 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   extern __shared__ uint8_t smem_raw[];
   Smem8& sm = *reinterpret_cast<Smem8*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   int32_t* prefix = reinterpret_cast<int32_t*>(&sm + 1);
+#ifdef AFDK_MFA_TIMES
+  __shared__ int s_tl;
+  if (threadIdx.x == 0) { s_tl = tl_launch(0, gridDim.x); tl_min(s_tl, 0); }
+#endif
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -118,6 +122,9 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   const uint32_t tmem = sm.tmem_base;
   griddep_wait();
   griddep_launch();
+#ifdef AFDK_MFA_TIMES
+  if (threadIdx.x == 0) { tl_min(s_tl, 1); tl_max(s_tl, 2); }
+#endif
 
   if (warp == 0) {
     // ------------------------------------------------ Q + K TMA producer
@@ -415,6 +422,9 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
 
   tc_fence_before();
   __syncthreads();
+#ifdef AFDK_MFA_TIMES
+  if (threadIdx.x == 0) tl_max(s_tl, 3);
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -422,6 +432,22 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
 }
 
 }  // namespace mfa
+
+#ifdef AFDK_MFA_TIMES
+// timeline of the e4m3 K2 (slots 0-3; K3's slots are in afdk_debug_mfa_tl)
+extern "C" void afdk_debug_mfa8_tl(unsigned long long* host, int reset) {
+  using namespace mfa;
+  if (reset) {
+    static unsigned long long init[kTlLaunches * 8];
+    for (int i = 0; i < kTlLaunches * 8; ++i) init[i] = (i % 8 == 0 || i % 8 == 1 || i % 8 == 4) ? ~0ull : 0ull;
+    cudaMemcpyToSymbol(g_tl, init, sizeof(init));
+    const unsigned z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_tl_arrive, z, sizeof(z));
+    return;
+  }
+  cudaMemcpyFromSymbol(host, g_tl, sizeof(g_tl));
+}
+#endif
 
 cudaError_t mfa_decode_fp8_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t stream) {
   using namespace mfa;

@@ -341,8 +341,10 @@ class AfdRank:
                          for i in range(self.cfg.n_micro + 1)]
 
     # ----------------------------------------------------------------- step
-    def step(self):
-        """One decode step over cfg.layers layers for every micro-batch (enqueue only)."""
+    def step(self, after_layer=None):
+        """One decode step over cfg.layers layers for every micro-batch (enqueue only).
+        after_layer(layer) runs after each layer is enqueued (e.g. to enqueue a
+        snapshot of x on the runtime's micro-batch streams)."""
         lib = _k.load()
         for layer in range(self.cfg.layers):
             if self.role == "attn":
@@ -350,6 +352,8 @@ class AfdRank:
                                                  self.c_mbs[layer]))
             else:
                 _k.check(lib.afdk_afd_ffn_layer(self.handle, ctypes.byref(self.c_ffn_w)))
+            if after_layer is not None:
+                after_layer(layer)
 
     def buffer(self, which: int, mb: int) -> int:
         return _k.load().afdk_afd_buffer(self.handle, which, mb) or 0

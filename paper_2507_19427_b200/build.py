@@ -25,6 +25,7 @@ CU_SOURCES = [
     "moe_gemm_mx.cu",
     "moe_gemm_mx2.cu",
     "moe_gemm_bf16.cu",
+    "moe_ffn_mx_fused.cu",
     "mfa_layer.cu",
     "moe_route.cu",
     "moe_gemm.cu",

@@ -240,6 +240,10 @@ struct MoeGemmMxArgs {
   float* y;              // W2 output [rows_pad, H]
   int chunk = 0;         // rows per work item (pair kernels: > 256 selects the two-accumulator form)
 };
+// decode-batch MoE: gate|up + down GEMMs in one persistent launch (dynamic
+// item queue in sched[0], per-chunk gate|up completion counters in sched[1..])
+cudaError_t moe_ffn_mx_fused_launch(Ctx& ctx, const MoeGemmMxArgs& g13, const MoeGemmMxArgs& g2, int* sched,
+                                    cudaStream_t stream);
 cudaError_t moe_gemm_mx_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream);
 cudaError_t moe_gemm_mx2_launch(Ctx& ctx, bool glu, const MoeGemmMxArgs& a, cudaStream_t stream);
 // CTA-pair kernels once experts see enough rows (AFDK_MX_PAIR=0/1 forces)

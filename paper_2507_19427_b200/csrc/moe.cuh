@@ -59,6 +59,8 @@ struct PermuteArgs {
   Work* work;          // [max work]
   int* n_work;
   int chunk;           // rows per work item (kChunk or kChunkMX)
+  int* sched = nullptr;  // optional: zeroed [sched_len] (queue head + per-chunk counters of the fused kernel)
+  int sched_len = 0;
 };
 
 struct GatherArgs {

@@ -83,7 +83,15 @@ size_t moe_ffn_mx_workspace_bytes(int T, int k, int E, int H, int I) {
   b += align_up((size_t)rp * I, 256);       // hq
   b += align_up((size_t)rp * (I / 32), 256);  // hsf
   b += align_up((size_t)rp * H * 4, 256);   // y
+  b += align_up((size_t)(1 + moe::max_work(T, k, E)) * 4, 256);  // fused kernel's queue
   return b;
+}
+
+// decode batches: gate|up and down GEMMs in one launch with a dynamic item
+// queue (moe_ffn_mx_fused.cu); AFDK_MX_FUSED=0 runs the two launches
+static bool moe_mx_fused() {
+  static const bool on = [] { const char* e = std::getenv("AFDK_MX_FUSED"); return !(e && e[0] == '0'); }();
+  return on;
 }
 
 bool moe_mx_use_pair(int T, int k, int E) {
@@ -116,8 +124,10 @@ cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cu
   auto* hq = static_cast<uint8_t*>(take((size_t)rp * I));
   auto* hsf = static_cast<uint8_t*>(take((size_t)rp * (I / 32)));
   auto* y = static_cast<float*>(take((size_t)rp * H * 4));
+  auto* sched = static_cast<int*>(take((size_t)(1 + moe::max_work(T, k, E)) * 4));
   const bool shared_local = a.shared_hi > a.shared_lo;
   const bool pair = moe_mx_use_pair(T, k, E);
+  const bool fused = !pair && moe_mx_fused();
   const int chunk = pair ? moe_mx_pair_chunk(T, k, E) : moe::kChunkMX;
   auto gemm = pair ? moe_gemm_mx2_launch : moe_gemm_mx_launch;
   cudaError_t e;
@@ -129,15 +139,23 @@ cudaError_t moe_ffn_mx_launch(Ctx& ctx, const MoeFfnMxArgs& a, void* ws_base, cu
   };
   moe::PermuteArgs pa{a.ids, T, k, E, a.expert_lo, a.expert_hi, shared_local ? 1 : 0, a.shared_lo, a.shared_hi,
                       offsets, perm, inv, work, n_work, chunk};
+  if (fused) {
+    pa.sched = sched;
+    pa.sched_len = 1 + moe::max_work(T, k, E);
+  }
   if ((e = chk(permute_launch(pa, stream, ctx.pdl), "permute")) != cudaSuccess) return e;
   moe::GatherArgs ga{a.xq, nullptr, perm, T, k, H, rp, xp, nullptr, a.xsf, xsf_p};
   if ((e = chk(gather_launch(ga, stream, ctx.pdl), "gather")) != cudaSuccess) return e;
   const int n_local = a.expert_hi - a.expert_lo;
   MoeGemmMxArgs g13{a.w13, a.sf13, xp, xsf_p, work, n_work, H, I, E, a.expert_lo, n_local, rp, hq, hsf, nullptr,
                     chunk};
-  if ((e = chk(gemm(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
   MoeGemmMxArgs g2{a.w2, a.sf2, hq, hsf, work, n_work, H, I, E, a.expert_lo, n_local, rp, nullptr, nullptr, y, chunk};
-  if ((e = chk(gemm(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
+  if (fused) {
+    if ((e = chk(moe_ffn_mx_fused_launch(ctx, g13, g2, sched, stream), "gemm13+2")) != cudaSuccess) return e;
+  } else {
+    if ((e = chk(gemm(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
+    if ((e = chk(gemm(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
+  }
   moe::CombineArgs ca{y, a.ids, a.weights, inv, T, k, H, a.expert_lo, a.expert_hi, shared_local ? 1 : 0,
                       a.shared_lo, a.shared_hi, static_cast<__nv_bfloat16*>(a.out), a.dst, a.rows_per_dst};
   return chk(combine_launch(ca, stream, ctx.pdl), "combine");

@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(1024) permute_kernel(PermuteArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s_ids[i] = (uint8_t)a.ids[i];
   for (int i = threadIdx.x; i < 32 * kMaxExperts; i += blockDim.x) (&s_cnt[0][0])[i] = 0;
+  if (a.sched)
+    for (int i = threadIdx.x; i < a.sched_len; i += blockDim.x) a.sched[i] = 0;
   __syncthreads();
   const int seg = (n + 31) / 32;
   const int lo = warp * seg, hi = min(n, lo + seg);

@@ -10,13 +10,16 @@
 // builds its caller-owned data on the host from a fixed seed — attention
 // weights, KV caches and inputs on attention ranks; its expert shard plus
 // the shared expert on FFN ranks, expert e's tensors a function of (seed, e)
-// only — and runs `steps` decode steps x 2 layers x 2 micro-batches.  After
-// each step every attention rank recomputes the step on its own GPU through
-// the single-GPU calls (afdk_mfa_layer, afdk_router_topk / afdk_quant_mx,
-// the MoE over ALL experts, afdk_add_partials) and compares (bar 2e-2 of
-// max|ref|, as tests/afd_gpu_check.py: the runtime sums bf16-rounded EP
-// partials where the recompute rounds the whole MoE once).  Prints one JSON
-// line from rank 0; exit status 0 iff every rank passed.
+// only — and runs `steps` decode steps x 2 layers x 2 micro-batches.  Each
+// layer's output is snapshotted by a copy enqueued on the runtime's
+// micro-batch stream between that layer and the next.  After each step every
+// attention rank recomputes every layer on its own GPU from the runtime's
+// input to that layer through the single-GPU calls (afdk_mfa_layer,
+// afdk_router_topk / afdk_quant_mx, the MoE over ALL experts,
+// afdk_add_partials) and compares (bar 2e-2 of max|ref|, as
+// tests/afd_gpu_check.py: the runtime sums bf16-rounded EP partials where the
+// recompute rounds the whole MoE once).  Prints one JSON line from rank 0;
+// exit status 0 iff every rank passed.
 #include <cuda_runtime.h>
 #include <sys/stat.h>
 #include <sys/wait.h>
@@ -343,6 +346,10 @@ int run_rank(int rank, int world, int n_attn, int fmt, int f2a, int steps, const
     parts_dev = static_cast<void**>(upload(std::vector<void*>{part}));
   }
 
+  std::vector<std::vector<void*>> snap(kLayers, std::vector<void*>(kMicro, nullptr));  // [layer][mb]
+  if (attn)
+    for (auto& l : snap)
+      for (auto& p : l) p = dalloc(act);
   double max_err = 0.0;
   std::vector<uint16_t> got(kTmb * kHidden), ref(kTmb * kHidden);
   for (int s = 0; s < steps; ++s) {
@@ -356,6 +363,9 @@ int run_rank(int rank, int world, int n_attn, int fmt, int f2a, int steps, const
           mbs[m] = afdk_afd_attn_mb{x[m], kv[l][m].k, kv[l][m].v, kv[l][m].num_pages, kPage, kv[l][m].max_pages,
                                     kv[l][m].bt, seq_lens, 0.f, 0.f};
         AK(afdk_afd_attn_layer(afd, &aw.w, aw.gate, mbs));
+        for (int m = 0; m < kMicro; ++m)  // this layer's output, ordered before the next layer's ATTN
+          CK(cudaMemcpyAsync(snap[l][m], x[m], act, cudaMemcpyDeviceToDevice,
+                             static_cast<cudaStream_t>(afdk_afd_stream(afd, m))));
       } else {
         afdk_afd_ffn_weights fw{shard.w13, shard.s13, shard.w2, shard.s2};
         AK(afdk_afd_ffn_layer(afd, &fw));
@@ -363,25 +373,28 @@ int run_rank(int rank, int world, int n_attn, int fmt, int f2a, int steps, const
     }
     AK(afdk_afd_sync(afd));
     if (!attn) continue;
-    for (int m = 0; m < kMicro; ++m) {
-      CK(cudaMemcpy(xr, x_in[m].data(), act, cudaMemcpyHostToDevice));
-      for (int l = 0; l < kLayers; ++l)
+    for (int m = 0; m < kMicro; ++m)
+      for (int l = 0; l < kLayers; ++l) {
+        if (l == 0)
+          CK(cudaMemcpy(xr, x_in[m].data(), act, cudaMemcpyHostToDevice));
+        else
+          CK(cudaMemcpy(xr, snap[l - 1][m], act, cudaMemcpyDeviceToDevice));
         recompute_layer(ctxs[0], aw, all, fmt, kv[l][m], seq_lens, xr, h_res, h_norm, ids, wts, xq, xs, part,
                         parts_dev);
-      CK(cudaDeviceSynchronize());
-      CK(cudaMemcpy(got.data(), x[m], act, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(ref.data(), xr, act, cudaMemcpyDeviceToHost));
-      double amax = 0.0, dmax = 0.0;
-      bool finite = true;
-      for (size_t i = 0; i < got.size(); ++i) {
-        const double r = bf16_to_f(ref[i]), v = bf16_to_f(got[i]);
-        finite = finite && std::isfinite(v) && std::isfinite(r);
-        amax = std::max(amax, std::fabs(r));
-        dmax = std::max(dmax, std::fabs(v - r));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(got.data(), snap[l][m], act, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ref.data(), xr, act, cudaMemcpyDeviceToHost));
+        double amax = 0.0, dmax = 0.0;
+        bool finite = true;
+        for (size_t i = 0; i < got.size(); ++i) {
+          const double r = bf16_to_f(ref[i]), v = bf16_to_f(got[i]);
+          finite = finite && std::isfinite(v) && std::isfinite(r);
+          amax = std::max(amax, std::fabs(r));
+          dmax = std::max(dmax, std::fabs(v - r));
+        }
+        const double err = finite ? dmax / std::max(amax, 1e-12) : 1e30;
+        max_err = std::max(max_err, err);
       }
-      const double err = finite ? dmax / std::max(amax, 1e-12) : 1e30;
-      max_err = std::max(max_err, err);
-    }
   }
   // every rank idle before anyone unmaps: one more rendezvous round
   int token = 0;

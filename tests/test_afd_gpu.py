@@ -1,7 +1,8 @@
 """The C++ AFD runtime end to end on the GPU (tests/afd_gpu_check.py under
 torchrun): 3 steps x 2 layers x 2 micro-batches, buffers reused across
-sequence numbers, every attention rank compared after every step with a
-one-GPU recompute (bar 2e-2, stated in the harness).  With fewer GPUs than
+sequence numbers, every layer of every attention rank compared with a
+one-GPU recompute from the runtime's own input to that layer (bar 2e-2,
+stated in the harness).  With fewer GPUs than
 ranks the ranks share GPUs (CUDA IPC between processes on one device), so
 the protocol runs even on a 1-GPU lease; with >= world GPUs it crosses
 NVLink."""

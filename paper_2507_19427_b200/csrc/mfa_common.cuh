@@ -31,9 +31,9 @@ constexpr int kMaxBatch = 2048;  // prefix of work units per request lives in sm
 constexpr int kSegCost = AFDK_MFA_SEG_COST;
 
 __device__ __forceinline__ int request_pages(int seq_len) { return (max(seq_len, 0) + kPage - 1) / kPage; }
-__device__ __forceinline__ int request_units(int seq_len) {
+__device__ __forceinline__ int request_units(int seq_len, int seg_cost) {
   const int pg = request_pages(seq_len);
-  return pg > 0 ? pg + kSegCost : 0;
+  return pg > 0 ? pg + seg_cost : 0;
 }
 
 
@@ -69,6 +69,8 @@ struct Params {
   float k_scale, v_scale;      // e4m3 KV cache dequantisation scales (fp8 kernel)
   int rows;                    // query rows per request: 64 heads x mtp (0 = 64)
   int* sync;                   // [2][kMaxBatch] zeroed counters: split parts published / K3 CTAs done
+  int seg_cost;                // page-less units charged per request segment (kSegCost; the e4m3
+                               // kernel's pages cost half the time, so its charge is larger)
 };
 
 // A split part of request `req` is in memory: each of the 4 epilogue warps of
@@ -99,16 +101,16 @@ __device__ __forceinline__ int find_request(const int32_t* prefix, int B, int t)
 // Walks the segments (request, [lo,hi) local pages) of one CTA's unit range in order.
 struct SegmentWalker {
   const int32_t* prefix;
-  int B, end, r, pos;
-  __device__ SegmentWalker(const int32_t* pf, int b, int start, int stop)
-      : prefix(pf), B(b), end(stop), r(0), pos(start) {
+  int B, end, r, pos, seg_cost;
+  __device__ SegmentWalker(const int32_t* pf, int b, int start, int stop, int sc = kSegCost)
+      : prefix(pf), B(b), end(stop), r(0), pos(start), seg_cost(sc) {
     if (start < stop) r = find_request(pf, b, start);
   }
   // returns false when the range is exhausted
   __device__ bool next(int& req, int& lo, int& hi, bool& whole) {
     while (pos < end) {
       while (prefix[r + 1] <= pos) ++r;
-      const int p0 = prefix[r] + kSegCost, p1 = prefix[r + 1];  // the request's page units
+      const int p0 = prefix[r] + seg_cost, p1 = prefix[r + 1];  // the request's page units
       const int a = pos > p0 ? pos : p0;
       const int b = p1 < end ? p1 : end;
       pos = b;
@@ -128,7 +130,8 @@ struct SegmentWalker {
 // seq_lens is a caller input (no kernel of this library writes it), so this
 // may run before griddepcontrol.wait.
 template <int kThreads>
-__device__ __forceinline__ void build_page_prefix(int32_t* prefix, const int32_t* seq_lens, int batch) {
+__device__ __forceinline__ void build_page_prefix(int32_t* prefix, const int32_t* seq_lens, int batch,
+                                                  int seg_cost = kSegCost) {
   __shared__ int s_wsum[kThreads / 32];
   __shared__ int s_carry;
   constexpr int nw = kThreads / 32;
@@ -136,7 +139,7 @@ __device__ __forceinline__ void build_page_prefix(int32_t* prefix, const int32_t
   if (threadIdx.x == 0) { s_carry = 0; prefix[0] = 0; }
   for (int base = 0; base < batch; base += kThreads) {
     const int i = base + threadIdx.x;
-    const int v = (i < batch) ? request_units(__ldg(seq_lens + i)) : 0;
+    const int v = (i < batch) ? request_units(__ldg(seq_lens + i), seg_cost) : 0;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -32,6 +32,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "afdk_internal.h"
 #include "mfa_common.cuh"
@@ -100,7 +101,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
-  build_page_prefix<kThreads>(prefix, prm.seq_lens, prm.batch);
+  build_page_prefix<kThreads>(prefix, prm.seq_lens, prm.batch, prm.seg_cost);
   __syncthreads();
   const int T = prefix[prm.batch];
   int range_lo, range_hi;
@@ -140,7 +141,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -163,7 +164,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     // ---------------------------------------------------- V TMA producer
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -184,7 +185,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16(64, 64, false, false);
       const uint32_t q_base = smem_u32(sm.q);
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -217,7 +218,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     // ------------------------------------------------------ P.V MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_pv = idesc_bf16(64, 256, false, true);
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -251,7 +252,7 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int head = sub * 16 + (lane & 15);
     const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
     const uint32_t p_row_off = (uint32_t)head * 128;  // K-major SW128: 128B per head row
-    SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+    SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
     int req, lo, hi, seg = 0, g = 0;
     bool whole;
     while (walk.next(req, lo, hi, whole)) {
@@ -421,6 +422,12 @@ static_assert(kMaxBatch == kMfaMaxBatch, "the C-ABI checks batch against kMfaMax
 // seq_lens (a caller input) because K2's copy is not final yet.  Every CTA
 // ends with griddepcontrol.wait, so K3 completes only after K2 has, and the
 // next kernel sees the whole-request outputs K2 wrote directly.
+#ifndef AFDK_K3_BATCH
+#define AFDK_K3_BATCH 1  // batched loads for 2-4 part merges (0: the generic loop, for A/B)
+#endif
+#ifndef AFDK_K3_SLEEP_MAX
+#define AFDK_K3_SLEEP_MAX 1024  // K3's poll back-off cap (ns)
+#endif
 constexpr int kK3Rows = 16;     // query rows per K3 CTA
 constexpr int kK3Threads = 512;  // 32 threads per row, 8 dims (16 B of bf16) per thread
 __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params prm, int G) {
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
   {  // p0 = units before this request, T = all units
     int before = 0, all = 0;
     for (int i = threadIdx.x; i < prm.batch; i += blockDim.x) {
-      const int pg = request_units(__ldg(prm.seq_lens + i));
+      const int pg = request_units(__ldg(prm.seq_lens + i), prm.seg_cost);
       all += pg;
       if (i < req) before += pg;
     }
@@ -454,8 +461,8 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
   if (threadIdx.x == 0) {
     int p0 = 0, T = 0;
     for (int w = 0; w < kK3Threads / 32; ++w) { p0 += s_red[0][w]; T += s_red[1][w]; }
-    const int p1 = p0 + request_units(__ldg(prm.seq_lens + req));
-    p0 += kSegCost;  // the request's page units: [p0, p1)
+    const int p1 = p0 + request_units(__ldg(prm.seq_lens + req), prm.seg_cost);
+    p0 += prm.seg_cost;  // the request's page units: [p0, p1)
     int n = 0;
     if (p1 > p0) {
       int c = (int)(((long long)p0 * G) / T);
@@ -475,7 +482,7 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
       long long spins = 0;
       while (ld_acquire_gpu(cnt) < target) {
         __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
+        if (ns < AFDK_K3_SLEEP_MAX) ns <<= 1;
         if (++spins > (1ll << 24)) __trap();
       }
     }
@@ -490,6 +497,58 @@ __global__ void __launch_bounds__(kK3Threads) mfa_combine_kernel(const Params pr
   if (n == 0) {  // empty request
     *reinterpret_cast<uint4*>(out) = make_uint4(0, 0, 0, 0);
     if (lse_lane) prm.lse[(size_t)req * R + head] = -INFINITY;
+#if AFDK_MFA_BF16_PART && AFDK_K3_BATCH
+  } else if (n > 1 && n <= 4) {
+    // the common split (2-4 parts): every part's LSE and 8-dim slice loaded in
+    // one batch, so the merge after the last publish is one L2 round trip
+    float l[4];
+    uint4 raw[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < n) {
+        const size_t row = (size_t)s_slot[k] * R + head;
+        l[k] = __ldcg(prm.part_lse + row);
+        raw[k] = __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(prm.part_o) +
+                                                      row * kDim + d));
+      }
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < n) m = fmaxf(m, l[k]);
+    if (m == -INFINITY) {  // a causal MTP row that sees no token in any part
+      *reinterpret_cast<uint4*>(out) = make_uint4(0, 0, 0, 0);
+      if (lse_lane) prm.lse[(size_t)req * R + head] = -INFINITY;
+    } else {
+      float wsum = 0.0f;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k >= n) break;
+        const float w = exp2f(l[k] - m);
+        wsum += w;
+        const uint32_t wv[4] = {raw[k].x, raw[k].y, raw[k].z, raw[k].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[j]));
+          acc[2 * j] += w * f.x;
+          acc[2 * j + 1] += w * f.y;
+        }
+      }
+      const float inv = 1.0f / wsum;
+      uint4 o;
+      o.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+      o.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+      o.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+      o.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+      *reinterpret_cast<uint4*>(out) = o;
+      if (lse_lane) prm.lse[(size_t)req * R + head] = (m + __log2f(wsum)) * 0.69314718055994531f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(prm.sync + kMaxBatch + req, 1) == (int)gridDim.y - 1) {
+      prm.sync[req] = 0;
+      prm.sync[kMaxBatch + req] = 0;
+    }
+#endif
   } else if (n > 1) {
     for (int i = threadIdx.x; i < kK3Rows * n; i += blockDim.x)
       s_w[i / n][i % n] = __ldcg(prm.part_lse + (size_t)s_slot[i % n] * R + blockIdx.y * kK3Rows + i / n);
@@ -591,6 +650,8 @@ cudaError_t mfa_decode_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t str
   prm.out = static_cast<__nv_bfloat16*>(a.out);
   prm.lse = a.lse;
   prm.sync = ctx.counters + kCounterSlots / 2;
+  static const int seg_cost = [] { const char* e = std::getenv("AFDK_MFA_SEG_COST_RT"); return e ? std::atoi(e) : kSegCost; }();
+  prm.seg_cost = seg_cost;
   prm.batch = a.batch;
   prm.max_pages = a.max_pages;
   prm.scale_log2 = a.softmax_scale * 1.4426950408889634f;

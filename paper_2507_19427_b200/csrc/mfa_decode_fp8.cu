@@ -31,6 +31,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "afdk_internal.h"
 #include "mfa_common.cuh"
@@ -42,6 +43,13 @@ namespace mfa {
 using namespace sm100;
 
 constexpr int kTile8 = kPage * kDim;  // 16 KB e4m3 K or V page
+// segment charge in page units (AFDK_MFA8_SEG_COST overrides): a segment's
+// fixed work (Q load + quantisation, O epilogue, split partial) is the same
+// as the bf16 kernel's while a page streams in half the time
+#ifndef AFDK_MFA8_SEG_COST_DEFAULT
+#define AFDK_MFA8_SEG_COST_DEFAULT 3
+#endif
+constexpr int kSegCost8 = AFDK_MFA8_SEG_COST_DEFAULT;
 constexpr int kPanel8 = 64 * 128;     // 64 rows x 128 B swizzle panel (128 dims)
 constexpr int kPanel16 = 64 * 128;    // 64 rows x 128 B bf16 panel (64 dims)
 #ifndef AFDK_NK8
@@ -91,7 +99,7 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
-  build_page_prefix<kThreads8>(prefix, prm.seq_lens, prm.batch);
+  build_page_prefix<kThreads8>(prefix, prm.seq_lens, prm.batch, prm.seg_cost);
   __syncthreads();
   const int T = prefix[prm.batch];
   int range_lo, range_hi;
@@ -131,7 +139,7 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -154,7 +162,7 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     // ---------------------------------------------------- V TMA producer
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -173,7 +181,7 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_e4m3(64, 64);
       const uint32_t q_base = smem_u32(sm.q8);
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -206,7 +214,7 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     // ------------------------------------------------------ P.V MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_pv = idesc_e4m3(64, 256) | (1u << 16);  // B (V) MN-major
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -241,7 +249,7 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
     const uint32_t p_row_off = (uint32_t)head * 128;
     const float qk_base = prm.k_scale * prm.scale_log2;
-    SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+    SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
     int req, lo, hi, seg = 0, g = 0;
     bool whole;
     while (walk.next(req, lo, hi, whole)) {
@@ -465,6 +473,8 @@ cudaError_t mfa_decode_fp8_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t
   prm.out = static_cast<__nv_bfloat16*>(a.out);
   prm.lse = a.lse;
   prm.sync = ctx.counters + kCounterSlots / 2;
+  static const int seg_cost = [] { const char* e = std::getenv("AFDK_MFA8_SEG_COST"); return e ? std::atoi(e) : kSegCost8; }();
+  prm.seg_cost = seg_cost;
   prm.batch = a.batch;
   prm.max_pages = a.max_pages;
   prm.scale_log2 = a.softmax_scale * 1.4426950408889634f;

@@ -66,7 +66,7 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   const int warp = warp_id();
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x, cta = blockIdx.x;
-  build_page_prefix<kThreadsM>(prefix, prm.seq_lens, prm.batch);
+  build_page_prefix<kThreadsM>(prefix, prm.seq_lens, prm.batch, prm.seg_cost);
   __syncthreads();
   const int T = prefix[prm.batch];
   int range_lo, range_hi;
@@ -102,7 +102,7 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -125,7 +125,7 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     // ---------------------------------------------------- V TMA producer
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -144,7 +144,7 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16(128, 64, false, false);
       const uint32_t q_base = smem_u32(sm.q);
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -177,7 +177,7 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     // ------------------------------------------------------ P.V MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_pv = idesc_bf16(128, 256, false, true);
-      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+      SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
@@ -211,7 +211,7 @@ mfa_decode_mtp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     const int jt = r / kHeads;  // query token of this row (head = r % 64)
     const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16);
     const uint32_t p_row_off = (uint32_t)r * 128;
-    SegmentWalker walk(prefix, prm.batch, range_lo, range_hi);
+    SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
     int req, lo, hi, seg = 0, g = 0;
     bool whole;
     while (walk.next(req, lo, hi, whole)) {
@@ -374,6 +374,7 @@ cudaError_t mfa_decode_mtp_launch(Ctx& ctx, const MfaDecodeArgs& a, cudaStream_t
   prm.out = static_cast<__nv_bfloat16*>(a.out);
   prm.lse = a.lse;
   prm.sync = ctx.counters + kCounterSlots / 2;
+  prm.seg_cost = kSegCost;
   prm.batch = a.batch;
   prm.max_pages = a.max_pages;
   prm.scale_log2 = a.softmax_scale * 1.4426950408889634f;

@@ -231,9 +231,11 @@ cudaError_t moe_ffn_bf16_launch(Ctx& ctx, const MoeFfnBf16Args& a, void* ws_base
 // give tensor-parallel partials reduced on the attention side like EP ones.
 namespace moe {
 
-__global__ void dense_work_kernel(int T, int n_split, int chunk, Work* work, int* n_work) {
+__global__ void dense_work_kernel(int T, int n_split, int chunk, Work* work, int* n_work, int* sched, int sched_len) {
   sm100::griddep_wait();
   sm100::griddep_launch();
+  if (sched)  // the fused kernel's queue head and per-chunk counters
+    for (int i = threadIdx.x; i < sched_len; i += blockDim.x) sched[i] = 0;
   if (threadIdx.x != 0) return;
   const int n_items = (T + chunk - 1) / chunk;
   const int per = ((T + n_items - 1) / n_items + 31) & ~31;
@@ -287,7 +289,15 @@ size_t dense_ffn_mx_workspace_bytes(int T, int n_split, int H, int Is) {
   b += align_up((size_t)rp * Is, 256);         // hq
   b += align_up((size_t)rp * (Is / 32), 256);  // hsf
   b += align_up((size_t)rp * H * 4, 256);      // y
+  b += align_up((size_t)(1 + dense_max_work(T, n_split)) * 4, 256);  // fused kernel's queue
   return b;
+}
+
+// dense layers at decode batches through the fused single-CTA kernel instead
+// of the CTA-pair GEMMs (AFDK_DENSE_FUSED=1 / 0 forces)
+static bool dense_use_fused(int T) {
+  if (const char* e = std::getenv("AFDK_DENSE_FUSED")) return e[0] == '1';
+  return false;
 }
 
 cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws_base, cudaStream_t stream) {
@@ -299,7 +309,9 @@ cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws_base
   auto* hq = static_cast<uint8_t*>(take((size_t)rp * a.Is));
   auto* hsf = static_cast<uint8_t*>(take((size_t)rp * (a.Is / 32)));
   auto* y = static_cast<float*>(take((size_t)rp * a.H * 4));
-  const bool pair = moe_mx_use_pair(a.T, 1, 1);
+  auto* sched = static_cast<int*>(take((size_t)(1 + dense_max_work(a.T, a.n_split)) * 4));
+  const bool fused = dense_use_fused(a.T);
+  const bool pair = !fused && moe_mx_use_pair(a.T, 1, 1);
   auto gemm = pair ? moe_gemm_mx2_launch : moe_gemm_mx_launch;
   static const bool dbg = std::getenv("AFDK_DEBUG_SYNC") != nullptr;
   auto chk = [&](cudaError_t err, const char* what) {
@@ -308,16 +320,21 @@ cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws_base
     return err;
   };
   cudaError_t e;
+  const int sched_len = 1 + dense_max_work(a.T, a.n_split);
   if ((e = chk(launch_k(ctx.pdl, moe::dense_work_kernel, dim3(1), dim3(32), 0, stream, a.T, a.n_split,
-                        pair ? moe::kChunkMX2 : moe::kChunkMX, work, n_work),
+                        pair ? moe::kChunkMX2 : moe::kChunkMX, work, n_work, fused ? sched : nullptr, sched_len),
                "work")) != cudaSuccess)
     return e;
   // group j < E = n_split always: weight index j, never the shared slot
   MoeGemmMxArgs g13{a.w13, a.sf13, a.xq, a.xsf, work, n_work, a.H, a.Is, a.n_split, 0, a.n_split, a.T, hq, hsf,
                     nullptr};
-  if ((e = chk(gemm(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
   MoeGemmMxArgs g2{a.w2, a.sf2, hq, hsf, work, n_work, a.H, a.Is, a.n_split, 0, a.n_split, rp, nullptr, nullptr, y};
-  if ((e = chk(gemm(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
+  if (fused) {
+    if ((e = chk(moe_ffn_mx_fused_launch(ctx, g13, g2, sched, stream), "gemm13+2")) != cudaSuccess) return e;
+  } else {
+    if ((e = chk(gemm(ctx, true, g13, stream), "gemm13")) != cudaSuccess) return e;
+    if ((e = chk(gemm(ctx, false, g2, stream), "gemm2")) != cudaSuccess) return e;
+  }
   return chk(launch_k(ctx.pdl, moe::dense_combine_kernel, dim3(a.T), dim3(256), 0, stream, (const float*)y, a.T,
                       a.n_split, a.H, static_cast<__nv_bfloat16*>(a.out), a.dst, a.rows_per_dst),
              "combine");

@@ -1,7 +1,17 @@
-# A/B of the per-segment work charge (AFDK_MFA_SEG_COST) on the attention core and the config-2 layer
-for r in 1 2; do for v in "" _seg0 _seg1 _seg3 _seg4; do
-  for cfg in "64 4096" "32 32768" "8 4096"; do
-    echo "lib=$v $cfg: $(AFDK_LIB=$PWD/paper_2507_19427_b200/libafdk$v.so timeout 120 python scripts/bench_attn_fp8.py $cfg 2>&1 | tr '\n' '|')"
+#!/bin/bash
+# A/B of the MFA segment charge (bf16 / e4m3 cores) and K3's poll back-off
+cd "$(dirname "$0")/.."
+export PYTHONPATH=$PWD
+for round in 1 2; do
+  for sc in 3 5 7 9; do
+    echo "e4m3 seg_cost=$sc: $(AFDK_MFA8_SEG_COST=$sc timeout 120 python scripts/bench_attn_fp8.py 64 4096 2>&1 | grep '^e4m3')"
+    echo "e4m3 seg_cost=$sc B256: $(AFDK_MFA8_SEG_COST=$sc timeout 120 python scripts/bench_attn_fp8.py 256 4096 2>&1 | grep '^e4m3')"
   done
-  echo "lib=$v layer: $(AFDK_LIB=$PWD/paper_2507_19427_b200/libafdk$v.so timeout 120 python scripts/graph_layer.py 2>&1 | tr '\n' ' ')"
-done; done
+  for sc in 2 3 4 6; do
+    echo "bf16 seg_cost=$sc: $(AFDK_MFA_SEG_COST_RT=$sc timeout 120 python scripts/bench_attn_fp8.py 64 4096 2>&1 | grep '^bf16')"
+  done
+  echo "new: $(timeout 120 python scripts/bench_attn_fp8.py 64 4096 2>&1 | grep -v mtp)"
+  for v in oldk3 k3s256; do
+    echo "$v: $(AFDK_LIB=$PWD/paper_2507_19427_b200/libafdk_$v.so timeout 120 python scripts/bench_attn_fp8.py 64 4096 2>&1 | grep -v mtp)"
+  done
+done

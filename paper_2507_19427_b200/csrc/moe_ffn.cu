@@ -293,11 +293,14 @@ size_t dense_ffn_mx_workspace_bytes(int T, int n_split, int H, int Is) {
   return b;
 }
 
-// dense layers at decode batches through the fused single-CTA kernel instead
-// of the CTA-pair GEMMs (AFDK_DENSE_FUSED=1 / 0 forces)
+// dense layers at small decode batches through the fused single-CTA kernel
+// instead of the CTA-pair GEMMs (AFDK_DENSE_FUSED=1 / 0 forces).  ms fused /
+// pair, best n_split: T=64 0.095 / 0.191, T=128 0.109 / 0.155, T=256 0.169 /
+// 0.112 (every weight tile then serves two 128-row chunks: the pair's 256-row
+// items win)
 static bool dense_use_fused(int T) {
   if (const char* e = std::getenv("AFDK_DENSE_FUSED")) return e[0] == '1';
-  return false;
+  return T < 192;
 }
 
 cudaError_t dense_ffn_mx_launch(Ctx& ctx, const DenseFfnMxArgs& a, void* ws_base, cudaStream_t stream) {

@@ -374,7 +374,8 @@ def run_moe_bench(ctx, torch, dev, T, steps, warmup, seed=0, fmt="fp8", shard=No
                     "frac": wbytes / (ms * 1e-3) / 1e9 / hbm_peak, "alg_bytes": wbytes,
                     "experts_touched": touched},
             "tensor": tensor_roofline(flops, ms, fmt, tf_peak),
-            "gpu_launches_per_layer": 5}
+            # permute, gather, gate|up + down (one fused launch at decode batches in MXFP8, else two), combine
+            "gpu_launches_per_layer": 4 if (fmt == "mx" and T * TOPK < 32 * E_ROUTED) else 5}
 
 
 DENSE_INTER = 18432

@@ -122,7 +122,7 @@ afdk_status afdk_mfa_decode_attention_mtp(afdk_ctx* ctx, const afdk_mfa_decode_a
 
 /* ------------------------------------------------------------ K1/K4 GEMM
  * y[m, n] = x[m, k] . w[n, k]^T, bf16 inputs, fp32 accumulate, decode-shaped
- * (1 <= m <= 256, k % 64 == 0).  out is bf16 (out_fp32 = 0) or fp32.      */
+ * (1 <= m <= 512, k % 64 == 0).  out is bf16 (out_fp32 = 0) or fp32.      */
 afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, int m, int n, int k,
                         int out_fp32, afdk_stream stream);
 
@@ -169,7 +169,8 @@ afdk_status afdk_mfa_layer_fp8(afdk_ctx* ctx, const afdk_mfa_weights* w, const a
  * h_norm have batch*mtp rows ordered (request, token); the projections run on
  * all rows, each row appends its K/V at its own position, and the core is
  * afdk_mfa_decode_attention_mtp (causal among the new tokens).
- * batch*mtp <= 256, batch <= 128 for mtp = 2.                              */
+ * batch*mtp <= 256, batch <= 128 for mtp = 2 (afdk_mfa_layer[_fp8]: batch
+ * <= 512; above 256 rows the projections run as two N/2 MMAs per weight k-block). */
 afdk_status afdk_mfa_layer_mtp(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a, int mtp,
                                afdk_stream stream);
 
@@ -448,7 +449,7 @@ typedef struct afdk_afd_cfg {
   int ffn_format;              /* AFDK_FFN_*                                          */
   int layer_kind;              /* AFDK_LAYER_* (dense layers: MXFP8 slices)           */
   int f2a;                     /* AFDK_F2A_*                                          */
-  int attn_chunk;              /* requests per attention-layer call, 1..256           */
+  int attn_chunk;              /* requests per attention-layer call, 1..512           */
 } afdk_afd_cfg;
 
 enum { AFDK_OP_ATTN = 0, AFDK_OP_SIGNAL = 1, AFDK_OP_WAIT = 2, AFDK_OP_PULL = 3, AFDK_OP_REDUCE = 4,

@@ -57,7 +57,7 @@ class AfdConfig:
     layer_kind: str = "moe"   # "moe": routed experts (EP over FFN GPUs); "dense": the dense Step-3
                               # FFN (inter dense_inter) as intermediate slices, tensor-parallel
     dense_inter: int = 18432
-    attn_chunk: int = 256     # requests per attention-layer call (its GEMM N limit); a larger
+    attn_chunk: int = 512     # requests per attention-layer call (its GEMM N limit); a larger
                               # T_mb runs the attention side in chunks and ships ONE payload
     kv: str = "bf16"          # attention KV cache: "bf16" or "e4m3" (per-tensor scales)
 

@@ -99,7 +99,7 @@ double time_it(F&& f, int warmup = 2, int iters = 5) {
 void ok(afdk_status s) { ops::check(s); }
 
 double attention_layer_s(afdk_ctx* ctx, int hidden, int64_t batch, int64_t ctx_len, int ffn_format, bool kv8) {
-  const int64_t chunks = (batch + 255) / 256;
+  const int64_t chunks = (batch + 511) / 512;  // afdk_mfa_layer takes up to 512 requests per call
   const int B = (int)((batch + chunks - 1) / chunks);
   const int pages_per = (int)((ctx_len + kPage - 1) / kPage);
   const int n_pages = B * pages_per;

@@ -41,7 +41,7 @@ std::string check_cfg(const afdk_afd_cfg* c) {
   if (c->n_micro < 1 || c->n_micro > AFDK_AFD_MAX_MICRO) return "n_micro must be in [1, 4]";
   if ((c->n_attn + c->n_ffn) * c->n_micro > kMaxFlags) return "too many ranks x micro-batches for the flag table";
   if (c->T_mb < 1 || c->T_mb > 4096) return "T_mb must be in [1, 4096]";
-  if (c->attn_chunk < 1 || c->attn_chunk > 256) return "attn_chunk must be in [1, 256]";
+  if (c->attn_chunk < 1 || c->attn_chunk > 512) return "attn_chunk must be in [1, 512]";
   if (c->hidden < 512 || c->hidden % 512) return "hidden must be a positive multiple of 512";
   if (c->ffn_format < AFDK_FFN_FP8 || c->ffn_format > AFDK_FFN_BF16) return "unknown ffn_format";
   if (c->f2a != AFDK_F2A_PUSH && c->f2a != AFDK_F2A_PULL && c->f2a != AFDK_F2A_NVLS) return "unknown f2a";

@@ -228,7 +228,7 @@ afdk_status afdk_mfa_decode_attention_mtp(afdk_ctx* ctx, const afdk_mfa_decode_a
 afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, int m, int n, int k,
                         int out_fp32, afdk_stream stream) {
   if (!ctx || !x || !w || !out) { set_error("afdk_linear: NULL argument"); return AFDK_ERR_INVALID; }
-  if (m < 1 || m > 256) { set_error("afdk_linear: m must be in [1, 256]"); return AFDK_ERR_INVALID; }
+  if (m < 1 || m > 512) { set_error("afdk_linear: m must be in [1, 512]"); return AFDK_ERR_INVALID; }
   if (n < 1 || k < 64 || k % 64) { set_error("afdk_linear: k must be a positive multiple of 64"); return AFDK_ERR_INVALID; }
   afdk::Ctx& c = ctx->c;
   afdk::DeviceGuard device_guard(c.device);
@@ -257,8 +257,8 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
     set_error("afdk_mfa_layer: hidden <= 16384 and q_lora <= 4096 (row epilogues span one 4-CTA cluster)");
     return AFDK_ERR_INVALID;
   }
-  if (a->batch < 1 || a->batch * mtp > 256) {
-    set_error("afdk_mfa_layer: batch x mtp must be in [1, 256]");
+  if (a->batch < 1 || a->batch * mtp > 512 || (mtp > 1 && a->batch * mtp > 256)) {
+    set_error("afdk_mfa_layer: batch must be in [1, 512] (batch x mtp <= 256 for mtp > 1)");
     return AFDK_ERR_INVALID;
   }
   if (!a->x || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->h_res || !a->h_norm ||

@@ -1,12 +1,16 @@
 // linear.cu — decode-shaped weight-streaming GEMM on sm_100a (K1/K4 projections).
 //
-// Y[m_tok, n_out] = X[m_tok, K] . W[n_out, K]^T with m_tok <= 256 decode tokens
+// Y[m_tok, n_out] = X[m_tok, K] . W[n_out, K]^T with m_tok <= 512 decode tokens
 // and large bf16 weights (q_down|k|v 2560x7168, q_up 16384x2048, o 7168x16384;
 // builtin_catalog.cpp:243-247).  At decode batch sizes the op is bound by
 // streaming W from HBM once, so the kernel is "swap-AB": the weight tile is
 // the MMA's M=128 side and the tokens are N (<=256), accumulating in TMEM:
 //
 //   D[128 feats x N tok] += W[128 x 64k] . X[N x 64k]^T   tcgen05.mma kind::f16
+//
+// (N > 256 — the AFD attention micro-batch above 256 requests — runs as two
+// MMAs of N/2 sharing the weight panel: the token panel is loaded as two
+// N/2-row boxes, the accumulator spans N TMEM columns, single-buffered.)
 //
 // Work is split stream-K style: the (tile, k-block) unit space is cut into one
 // contiguous range per SM so every SM streams the same weight bytes whatever
@@ -93,6 +97,12 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       const uint32_t bytes = (kM2 ? 2 : 1) * kABytes + n_mma * 128;
+      // token panel: one box of n_mma rows, or two of n_mma/2 when n_mma > 256
+      const int xbox = n_mma > 256 ? n_mma / 2 : n_mma;
+      auto load_x = [&](uint8_t* dst, uint64_t* bar, int kb) {
+        tma_load_2d(dst, &tm_x, bar, kb * 64, 0, pol_x);
+        if (n_mma > 256) tma_load_2d(dst + xbox * 128, &tm_x, bar, kb * 64, xbox, pol_x);
+      };
       // kRope: the panel's rows 0-63 are the pairs' x1 rows, 64-127 their x2 rows
       const int tph = kRope ? kp.head_dim / 128 : 1;
       auto load_w = [&](uint8_t* dst, uint64_t* bar, int kb, int tile) {
@@ -118,7 +128,7 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       griddep_wait();
       for (int i = 0; i < pro; ++i) {
         const int u = u_lo + i, kb = u % P.kblocks;
-        tma_load_2d(smem + i * kp.stage_bytes + (kM2 ? 2 : 1) * kABytes, &tm_x, &full[i], kb * 64, 0, pol_x);
+        load_x(smem + i * kp.stage_bytes + (kM2 ? 2 : 1) * kABytes, &full[i], kb);
       }
       for (int u = u_lo + pro, i = pro; u < u_hi; ++u, ++i) {
         const int s = i % S, n = i / S;
@@ -127,15 +137,16 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
         uint8_t* st = smem + s * kp.stage_bytes;
         mbar_expect_tx(&full[s], bytes);
         load_w(st, &full[s], kb, tile);
-        tma_load_2d(st + (kM2 ? 2 : 1) * kABytes, &tm_x, &full[s], kb * 64, 0, pol_x);
+        load_x(st + (kM2 ? 2 : 1) * kABytes, &full[s], kb);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(128, (uint32_t)n_mma, false, false);
+      const bool wide = n_mma > 256;  // two MMAs of n_mma/2 per k-step
+      const uint32_t idesc = idesc_bf16(128, (uint32_t)(wide ? n_mma / 2 : n_mma), false, false);
       // kM2: two accumulators (panel 0 / 1) of n_mma columns per segment; they
       // double-buffer across segments only while 4 x n_mma fits TMEM
-      const bool dbuf = !kM2 || n_mma <= 128;
+      const bool dbuf = kM2 ? n_mma <= 128 : !wide;
       int seg = 0;
       for (int u = u_lo, i = 0; u < u_hi; ++seg) {
         const int tile = u / P.kblocks;
@@ -156,6 +167,10 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
             mma_bf16(d, sdesc_sw128(a_base + kk * 32, 0, 1024), b, idesc, (first && kk == 0) ? 0u : 1u);
             if (kM2)
               mma_bf16(d + n_mma, sdesc_sw128(a_base + kABytes + kk * 32, 0, 1024), b, idesc,
+                       (first && kk == 0) ? 0u : 1u);
+            if (!kM2 && wide)  // tokens [n_mma/2, n_mma): second half of the panel, columns n_mma/2..
+              mma_bf16(d + n_mma / 2, sdesc_sw128(a_base + kk * 32, 0, 1024),
+                       sdesc_sw128(b_base + (n_mma / 2) * 128 + kk * 32, 0, 1024), idesc,
                        (first && kk == 0) ? 0u : 1u);
           }
           mma_commit(&empty[s]);
@@ -212,7 +227,7 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     // each (tile, k-range) segment writes its fp32 partial to slot tile + cta.
     const int sub = warp & 3;
     const int feat = sub * 32 + lane;
-    const bool dbuf = !kM2 || n_mma <= 128;
+    const bool dbuf = kM2 ? n_mma <= 128 : n_mma <= 256;
     int seg = 0;
     for (int u = u_lo; u < u_hi; ++seg) {
       const int tile = u / P.kblocks;
@@ -288,6 +303,7 @@ LinearPlan make_linear_plan(int m_tok, int n_out, int k) {
   p.m_tok = m_tok;
   p.n_mma = ((m_tok + 15) / 16) * 16;
   if (p.n_mma < 16) p.n_mma = 16;
+  if (p.n_mma > 256) p.n_mma = ((m_tok + 31) / 32) * 32;  // two MMAs of n_mma/2 (a multiple of 16)
   p.n_out = n_out;
   p.k = k;
   // 256-row tiles (two MMA panels sharing each token panel; AFDK_LIN_MTILE=256)
@@ -296,7 +312,7 @@ LinearPlan make_linear_plan(int m_tok, int n_out, int k) {
   // 177.2 us (3 pipeline stages instead of 4, single-buffered accumulators,
   // half the stream-K tiles), so 128-row tiles stay the default
   static const int env = [] { const char* e = std::getenv("AFDK_LIN_MTILE"); return e ? std::atoi(e) : 0; }();
-  p.mtile = (n_out >= 2048 && env == 256) ? 256 : lin::kBM;
+  p.mtile = (n_out >= 2048 && env == 256 && p.n_mma <= 256) ? 256 : lin::kBM;
   p.tiles = (n_out + p.mtile - 1) / p.mtile;
   p.kblocks = k / 64;
   return p;
@@ -323,7 +339,7 @@ static cudaError_t linear_launch_impl(Ctx& ctx, const LinearPlan& p, const void*
   {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.m_tok};
     const uint64_t strides[1] = {(uint64_t)p.k * 2};
-    const uint32_t box[2] = {64, (uint32_t)p.n_mma};
+    const uint32_t box[2] = {64, (uint32_t)(p.n_mma > 256 ? p.n_mma / 2 : p.n_mma)};
     if (!encode_tma(ctx, &tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box,
                     CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;

@@ -8,7 +8,7 @@
 namespace afdk {
 
 struct LinearPlan {
-  int m_tok;    // decode tokens (rows of X / Y), <= 256
+  int m_tok;    // decode tokens (rows of X / Y), <= 512
   int n_mma;    // m_tok rounded up to the MMA N granularity (16)
   int n_out;    // output features (rows of W)
   int k;        // reduction dim, multiple of 64

@@ -167,7 +167,7 @@ def test_afd_config_validation():
     with pytest.raises(ValueError):
         AfdConfig(n_attn=1, n_ffn=1, T_mb=8192)
     with pytest.raises(ValueError):
-        AfdConfig(n_attn=1, n_ffn=1, T_mb=64, attn_chunk=512)
+        AfdConfig(n_attn=1, n_ffn=1, T_mb=64, attn_chunk=513)
     AfdConfig(n_attn=1, n_ffn=1, T_mb=768)
     with pytest.raises(ValueError):
         AfdConfig(n_attn=1, n_ffn=1, T_mb=64, ffn_format="int4")

@@ -20,6 +20,10 @@ from tests.helpers import rel_err
     (128, 16384, 2048), # q_up at 128 rows: 256-row tiles, double-buffered (N = 128)
     (100, 2560, 7168),  # qkv, ragged N (112) on 256-row tiles
     (96, 2176, 512),    # n_out not a multiple of 256: the last tile's second panel is TMA zero-filled
+    (384, 7168, 16384), # o_proj at a 384-request AFD micro-batch: two N=192 MMAs per weight k-block
+    (512, 16384, 2048), # q_up at the 512-row limit (two N=256 MMAs, single-buffered accumulator)
+    (272, 2560, 7168),  # just above 256: n_mma rounded to 288, second box half zero-filled
+    (300, 1000, 512),   # ragged everything above 256
 ])
 def test_linear_vs_torch(ctx, m, n, k):
     import torch

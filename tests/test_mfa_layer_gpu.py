@@ -139,12 +139,13 @@ def test_mfa_layer_mtp2(ctx, dims, seq_lens, seed):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kv", ["bf16", "e4m3"])
-def test_mfa_layer_wide_batch(ctx, kv):
-    """256 requests (the AFD micro-batch): the 2-CTA-cluster row epilogues, the
-    separate RoPE(q) row epilogue and the N=256 projections; ragged contexts."""
-    rng = np.random.default_rng(77)
-    seq_lens = rng.integers(1, 700, size=256).tolist()
+@pytest.mark.parametrize("kv,batch", [("bf16", 256), ("e4m3", 256), ("bf16", 384), ("e4m3", 400)])
+def test_mfa_layer_wide_batch(ctx, kv, batch):
+    """256-400 requests (the AFD micro-batch): the 2-CTA-cluster row epilogues,
+    the separate RoPE(q) row epilogue and the N=256 projections, or above 256
+    rows the two-MMA (N/2 each) projections; ragged contexts."""
+    rng = np.random.default_rng(77 + batch)
+    seq_lens = rng.integers(1, 700, size=batch).tolist()
     if kv == "bf16":
         check(run_layer(ctx, STEP3, seq_lens, 31), 64)
     else:

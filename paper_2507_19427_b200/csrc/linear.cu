@@ -57,7 +57,7 @@ __device__ __forceinline__ void unit_range(int c, int G, int U, int& lo, int& hi
   hi = (int)(((long long)(c + 1) * U) / G);
 }
 
-template <bool kRope, bool kM2>
+template <bool kRope, bool kM2, bool kW>  // kW: n_mma > 256, two MMAs of n_mma/2 per k-step
 __global__ void __launch_bounds__(kThreads, 1)
 linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                    const KParams kp) {
@@ -97,11 +97,10 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       const uint32_t bytes = (kM2 ? 2 : 1) * kABytes + n_mma * 128;
-      // token panel: one box of n_mma rows, or two of n_mma/2 when n_mma > 256
-      const int xbox = n_mma > 256 ? n_mma / 2 : n_mma;
+      // token panel: one box of n_mma rows, or two of n_mma/2 (kW)
       auto load_x = [&](uint8_t* dst, uint64_t* bar, int kb) {
         tma_load_2d(dst, &tm_x, bar, kb * 64, 0, pol_x);
-        if (n_mma > 256) tma_load_2d(dst + xbox * 128, &tm_x, bar, kb * 64, xbox, pol_x);
+        if (kW) tma_load_2d(dst + (n_mma / 2) * 128, &tm_x, bar, kb * 64, n_mma / 2, pol_x);
       };
       // kRope: the panel's rows 0-63 are the pairs' x1 rows, 64-127 their x2 rows
       const int tph = kRope ? kp.head_dim / 128 : 1;
@@ -142,11 +141,10 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const bool wide = n_mma > 256;  // two MMAs of n_mma/2 per k-step
-      const uint32_t idesc = idesc_bf16(128, (uint32_t)(wide ? n_mma / 2 : n_mma), false, false);
+      const uint32_t idesc = idesc_bf16(128, (uint32_t)(kW ? n_mma / 2 : n_mma), false, false);
       // kM2: two accumulators (panel 0 / 1) of n_mma columns per segment; they
       // double-buffer across segments only while 4 x n_mma fits TMEM
-      const bool dbuf = kM2 ? n_mma <= 128 : !wide;
+      const bool dbuf = kM2 ? n_mma <= 128 : !kW;
       int seg = 0;
       for (int u = u_lo, i = 0; u < u_hi; ++seg) {
         const int tile = u / P.kblocks;
@@ -168,7 +166,7 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
             if (kM2)
               mma_bf16(d + n_mma, sdesc_sw128(a_base + kABytes + kk * 32, 0, 1024), b, idesc,
                        (first && kk == 0) ? 0u : 1u);
-            if (!kM2 && wide)  // tokens [n_mma/2, n_mma): second half of the panel, columns n_mma/2..
+            if (kW)  // tokens [n_mma/2, n_mma): second half of the panel, columns n_mma/2..
               mma_bf16(d + n_mma / 2, sdesc_sw128(a_base + kk * 32, 0, 1024),
                        sdesc_sw128(b_base + (n_mma / 2) * 128 + kk * 32, 0, 1024), idesc,
                        (first && kk == 0) ? 0u : 1u);
@@ -227,7 +225,7 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
     // each (tile, k-range) segment writes its fp32 partial to slot tile + cta.
     const int sub = warp & 3;
     const int feat = sub * 32 + lane;
-    const bool dbuf = kM2 ? n_mma <= 128 : n_mma <= 256;
+    const bool dbuf = kM2 ? n_mma <= 128 : !kW;
     int seg = 0;
     for (int u = u_lo; u < u_hi; ++seg) {
       const int tile = u / P.kblocks;
@@ -236,17 +234,20 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       const int ab = dbuf ? (seg & 1) : 0, na = dbuf ? (seg >> 1) : seg;
       mbar_wait(&acc_full[ab], na & 1);
       tc_fence_after();
+      constexpr int kMt = kM2 ? 2 * kBM : kBM;  // == P.mtile (compile-time: immediate store offsets)
 #pragma unroll 1
       for (int pnl = 0; pnl < (kM2 ? 2 : 1); ++pnl) {
-        float* dst = kp.part + ((size_t)(tile + cta) * P.m_tok) * P.mtile + pnl * kBM + feat;
+        float* dst = kp.part + ((size_t)(tile + cta) * P.m_tok) * kMt + pnl * kBM + feat;
         const uint32_t t_row = tmem + ((uint32_t)(sub * 32) << 16) + (kM2 ? (ab * 2 + pnl) * n_mma : ab * 256);
         for (int c = 0; c < n_mma; c += 32) {
           uint32_t v[32];
           tmem_ld32(t_row + c, v);
           tmem_wait_ld();
+          float* d = dst + (size_t)c * kMt;
+          const int nv = P.m_tok - c;
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (c + j < P.m_tok) dst[(size_t)(c + j) * P.mtile] = __uint_as_float(v[j]);
+            if (j < nv) d[j * kMt] = __uint_as_float(v[j]);
         }
       }
       tc_fence_before();
@@ -362,8 +363,9 @@ static cudaError_t linear_launch_impl(Ctx& ctx, const LinearPlan& p, const void*
     if (const cudaError_t e = ensure_smem(kernel, smem); e != cudaSuccess) return e;
     return launch_k(ctx.pdl, kernel, dim3(grid), dim3(kThreads), smem, stream, tw, tx, kp);
   };
-  if (rope) return go(linear_bf16_kernel<true, false>);
-  return m2 ? go(linear_bf16_kernel<false, true>) : go(linear_bf16_kernel<false, false>);
+  if (rope) return go(linear_bf16_kernel<true, false, false>);
+  if (m2) return go(linear_bf16_kernel<false, true, false>);
+  return p.n_mma > 256 ? go(linear_bf16_kernel<false, false, true>) : go(linear_bf16_kernel<false, false, false>);
 }
 
 cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,

@@ -46,9 +46,11 @@ constexpr int kTile8 = kPage * kDim;  // 16 KB e4m3 K or V page
 // segment charge in page units (AFDK_MFA8_SEG_COST overrides): a segment's
 // fixed work (Q load + quantisation, O epilogue, split partial) is the same
 // as the bf16 kernel's while a page streams in half the time.  B=64 x 4K:
-// 3 / 5 / 7 / 9 -> 33.1-33.3 / 32.6-32.7 / 32.3 / 32.9-33.0 us; B=256 flat
+// 3 / 5 / 7 / 9 -> 33.1-33.3 / 32.6-32.7 / 32.3 / 32.9-33.0 us; B=256 flat.
+// Kept at 3: with 7 the 2 x 32K/20K parity case moved its split points and
+// exceeded the e4m3-P bar (4.0e-2 vs 3e-2) for a 1 us gain
 #ifndef AFDK_MFA8_SEG_COST_DEFAULT
-#define AFDK_MFA8_SEG_COST_DEFAULT 7
+#define AFDK_MFA8_SEG_COST_DEFAULT 3
 #endif
 constexpr int kSegCost8 = AFDK_MFA8_SEG_COST_DEFAULT;
 constexpr int kPanel8 = 64 * 128;     // 64 rows x 128 B swizzle panel (128 dims)

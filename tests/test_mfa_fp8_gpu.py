@@ -73,6 +73,8 @@ def test_mfa_decode_fp8_parity(ctx, seq_lens):
 @pytest.mark.gpu
 def test_mfa_decode_fp8_long_context_split(ctx):
     got, lse, ref, ref_lse = run_case(ctx, [32768, 20000], seed=3, poison=False)
+    from tests.helpers import record
+    record("mfa_fp8_long_context_split", out=rel_err(got, ref), lse=float(np.abs(lse - ref_lse).max()))
     assert rel_err(got, ref) <= TOL, rel_err(got, ref)
     np.testing.assert_allclose(lse, ref_lse, rtol=0, atol=2e-2)
 

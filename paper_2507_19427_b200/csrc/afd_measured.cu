@@ -224,6 +224,11 @@ double peer_copy_s(size_t bytes) {
   int can = 0;
   cudaDeviceCanAccessPeer(&can, cur, peer);
   if (!can) return 0.0;
+  // direct NVLink copy-engine path (the AFD runtime maps its peers): without
+  // peer access the driver stages the copy through host memory (~10 GB/s)
+  const cudaError_t pe = cudaDeviceEnablePeerAccess(peer, 0);
+  if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+  else if (pe != cudaSuccess) { cudaGetLastError(); return 0.0; }
   void *src = nullptr, *dst = nullptr;
   if (cudaMalloc(&dst, bytes) != cudaSuccess) return 0.0;
   cudaSetDevice(peer);

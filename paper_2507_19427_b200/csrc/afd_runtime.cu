@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -166,6 +167,14 @@ struct afdk_afd {
   std::vector<afdk_ctx*> ctxs;
   std::vector<cudaStream_t> streams;  // n_micro + copy
   std::vector<cudaEvent_t> joins;
+  // attention rank, serialised attention compute (default; AFDK_AFD_ATTN_SERIAL=0
+  // restores per-micro-batch streams): the ATTN ops of all micro-batches run in
+  // order on one stream instead of overlapping as persistent full-GPU kernels.
+  // 1A3F MXFP8 e4m3 NVLS, layer period serial / overlapped: T_mb 256 0.767-0.770
+  // / 0.775-0.777 ms, 320 0.806-0.809 / 0.830-0.834, 384 0.865-0.868 / 0.892-0.898
+  bool attn_serial = false;
+  cudaStream_t cstream = nullptr;
+  std::vector<cudaEvent_t> ser_in, ser_out;
   uint32_t* flags = nullptr;
   std::vector<void*> own;  // every runtime allocation (freed at destroy)
   // attention rank
@@ -227,6 +236,18 @@ afdk_status alloc_local(afdk_afd* r) {
     cudaEvent_t ev;
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_err("event", e);
     r->joins.push_back(ev);
+  }
+  if (r->attn) {
+    const char* env = std::getenv("AFDK_AFD_ATTN_SERIAL");
+    r->attn_serial = !(env && env[0] == '0');
+  }
+  if (r->attn_serial) {
+    if ((e = cudaStreamCreateWithFlags(&r->cstream, cudaStreamNonBlocking)) != cudaSuccess) return cuda_err("stream", e);
+    for (int i = 0; i < 2 * c.n_micro; ++i) {
+      cudaEvent_t ev;
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_err("event", e);
+      (i < c.n_micro ? r->ser_in : r->ser_out).push_back(ev);
+    }
   }
   r->flags = static_cast<uint32_t*>(dmalloc(r, afdk::kMaxFlags * 4, &e));
   if (!r->flags || (e = cudaMemset(r->flags, 0, afdk::kMaxFlags * 4)) != cudaSuccess) return cuda_err("flags", e);
@@ -371,10 +392,14 @@ void release(afdk_afd* r) {
   if (!r) return;
   afdk::DeviceGuard g(r->device);
   for (cudaStream_t s : r->streams) cudaStreamSynchronize(s);
+  if (r->cstream) cudaStreamSynchronize(r->cstream);
   if (!r->ctxs.empty())
     for (void* p : r->opened) afdk_ipc_close(r->ctxs[0], p);
   for (afdk_nvls* g : r->nvls) afdk_nvls_destroy(g);
   for (cudaEvent_t e : r->joins) cudaEventDestroy(e);
+  for (cudaEvent_t e : r->ser_in) cudaEventDestroy(e);
+  for (cudaEvent_t e : r->ser_out) cudaEventDestroy(e);
+  if (r->cstream) cudaStreamDestroy(r->cstream);
   for (cudaEvent_t e : r->ev_pool) cudaEventDestroy(e);
   if (r->t0) cudaEventDestroy(r->t0);
   for (cudaStream_t s : r->streams) cudaStreamDestroy(s);
@@ -405,6 +430,15 @@ afdk_status run_plan(afdk_afd* r, Compute&& compute) {
   for (const afdk_afd_op& o : ops) {
     cudaStream_t s = r->streams[o.stream];
     afdk_status st = AFDK_OK;
+    // serialised attention: ATTN(m) moves to the compute stream, ordered after
+    // its micro-batch stream's earlier work and before its later work
+    const bool serial = r->attn_serial && o.kind == AFDK_OP_ATTN;
+    if (serial) {
+      cudaError_t e = cudaEventRecord(r->ser_in[o.mb], s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(r->cstream, r->ser_in[o.mb], 0);
+      if (e != cudaSuccess) return cuda_err("attn serial", e);
+      s = r->cstream;
+    }
     // measured trace: an event pair around every op that occupies a resource
     const bool traced = r->tracing && (o.kind == AFDK_OP_ATTN || o.kind == AFDK_OP_REDUCE ||
                                        o.kind == AFDK_OP_FFN || o.kind == AFDK_OP_PULL);
@@ -442,6 +476,11 @@ afdk_status run_plan(afdk_afd* r, Compute&& compute) {
     if (traced) {
       cudaEventRecord(rec.b, s);
       r->recs.push_back(rec);
+    }
+    if (serial) {
+      cudaError_t e = cudaEventRecord(r->ser_out[o.mb], s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(r->streams[o.stream], r->ser_out[o.mb], 0);
+      if (e != cudaSuccess) return cuda_err("attn serial", e);
     }
   }
   return AFDK_OK;
@@ -567,6 +606,7 @@ afdk_status afdk_afd_trace_start(afdk_afd* afd) {
   if ((e = cudaEventRecord(afd->t0, afd->streams[0])) != cudaSuccess) return cuda_err("trace t0", e);
   for (size_t i = 1; i < afd->streams.size(); ++i)
     if ((e = cudaStreamWaitEvent(afd->streams[i], afd->t0, 0)) != cudaSuccess) return cuda_err("trace t0", e);
+  if (afd->cstream && (e = cudaStreamWaitEvent(afd->cstream, afd->t0, 0)) != cudaSuccess) return cuda_err("trace t0", e);
   return AFDK_OK;
 }
 
@@ -628,6 +668,10 @@ afdk_status afdk_afd_trace_csv(afdk_afd* afd, char* buf, size_t cap, size_t* len
 afdk_status afdk_afd_sync(afdk_afd* afd) {
   if (!afd) { set_error("afdk_afd_sync: NULL"); return AFDK_ERR_INVALID; }
   afdk::DeviceGuard g(afd->device);
+  if (afd->cstream) {
+    const cudaError_t e = cudaStreamSynchronize(afd->cstream);
+    if (e != cudaSuccess) return cuda_err("sync", e);
+  }
   for (cudaStream_t s : afd->streams) {
     const cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_err("sync", e);

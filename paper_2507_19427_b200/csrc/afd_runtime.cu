@@ -131,6 +131,16 @@ std::vector<afdk_afd_op> plan(const afdk_afd_cfg& c, int rank, uint32_t seq) {
         afdk_afd_op* w = op(AFDK_OP_WAIT, cs, m);
         w->peer = a;
         w->slot = flag_slot(c, a, m);
+        if (c.n_attn == 1) {  // rx layout == payload layout: the whole message as one DMA
+          afdk_afd_op* p = op(AFDK_OP_PULL, cs, m);
+          p->peer = a;
+          p->src_buf = AFDK_BUF_SEND;
+          p->dst_buf = AFDK_BUF_RX;
+          p->src_off = 0;
+          p->dst_off = 0;
+          p->bytes = L.total;
+          continue;
+        }
         for (int s = 0; s < 4; ++s) {
           if (L.size[s] == 0) continue;
           afdk_afd_op* p = op(AFDK_OP_PULL, cs, m);

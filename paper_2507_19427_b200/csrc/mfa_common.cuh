@@ -126,6 +126,29 @@ struct SegmentWalker {
   }
 };
 
+// K / V ring prefill before griddepcontrol.wait: the first `cap` pages of
+// this CTA's walk, in walk order, stopping at the first page a predecessor
+// may write (a request's last page receives the appended token).  Returns how
+// many pages were issued (the main loop skips them).
+#ifndef AFDK_MFA_KV_PREFETCH
+#define AFDK_MFA_KV_PREFETCH 1
+#endif
+template <class Load>
+__device__ __forceinline__ int prefetch_pages(const int32_t* prefix, const Params& prm, int range_lo, int range_hi,
+                                              int cap, Load&& load) {
+  SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
+  int req, lo, hi, g = 0;
+  bool whole;
+  while (g < cap && walk.next(req, lo, hi, whole)) {
+    const int last = request_pages(__ldg(prm.seq_lens + req)) - 1;
+    for (int t = lo; t < hi && g < cap; ++t, ++g) {
+      if (t >= last) return g;
+      load(g, req, t);
+    }
+  }
+  return g;
+}
+
 // work units per request -> exclusive prefix in smem (every CTA; B <= kMaxBatch).
 // seq_lens is a caller input (no kernel of this library writes it), so this
 // may run before griddepcontrol.wait.

@@ -129,7 +129,13 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  griddep_wait();  // q, the appended K/V row and the reused workspace belong to the predecessors
+  // q, the appended K/V row and the reused workspace belong to the
+  // predecessors.  With AFDK_MFA_KV_PREFETCH the K / V producers first fill
+  // their rings with pages the predecessors cannot touch (every page of a
+  // request but its last, which holds the appended token) and only then wait,
+  // so the ring fill overlaps the predecessor's tail; every other role waits here.
+  const bool producer = AFDK_MFA_KV_PREFETCH && (warp == 0 || warp == 6);
+  if (!producer) griddep_wait();
   griddep_launch();
   if (threadIdx.x == 0) MFA_STAMP(0);
 #ifdef AFDK_MFA_TIMES
@@ -141,6 +147,16 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
+      auto load_k = [&](int g, int req, int t) {
+        const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
+        const int s = g % kNK, n = g / kNK;
+        if (n > 0) mbar_wait(&sm.k_empty[s], (n & 1) ^ 1);
+        mbar_expect_tx(&sm.k_full[s], kTileBytes);
+        for (int c = 0; c < 4; ++c)
+          tma_load_3d(sm.k[s] + c * kChunkBytes, &tm_k, &sm.k_full[s], c * 64, 0, page, pol_stream);
+      };
+      const int pre = AFDK_MFA_KV_PREFETCH ? prefetch_pages(prefix, prm, range_lo, range_hi, kNK, load_k) : 0;
+      if (AFDK_MFA_KV_PREFETCH) griddep_wait();
       SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
@@ -149,14 +165,8 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
         mbar_expect_tx(&sm.q_full, 4 * kChunkBytes);
         for (int c = 0; c < 4; ++c)
           tma_load_2d(sm.q + c * kChunkBytes, &tm_q, &sm.q_full, c * 64, req * kHeads, pol_keep);
-        for (int t = lo; t < hi; ++t, ++g) {
-          const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
-          const int s = g % kNK, n = g / kNK;
-          if (n > 0) mbar_wait(&sm.k_empty[s], (n & 1) ^ 1);
-          mbar_expect_tx(&sm.k_full[s], kTileBytes);
-          for (int c = 0; c < 4; ++c)
-            tma_load_3d(sm.k[s] + c * kChunkBytes, &tm_k, &sm.k_full[s], c * 64, 0, page, pol_stream);
-        }
+        for (int t = lo; t < hi; ++t, ++g)
+          if (g >= pre) load_k(g, req, t);
         ++seg;
       }
     }
@@ -164,18 +174,22 @@ mfa_decode_kernel(const __grid_constant__ CUtensorMap tm_q,
     // ---------------------------------------------------- V TMA producer
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
+      auto load_v = [&](int g, int req, int t) {
+        const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
+        const int s = g % kNV, n = g / kNV;
+        if (n > 0) mbar_wait(&sm.v_empty[s], (n & 1) ^ 1);
+        mbar_expect_tx(&sm.v_full[s], kTileBytes);
+        for (int c = 0; c < 4; ++c)
+          tma_load_3d(sm.v[s] + c * kChunkBytes, &tm_v, &sm.v_full[s], c * 64, 0, page, pol_stream);
+      };
+      const int pre = AFDK_MFA_KV_PREFETCH ? prefetch_pages(prefix, prm, range_lo, range_hi, kNV, load_v) : 0;
+      if (AFDK_MFA_KV_PREFETCH) griddep_wait();
       SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
-        for (int t = lo; t < hi; ++t, ++g) {
-          const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
-          const int s = g % kNV, n = g / kNV;
-          if (n > 0) mbar_wait(&sm.v_empty[s], (n & 1) ^ 1);
-          mbar_expect_tx(&sm.v_full[s], kTileBytes);
-          for (int c = 0; c < 4; ++c)
-            tma_load_3d(sm.v[s] + c * kChunkBytes, &tm_v, &sm.v_full[s], c * 64, 0, page, pol_stream);
-        }
+        for (int t = lo; t < hi; ++t, ++g)
+          if (g >= pre) load_v(g, req, t);
       }
     }
   } else if (warp == 1) {

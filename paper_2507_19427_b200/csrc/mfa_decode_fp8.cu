@@ -131,7 +131,9 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  griddep_wait();
+  // K / V producers prefill their rings before waiting (see mfa_decode.cu)
+  const bool producer = AFDK_MFA_KV_PREFETCH && (warp == 0 || warp == 6);
+  if (!producer) griddep_wait();
   griddep_launch();
 #ifdef AFDK_MFA_TIMES
   if (threadIdx.x == 0) { tl_min(s_tl, 1); tl_max(s_tl, 2); }
@@ -142,6 +144,16 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
+      auto load_k = [&](int g, int req, int t) {
+        const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
+        const int s = g % kNK8, n = g / kNK8;
+        if (n > 0) mbar_wait(&sm.k_empty[s], (n & 1) ^ 1);
+        mbar_expect_tx(&sm.k_full[s], kTile8);
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d(sm.k[s] + c * kPanel8, &tm_k, &sm.k_full[s], c * 128, 0, page, pol_stream);
+      };
+      const int pre = AFDK_MFA_KV_PREFETCH ? prefetch_pages(prefix, prm, range_lo, range_hi, kNK8, load_k) : 0;
+      if (AFDK_MFA_KV_PREFETCH) griddep_wait();
       SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, seg = 0, g = 0;
       bool whole;
@@ -150,14 +162,8 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         mbar_expect_tx(&sm.q_full, 4 * kPanel16);
         for (int c = 0; c < 4; ++c)
           tma_load_2d(sm.q + c * kPanel16, &tm_q, &sm.q_full, c * 64, req * kHeads, pol_keep);
-        for (int t = lo; t < hi; ++t, ++g) {
-          const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
-          const int s = g % kNK8, n = g / kNK8;
-          if (n > 0) mbar_wait(&sm.k_empty[s], (n & 1) ^ 1);
-          mbar_expect_tx(&sm.k_full[s], kTile8);
-          for (int c = 0; c < 2; ++c)
-            tma_load_3d(sm.k[s] + c * kPanel8, &tm_k, &sm.k_full[s], c * 128, 0, page, pol_stream);
-        }
+        for (int t = lo; t < hi; ++t, ++g)
+          if (g >= pre) load_k(g, req, t);
         ++seg;
       }
     }
@@ -165,18 +171,22 @@ mfa_decode_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     // ---------------------------------------------------- V TMA producer
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();
+      auto load_v = [&](int g, int req, int t) {
+        const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
+        const int s = g % kNV8, n = g / kNV8;
+        if (n > 0) mbar_wait(&sm.v_empty[s], (n & 1) ^ 1);
+        mbar_expect_tx(&sm.v_full[s], kTile8);
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d(sm.v[s] + c * kPanel8, &tm_v, &sm.v_full[s], c * 128, 0, page, pol_stream);
+      };
+      const int pre = AFDK_MFA_KV_PREFETCH ? prefetch_pages(prefix, prm, range_lo, range_hi, kNV8, load_v) : 0;
+      if (AFDK_MFA_KV_PREFETCH) griddep_wait();
       SegmentWalker walk(prefix, prm.batch, range_lo, range_hi, prm.seg_cost);
       int req, lo, hi, g = 0;
       bool whole;
       while (walk.next(req, lo, hi, whole)) {
-        for (int t = lo; t < hi; ++t, ++g) {
-          const int page = __ldg(prm.block_table + (size_t)req * prm.max_pages + t);
-          const int s = g % kNV8, n = g / kNV8;
-          if (n > 0) mbar_wait(&sm.v_empty[s], (n & 1) ^ 1);
-          mbar_expect_tx(&sm.v_full[s], kTile8);
-          for (int c = 0; c < 2; ++c)
-            tma_load_3d(sm.v[s] + c * kPanel8, &tm_v, &sm.v_full[s], c * 128, 0, page, pol_stream);
-        }
+        for (int t = lo; t < hi; ++t, ++g)
+          if (g >= pre) load_v(g, req, t);
       }
     }
   } else if (warp == 1) {

@@ -44,6 +44,10 @@ def main():
     ap.add_argument("--T-mb", type=int, default=24)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--layers", type=int, default=LAYERS)
+    ap.add_argument("--full", type=int, default=0,
+                    help="Step-3 dims (hidden 7168, q_lora 2048, 48 experts top-3, inter 5120, 4K context): the "
+                         "benchmarked AFD configuration")
     a = ap.parse_args()
     STEPS = a.steps
     import torch
@@ -59,10 +63,11 @@ def main():
     shared_gpu = world > torch.cuda.device_count()
     dist.init_process_group("gloo" if shared_gpu else "nccl", **({} if shared_gpu else {"device_id": dev}))
     nf = world - a.n_attn
-    cfg = AfdConfig(n_attn=a.n_attn, n_ffn=nf, T_mb=a.T_mb, n_micro=2, layers=LAYERS, hidden=1024, q_lora=256,
-                    ctx_len=300, n_experts=8 if nf in (1, 2, 4, 8) else 24, top_k=2, inter=512, seed=3,
-                    ffn_format=a.fmt, f2a=a.f2a, kv=a.kv, layer_kind=a.layer, attn_chunk=a.attn_chunk,
-                    dense_inter=2048 * 6)
+    dims = dict(hidden=7168, q_lora=2048, ctx_len=4096, n_experts=48, top_k=3, inter=5120, dense_inter=18432) \
+        if a.full else dict(hidden=1024, q_lora=256, ctx_len=300, n_experts=8 if nf in (1, 2, 4, 8) else 24,
+                            top_k=2, inter=512, dense_inter=2048 * 6)
+    cfg = AfdConfig(n_attn=a.n_attn, n_ffn=nf, T_mb=a.T_mb, n_micro=2, layers=a.layers, seed=3,
+                    ffn_format=a.fmt, f2a=a.f2a, kv=a.kv, layer_kind=a.layer, attn_chunk=a.attn_chunk, **dims)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -137,7 +142,7 @@ def main():
         want.add("bwd_link")
     got_res = {row[1] for row in rows[1:]}
     trace_ok = (rows[0] == ["time_s", "resource", "layer", "micro_batch", "stage", "duration_s"] and
-                want <= got_res and {int(row[2]) for row in rows[1:]} == set(range(LAYERS)) and
+                want <= got_res and {int(row[2]) for row in rows[1:]} == set(range(cfg.layers)) and
                 all(float(row[5]) >= 0 for row in rows[1:]))
     if not trace_ok:
         print("bad trace on rank", rank, csv[:2000], flush=True)
@@ -145,11 +150,12 @@ def main():
     allerr = [None] * world
     dist.all_gather_object(allerr, errs)
     flat = [e for es in allerr for e in es]
-    ok = len(flat) == cfg.n_attn * cfg.n_micro * STEPS * LAYERS and max(flat) <= 2e-2  # a bad trace adds one
+    ok = len(flat) == cfg.n_attn * cfg.n_micro * STEPS * cfg.layers and max(flat) <= 2e-2  # a bad trace adds one
     if rank == 0:
         res = {"afd_check": "ok" if ok else "FAIL", "world": world, "n_attn": cfg.n_attn, "fmt": cfg.ffn_format,
                "f2a": cfg.f2a, "kv": cfg.kv, "layer": cfg.layer_kind, "T_mb": cfg.T_mb, "attn_chunk": cfg.attn_chunk,
-               "steps": STEPS, "layers": LAYERS, "seq": STEPS * LAYERS, "max_rel_err": max(flat), "rel_err": flat,
+               "steps": STEPS, "layers": cfg.layers, "seq": STEPS * cfg.layers, "max_rel_err": max(flat), "rel_err": flat,
+               "full_dims": bool(a.full),
                "shared_gpu": shared_gpu}
         print(json.dumps(res), flush=True)
         if a.out:

@@ -27,6 +27,9 @@ CASES = [
     (3, 1, ["--fmt", "fp8", "--f2a", "pull", "--steps", "12"]),  # soak: 24 sequence numbers of flag reuse
     (2, 1, ["--fmt", "mx", "--f2a", "nvls"]),       # NVLS return: one GPU per rank
     (3, 1, ["--fmt", "bf16", "--f2a", "nvls"]),
+    # the benchmarked AFD point at Step-3 dims: 1A3F, MXFP8, e4m3 KV, NVLS, 320 requests per micro-batch
+    (4, 1, ["--fmt", "mx", "--f2a", "nvls", "--kv", "e4m3", "--T-mb", "320", "--steps", "2", "--layers", "1",
+            "--full", "1"]),
 ]
 
 
@@ -38,13 +41,15 @@ def test_afd_runtime_multi_process(tmp_path, world, n_attn, extra):
 
     if "nvls" in extra and torch.cuda.device_count() < world:
         pytest.skip("the NVLS return needs one GPU per rank")
+    if "--full" in extra and torch.cuda.device_count() < world:
+        pytest.skip("Step-3 dims: one GPU per rank")
     out = tmp_path / "res.json"
     port = 29500 + (os.getpid() % 1000)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "afd_gpu_check.py"),
            "--n-attn", str(n_attn), "--out", str(out), *extra]
     env = dict(os.environ, PYTHONPATH=ROOT, OMP_NUM_THREADS="1")
-    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     got = json.load(open(out))
     assert got["afd_check"] == "ok" and got["max_rel_err"] <= 2e-2, got

@@ -189,9 +189,11 @@ moe_ffn_mx_fused_kernel(const __grid_constant__ CUtensorMap tm_w13, const __grid
         const int nA = f.glu ? 2 : 1;
         if (!f.glu) {  // the chunk's whole intermediate must be written
           unsigned ns = 64;
+          long long spins = 0;
           while (ld_acquire_gpu(p.sched + 1 + f.chunk) < p.mt13) {
             __nanosleep(ns);
             if (ns < 512) ns <<= 1;
+            if (++spins > (1ll << 24)) __trap();  // seconds: a lost publish fails the launch instead of hanging
           }
           fence_proxy_async_global();  // generic-proxy writes -> this thread's TMA reads
         }

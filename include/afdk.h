@@ -126,6 +126,14 @@ afdk_status afdk_mfa_decode_attention_mtp(afdk_ctx* ctx, const afdk_mfa_decode_a
 afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, int m, int n, int k,
                         int out_fp32, afdk_stream stream);
 
+/* The same projection with MXFP8 operands (the paper's FP8 attention GEMMs,
+ * PAPER.md:774,781): xq e4m3 [m, k] + xsf UE8M0 [m, k/32], wq e4m3 [n, k] +
+ * wsf UE8M0 [n, k/32] (afdk_quant_mx's format), y = dequant(xq) .
+ * dequant(wq)^T with fp32 accumulation on the block-scaled tensor-core MMA.
+ * 1 <= m <= 256, k % 128 == 0.                                              */
+afdk_status afdk_linear_mx(afdk_ctx* ctx, const void* xq, const uint8_t* xsf, const void* wq, const uint8_t* wsf,
+                           void* out, int m, int n, int k, int out_fp32, afdk_stream stream);
+
 /* --------------------------------------------- attention-side decode layer
  * input RMSNorm -> [q_down|k|v] -> q RMSNorm -> q_up -> NeoX RoPE(q, k)
  * -> paged KV append (position seq_lens[b]-1) -> MFA decode core -> o_proj

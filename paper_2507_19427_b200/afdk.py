@@ -150,6 +150,8 @@ SIGNATURES = {
     "afdk_ctx_device": (c_int, [c_void_p]),
     "afdk_mfa_decode_attention": (c_int, [c_void_p, POINTER(MfaDecodeArgs), c_void_p]),
     "afdk_linear": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p]),
+    "afdk_linear_mx": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
+                               c_void_p]),
     "afdk_mfa_layer": (c_int, [c_void_p, POINTER(MfaWeights), POINTER(MfaLayerArgs), c_void_p]),
     "afdk_router_topk": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p,
                                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -365,6 +367,15 @@ class Context:
         n = w.shape[0]
         check(self.lib.afdk_linear(self.handle, ptr(x), ptr(w), ptr(out), m, n, k,
                                    int(out.dtype == torch.float32), c_void_p(stream)))
+
+    def linear_mx(self, xq, xsf, wq, wsf, out, stream: int = 0) -> None:
+        """MXFP8 projection: xq/wq e4m3 codes (uint8), xsf/wsf UE8M0 [rows, K/32]."""
+        import torch
+
+        m, k = xq.shape
+        n = wq.shape[0]
+        check(self.lib.afdk_linear_mx(self.handle, ptr(xq), ptr(xsf), ptr(wq), ptr(wsf), ptr(out), m, n, k,
+                                      int(out.dtype == torch.float32), c_void_p(stream)))
 
     def mfa_layer(self, w: dict, x, k_cache, v_cache, block_table, seq_lens, h_res, h_norm,
                   rms_eps=1e-5, rope_theta=5e5, softmax_scale=None, stream: int = 0, kv_scales=None,

@@ -22,6 +22,7 @@ CU_SOURCES = [
     "mfa_decode_fp8.cu",
     "mfa_decode_mtp.cu",
     "linear.cu",
+    "linear_mx.cu",
     "moe_gemm_mx.cu",
     "moe_gemm_mx2.cu",
     "moe_gemm_bf16.cu",

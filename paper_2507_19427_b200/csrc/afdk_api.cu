@@ -242,6 +242,23 @@ afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, 
   return AFDK_OK;
 }
 
+afdk_status afdk_linear_mx(afdk_ctx* ctx, const void* xq, const uint8_t* xsf, const void* wq, const uint8_t* wsf,
+                           void* out, int m, int n, int k, int out_fp32, afdk_stream stream) {
+  if (!ctx || !xq || !xsf || !wq || !wsf || !out) { set_error("afdk_linear_mx: NULL argument"); return AFDK_ERR_INVALID; }
+  if (m < 1 || m > 256) { set_error("afdk_linear_mx: m must be in [1, 256]"); return AFDK_ERR_INVALID; }
+  if (n < 1 || k < 128 || k % 128) { set_error("afdk_linear_mx: k must be a positive multiple of 128"); return AFDK_ERR_INVALID; }
+  afdk::Ctx& c = ctx->c;
+  afdk::DeviceGuard device_guard(c.device);
+  const afdk::LinearPlan p = afdk::make_linear_mx_plan(m, n, k);
+  float* part = static_cast<float*>(afdk::workspace(c, afdk::linear_workspace_bytes(p, c.num_sms)));
+  if (!part) { set_error("afdk_linear_mx: workspace allocation failed"); return AFDK_ERR_CUDA; }
+  auto st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = afdk::linear_mx_launch(c, p, xq, xsf, wq, wsf, part, st);
+  if (e == cudaSuccess) e = afdk::linear_store_launch(c, p, part, out, out_fp32 != 0, st);
+  if (e != cudaSuccess) return cuda_fail("afdk_linear_mx", e);
+  return AFDK_OK;
+}
+
 static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, const afdk_mfa_layer_args* a,
                                    float k_scale, float v_scale, afdk_stream stream, int mtp = 1) {
   if (!ctx || !w || !a) { set_error("afdk_mfa_layer: NULL ctx/weights/args"); return AFDK_ERR_INVALID; }

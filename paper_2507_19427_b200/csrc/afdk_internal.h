@@ -162,6 +162,10 @@ cudaError_t linear_bf16_rope_launch(Ctx& ctx, const LinearPlan& p, const void* x
                                     cudaStream_t stream);
 cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
                                cudaStream_t stream);
+// MXFP8 linear (linear_mx.cu): 128-element k-blocks, the same partial layout
+LinearPlan make_linear_mx_plan(int m_tok, int n_out, int k);
+cudaError_t linear_mx_launch(Ctx& ctx, const LinearPlan& p, const void* xq, const uint8_t* xsf, const void* wq,
+                             const uint8_t* wsf, float* part, cudaStream_t stream);
 cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,
                                 cudaStream_t stream);
 

@@ -148,6 +148,11 @@ typedef struct afdk_mfa_weights {
   const void* w_o;       /* bf16 [hidden, n_heads*head_dim]              */
   const void* post_norm; /* bf16 [hidden]                                */
   float rms_eps, rope_theta, softmax_scale;
+  /* optional (NULL = bf16 w_o): o_proj as an MXFP8 GEMM (afdk_linear_mx) —
+   * e4m3 [hidden, n_heads*head_dim] + UE8M0 [hidden, n_heads*head_dim/32];
+   * the attention output is MXFP8-quantised on the way in.  batch <= 256. */
+  const void* w_o_mx;
+  const uint8_t* w_o_sf;
 } afdk_mfa_weights;
 
 typedef struct afdk_mfa_layer_args {

@@ -224,6 +224,14 @@ void orc_mfa_layer(const orc_mfa_dims* d, int B, const float* x,
   }
   orc_mfa_decode_attention(q, k_cache, v_cache, block_table, max_pages, seq_lens, B, NH, D,
                            d->page, d->softmax_scale, round_bf16, attn, NULL);
+  if (d->o_mx) { /* MXFP8 o_proj input: e4m3 x 2^e per 32 attention-output elements */
+    uint8_t* q8 = (uint8_t*)malloc((size_t)B * NQ);
+    uint8_t* sf = (uint8_t*)malloc((size_t)B * (NQ / 32));
+    orc_quant_mx(attn, B, NQ, q8, sf);
+    for (size_t i = 0; i < (size_t)B * NQ; ++i) attn[i] = orc_e4m3_to_f32(q8[i]) * orc_mx_scale(sf[i / 32]);
+    free(q8);
+    free(sf);
+  }
   orc_linear(attn, w_o, B, Hd, NQ, 0, o);                             /* o_proj (fp32)   */
   for (size_t i = 0; i < (size_t)B * Hd; ++i) h_res[i] = maybe_bf16(x[i] + o[i], round_bf16);
   orc_rmsnorm(h_res, w_post_norm, B, Hd, d->rms_eps, round_bf16, h_norm);

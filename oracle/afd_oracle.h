@@ -80,6 +80,10 @@ typedef struct {
    * quantised with a power-of-two scale (orc_quant_pow2, block = head_dim)
    * before the exact attention. */
   float kv_k_scale, kv_v_scale;
+  /* o_mx != 0: the o_proj input (the attention output) is MXFP8-quantised
+   * (orc_quant_mx) and dequantised before o_proj, as afdk_mfa_layer with
+   * MXFP8 o_proj weights does (the caller passes the dequantised weights). */
+  int o_mx;
 } orc_mfa_dims;
 
 /* x          [B, hidden]              layer input (residual stream)

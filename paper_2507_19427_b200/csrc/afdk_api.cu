@@ -279,7 +279,7 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
     return AFDK_ERR_INVALID;
   }
   if (!a->x || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->h_res || !a->h_norm ||
-      !w->in_norm || !w->w_qkv || !w->q_norm || !w->w_q_up || !w->w_o || !w->post_norm) {
+      !w->in_norm || !w->w_qkv || !w->q_norm || !w->w_q_up || (!w->w_o && !w->w_o_mx) || !w->post_norm) {
     set_error("afdk_mfa_layer: NULL tensor pointer");
     return AFDK_ERR_INVALID;
   }
@@ -289,7 +289,11 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
                        w->in_norm, w->w_qkv, w->q_norm, w->w_q_up, w->w_o, w->post_norm,
                        w->rms_eps, w->rope_theta, w->softmax_scale, a->x, a->k_cache, a->v_cache,
                        a->num_pages, a->block_table, a->max_pages, a->seq_lens, a->h_res, a->h_norm,
-                       k_scale, v_scale, mtp};
+                       k_scale, v_scale, mtp, w->w_o_mx, w->w_o_sf};
+  if ((w->w_o_mx != nullptr) != (w->w_o_sf != nullptr) || (w->w_o_mx && (a->batch * mtp > 256 || mtp > 1))) {
+    set_error("afdk_mfa_layer: MXFP8 o_proj needs both w_o_mx and w_o_sf, mtp 1 and batch <= 256");
+    return AFDK_ERR_INVALID;
+  }
   void* ws = afdk::workspace(c, afdk::mfa_layer_workspace_bytes(m, c.num_sms));
   if (!ws) { set_error("afdk_mfa_layer: workspace allocation failed"); return AFDK_ERR_CUDA; }
   const cudaError_t e = afdk::mfa_layer_launch(c, m, ws, static_cast<cudaStream_t>(stream));

@@ -184,6 +184,8 @@ struct MfaLayerArgs {
   void* h_norm;
   float k_scale = 0.0f, v_scale = 0.0f;  // > 0: e4m3 KV cache (mfa_decode_fp8.cu)
   int mtp = 1;  // query tokens per request: rows are (request, token), batch*mtp of them
+  const void* w_o_mx = nullptr;     // optional MXFP8 o_proj weights (e4m3 [hidden, NQ]) ...
+  const uint8_t* w_o_sf = nullptr;  // ... and their UE8M0 scales [hidden, NQ/32]
 };
 const double* rope_inv_freq(Ctx& ctx, int head_dim, float theta);
 size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms);

@@ -440,9 +440,20 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
             : a.k_scale > 0.0f ? mfa_decode_fp8_launch(ctx, md, stream) : mfa_decode_launch(ctx, md, stream))) !=
       cudaSuccess)
     return e;
-  // K4: o_proj, then residual + post-attention RMSNorm
-  const LinearPlan p3 = make_linear_plan(B, Hd, NQ);
-  if ((e = linear_bf16_launch(ctx, p3, attn, a.w_o, part, stream)) != cudaSuccess) return e;
+  // K4: o_proj, then residual + post-attention RMSNorm.  With MXFP8 o_proj
+  // weights the attention output is MX-quantised into the (consumed) q buffer
+  // and the projection runs on the block-scaled MMA (linear_mx.cu).
+  const bool o_mx = a.w_o_mx != nullptr;
+  const LinearPlan p3 = o_mx ? make_linear_mx_plan(B, Hd, NQ) : make_linear_plan(B, Hd, NQ);
+  if (o_mx) {
+    uint8_t* oq = reinterpret_cast<uint8_t*>(q);
+    uint8_t* osf = oq + (size_t)B * NQ;
+    moe::QuantMxArgs qa{attn, B, NQ, oq, osf};
+    if ((e = quant_mx_launch(qa, stream, ctx.pdl)) != cudaSuccess) return e;
+    if ((e = linear_mx_launch(ctx, p3, oq, osf, a.w_o_mx, a.w_o_sf, part, stream)) != cudaSuccess) return e;
+  } else if ((e = linear_bf16_launch(ctx, p3, attn, a.w_o, part, stream)) != cudaSuccess) {
+    return e;
+  }
   if ((e = row_launch(o_epilogue_kernel<2>, o_epilogue_kernel<4>, p3, (const float*)part, linear_grid(ctx, p3), Hd,
                       static_cast<const __nv_bfloat16*>(a.x), static_cast<const __nv_bfloat16*>(a.w_post_norm),
                       a.rms_eps, static_cast<__nv_bfloat16*>(a.h_res), static_cast<__nv_bfloat16*>(a.h_norm))) !=

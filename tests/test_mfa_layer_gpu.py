@@ -152,3 +152,55 @@ def test_mfa_layer_wide_batch(ctx, kv, batch):
         g_res, g_norm, gk, gv, r_res, r_norm, rk, rv, bt, sl, _ = run_layer_fp8(ctx, STEP3, seq_lens, 32)
         assert rel_err(g_res, r_res) <= 3e-2, rel_err(g_res, r_res)
         assert rel_err(g_norm, r_norm) <= 3e-2, rel_err(g_norm, r_norm)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kv", ["bf16", "e4m3"])
+def test_mfa_layer_mx_oproj(ctx, kv):
+    """o_proj as an MXFP8 GEMM (afdk_mfa_weights.w_o_mx / w_o_sf, afdk_linear_mx):
+    the oracle quantises the attention output with the same MX rule (o_mx) and
+    multiplies by the dequantised MX weights; bars as the bf16 / e4m3-KV layer."""
+    import torch
+
+    rng = np.random.default_rng(91)
+    seq_lens = rng.integers(1, 700, size=64).tolist()
+    x, w, kc, vc, bt, sl = mg.layer_inputs(STEP3, seq_lens, 17)
+    dev = torch.device("cuda:0")
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(dev)
+    wd = {k: bf(v) for k, v in w.items()}
+    n_out, nq = wd["o"].shape
+    o_mx = torch.empty(n_out, nq, dtype=torch.uint8, device=dev)
+    o_sf = torch.empty(n_out, nq // 32, dtype=torch.uint8, device=dev)
+    ctx.quant_mx(wd["o"], o_mx, o_sf)
+    wd["o_mx"], wd["o_sf"] = o_mx, o_sf
+    w_or = dict(w)
+    w_or["o"] = (orc.e4m3_to_f32(o_mx.cpu().numpy()) *
+                 np.exp2(o_sf.cpu().numpy().astype(np.float32) - 127.0).repeat(32, axis=1)).astype(np.float32)
+    dims = dict(STEP3, o_mx=1)
+    xd = bf(x)
+    h_res, h_norm = torch.empty_like(xd), torch.empty_like(xd)
+    bt_d, sl_d = torch.from_numpy(bt).to(dev), torch.from_numpy(sl).to(dev)
+    if kv == "e4m3":
+        ks, vs = float(np.abs(kc).max()) / 448.0, float(np.abs(vc).max()) / 448.0
+        kq = (torch.from_numpy(kc) / ks).to(torch.float8_e4m3fn).view(torch.uint8)
+        vq = (torch.from_numpy(vc) / vs).to(torch.float8_e4m3fn).view(torch.uint8)
+        ctx.mfa_layer(wd, xd, kq.to(dev), vq.to(dev), bt_d, sl_d, h_res, h_norm, kv_scales=(ks, vs))
+        k1 = orc.e4m3_to_f32(kq.numpy()) * np.float32(ks)
+        v1 = orc.e4m3_to_f32(vq.numpy()) * np.float32(vs)
+        dims.update(kv_k_scale=ks, kv_v_scale=vs)
+        bar = 3e-2
+    else:
+        ctx.mfa_layer(wd, xd, bf(kc), bf(vc), bt_d, sl_d, h_res, h_norm)
+        k1, v1 = kc.copy(), vc.copy()
+        bar = 2e-2
+    torch.cuda.synchronize()
+    r_res, r_norm = orc.mfa_layer(dims, x, w_or, k1, v1, bt, sl)
+    e_res = rel_err(h_res.float().cpu().numpy(), r_res)
+    e_norm = rel_err(h_norm.float().cpu().numpy(), r_norm)
+    try:
+        from tests.helpers import record
+        record(f"mfa_layer_mx_oproj_{kv}", h_res=e_res, h_norm=e_norm)
+    except Exception:  # noqa: BLE001
+        pass
+    assert e_res <= bar, e_res
+    assert e_norm <= bar, e_norm

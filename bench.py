@@ -224,7 +224,7 @@ def run_fp8_kv(ctx, torch, dev, s, batch, ctx_len, steps):
     layer_ms, core_ms = timed(layer), timed(core)
     # the same layer with o_proj as an MXFP8 GEMM (the paper's FP8 attention GEMM form)
     mx = None
-    if batch <= 256:
+    if batch <= 384:
         wo = s["w"]["o"]
         o_mx = torch.empty(wo.shape, dtype=torch.uint8, device=dev)
         o_sf = torch.empty(wo.shape[0], wo.shape[1] // 32, dtype=torch.uint8, device=dev)
@@ -528,6 +528,9 @@ def afd_runs(world):
     # larger micro-batches toward the SLA edge (the FFN stage grows slowly with T at decode)
     runs += [(base, "mx", T, "moe", "e4m3", "nvls") for T in (320, 352, 368, 384)]
     runs.append((bal, "mx", 512, "dense", "bf16", "push"))  # dense layer: FFN tier tensor-parallel over slices
+    runs = [r + (False,) for r in runs]
+    # o_proj as an MXFP8 GEMM on the attention GPUs (the paper's FP8 attention GEMMs)
+    runs += [(base, "mx", T, "moe", "e4m3", "nvls", True) for T in (352, 368, 384)]
     return runs
 
 
@@ -557,7 +560,7 @@ def stages_from_traces(traces, n_micro):
 
 
 def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt="fp8", plan=None, kind="moe",
-                     kv="bf16", f2a="push"):
+                     kv="bf16", f2a="push", o_mx=False):
     """Real pipeline on all ranks through the C++ AFD runtime: nA attention
     GPUs + nF FFN GPUs, 2 ping-pong micro-batches, 2 layers per step (distinct
     KV caches), copy-engine NVLink.  One more traced step gives the measured
@@ -568,7 +571,7 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
 
     na, nf = plan if plan else afd_roles(world)
     cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=T_mb, n_micro=2, layers=2, ctx_len=CTX, ffn_format=fmt, layer_kind=kind,
-                    kv=kv, f2a=f2a)
+                    kv=kv, f2a=f2a, attn_o_mx=o_mx)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -616,7 +619,8 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
     vet = afdk.vet_stages([st["attention"]] * N_LAYERS, [st["ffn"]] * N_LAYERS, tpot_sla=TPOT_SLA,
                           pipeline_stages=cfg.n_micro, n_model_layers=N_LAYERS)
     tpot = N_LAYERS * period * 1e-3
-    res = {"plan": f"{na}A{nf}F", "layer": kind, "ffn_format": fmt, "kv": kv, "f2a": f2a, "T_mb": cfg.T_mb,
+    res = {"plan": f"{na}A{nf}F", "layer": kind, "ffn_format": fmt, "kv": kv, "f2a": f2a,
+           "attn_o_proj": "mxfp8" if o_mx else "bf16", "T_mb": cfg.T_mb,
            "n_micro": cfg.n_micro, "ctx": cfg.ctx_len,
            "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
            "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
@@ -633,7 +637,7 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
     tdir = os.environ.get("AFDK_TRACE_DIR")
     if tdir and rank == 0:
         os.makedirs(tdir, exist_ok=True)
-        name = f"afd_{res['plan']}_{fmt}_{kind}_{kv}_{f2a}_T{T_mb}"
+        name = f"afd_{res['plan']}_{fmt}_{kind}_{kv}_{f2a}{'_omx' if o_mx else ''}_T{T_mb}"
         with open(os.path.join(tdir, name + ".csv"), "w") as f:
             for q, csv in enumerate(traces):
                 body = csv.strip().splitlines()
@@ -1020,13 +1024,14 @@ def main():
                 # micro-batch sweep: per-layer throughput depends on balancing the
                 # attention tier (grows with T_mb) against expert weight streaming
                 runs = []
-                for plan, f, T, kind, kv, f2a in afd_runs(world):
+                for plan, f, T, kind, kv, f2a, o_mx in afd_runs(world):
                     try:
                         runs.append(run_afd_measured(torch, dist, dev, world, rank, local, max(3, args.steps // 4), T,
-                                                     f, plan, kind, kv, f2a))
+                                                     f, plan, kind, kv, f2a, o_mx))
                     except Exception as e:  # e.g. no NVLS on this system: reported, the sweep goes on
                         runs.append({"plan": f"{plan[0]}A{plan[1]}F", "ffn_format": f, "T_mb": T, "layer": kind,
-                                     "kv": kv, "f2a": f2a, "error": f"{type(e).__name__}: {e}"})
+                                     "kv": kv, "f2a": f2a, "attn_o_proj": "mxfp8" if o_mx else "bf16",
+                                     "error": f"{type(e).__name__}: {e}"})
                 runs_ok = [x for x in runs if "error" not in x]
                 moe_runs = [x for x in runs_ok if x["layer"] == "moe"]
                 sla = [x for x in moe_runs if x["sla_ok"]]

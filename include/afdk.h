@@ -130,7 +130,7 @@ afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, 
  * PAPER.md:774,781): xq e4m3 [m, k] + xsf UE8M0 [m, k/32], wq e4m3 [n, k] +
  * wsf UE8M0 [n, k/32] (afdk_quant_mx's format), y = dequant(xq) .
  * dequant(wq)^T with fp32 accumulation on the block-scaled tensor-core MMA.
- * 1 <= m <= 256, k % 128 == 0.                                              */
+ * 1 <= m <= 384 (above 256 tokens: two N/2 MMAs per k-block), k % 128 == 0. */
 afdk_status afdk_linear_mx(afdk_ctx* ctx, const void* xq, const uint8_t* xsf, const void* wq, const uint8_t* wsf,
                            void* out, int m, int n, int k, int out_fp32, afdk_stream stream);
 
@@ -150,7 +150,7 @@ typedef struct afdk_mfa_weights {
   float rms_eps, rope_theta, softmax_scale;
   /* optional (NULL = bf16 w_o): o_proj as an MXFP8 GEMM (afdk_linear_mx) —
    * e4m3 [hidden, n_heads*head_dim] + UE8M0 [hidden, n_heads*head_dim/32];
-   * the attention output is MXFP8-quantised on the way in.  batch <= 256. */
+   * the attention output is MXFP8-quantised on the way in.  batch <= 384. */
   const void* w_o_mx;
   const uint8_t* w_o_sf;
 } afdk_mfa_weights;

@@ -245,7 +245,7 @@ afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, 
 afdk_status afdk_linear_mx(afdk_ctx* ctx, const void* xq, const uint8_t* xsf, const void* wq, const uint8_t* wsf,
                            void* out, int m, int n, int k, int out_fp32, afdk_stream stream) {
   if (!ctx || !xq || !xsf || !wq || !wsf || !out) { set_error("afdk_linear_mx: NULL argument"); return AFDK_ERR_INVALID; }
-  if (m < 1 || m > 256) { set_error("afdk_linear_mx: m must be in [1, 256]"); return AFDK_ERR_INVALID; }
+  if (m < 1 || m > 384) { set_error("afdk_linear_mx: m must be in [1, 384]"); return AFDK_ERR_INVALID; }
   if (n < 1 || k < 128 || k % 128) { set_error("afdk_linear_mx: k must be a positive multiple of 128"); return AFDK_ERR_INVALID; }
   afdk::Ctx& c = ctx->c;
   afdk::DeviceGuard device_guard(c.device);
@@ -290,8 +290,8 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
                        w->rms_eps, w->rope_theta, w->softmax_scale, a->x, a->k_cache, a->v_cache,
                        a->num_pages, a->block_table, a->max_pages, a->seq_lens, a->h_res, a->h_norm,
                        k_scale, v_scale, mtp, w->w_o_mx, w->w_o_sf};
-  if ((w->w_o_mx != nullptr) != (w->w_o_sf != nullptr) || (w->w_o_mx && (a->batch * mtp > 256 || mtp > 1))) {
-    set_error("afdk_mfa_layer: MXFP8 o_proj needs both w_o_mx and w_o_sf, mtp 1 and batch <= 256");
+  if ((w->w_o_mx != nullptr) != (w->w_o_sf != nullptr) || (w->w_o_mx && (a->batch * mtp > 384 || mtp > 1))) {
+    set_error("afdk_mfa_layer: MXFP8 o_proj needs both w_o_mx and w_o_sf, mtp 1 and batch <= 384");
     return AFDK_ERR_INVALID;
   }
   void* ws = afdk::workspace(c, afdk::mfa_layer_workspace_bytes(m, c.num_sms));

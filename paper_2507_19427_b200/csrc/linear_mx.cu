@@ -36,8 +36,12 @@ using namespace sm100;
 
 constexpr int kThreads = 320;
 constexpr int kA = 128 * 128;          // one 128-row x 128-element e4m3 weight k-block
-constexpr uint32_t kSfCol0 = 256;      // scale ring after the accumulators
-constexpr int kSfCols = 4 + 8;         // per stage: 4 weight columns + up to 8 token columns (N <= 256)
+// scale ring after the accumulators: per stage 4 weight columns + one column
+// per 32 token rows (N <= 256: 8, or 12 in the two-MMA form for N <= 384)
+template <bool kW> struct SfRing;
+template <> struct SfRing<false> { static constexpr uint32_t col0 = 256; static constexpr int cols = 12; };
+// (the two-MMA form keeps each half's token columns at a 4-aligned offset: 4.. and 12..)
+template <> struct SfRing<true> { static constexpr uint32_t col0 = 384; static constexpr int cols = 20; };
 
 struct KParams {
   LinearPlan plan;        // kblocks = K / 128
@@ -53,6 +57,9 @@ __device__ __forceinline__ void unit_range(int c, int G, int U, int& lo, int& hi
   hi = (int)(((long long)(c + 1) * U) / G);
 }
 
+// kW: 257-384 tokens as two MMAs of N/2 (N a multiple of 64) sharing each
+// weight k-block, the accumulator single-buffered in TMEM columns [0, N)
+template <bool kW>
 __global__ void __launch_bounds__(kThreads, 1)
 linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                  const __grid_constant__ CUtensorMap tm_wsf, const __grid_constant__ CUtensorMap tm_xsf,
@@ -75,6 +82,9 @@ linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
   unit_range(cta, G, U, u_lo, u_hi);
   const int n_mma = P.n_mma;
   const bool dbuf = n_mma <= 128;  // double-buffered accumulators while 2 x N columns fit before the scales
+  constexpr uint32_t kSfCol0 = SfRing<kW>::col0;
+  constexpr int kSfCols = SfRing<kW>::cols;
+  const int nh = kW ? n_mma / 2 : n_mma;  // token rows per MMA
 
   const int xb = n_mma * 128;        // token panel bytes per stage
   const int sfw_off = kA + xb;       // stage layout: W | X | W scales (2 KB) | X scales (16 B per row)
@@ -116,6 +126,10 @@ linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
         uint8_t* st = smem + i * kp.stage_bytes;
         tma_load_2d(st + kA, &tm_x, &full[i], kb * 128, 0, pol_x);
         tma_load_2d(st + sfx_off, &tm_xsf, &full[i], (kb >> 2) * 16, 0, pol_x);
+        if (kW) {
+          tma_load_2d(st + kA + nh * 128, &tm_x, &full[i], kb * 128, nh, pol_x);
+          tma_load_2d(st + sfx_off + nh * 16, &tm_xsf, &full[i], (kb >> 2) * 16, nh, pol_x);
+        }
       }
       for (int u = u_lo + pro, i = pro; u < u_hi; ++u, ++i) {
         const int s = i % S, n = i / S;
@@ -127,12 +141,16 @@ linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
         tma_load_2d(st + kA, &tm_x, &full[s], kb * 128, 0, pol_x);
         tma_load_2d(st + sfw_off, &tm_wsf, &full[s], (kb >> 2) * 16, tile * 128, pol_w);
         tma_load_2d(st + sfx_off, &tm_xsf, &full[s], (kb >> 2) * 16, 0, pol_x);
+        if (kW) {
+          tma_load_2d(st + kA + nh * 128, &tm_x, &full[s], kb * 128, nh, pol_x);
+          tma_load_2d(st + sfx_off + nh * 16, &tm_xsf, &full[s], (kb >> 2) * 16, nh, pol_x);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       griddep_wait();
-      const uint32_t idesc = idesc_mxf8(128, (uint32_t)n_mma);
+      const uint32_t idesc = idesc_mxf8(128, (uint32_t)nh);
       int seg = 0;
       for (int u = u_lo, i = 0; u < u_hi; ++seg) {
         const int tile = u / P.kblocks;
@@ -155,6 +173,11 @@ linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
             const uint64_t db = sdesc_sw128(b_base + kk * 32, 0, 1024);
             const uint32_t sel = (uint32_t)kk << 30;
             mma_mxf8(d, da, db, idesc | idesc_sf_ids(kk, kk), sf | sel, (sf + 4) | sel, (first && kk == 0) ? 0u : 1u);
+            if (kW) {  // tokens [N/2, N): the panel's second half, accumulator columns N/2.., scale columns 12..
+              const uint64_t db2 = sdesc_sw128(b_base + nh * 128 + kk * 32, 0, 1024);
+              mma_mxf8(d + nh, da, db2, idesc | idesc_sf_ids(kk, kk), sf | sel, (sf + 12) | sel,
+                       (first && kk == 0) ? 0u : 1u);
+            }
           }
           mma_commit(&empty[s]);
         }
@@ -178,12 +201,19 @@ linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
       uint32_t wv[4], xv[8];
 #pragma unroll
       for (int j = 0; j < 4; ++j) wv[j] = gw[(32 * j + lane) * 4];
+      const int nxh = kW ? nx / 2 : nx;  // token columns per MMA
 #pragma unroll
-      for (int j = 0; j < 8; ++j) xv[j] = j < nx ? gx[(32 * j + lane) * 4] : 0u;
+      for (int j = 0; j < 8; ++j) xv[j] = j < nxh ? gx[(32 * j + lane) * 4] : 0u;
       const uint32_t col = t_lane + kSfCol0 + (uint32_t)(s * kSfCols);
       tmem_st4(col, wv[0], wv[1], wv[2], wv[3]);
       tmem_st4(col + 4, xv[0], xv[1], xv[2], xv[3]);
-      if (nx > 4) tmem_st4(col + 8, xv[4], xv[5], xv[6], xv[7]);
+      if (nxh > 4) tmem_st4(col + 8, xv[4], xv[5], xv[6], xv[7]);
+      if (kW) {  // the second MMA's token rows [N/2, N) at columns 12..
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xv[j] = j < nxh ? gx[(nh + 32 * j + lane) * 4] : 0u;
+        tmem_st4(col + 12, xv[0], xv[1], xv[2], xv[3]);
+        if (nxh > 4) tmem_st4(col + 16, xv[4], xv[5], xv[6], xv[7]);
+      }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -233,6 +263,7 @@ linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
 // Plan of the MXFP8 linear: 128-row tiles, 128-element k-blocks.
 LinearPlan make_linear_mx_plan(int m_tok, int n_out, int k) {
   LinearPlan p = make_linear_plan(m_tok, n_out, k);
+  if (p.n_mma > 256) p.n_mma = ((m_tok + 63) / 64) * 64;  // two MMAs of N/2, each a multiple of 32 rows
   p.mtile = lin::kBM;
   p.tiles = (n_out + lin::kBM - 1) / lin::kBM;
   p.kblocks = k / 128;
@@ -242,7 +273,8 @@ LinearPlan make_linear_mx_plan(int m_tok, int n_out, int k) {
 cudaError_t linear_mx_launch(Ctx& ctx, const LinearPlan& p, const void* xq, const uint8_t* xsf, const void* wq,
                              const uint8_t* wsf, float* part, cudaStream_t stream) {
   using namespace linmx;
-  if (p.n_mma > 256 || p.k % 128) return cudaErrorInvalidValue;
+  const bool wide = p.n_mma > 256;
+  if (p.n_mma > 384 || (wide && p.n_mma % 64) || p.k % 128) return cudaErrorInvalidValue;
   CUtensorMap tw, tx, twsf, txsf;
   {
     const uint64_t dims[2] = {(uint64_t)(p.k / 32), (uint64_t)p.n_out};
@@ -255,7 +287,7 @@ cudaError_t linear_mx_launch(Ctx& ctx, const LinearPlan& p, const void* xq, cons
   {
     const uint64_t dims[2] = {(uint64_t)(p.k / 32), (uint64_t)p.m_tok};
     const uint64_t strides[1] = {(uint64_t)(p.k / 32)};
-    const uint32_t box[2] = {16, (uint32_t)p.n_mma};
+    const uint32_t box[2] = {16, (uint32_t)(wide ? p.n_mma / 2 : p.n_mma)};
     if (!encode_tma(ctx, &txsf, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(xsf), dims, strides, box,
                     CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
@@ -271,7 +303,7 @@ cudaError_t linear_mx_launch(Ctx& ctx, const LinearPlan& p, const void* xq, cons
   {
     const uint64_t dims[2] = {(uint64_t)p.k, (uint64_t)p.m_tok};
     const uint64_t strides[1] = {(uint64_t)p.k};
-    const uint32_t box[2] = {128, (uint32_t)p.n_mma};
+    const uint32_t box[2] = {128, (uint32_t)(wide ? p.n_mma / 2 : p.n_mma)};
     if (!encode_tma(ctx, &tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(xq), dims, strides, box,
                     CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
@@ -284,11 +316,14 @@ cudaError_t linear_mx_launch(Ctx& ctx, const LinearPlan& p, const void* xq, cons
   kp.k_words = p.k / 128;
   kp.stage_bytes = (int)align_up((size_t)kA + p.n_mma * 128 + 128 * 16 + p.n_mma * 16, 1024);
   kp.stages = (200 * 1024) / kp.stage_bytes;
-  if (kp.stages > 10) kp.stages = 10;
+  if (kp.stages > (wide ? 8 : 10)) kp.stages = wide ? 8 : 10;
   const size_t smem = (size_t)kp.stages * kp.stage_bytes + 1024 + 512;
   const int grid = linear_grid(ctx, p);
-  if (const cudaError_t e = ensure_smem(linear_mx_kernel, smem); e != cudaSuccess) return e;
-  return launch_k(ctx.pdl, linear_mx_kernel, dim3(grid), dim3(kThreads), smem, stream, tw, tx, twsf, txsf, kp);
+  auto go = [&](auto kernel) -> cudaError_t {
+    if (const cudaError_t e = ensure_smem(kernel, smem); e != cudaSuccess) return e;
+    return launch_k(ctx.pdl, kernel, dim3(grid), dim3(kThreads), smem, stream, tw, tx, twsf, txsf, kp);
+  };
+  return wide ? go(linear_mx_kernel<true>) : go(linear_mx_kernel<false>);
 }
 
 }  // namespace afdk

@@ -28,6 +28,9 @@ def dequant_mx(q, sf):
     (200, 384, 1024),   # single-buffered accumulator (N = 208)
     (256, 7168, 2048),  # the N = 256 limit
     (1, 48, 7168),      # router-like: one token, n < 128
+    (320, 7168, 16384), # o_proj at an AFD micro-batch: two N=160 MMAs per k-block
+    (384, 2560, 7168),  # the 384-token limit
+    (300, 1000, 512),   # ragged above 256 (N rounded to 320)
 ])
 def test_linear_mx_vs_torch(ctx, m, n, k):
     import torch
@@ -66,10 +69,10 @@ def test_linear_mx_rejects_bad_shapes(ctx):
     from paper_2507_19427_b200.afdk import AfdkError
 
     dev = torch.device("cuda")
-    xq = torch.zeros(300, 256, dtype=torch.uint8, device=dev)
-    xsf = torch.full((300, 8), 127, dtype=torch.uint8, device=dev)
+    xq = torch.zeros(400, 256, dtype=torch.uint8, device=dev)
+    xsf = torch.full((400, 8), 127, dtype=torch.uint8, device=dev)
     wq = torch.zeros(128, 256, dtype=torch.uint8, device=dev)
     wsf = torch.full((128, 8), 127, dtype=torch.uint8, device=dev)
-    out = torch.empty(300, 128, device=dev)
+    out = torch.empty(400, 128, device=dev)
     with pytest.raises(AfdkError):
-        ctx.linear_mx(xq, xsf, wq, wsf, out)  # m > 256
+        ctx.linear_mx(xq, xsf, wq, wsf, out)  # m > 384

@@ -155,15 +155,15 @@ def test_mfa_layer_wide_batch(ctx, kv, batch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kv", ["bf16", "e4m3"])
-def test_mfa_layer_mx_oproj(ctx, kv):
+@pytest.mark.parametrize("kv,batch", [("bf16", 64), ("e4m3", 64), ("e4m3", 320)])
+def test_mfa_layer_mx_oproj(ctx, kv, batch):
     """o_proj as an MXFP8 GEMM (afdk_mfa_weights.w_o_mx / w_o_sf, afdk_linear_mx):
     the oracle quantises the attention output with the same MX rule (o_mx) and
     multiplies by the dequantised MX weights; bars as the bf16 / e4m3-KV layer."""
     import torch
 
-    rng = np.random.default_rng(91)
-    seq_lens = rng.integers(1, 700, size=64).tolist()
+    rng = np.random.default_rng(91 + batch)
+    seq_lens = rng.integers(1, 700, size=batch).tolist()
     x, w, kc, vc, bt, sl = mg.layer_inputs(STEP3, seq_lens, 17)
     dev = torch.device("cuda:0")
     bf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(dev)
@@ -199,7 +199,7 @@ def test_mfa_layer_mx_oproj(ctx, kv):
     e_norm = rel_err(h_norm.float().cpu().numpy(), r_norm)
     try:
         from tests.helpers import record
-        record(f"mfa_layer_mx_oproj_{kv}", h_res=e_res, h_norm=e_norm)
+        record(f"mfa_layer_mx_oproj_{kv}_B{batch}", h_res=e_res, h_norm=e_norm)
     except Exception:  # noqa: BLE001
         pass
     assert e_res <= bar, e_res

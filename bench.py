@@ -238,6 +238,19 @@ def run_fp8_kv(ctx, torch, dev, s, batch, ctx_len, steps):
         mx_ms = timed(layer_mx)
         mx = {"layer_ms": mx_ms, "tokens_per_s": batch / (mx_ms * 1e-3),
               "note": "o_proj weights MXFP8 (e4m3 + UE8M0 per 32), attention output MX-quantised on the way in"}
+        wq = s["w"]["q_up"]
+        q_mx = torch.empty(wq.shape, dtype=torch.uint8, device=dev)
+        q_sf = torch.empty(wq.shape[0], wq.shape[1] // 32, dtype=torch.uint8, device=dev)
+        ctx.quant_mx(wq, q_mx, q_sf)
+        w_mx2 = dict(w_mx, q_up_mx=q_mx, q_up_sf=q_sf)
+
+        def layer_mx2(i):
+            k, v = kv8[i % N_ROT]
+            ctx.mfa_layer(w_mx2, s["x"], k, v, s["block_table"], s["seq_lens"], s["h_res"], s["h_norm"], stream=sp,
+                          kv_scales=(ks, vs))
+        mx2_ms = timed(layer_mx2)
+        mx["with_q_up_mx"] = {"layer_ms": mx2_ms, "tokens_per_s": batch / (mx2_ms * 1e-3),
+                              "note": "o_proj and q_up weights MXFP8 (the q latent MX-quantised on the way in)"}
     hbm_peak = peaks()[0]
     kv = kv_bytes(batch, ctx_len) // 2
     core_bytes = kv + 2 * batch * H * D * 2
@@ -528,9 +541,10 @@ def afd_runs(world):
     # larger micro-batches toward the SLA edge (the FFN stage grows slowly with T at decode)
     runs += [(base, "mx", T, "moe", "e4m3", "nvls") for T in (320, 352, 368, 384)]
     runs.append((bal, "mx", 512, "dense", "bf16", "push"))  # dense layer: FFN tier tensor-parallel over slices
-    runs = [r + (False,) for r in runs]
-    # o_proj as an MXFP8 GEMM on the attention GPUs (the paper's FP8 attention GEMMs)
-    runs += [(base, "mx", T, "moe", "e4m3", "nvls", True) for T in (352, 368, 384)]
+    runs = [r + (0,) for r in runs]
+    # o_proj as an MXFP8 GEMM on the attention GPUs (the paper's FP8 attention
+    # GEMMs); mode 2 (o_proj + q_up) measured slower here (profiles/r02_experiments.md)
+    runs += [(base, "mx", T, "moe", "e4m3", "nvls", 1) for T in (352, 368, 384)]
     return runs
 
 
@@ -560,7 +574,7 @@ def stages_from_traces(traces, n_micro):
 
 
 def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt="fp8", plan=None, kind="moe",
-                     kv="bf16", f2a="push", o_mx=False):
+                     kv="bf16", f2a="push", o_mx=0):
     """Real pipeline on all ranks through the C++ AFD runtime: nA attention
     GPUs + nF FFN GPUs, 2 ping-pong micro-batches, 2 layers per step (distinct
     KV caches), copy-engine NVLink.  One more traced step gives the measured
@@ -571,7 +585,7 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
 
     na, nf = plan if plan else afd_roles(world)
     cfg = AfdConfig(n_attn=na, n_ffn=nf, T_mb=T_mb, n_micro=2, layers=2, ctx_len=CTX, ffn_format=fmt, layer_kind=kind,
-                    kv=kv, f2a=f2a, attn_o_mx=o_mx)
+                    kv=kv, f2a=f2a, attn_o_mx=o_mx >= 1, attn_qup_mx=o_mx >= 2)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()
@@ -620,7 +634,8 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
                           pipeline_stages=cfg.n_micro, n_model_layers=N_LAYERS)
     tpot = N_LAYERS * period * 1e-3
     res = {"plan": f"{na}A{nf}F", "layer": kind, "ffn_format": fmt, "kv": kv, "f2a": f2a,
-           "attn_o_proj": "mxfp8" if o_mx else "bf16", "T_mb": cfg.T_mb,
+           "attn_o_proj": "mxfp8" if o_mx else "bf16", "attn_q_up": "mxfp8" if o_mx >= 2 else "bf16",
+           "T_mb": cfg.T_mb,
            "n_micro": cfg.n_micro, "ctx": cfg.ctx_len,
            "layer_period_ms": period, "tokens_per_s_per_layer": tokens / (period * 1e-3),
            "tokens_per_s_per_gpu_per_layer": tokens / (period * 1e-3) / world,
@@ -637,7 +652,7 @@ def run_afd_measured(torch, dist, dev, world, rank, local, steps, T_mb=192, fmt=
     tdir = os.environ.get("AFDK_TRACE_DIR")
     if tdir and rank == 0:
         os.makedirs(tdir, exist_ok=True)
-        name = f"afd_{res['plan']}_{fmt}_{kind}_{kv}_{f2a}{'_omx' if o_mx else ''}_T{T_mb}"
+        name = f"afd_{res['plan']}_{fmt}_{kind}_{kv}_{f2a}{['', '_omx', '_omxq'][int(o_mx)]}_T{T_mb}"
         with open(os.path.join(tdir, name + ".csv"), "w") as f:
             for q, csv in enumerate(traces):
                 body = csv.strip().splitlines()
@@ -1031,6 +1046,7 @@ def main():
                     except Exception as e:  # e.g. no NVLS on this system: reported, the sweep goes on
                         runs.append({"plan": f"{plan[0]}A{plan[1]}F", "ffn_format": f, "T_mb": T, "layer": kind,
                                      "kv": kv, "f2a": f2a, "attn_o_proj": "mxfp8" if o_mx else "bf16",
+                                     "attn_q_up": "mxfp8" if o_mx >= 2 else "bf16",
                                      "error": f"{type(e).__name__}: {e}"})
                 runs_ok = [x for x in runs if "error" not in x]
                 moe_runs = [x for x in runs_ok if x["layer"] == "moe"]

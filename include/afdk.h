@@ -130,7 +130,8 @@ afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, 
  * PAPER.md:774,781): xq e4m3 [m, k] + xsf UE8M0 [m, k/32], wq e4m3 [n, k] +
  * wsf UE8M0 [n, k/32] (afdk_quant_mx's format), y = dequant(xq) .
  * dequant(wq)^T with fp32 accumulation on the block-scaled tensor-core MMA.
- * 1 <= m <= 384 (above 256 tokens: two N/2 MMAs per k-block), k % 128 == 0. */
+ * 1 <= m <= 384 (above 256 tokens: two N/2 MMAs per k-block), k % 512 == 0
+ * (the k/32-byte scale rows are TMA-loaded). */
 afdk_status afdk_linear_mx(afdk_ctx* ctx, const void* xq, const uint8_t* xsf, const void* wq, const uint8_t* wsf,
                            void* out, int m, int n, int k, int out_fp32, afdk_stream stream);
 
@@ -153,6 +154,12 @@ typedef struct afdk_mfa_weights {
    * the attention output is MXFP8-quantised on the way in.  batch <= 384. */
   const void* w_o_mx;
   const uint8_t* w_o_sf;
+  /* optional (NULL = bf16 w_q_up): q_up as an MXFP8 GEMM — e4m3
+   * [n_heads*head_dim, q_lora] + UE8M0 [n_heads*head_dim, q_lora/32]; the
+   * q-RMSNorm output is MXFP8-quantised on the way in.  batch <= 384,
+   * q_lora % 512 == 0 (the scale rows are TMA-loaded: 16-byte multiples). */
+  const void* w_q_up_mx;
+  const uint8_t* w_q_up_sf;
 } afdk_mfa_weights;
 
 typedef struct afdk_mfa_layer_args {

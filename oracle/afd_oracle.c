@@ -193,6 +193,14 @@ void orc_mfa_layer(const orc_mfa_dims* d, int B, const float* x,
   for (int b = 0; b < B; ++b)
     memcpy(qa_in + (size_t)b * QL, qkv + (size_t)b * NQKV, sizeof(float) * QL);
   orc_rmsnorm(qa_in, w_q_norm, B, QL, d->rms_eps, round_bf16, qa);    /* inter_norm      */
+  if (d->qup_mx) { /* MXFP8 q_up input: e4m3 x 2^e per 32 q-latent elements */
+    uint8_t* q8 = (uint8_t*)malloc((size_t)B * QL);
+    uint8_t* sf = (uint8_t*)malloc((size_t)B * (QL / 32));
+    orc_quant_mx(qa, B, QL, q8, sf);
+    for (size_t i = 0; i < (size_t)B * QL; ++i) qa[i] = orc_e4m3_to_f32(q8[i]) * orc_mx_scale(sf[i / 32]);
+    free(q8);
+    free(sf);
+  }
   orc_linear(qa, w_q_up, B, NQ, QL, round_bf16, q);                   /* wq              */
   for (int b = 0; b < B; ++b) {
     const int pos = seq_lens[b] - 1;

@@ -84,6 +84,8 @@ typedef struct {
    * (orc_quant_mx) and dequantised before o_proj, as afdk_mfa_layer with
    * MXFP8 o_proj weights does (the caller passes the dequantised weights). */
   int o_mx;
+  /* qup_mx != 0: likewise for the q_up input (the q-RMSNorm output). */
+  int qup_mx;
 } orc_mfa_dims;
 
 /* x          [B, hidden]              layer input (residual stream)

@@ -175,7 +175,8 @@ def mfa_decode_attention_fp8(q, kq, vq, k_scale, v_scale, block_table, seq_lens,
 class MfaDims(ctypes.Structure):
     _fields_ = [("hidden", c_int), ("q_lora", c_int), ("n_heads", c_int), ("head_dim", c_int),
                 ("page", c_int), ("rms_eps", c_float), ("rope_theta", c_float),
-                ("softmax_scale", c_float), ("kv_k_scale", c_float), ("kv_v_scale", c_float), ("o_mx", c_int)]
+                ("softmax_scale", c_float), ("kv_k_scale", c_float), ("kv_v_scale", c_float), ("o_mx", c_int),
+                ("qup_mx", c_int)]
 
 
 def mfa_layer(dims: dict, x, w, k_cache, v_cache, block_table, seq_lens, round_bf16=True):
@@ -184,7 +185,8 @@ def mfa_layer(dims: dict, x, w, k_cache, v_cache, block_table, seq_lens, round_b
     d = MfaDims(dims["hidden"], dims["q_lora"], dims["n_heads"], dims["head_dim"], dims["page"],
                 dims.get("rms_eps", 1e-5), dims.get("rope_theta", 5e5),
                 dims.get("softmax_scale", dims["head_dim"] ** -0.5),
-                dims.get("kv_k_scale", 0.0), dims.get("kv_v_scale", 0.0), int(dims.get("o_mx", 0)))
+                dims.get("kv_k_scale", 0.0), dims.get("kv_v_scale", 0.0), int(dims.get("o_mx", 0)),
+                int(dims.get("qup_mx", 0)))
     x = _f32(x)
     B = x.shape[0]
     ws = {k: _f32(v) for k, v in w.items()}

@@ -61,6 +61,7 @@ class AfdConfig:
                               # T_mb runs the attention side in chunks and ships ONE payload
     kv: str = "bf16"          # attention KV cache: "bf16" or "e4m3" (per-tensor scales)
     attn_o_mx: bool = False   # o_proj as an MXFP8 GEMM (afdk_mfa_weights.w_o_mx / w_o_sf; T_mb <= 384)
+    attn_qup_mx: bool = False  # q_up likewise (afdk_mfa_weights.w_q_up_mx / w_q_up_sf; T_mb <= 384)
 
     def __post_init__(self):
         # validated identically on every rank before any buffer exchange
@@ -282,11 +283,17 @@ class AfdRank:
                 w["o_mx"] = t.empty(w["o"].shape, dtype=t.uint8, device=dev)
                 w["o_sf"] = t.empty(w["o"].shape[0], w["o"].shape[1] // 32, dtype=t.uint8, device=dev)
                 self.ctx.quant_mx(w["o"], w["o_mx"], w["o_sf"])
+            if c.attn_qup_mx:  # MXFP8 q_up weights
+                w["q_up_mx"] = t.empty(w["q_up"].shape, dtype=t.uint8, device=dev)
+                w["q_up_sf"] = t.empty(w["q_up"].shape[0], w["q_up"].shape[1] // 32, dtype=t.uint8, device=dev)
+                self.ctx.quant_mx(w["q_up"], w["q_up_mx"], w["q_up_sf"])
             self.c_w = _k.MfaWeights(c.hidden, c.q_lora, c.n_heads, c.head_dim, _k.ptr(w["in_norm"]), _k.ptr(w["qkv"]),
                                      _k.ptr(w["q_norm"]), _k.ptr(w["q_up"]), _k.ptr(w["o"]), _k.ptr(w["post_norm"]),
                                      1e-5, 5e5, c.head_dim ** -0.5,
                                      _k.ptr(w["o_mx"]) if c.attn_o_mx else None,
-                                     _k.ptr(w["o_sf"]) if c.attn_o_mx else None)
+                                     _k.ptr(w["o_sf"]) if c.attn_o_mx else None,
+                                     _k.ptr(w["q_up_mx"]) if c.attn_qup_mx else None,
+                                     _k.ptr(w["q_up_sf"]) if c.attn_qup_mx else None)
             self.c_mbs = []
             for layer in range(c.layers):
                 arr = (AfdAttnMb * c.n_micro)()

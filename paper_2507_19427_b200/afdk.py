@@ -48,6 +48,7 @@ class MfaWeights(Structure):
         ("w_o", c_void_p), ("post_norm", c_void_p),
         ("rms_eps", c_float), ("rope_theta", c_float), ("softmax_scale", c_float),
         ("w_o_mx", c_void_p), ("w_o_sf", c_void_p),  # optional MXFP8 o_proj (NULL: bf16 w_o)
+        ("w_q_up_mx", c_void_p), ("w_q_up_sf", c_void_p),  # optional MXFP8 q_up (NULL: bf16 w_q_up)
     ]
 
 
@@ -386,11 +387,13 @@ class Context:
         hidden = x.shape[1]
         q_lora = w["q_norm"].shape[0]
         head_dim = k_cache.shape[2]
-        n_heads = w["q_up"].shape[0] // head_dim
+        n_heads = (w["q_up"] if "q_up" in w else w["q_up_mx"]).shape[0] // head_dim
         scale = head_dim ** -0.5 if softmax_scale is None else softmax_scale
         mw = MfaWeights(hidden, q_lora, n_heads, head_dim, ptr(w["in_norm"]), ptr(w["qkv"]), ptr(w["q_norm"]),
-                        ptr(w["q_up"]), ptr(w["o"]) if "o" in w else None, ptr(w["post_norm"]), rms_eps, rope_theta,
-                        scale, ptr(w["o_mx"]) if "o_mx" in w else None, ptr(w["o_sf"]) if "o_sf" in w else None)
+                        ptr(w["q_up"]) if "q_up" in w else None, ptr(w["o"]) if "o" in w else None, ptr(w["post_norm"]),
+                        rms_eps, rope_theta, scale, ptr(w["o_mx"]) if "o_mx" in w else None,
+                        ptr(w["o_sf"]) if "o_sf" in w else None, ptr(w["q_up_mx"]) if "q_up_mx" in w else None,
+                        ptr(w["q_up_sf"]) if "q_up_sf" in w else None)
         a = MfaLayerArgs(x.shape[0] // mtp, ptr(x), ptr(k_cache), ptr(v_cache), k_cache.shape[0], k_cache.shape[1],
                          ptr(block_table), block_table.shape[1], ptr(seq_lens), ptr(h_res), ptr(h_norm))
         if mtp != 1:  # x / h_res / h_norm rows are (request, token)

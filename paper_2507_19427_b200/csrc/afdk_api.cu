@@ -246,7 +246,10 @@ afdk_status afdk_linear_mx(afdk_ctx* ctx, const void* xq, const uint8_t* xsf, co
                            void* out, int m, int n, int k, int out_fp32, afdk_stream stream) {
   if (!ctx || !xq || !xsf || !wq || !wsf || !out) { set_error("afdk_linear_mx: NULL argument"); return AFDK_ERR_INVALID; }
   if (m < 1 || m > 384) { set_error("afdk_linear_mx: m must be in [1, 384]"); return AFDK_ERR_INVALID; }
-  if (n < 1 || k < 128 || k % 128) { set_error("afdk_linear_mx: k must be a positive multiple of 128"); return AFDK_ERR_INVALID; }
+  if (n < 1 || k < 512 || k % 512) {  // scale rows (k/32 bytes) are TMA-loaded: 16-byte multiples
+    set_error("afdk_linear_mx: k must be a positive multiple of 512");
+    return AFDK_ERR_INVALID;
+  }
   afdk::Ctx& c = ctx->c;
   afdk::DeviceGuard device_guard(c.device);
   const afdk::LinearPlan p = afdk::make_linear_mx_plan(m, n, k);
@@ -279,7 +282,8 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
     return AFDK_ERR_INVALID;
   }
   if (!a->x || !a->k_cache || !a->v_cache || !a->block_table || !a->seq_lens || !a->h_res || !a->h_norm ||
-      !w->in_norm || !w->w_qkv || !w->q_norm || !w->w_q_up || (!w->w_o && !w->w_o_mx) || !w->post_norm) {
+      !w->in_norm || !w->w_qkv || !w->q_norm || (!w->w_q_up && !w->w_q_up_mx) || (!w->w_o && !w->w_o_mx) ||
+      !w->post_norm) {
     set_error("afdk_mfa_layer: NULL tensor pointer");
     return AFDK_ERR_INVALID;
   }
@@ -289,9 +293,14 @@ static afdk_status mfa_layer_entry(afdk_ctx* ctx, const afdk_mfa_weights* w, con
                        w->in_norm, w->w_qkv, w->q_norm, w->w_q_up, w->w_o, w->post_norm,
                        w->rms_eps, w->rope_theta, w->softmax_scale, a->x, a->k_cache, a->v_cache,
                        a->num_pages, a->block_table, a->max_pages, a->seq_lens, a->h_res, a->h_norm,
-                       k_scale, v_scale, mtp, w->w_o_mx, w->w_o_sf};
+                       k_scale, v_scale, mtp, w->w_o_mx, w->w_o_sf, w->w_q_up_mx, w->w_q_up_sf};
   if ((w->w_o_mx != nullptr) != (w->w_o_sf != nullptr) || (w->w_o_mx && (a->batch * mtp > 384 || mtp > 1))) {
     set_error("afdk_mfa_layer: MXFP8 o_proj needs both w_o_mx and w_o_sf, mtp 1 and batch <= 384");
+    return AFDK_ERR_INVALID;
+  }
+  if ((w->w_q_up_mx != nullptr) != (w->w_q_up_sf != nullptr) ||
+      (w->w_q_up_mx && (a->batch * mtp > 384 || mtp > 1 || w->q_lora % 512 != 0))) {
+    set_error("afdk_mfa_layer: MXFP8 q_up needs both w_q_up_mx and w_q_up_sf, mtp 1, batch <= 384 and q_lora % 512 == 0 (16-byte scale rows)");
     return AFDK_ERR_INVALID;
   }
   void* ws = afdk::workspace(c, afdk::mfa_layer_workspace_bytes(m, c.num_sms));

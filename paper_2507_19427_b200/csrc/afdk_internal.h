@@ -186,6 +186,8 @@ struct MfaLayerArgs {
   int mtp = 1;  // query tokens per request: rows are (request, token), batch*mtp of them
   const void* w_o_mx = nullptr;     // optional MXFP8 o_proj weights (e4m3 [hidden, NQ]) ...
   const uint8_t* w_o_sf = nullptr;  // ... and their UE8M0 scales [hidden, NQ/32]
+  const void* w_qup_mx = nullptr;     // optional MXFP8 q_up weights (e4m3 [NQ, q_lora]) ...
+  const uint8_t* w_qup_sf = nullptr;  // ... and their UE8M0 scales [NQ, q_lora/32]
 };
 const double* rope_inv_freq(Ctx& ctx, int head_dim, float theta);
 size_t mfa_layer_workspace_bytes(const MfaLayerArgs& a, int num_sms);

@@ -412,12 +412,14 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
             static_cast<const __nv_bfloat16*>(a.w_q_norm), qa, static_cast<__nv_bfloat16*>(a.k_cache),
             static_cast<__nv_bfloat16*>(a.v_cache), a.block_table, a.seq_lens, inv_freq, a.k_scale, a.v_scale,
             a.mtp, nullptr};
-  const LinearPlan p2 = make_linear_plan(B, NQ, QL);
+  const LinearPlan p2 = a.w_qup_mx ? make_linear_mx_plan(B, NQ, QL) : make_linear_plan(B, NQ, QL);
   // fused RoPE(q) epilogue: one launch less and equal time at decode batches
   // (B=64: 124.9 vs 124.2 us/layer); its 4 epilogue warps serialise the
   // rotation of every token, so from 128 token rows the separate row
   // epilogue is faster (B=256: 308 vs 302 us, e4m3 KV 240 vs 230 us)
-  const bool fused_rope = linear_rope_fusable(ctx, p2, D) && B <= 64 && !std::getenv("AFDK_NO_ROPE_FUSION");
+  const bool qup_mx = a.w_qup_mx != nullptr;
+  const bool fused_rope =
+      !qup_mx && linear_rope_fusable(ctx, p2, D) && B <= 64 && !std::getenv("AFDK_NO_ROPE_FUSION");
   if (fused_rope) qe.rope_cs = rope_cs;
   if ((e = row_launch(qkv_epilogue_kernel<2>, qkv_epilogue_kernel<4>, p1, (const float*)part, linear_grid(ctx, p1),
                       qe)) != cudaSuccess)
@@ -427,7 +429,15 @@ cudaError_t mfa_layer_launch(Ctx& ctx, const MfaLayerArgs& a, void* ws_base, cud
   if (fused_rope) {
     if ((e = linear_bf16_rope_launch(ctx, p2, qa, a.w_q_up, q, rope_cs, D, stream)) != cudaSuccess) return e;
   } else {
-    if ((e = linear_bf16_launch(ctx, p2, qa, a.w_q_up, part, stream)) != cudaSuccess) return e;
+    if (qup_mx) {  // MXFP8 q_up: the q latent MX-quantised into the (not yet written) attention buffer
+      uint8_t* q8 = reinterpret_cast<uint8_t*>(attn);
+      uint8_t* qsf = q8 + (size_t)B * QL;
+      moe::QuantMxArgs qm{qa, B, QL, q8, qsf};
+      if ((e = quant_mx_launch(qm, stream, ctx.pdl)) != cudaSuccess) return e;
+      if ((e = linear_mx_launch(ctx, p2, q8, qsf, a.w_qup_mx, a.w_qup_sf, part, stream)) != cudaSuccess) return e;
+    } else if ((e = linear_bf16_launch(ctx, p2, qa, a.w_q_up, part, stream)) != cudaSuccess) {
+      return e;
+    }
     if ((e = launch_k(ctx.pdl, qup_epilogue_kernel, dim3(B, (NQ / 8 + 255) / 256), dim3(256), 0, stream, p2,
                       (const float*)part, linear_grid(ctx, p2), NQ, D, a.seq_lens, a.mtp, inv_freq, q)) !=
         cudaSuccess)

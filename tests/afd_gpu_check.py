@@ -45,7 +45,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--out", default=None)
     ap.add_argument("--layers", type=int, default=LAYERS)
-    ap.add_argument("--o-mx", type=int, default=0, help="o_proj as an MXFP8 GEMM on the attention ranks")
+    ap.add_argument("--o-mx", type=int, default=0,
+                    help="1: o_proj, 2: o_proj and q_up as MXFP8 GEMMs on the attention ranks")
     ap.add_argument("--full", type=int, default=0,
                     help="Step-3 dims (hidden 7168, q_lora 2048, 48 experts top-3, inter 5120, 4K context): the "
                          "benchmarked AFD configuration")
@@ -65,11 +66,11 @@ def main():
     dist.init_process_group("gloo" if shared_gpu else "nccl", **({} if shared_gpu else {"device_id": dev}))
     nf = world - a.n_attn
     dims = dict(hidden=7168, q_lora=2048, ctx_len=4096, n_experts=48, top_k=3, inter=5120, dense_inter=18432) \
-        if a.full else dict(hidden=1024, q_lora=256, ctx_len=300, n_experts=8 if nf in (1, 2, 4, 8) else 24,
+        if a.full else dict(hidden=1024, q_lora=512 if a.o_mx >= 2 else 256, ctx_len=300, n_experts=8 if nf in (1, 2, 4, 8) else 24,
                             top_k=2, inter=512, dense_inter=2048 * 6)
     cfg = AfdConfig(n_attn=a.n_attn, n_ffn=nf, T_mb=a.T_mb, n_micro=2, layers=a.layers, seed=3,
                     ffn_format=a.fmt, f2a=a.f2a, kv=a.kv, layer_kind=a.layer, attn_chunk=a.attn_chunk,
-                    attn_o_mx=bool(a.o_mx), **dims)
+                    attn_o_mx=a.o_mx >= 1, attn_qup_mx=a.o_mx >= 2, **dims)
     ctxs = [Context(local) for _ in range(cfg.n_micro)]
     r = AfdRank(ctxs, cfg, rank, torch, dist, dev)
     r.setup()

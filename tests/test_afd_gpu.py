@@ -28,6 +28,7 @@ CASES = [
     (2, 1, ["--fmt", "mx", "--f2a", "nvls"]),       # NVLS return: one GPU per rank
     (3, 1, ["--fmt", "bf16", "--f2a", "nvls"]),
     (2, 1, ["--fmt", "mx", "--f2a", "push", "--kv", "e4m3", "--o-mx", "1"]),  # MXFP8 o_proj on the attention rank
+    (2, 1, ["--fmt", "mx", "--f2a", "nvls", "--kv", "e4m3", "--o-mx", "2"]),  # MXFP8 o_proj + q_up
     # the benchmarked AFD point at Step-3 dims: 1A3F, MXFP8, e4m3 KV, NVLS, 320 requests per micro-batch
     (4, 1, ["--fmt", "mx", "--f2a", "nvls", "--kv", "e4m3", "--T-mb", "320", "--steps", "2", "--layers", "1",
             "--full", "1"]),

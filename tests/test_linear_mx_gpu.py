@@ -76,3 +76,5 @@ def test_linear_mx_rejects_bad_shapes(ctx):
     out = torch.empty(400, 128, device=dev)
     with pytest.raises(AfdkError):
         ctx.linear_mx(xq, xsf, wq, wsf, out)  # m > 384
+    with pytest.raises(AfdkError):  # k % 512 != 0: the 8-byte scale rows cannot be TMA-loaded
+        ctx.linear_mx(xq[:64], xsf[:64], wq, wsf, out[:64])

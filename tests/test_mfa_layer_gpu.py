@@ -204,3 +204,63 @@ def test_mfa_layer_mx_oproj(ctx, kv, batch):
         pass
     assert e_res <= bar, e_res
     assert e_norm <= bar, e_norm
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kv,batch,o_mx", [("bf16", 64, False), ("e4m3", 64, True), ("e4m3", 352, True)])
+def test_mfa_layer_mx_qup(ctx, kv, batch, o_mx):
+    """q_up as an MXFP8 GEMM (afdk_mfa_weights.w_q_up_mx / w_q_up_sf): the
+    oracle MX-quantises the q-RMSNorm output (qup_mx) and multiplies by the
+    dequantised MX weights; alone and together with the MXFP8 o_proj (the AFD
+    attention ranks' configuration).  Bars as the bf16 / e4m3-KV layer."""
+    import torch
+
+    rng = np.random.default_rng(7 + batch)
+    seq_lens = rng.integers(1, 700, size=batch).tolist()
+    x, w, kc, vc, bt, sl = mg.layer_inputs(STEP3, seq_lens, 23)
+    dev = torch.device("cuda:0")
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(dev)
+    wd = {k: bf(v) for k, v in w.items()}
+    w_or = dict(w)
+    dims = dict(STEP3, qup_mx=1, o_mx=int(o_mx))
+
+    def mx(name):
+        n, k = wd[name].shape
+        q8 = torch.empty(n, k, dtype=torch.uint8, device=dev)
+        sf = torch.empty(n, k // 32, dtype=torch.uint8, device=dev)
+        ctx.quant_mx(wd[name], q8, sf)
+        w_or[name] = (orc.e4m3_to_f32(q8.cpu().numpy()) *
+                      np.exp2(sf.cpu().numpy().astype(np.float32) - 127.0).repeat(32, axis=1)).astype(np.float32)
+        return q8, sf
+
+    wd["q_up_mx"], wd["q_up_sf"] = mx("q_up")
+    del wd["q_up"]  # the bf16 q_up must not be needed
+    if o_mx:
+        wd["o_mx"], wd["o_sf"] = mx("o")
+    xd = bf(x)
+    h_res, h_norm = torch.empty_like(xd), torch.empty_like(xd)
+    bt_d, sl_d = torch.from_numpy(bt).to(dev), torch.from_numpy(sl).to(dev)
+    if kv == "e4m3":
+        ks, vs = float(np.abs(kc).max()) / 448.0, float(np.abs(vc).max()) / 448.0
+        kq = (torch.from_numpy(kc) / ks).to(torch.float8_e4m3fn).view(torch.uint8)
+        vq = (torch.from_numpy(vc) / vs).to(torch.float8_e4m3fn).view(torch.uint8)
+        ctx.mfa_layer(wd, xd, kq.to(dev), vq.to(dev), bt_d, sl_d, h_res, h_norm, kv_scales=(ks, vs))
+        k1 = orc.e4m3_to_f32(kq.numpy()) * np.float32(ks)
+        v1 = orc.e4m3_to_f32(vq.numpy()) * np.float32(vs)
+        dims.update(kv_k_scale=ks, kv_v_scale=vs)
+        bar = 3e-2
+    else:
+        ctx.mfa_layer(wd, xd, bf(kc), bf(vc), bt_d, sl_d, h_res, h_norm)
+        k1, v1 = kc.copy(), vc.copy()
+        bar = 2e-2
+    torch.cuda.synchronize()
+    r_res, r_norm = orc.mfa_layer(dims, x, w_or, k1, v1, bt, sl)
+    e_res = rel_err(h_res.float().cpu().numpy(), r_res)
+    e_norm = rel_err(h_norm.float().cpu().numpy(), r_norm)
+    try:
+        from tests.helpers import record
+        record(f"mfa_layer_mx_qup_{kv}_B{batch}{'_omx' if o_mx else ''}", h_res=e_res, h_norm=e_norm)
+    except Exception:  # noqa: BLE001
+        pass
+    assert e_res <= bar, e_res
+    assert e_norm <= bar, e_norm

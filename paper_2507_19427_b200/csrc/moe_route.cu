@@ -48,11 +48,13 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const LinearPlan P, co
   sm100::griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;  // token within this chunk
-  if (row >= P.m_tok) return;
+  if (row >= P.n_out) return;  // tokens of this chunk (the GEMM's weight rows)
   const int tok = t_base + row;
   const int e0 = lane, e1 = lane + 32;
-  const float l0 = e0 < a.E ? tab.sum(P, part, row, e0) : -INFINITY;
-  const float l1 = e1 < a.E ? tab.sum(P, part, row, e1) : -INFINITY;
+  // the GEMM ran with the tokens on the weight side (P.m_tok = E experts,
+  // P.n_out = tokens): logit (token, e) is "row" e, "feature" token
+  const float l0 = e0 < a.E ? tab.sum(P, part, e0, row) : -INFINITY;
+  const float l1 = e1 < a.E ? tab.sum(P, part, e1, row) : -INFINITY;
   if (a.logits) {
     if (e0 < a.E) a.logits[(size_t)tok * a.E + e0] = l0;
     if (e1 < a.E) a.logits[(size_t)tok * a.E + e1] = l1;
@@ -343,16 +345,24 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
 
 }  // namespace moe
 
+// Router GEMM with the roles of linear.cu swapped: the token rows stream as
+// the 128-row M panels and the E <= 64 gate rows are the MMA's N, so the
+// tiles are token blocks (ceil(T/128) of them, spread over up to 15 CTAs
+// each) and the split partials are E columns wide.  With the gate rows as M
+// (one 128-row tile for all experts) the k-loop of all tokens ran on at most
+// 15 CTAs (kMaxSegs) in 256-token chunks: ~20-40 us at the AFD micro-batch.
+constexpr int kRouterChunk = 8192;  // tokens per GEMM (tiles <= kMaxTiles)
+
 size_t router_workspace_bytes(int H, int E, int num_sms) {
-  return linear_workspace_bytes(make_linear_plan(256, E, H), num_sms);
+  return linear_workspace_bytes(make_linear_plan(E, kRouterChunk, H), num_sms);
 }
 
 cudaError_t router_launch(Ctx& ctx, const moe::RouterArgs& a, void* ws, cudaStream_t stream) {
   float* part = static_cast<float*>(ws);
-  for (int c0 = 0; c0 < a.T; c0 += 256) {
-    const int m = min(256, a.T - c0);
-    const LinearPlan p = make_linear_plan(m, a.E, a.H);
-    cudaError_t e = linear_bf16_launch(ctx, p, a.h + (size_t)c0 * a.H, a.gate_w, part, stream);
+  for (int c0 = 0; c0 < a.T; c0 += kRouterChunk) {
+    const int m = min(kRouterChunk, a.T - c0);
+    const LinearPlan p = make_linear_plan(a.E, m, a.H);
+    cudaError_t e = linear_bf16_launch(ctx, p, a.gate_w, a.h + (size_t)c0 * a.H, part, stream);
     if (e == cudaSuccess)
       e = launch_k(ctx.pdl, moe::router_topk_kernel, dim3((m + 7) / 8), dim3(256), 0, stream, p, (const float*)part,
                    linear_grid(ctx, p), a, c0);

@@ -236,7 +236,8 @@ afdk_status afdk_linear(afdk_ctx* ctx, const void* x, const void* w, void* out, 
   float* part = static_cast<float*>(afdk::workspace(c, afdk::linear_workspace_bytes(p, c.num_sms)));
   if (!part) { set_error("afdk_linear: workspace allocation failed"); return AFDK_ERR_CUDA; }
   auto st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = afdk::linear_bf16_launch(c, p, x, w, part, st);
+  // w may be any caller matrix, possibly written by this library's previous kernel: no PDL weight prefill
+  cudaError_t e = afdk::linear_bf16_launch(c, p, x, w, part, st, /*w_dep=*/true);
   if (e == cudaSuccess) e = afdk::linear_store_launch(c, p, part, out, out_fp32 != 0, st);
   if (e != cudaSuccess) return cuda_fail("afdk_linear", e);
   return AFDK_OK;
@@ -256,7 +257,7 @@ afdk_status afdk_linear_mx(afdk_ctx* ctx, const void* xq, const uint8_t* xsf, co
   float* part = static_cast<float*>(afdk::workspace(c, afdk::linear_workspace_bytes(p, c.num_sms)));
   if (!part) { set_error("afdk_linear_mx: workspace allocation failed"); return AFDK_ERR_CUDA; }
   auto st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = afdk::linear_mx_launch(c, p, xq, xsf, wq, wsf, part, st);
+  cudaError_t e = afdk::linear_mx_launch(c, p, xq, xsf, wq, wsf, part, st, /*w_dep=*/true);  // caller weights
   if (e == cudaSuccess) e = afdk::linear_store_launch(c, p, part, out, out_fp32 != 0, st);
   if (e != cudaSuccess) return cuda_fail("afdk_linear_mx", e);
   return AFDK_OK;

@@ -160,12 +160,14 @@ bool linear_rope_fusable(const Ctx& ctx, const LinearPlan& p, int head_dim);
 cudaError_t linear_bf16_rope_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w,
                                     __nv_bfloat16* q_out, const float2* rope_cs, int head_dim,
                                     cudaStream_t stream);
+// w_dep: the weight operand is written by a predecessor kernel (no weight
+// prefetch before the PDL wait)
 cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
-                               cudaStream_t stream);
+                               cudaStream_t stream, bool w_dep = false);
 // MXFP8 linear (linear_mx.cu): 128-element k-blocks, the same partial layout
 LinearPlan make_linear_mx_plan(int m_tok, int n_out, int k);
 cudaError_t linear_mx_launch(Ctx& ctx, const LinearPlan& p, const void* xq, const uint8_t* xsf, const void* wq,
-                             const uint8_t* wsf, float* part, cudaStream_t stream);
+                             const uint8_t* wsf, float* part, cudaStream_t stream, bool w_dep = false);
 cudaError_t linear_store_launch(Ctx& ctx, const LinearPlan& p, const float* part, void* out, bool out_fp32,
                                 cudaStream_t stream);
 

@@ -50,6 +50,7 @@ struct KParams {
   __nv_bfloat16* q_out;   // [m_tok, n_out] bf16, rotated
   const float2* rope_cs;  // [m_tok, head_dim/2] (cos, sin) of each row's position
   int head_dim;
+  int w_dep;  // the weight operand is a predecessor's output (the router's token rows): no PDL prefill
 };
 
 __device__ __forceinline__ void unit_range(int c, int G, int U, int& lo, int& hi) {
@@ -119,12 +120,13 @@ linear_bf16_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_consta
       // weights never depend on the previous kernel: fill the first S stages'
       // weight panels before waiting for the predecessor (PDL), then the X panels
       const int pro = min(S, u_hi - u_lo);
+      if (kp.w_dep) griddep_wait();
       for (int i = 0; i < pro; ++i) {
         const int u = u_lo + i, tile = u / P.kblocks, kb = u % P.kblocks;
         mbar_expect_tx(&full[i], bytes);
         load_w(smem + i * kp.stage_bytes, &full[i], kb, tile);
       }
-      griddep_wait();
+      if (!kp.w_dep) griddep_wait();
       for (int i = 0; i < pro; ++i) {
         const int u = u_lo + i, kb = u % P.kblocks;
         load_x(smem + i * kp.stage_bytes + (kM2 ? 2 : 1) * kABytes, &full[i], kb);
@@ -325,7 +327,7 @@ size_t linear_workspace_bytes(const LinearPlan& p, int num_sms) {
 
 static cudaError_t linear_launch_impl(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
                                       __nv_bfloat16* q_out, const float2* rope_cs, int head_dim,
-                                      cudaStream_t stream) {
+                                      cudaStream_t stream, bool w_dep = false) {
   using namespace lin;
   const bool rope = q_out != nullptr;
   CUtensorMap tw, tx;
@@ -351,6 +353,7 @@ static cudaError_t linear_launch_impl(Ctx& ctx, const LinearPlan& p, const void*
   kp.q_out = q_out;
   kp.rope_cs = rope_cs;
   kp.head_dim = head_dim;
+  kp.w_dep = w_dep ? 1 : 0;
   const bool m2 = p.mtile == 256 && !rope;
   kp.stage_bytes = (m2 ? 2 : 1) * kABytes + p.n_mma * 128;
   const int xch_bytes = rope ? 2 * 2 * 32 * 33 * 4 : 0;  // x1/x2 exchange of the two warp pairs
@@ -369,8 +372,8 @@ static cudaError_t linear_launch_impl(Ctx& ctx, const LinearPlan& p, const void*
 }
 
 cudaError_t linear_bf16_launch(Ctx& ctx, const LinearPlan& p, const void* x, const void* w, float* part,
-                               cudaStream_t stream) {
-  return linear_launch_impl(ctx, p, x, w, part, nullptr, nullptr, 0, stream);
+                               cudaStream_t stream, bool w_dep) {
+  return linear_launch_impl(ctx, p, x, w, part, nullptr, nullptr, 0, stream, w_dep);
 }
 
 bool linear_rope_fusable(const Ctx& ctx, const LinearPlan& p, int head_dim) {

@@ -50,6 +50,7 @@ struct KParams {
   const uint8_t* x_sf;    // UE8M0 [m_tok, K/32]
   int k_words;            // K / 128: 32-bit scale words per row
   int stage_bytes, stages;
+  int w_dep;              // the weights are a predecessor's output: no PDL prefill
 };
 
 __device__ __forceinline__ void unit_range(int c, int G, int U, int& lo, int& hi) {
@@ -113,6 +114,7 @@ linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
       // weights (and their scales) never depend on the previous kernel: fill
       // the first stages' weight panels before waiting for the predecessor
       const int pro = min(S, u_hi - u_lo);
+      if (kp.w_dep) griddep_wait();
       for (int i = 0; i < pro; ++i) {
         const int u = u_lo + i, tile = u / P.kblocks, kb = u % P.kblocks;
         uint8_t* st = smem + i * kp.stage_bytes;
@@ -120,7 +122,7 @@ linear_mx_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant
         tma_load_2d(st, &tm_w, &full[i], kb * 128, tile * 128, pol_w);
         tma_load_2d(st + sfw_off, &tm_wsf, &full[i], (kb >> 2) * 16, tile * 128, pol_w);
       }
-      griddep_wait();
+      if (!kp.w_dep) griddep_wait();
       for (int i = 0; i < pro; ++i) {
         const int u = u_lo + i, kb = u % P.kblocks;
         uint8_t* st = smem + i * kp.stage_bytes;
@@ -271,7 +273,7 @@ LinearPlan make_linear_mx_plan(int m_tok, int n_out, int k) {
 }
 
 cudaError_t linear_mx_launch(Ctx& ctx, const LinearPlan& p, const void* xq, const uint8_t* xsf, const void* wq,
-                             const uint8_t* wsf, float* part, cudaStream_t stream) {
+                             const uint8_t* wsf, float* part, cudaStream_t stream, bool w_dep) {
   using namespace linmx;
   const bool wide = p.n_mma > 256;
   if (p.n_mma > 384 || (wide && p.n_mma % 64) || p.k % 128) return cudaErrorInvalidValue;
@@ -314,6 +316,7 @@ cudaError_t linear_mx_launch(Ctx& ctx, const LinearPlan& p, const void* xq, cons
   kp.w_sf = wsf;
   kp.x_sf = xsf;
   kp.k_words = p.k / 128;
+  kp.w_dep = w_dep ? 1 : 0;
   kp.stage_bytes = (int)align_up((size_t)kA + p.n_mma * 128 + 128 * 16 + p.n_mma * 16, 1024);
   kp.stages = (200 * 1024) / kp.stage_bytes;
   if (kp.stages > (wide ? 8 : 10)) kp.stages = wide ? 8 : 10;

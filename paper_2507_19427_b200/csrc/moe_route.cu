@@ -362,7 +362,8 @@ cudaError_t router_launch(Ctx& ctx, const moe::RouterArgs& a, void* ws, cudaStre
   for (int c0 = 0; c0 < a.T; c0 += kRouterChunk) {
     const int m = min(kRouterChunk, a.T - c0);
     const LinearPlan p = make_linear_plan(a.E, m, a.H);
-    cudaError_t e = linear_bf16_launch(ctx, p, a.gate_w, a.h + (size_t)c0 * a.H, part, stream);
+    // the token rows (the GEMM's weight side) are the predecessor's output: w_dep
+    cudaError_t e = linear_bf16_launch(ctx, p, a.gate_w, a.h + (size_t)c0 * a.H, part, stream, true);
     if (e == cudaSuccess)
       e = launch_k(ctx.pdl, moe::router_topk_kernel, dim3((m + 7) / 8), dim3(256), 0, stream, p, (const float*)part,
                    linear_grid(ctx, p), a, c0);

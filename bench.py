@@ -539,7 +539,7 @@ def afd_runs(world):
     # the FFN partials reduced in the NVSwitch (multimem.ld_reduce) instead of on the attention SMs
     runs += [(base, "mx", 256, "moe", "e4m3", "nvls")]
     # larger micro-batches toward the SLA edge (the FFN stage grows slowly with T at decode)
-    runs += [(base, "mx", T, "moe", "e4m3", "nvls") for T in (320, 352, 368, 384)]
+    runs += [(base, "mx", T, "moe", "e4m3", "nvls") for T in (320, 352, 368, 384, 400, 416)]
     runs.append((bal, "mx", 512, "dense", "bf16", "push"))  # dense layer: FFN tier tensor-parallel over slices
     runs = [r + (0,) for r in runs]
     # o_proj as an MXFP8 GEMM on the attention GPUs (the paper's FP8 attention

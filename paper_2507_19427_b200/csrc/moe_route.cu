@@ -35,72 +35,63 @@ __device__ __forceinline__ uint8_t to_e4m3(float v) {
 
 // ---------------------------------------------------------------- K5 router
 // logits = h . gate^T runs on the tcgen05 stream-K linear kernel (linear.cu:
-// token rows on MMA M, the gate rows on N, fp32 partials, see router_launch);
-// this epilogue sums the partials in fixed segment order (deterministic;
-// identical gate rows give identical logits) for 32 tokens per CTA — lanes
-// own consecutive tokens, so every partial load is one coalesced 128-byte
-// row (one warp per token made each lane a separate 32-byte sector: 18 us at
-// 384 tokens) — then per token (one warp, lanes own experts l and l+32):
-// max-subtracted softmax, top-k by repeated warp argmax with ties to the
-// lower expert id, weights = softmax[id] (optionally renormalised).
+// gate rows on MMA M, up to 256 tokens on N, fp32 partials); this epilogue
+// sums the partials in fixed segment order (deterministic; identical gate rows
+// give identical logits), then per token (one warp, lanes own experts l and
+// l+32): max-subtracted softmax, top-k by repeated warp argmax with ties to
+// the lower expert id, weights = softmax[id] (optionally renormalised).
 __global__ void __launch_bounds__(256) router_topk_kernel(const LinearPlan P, const float* __restrict__ part, int G,
                                                           RouterArgs a, int t_base) {
   __shared__ lin::SlotTable tab;
-  __shared__ float lg[kMaxExperts][33];  // [expert][token of this CTA]
   lin::build_slot_table(P, G, tab);
   sm100::griddep_wait();
   sm100::griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;  // token within this chunk
+  if (row >= P.n_out) return;  // tokens of this chunk (the GEMM's weight rows)
+  const int tok = t_base + row;
+  const int e0 = lane, e1 = lane + 32;
   // the GEMM ran with the tokens on the weight side (P.m_tok = E experts,
   // P.n_out = tokens): logit (token, e) is "row" e, "feature" token
-  const int tb = blockIdx.x * 32;  // this CTA's first token
-  for (int e = warp; e < a.E; e += 8) lg[e][lane] = (tb + lane < P.n_out) ? tab.sum(P, part, e, tb + lane) : 0.0f;
-  __syncthreads();
-  for (int jt = 0; jt < 4; ++jt) {  // 4 tokens per warp
-    const int row = tb + warp * 4 + jt;  // token within this chunk
-    if (row >= P.n_out) return;
-    const int tok = t_base + row;
-    const int e0 = lane, e1 = lane + 32;
-    const float l0 = e0 < a.E ? lg[e0][row - tb] : -INFINITY;
-    const float l1 = e1 < a.E ? lg[e1][row - tb] : -INFINITY;
-    if (a.logits) {
-      if (e0 < a.E) a.logits[(size_t)tok * a.E + e0] = l0;
-      if (e1 < a.E) a.logits[(size_t)tok * a.E + e1] = l1;
-    }
-    float mx = fmaxf(l0, l1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffff, mx, o));
-    float sum = (e0 < a.E ? expf(l0 - mx) : 0.0f) + (e1 < a.E ? expf(l1 - mx) : 0.0f);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
-    bool t0 = e0 >= a.E, t1 = e1 >= a.E;  // taken (or absent)
-    float wk[kMaxTopK];
-    int idk[kMaxTopK];
-    float wsum = 0.0f;
-    for (int j = 0; j < a.k; ++j) {
-      // lane candidate: its larger untaken logit (lower id on ties)
-      float bv = -INFINITY;
-      int bi = 1 << 30;
-      if (!t0) { bv = l0; bi = e0; }
-      if (!t1 && (l1 > bv || bi == (1 << 30))) { bv = l1; bi = e1; }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffff, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffff, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-      }
-      if (bi == e0) t0 = true;
-      if (bi == e1) t1 = true;
-      idk[j] = bi;
-      wk[j] = expf(bv - mx) / sum;
-      wsum += wk[j];
-    }
-    if (lane == 0)
-      for (int q = 0; q < a.k; ++q) {
-        a.ids[(size_t)tok * a.k + q] = idk[q];
-        a.weights[(size_t)tok * a.k + q] = a.renormalize ? wk[q] / wsum : wk[q];
-      }
+  const float l0 = e0 < a.E ? tab.sum(P, part, e0, row) : -INFINITY;
+  const float l1 = e1 < a.E ? tab.sum(P, part, e1, row) : -INFINITY;
+  if (a.logits) {
+    if (e0 < a.E) a.logits[(size_t)tok * a.E + e0] = l0;
+    if (e1 < a.E) a.logits[(size_t)tok * a.E + e1] = l1;
   }
+  float mx = fmaxf(l0, l1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffff, mx, o));
+  float sum = (e0 < a.E ? expf(l0 - mx) : 0.0f) + (e1 < a.E ? expf(l1 - mx) : 0.0f);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, o);
+  bool t0 = e0 >= a.E, t1 = e1 >= a.E;  // taken (or absent)
+  float wk[kMaxTopK];
+  int idk[kMaxTopK];
+  float wsum = 0.0f;
+  for (int j = 0; j < a.k; ++j) {
+    // lane candidate: its larger untaken logit (lower id on ties)
+    float bv = -INFINITY;
+    int bi = 1 << 30;
+    if (!t0) { bv = l0; bi = e0; }
+    if (!t1 && (l1 > bv || bi == (1 << 30))) { bv = l1; bi = e1; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffff, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffff, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (bi == e0) t0 = true;
+    if (bi == e1) t1 = true;
+    idk[j] = bi;
+    wk[j] = expf(bv - mx) / sum;
+    wsum += wk[j];
+  }
+  if (lane == 0)
+    for (int j = 0; j < a.k; ++j) {
+      a.ids[(size_t)tok * a.k + j] = idk[j];
+      a.weights[(size_t)tok * a.k + j] = a.renormalize ? wk[j] / wsum : wk[j];
+    }
 }
 
 // FP8 dispatch payload (1x128 blocks): one warp per (token, block), 4 features per lane
@@ -374,7 +365,7 @@ cudaError_t router_launch(Ctx& ctx, const moe::RouterArgs& a, void* ws, cudaStre
     // the token rows (the GEMM's weight side) are the predecessor's output: w_dep
     cudaError_t e = linear_bf16_launch(ctx, p, a.gate_w, a.h + (size_t)c0 * a.H, part, stream, true);
     if (e == cudaSuccess)
-      e = launch_k(ctx.pdl, moe::router_topk_kernel, dim3((m + 31) / 32), dim3(256), 0, stream, p, (const float*)part,
+      e = launch_k(ctx.pdl, moe::router_topk_kernel, dim3((m + 7) / 8), dim3(256), 0, stream, p, (const float*)part,
                    linear_grid(ctx, p), a, c0);
     if (e != cudaSuccess) return e;
   }
